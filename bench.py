@@ -1,0 +1,279 @@
+"""Benchmark: end-to-end RT0 / NE0 assembly (symbolic + numeric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl efem|reference]
+
+One JSON line on rank 0.  A "step" is one pass of the whole hot path over the
+device-resident mesh of the chosen BASELINE config: DOF enumeration + signs,
+sparsity pattern, local matrices and CSR values (efem_assemble_symbolic +
+efem_assemble_numeric + efem_plan_check).  L2 is flushed between timed steps
+(a 512 MiB write, untimed).  value = elements / second over all ranks.
+See DESIGN.md "Measurement" for the roofline bytes and the oracle baseline.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import CONFIGS, ELEMENT_NAMES, counts  # noqa: E402
+
+METRIC = "elements assembled/sec (local matrices + CSR)"
+UNIT = "elem/s"
+
+
+def algorithmic_bytes(cfg):
+    """north_star: mesh in (coords fp64 + int32 connectivity) + CSR out
+    (int32 row_ptr / col_idx, fp64 vals for M and K on one pattern)."""
+    N, T, R, nnz = counts(cfg["dim"], cfg["element"], cfg["n"])
+    mesh_in = N * cfg["dim"] * 8 + T * (cfg["dim"] + 1) * 4
+    csr_out = (R + 1) * 4 + nnz * 4 + 2 * nnz * 8
+    return mesh_in + csr_out, T
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(cfg, budget_elems=None):
+    """The oracle as it stands, single thread, on a bounded sample of the same
+    workload: the first T_s elements of the config's mesh (all their DOFs and
+    rows), mesh already in host RAM."""
+    import numpy as np
+
+    from oracle import oracle as ora
+
+    coords, elems = ora.build_mesh(cfg["dim"], cfg["n"], cfg["alpha"], cfg["seed"])
+    if budget_elems is None:
+        budget_elems = (1 << 21) if cfg["dim"] == 2 else (1 << 20)
+    ts = min(elems.shape[0], budget_elems)
+    sub = np.ascontiguousarray(elems[:ts])
+    t0 = time.perf_counter()
+    ora.assemble(cfg["dim"], cfg["element"], coords, sub)
+    dt = time.perf_counter() - t0
+    return {"value": ts / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {ts} of {elems.shape[0]} elements of {cfg['name']} ({dt:.1f} s, 1 thread, "
+                      f"g++ -O2 -ffp-contract=off, std::map accumulator)"}
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    budget = (1 << 19) if cfg["dim"] == 2 else (1 << 18)
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, budget_elems=1 << 12)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(cfg, budget_elems=budget))
+    total = time.perf_counter() - t0
+    ts = min(budget, counts(cfg["dim"], cfg["element"], cfg["n"])[1])
+    value = ts * args.steps / sum(ts / v["value"] for v in vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg["name"], "element": ELEMENT_NAMES[cfg["element"]],
+                                            "dim": cfg["dim"], "n": cfg["n"], "jitter": cfg["alpha"],
+                                            "seed": cfg["seed"], "sample_elems": ts},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": vals[-1]["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_efem(args, cfg):
+    import torch
+
+    from paper_1409_4618_b200 import api
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        raise SystemExit("multi-GPU bench path not built yet (DESIGN.md: next row a6)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    coords, elems = api.build_mesh(cfg["dim"], cfg["n"], cfg["alpha"], cfg["seed"], device=dev)
+    asm = api.Assembler(coords, elems, cfg["element"])
+    asm.symbolic()
+    out = asm.alloc_csr()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        asm.symbolic()
+        asm.numeric(out, api.ALL)
+        asm.check()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    # timed region: K steps, each bracketed by its own events, L2 flushed in between (untimed)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = api.launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.fill_(k & 0xff)
+            starts[k].record(stream)
+            step()
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+    launches = api.launch_count() - l0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    T = elems.shape[0]
+    value = T * args.steps / (total_ms * 1e-3)
+
+    # dominant kernel (numeric: k_row_fill + row_ptr copy), timed alone the same way
+    nk = max(args.steps, 5)
+    ks = [torch.cuda.Event(enable_timing=True) for _ in range(nk)]
+    ke = [torch.cuda.Event(enable_timing=True) for _ in range(nk)]
+    for k in range(nk):
+        flush.fill_(k & 0xff)
+        ks[k].record(stream)
+        asm.numeric(out, api.ALL)
+        ke[k].record(stream)
+    torch.cuda.synchronize()
+    asm.check()
+    num_ms = sum(s.elapsed_time(e) for s, e in zip(ks, ke)) / nk
+    sym_ms = total_ms / args.steps - num_ms
+
+    alg_bytes, _ = algorithmic_bytes(cfg)
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured" if peak else "fallback"
+    peak = peak or 6650.0
+    achieved = alg_bytes / (num_ms * 1e-3) / 1e9
+    e2e_gbs = alg_bytes / (total_ms / args.steps * 1e-3) / 1e9
+
+    # end to end through the public API with HOST buffers (copies inside the timed region)
+    h_c = coords.cpu().pin_memory()
+    h_e = elems.cpu().pin_memory()
+    h_out = api.CSR(*(torch.empty_like(t, device="cpu").pin_memory() for t in
+                      (out.row_ptr, out.col_idx, out.vals_M, out.vals_K)))
+    d_out = asm.alloc_csr()
+    asm.assemble_host(h_c, h_e, d_out, h_out)  # warm
+    e2e_steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        asm.assemble_host(h_c, h_e, d_out, h_out)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    h2d = h_c.numel() * 8 + h_e.numel() * 4
+    d2h = (h_out.row_ptr.numel() + h_out.col_idx.numel()) * 4 + 2 * h_out.vals_M.numel() * 8
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "element": ELEMENT_NAMES[cfg["element"]], "dim": cfg["dim"],
+                   "n": cfg["n"], "jitter": cfg["alpha"], "seed": cfg["seed"], "n_elems": T,
+                   "n_rows": asm.n_rows, "nnz": asm.nnz, "l2": "flushed between timed steps (512 MiB write)"},
+        "phase_ms": {"symbolic": sym_ms, "numeric": num_ms},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "k_row_fill (numeric)",
+                     "peak_source": peak_src, "algorithmic_bytes": alg_bytes,
+                     "e2e_achieved": e2e_gbs, "e2e_frac": e2e_gbs / peak},
+        "e2e": {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="efem", choices=["efem", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_efem(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

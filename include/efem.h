@@ -1,0 +1,186 @@
+/*
+ * efem.h -- C-ABI of libefem.so: B200 (sm_100a) assembly of the global mass
+ * and stiffness matrices of lowest-order Raviart-Thomas (RT0, H(div)) and
+ * Nedelec (NE0, H(curl)) edge elements on affine triangle / tetrahedron
+ * meshes into CSR.
+ *
+ * Paper: I. Anjam, J. Valdman, "Fast MATLAB assembly of FEM matrices in 2D and
+ * 3D: Edge elements", arXiv:1409.4618.  "PAPER.md:N" cites line N of its LaTeX
+ * source.  The four matrices are (Sec. 2.4)
+ *     M_ij = int_Omega eta_i . eta_j,
+ *     K_ij = int_Omega div eta_i div eta_j      (RT0)
+ *     K_ij = int_Omega curl eta_i . curl eta_j  (NE0),
+ * over the global, sign-corrected Piola-mapped basis (PAPER.md:240-245,
+ * 291-331).  The readings of the paper this library takes (3D RT
+ * normalisation, 3D sign rules, DOF order ...) are listed in DESIGN.md.
+ *
+ * Conventions shared by every call
+ *   - All arrays are DEVICE memory owned by the caller (PyTorch tensors in
+ *     the Python binding) unless a parameter name starts with h_.  The
+ *     library never frees caller memory.
+ *   - Every call that takes a cudaStream_t only enqueues work on that stream
+ *     unless documented as "synchronising".
+ *   - Indices are 0-based int32; meshes with > 2^31-1 entries are rejected
+ *     with EFEM_EOVERFLOW.
+ *   - Every call returns an efem_status; on error no output is guaranteed and
+ *     efem_last_error() returns a thread-local message.
+ */
+#ifndef EFEM_H
+#define EFEM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* efem_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    EFEM_OK = 0,
+    EFEM_EINVAL = -1,      /* bad argument: dim not in {2,3}, n < 1, NULL pointer, node id out of range,
+                              jitter outside [0, 1/(2 sqrt(2 d))) ... */
+    EFEM_EDEGENERATE = -2, /* an element has det B_K == 0 (or non-finite); efem_last_bad_element() names it */
+    EFEM_ENOMEM = -3,      /* host allocation failed */
+    EFEM_EWORKSPACE = -4,  /* workspace NULL or smaller than efem_plan_create reported */
+    EFEM_EOVERFLOW = -5,   /* a count does not fit int32 (nnz >= 2^31, T*(d+1) >= 2^31 ...) */
+    EFEM_ECUDA = -6,       /* CUDA runtime error; message in efem_last_error() */
+    EFEM_ENCCL = -7,       /* NCCL error (distributed entry points) */
+    EFEM_ECAPACITY = -8,   /* a node touches more elements / owns more entities than the
+                              per-thread capacity (EFEM_MAX_NODE_ELEMS etc.); mesh too irregular */
+    EFEM_ESTATE = -9       /* calls made out of order (e.g. numeric before symbolic) */
+} efem_status;
+
+typedef enum {
+    EFEM_RT0 = 0, /* Raviart-Thomas: 2D -> one DOF per edge (normal flux), 3D -> one per face */
+    EFEM_NED0 = 1 /* Nedelec (first kind): one DOF per edge (tangential moment), 2D and 3D */
+} efem_element;
+
+/* forms bitmask for efem_assemble_numeric */
+enum { EFEM_MASS = 1, EFEM_STIFF = 2, EFEM_PATTERN = 4, EFEM_ALL = 7 };
+
+/* capacities of the per-thread register / local-memory lists */
+enum { EFEM_MAX_NODE_ENTITIES = 64, EFEM_MAX_ROW_ELEMS = 32, EFEM_MAX_ROW_NNZ = 128 };
+
+/* A mesh (nodes2coord, elems2nodes).
+ *   coords : n_nodes x dim fp64, row-major (node i at coords[i*dim .. i*dim+dim-1])
+ *   elems  : n_elems x (dim+1) int32, row-major; any vertex order (the sign
+ *            data absorbs orientation). */
+typedef struct {
+    int32_t dim;
+    int64_t n_nodes;
+    int64_t n_elems;
+    const double* coords;
+    const int32_t* elems;
+} efem_mesh;
+
+/* Global DOF tables.
+ *   dofs2nodes : n_dofs x 2 (edges) or x 3 (3D RT faces) int32, each row the
+ *                ascending node ids of the entity; rows in lexicographic order
+ *                (DOF id = rank; reading C10)
+ *   elems2dofs : n_elems x m int32 (m = 3 / 4 / 6 local DOFs, Fig. 1 order)
+ *   signs      : n_elems x m int8, +1 / -1 */
+typedef struct {
+    int64_t n_dofs;
+    int32_t* dofs2nodes;
+    int32_t* elems2dofs;
+    int8_t* signs;
+} efem_dofs;
+
+/* CSR output; M and K share one pattern (all structural entries kept,
+ * columns ascending within a row).  row_ptr: n_rows+1, col_idx/vals: nnz. */
+typedef struct {
+    int64_t n_rows;
+    int64_t nnz;
+    int32_t* row_ptr;
+    int32_t* col_idx;
+    double* vals_mass;
+    double* vals_stiff;
+} efem_csr;
+
+typedef struct efem_plan_s* efem_plan;
+
+/* ---- meshes (input generator, untimed) -------------------------------------- */
+
+/* Sizes of the structured unit-square / unit-cube mesh with n cells per axis:
+ * 2D -> (n+1)^2 nodes, 2 n^2 triangles; 3D -> (n+1)^3 nodes, 6 n^3 Kuhn tets. */
+efem_status efem_mesh_sizes(int dim, int n, int64_t* n_nodes, int64_t* n_elems);
+
+/* Seeded structured mesh (SPEC.md:49-58 for the split):
+ * node id = i + (n+1) j (+ (n+1)^2 k); interior nodes jittered uniformly by
+ * +-jitter_frac/n per axis from a SplitMix64 counter hash of (seed, node*dim+axis);
+ * 2D cells split along the lower-left/upper-right diagonal, 3D cubes into the
+ * 6 Kuhn tets around the (0,0,0)-(1,1,1) diagonal.  m->coords / m->elems must
+ * point to caller-allocated device arrays of the sizes above; m->dim,
+ * n_nodes, n_elems are filled in.  Bit-identical to the CPU oracle's
+ * generator. */
+efem_status efem_build_mesh(int dim, int n, double jitter_frac, uint64_t seed, double* coords, int32_t* elems,
+                            efem_stream_t stream);
+
+/* ---- plans ------------------------------------------------------------------- */
+
+/* Create a host-side plan for assembling `element` on `mesh` (device arrays,
+ * which must stay alive and unchanged while the plan is used).  Returns in
+ * *ws_bytes the device workspace the plan needs (an upper bound derived from
+ * n_nodes, n_elems).  No device work.  Errors: EFEM_EINVAL, EFEM_EOVERFLOW,
+ * EFEM_ENOMEM. */
+efem_status efem_plan_create(efem_plan* plan, const efem_mesh* mesh, efem_element element, size_t* ws_bytes);
+
+/* Attach the caller-allocated device workspace (>= *ws_bytes, 256-byte
+ * aligned).  Contents are the plan's state between the calls below; the
+ * caller must not touch it. */
+efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes);
+
+efem_status efem_plan_destroy(efem_plan plan);
+
+/* ---- the hot path ------------------------------------------------------------ */
+
+/* DOF enumeration + orientation (Sec. 3 get_edges /
+ * get_faces / signs_edges / signs_faces).  Synchronising (reads n_dofs back).
+ * out->n_dofs is always set.  If out->dofs2nodes / elems2dofs / signs are
+ * non-NULL they are filled (each may be NULL independently).  Idempotent:
+ * a second call on the same plan only copies the tables out. */
+efem_status efem_enumerate_dofs(efem_plan plan, efem_dofs* out, efem_stream_t stream);
+
+/* Symbolic assembly: DOF enumeration (if not yet done) + CSR sparsity pattern
+ * sizes: the structural pattern is the union over elements of
+ * dofs(K) x dofs(K) (reading C9).  Synchronising (reads nnz
+ * back).  If row_ptr != NULL it receives the n_rows+1 row offsets.  Returns
+ * EFEM_EOVERFLOW when nnz >= 2^31. */
+efem_status efem_assemble_symbolic(efem_plan plan, int64_t* n_rows, int64_t* nnz, int32_t* row_ptr,
+                                   efem_stream_t stream);
+
+/* Numeric assembly into caller-allocated CSR arrays (sizes from symbolic):
+ * local matrices computed in fp64 registers and summed
+ * per row in ascending element order.  forms: EFEM_PATTERN writes row_ptr and
+ * col_idx, EFEM_MASS vals_mass, EFEM_STIFF vals_stiff (NULL allowed for
+ * arrays whose bit is clear).  Asynchronous: degenerate elements are
+ * reported by efem_plan_check. */
+efem_status efem_assemble_numeric(efem_plan plan, unsigned forms, efem_csr* out, efem_stream_t stream);
+
+/* Synchronising: returns EFEM_EDEGENERATE / EFEM_ECAPACITY if a kernel since
+ * the last check flagged one, else EFEM_OK (or EFEM_ECUDA). */
+efem_status efem_plan_check(efem_plan plan, efem_stream_t stream);
+
+/* End-to-end convenience used for the "e2e" number: HOST mesh in, HOST CSR
+ * out.  Copies h_coords / h_elems into the plan's device mesh arrays (the
+ * plan must have been created on device arrays of the same sizes), runs
+ * symbolic + numeric, checks, and copies row_ptr / col_idx / vals back into
+ * h_out (host arrays with capacity h_out->nnz, h_out->n_rows+1 set by the
+ * caller from a previous symbolic call).  d_out are device CSR arrays of the
+ * same capacity.  Synchronising. */
+efem_status efem_assemble_host(efem_plan plan, const double* h_coords, const int32_t* h_elems, efem_csr* d_out,
+                               efem_csr* h_out, efem_stream_t stream);
+
+/* ---- diagnostics ------------------------------------------------------------- */
+const char* efem_status_string(efem_status status);
+const char* efem_last_error(void);
+int64_t efem_last_bad_element(void);
+/* number of kernel launches issued by the library since process start */
+int64_t efem_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EFEM_H */

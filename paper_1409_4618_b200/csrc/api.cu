@@ -1,0 +1,403 @@
+// api.cu -- the C-ABI of include/efem.h: plans, workspace layout, the
+// enumerate -> symbolic -> numeric pipeline, status plumbing.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "efem_internal.cuh"
+
+namespace efem {
+
+// launchers defined in dofs.cu / assemble.cu
+efem_status launch_incidence(Plan& p, cudaStream_t s);
+efem_status launch_incidence_fill(Plan& p, cudaStream_t s);
+efem_status launch_entities_any(Plan& p, bool fill, cudaStream_t s);
+efem_status launch_signs(Plan& p, int8_t* out, cudaStream_t s);
+efem_status launch_rows_any(Plan& p, bool fill, unsigned forms, efem_csr* out, cudaStream_t s);
+
+namespace {
+thread_local std::string g_last_error;
+thread_local int64_t g_bad_element = -1;
+std::atomic<int64_t> g_launches{0};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Layout {
+    size_t hdr, cnt, n2e_ptr, n2e, ent_cnt, ent_ptr, d2n, e2d, row_cnt, row_ptr, cub, total;
+};
+
+Layout layout(const Plan& p, size_t cub_bytes) {
+    Layout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += align256(bytes);
+        return o;
+    };
+    const size_t N1 = (size_t)p.n_nodes + 1;
+    L.hdr = take(sizeof(WsHeader));
+    L.cnt = take(N1 * 4);
+    L.n2e_ptr = take(N1 * 4);
+    L.n2e = take((size_t)p.n_elems * p.nv * 4);
+    L.ent_cnt = take(N1 * 4);
+    L.ent_ptr = take(N1 * 4);
+    L.d2n = take((size_t)p.r_max * p.ek * 4);
+    L.e2d = take((size_t)p.n_elems * p.m * 4);
+    L.row_cnt = take(((size_t)p.r_max + 1) * 4);
+    L.row_ptr = take(((size_t)p.r_max + 1) * 4);
+    L.cub = take(cub_bytes);
+    L.total = off;
+    return L;
+}
+
+efem_status scan(Plan& p, const int32_t* in, int32_t* out, int64_t n, cudaStream_t s) {
+    size_t bytes = p.cub_bytes;
+    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, in, out, (int)n, s));
+    count_launch();
+    return EFEM_OK;
+}
+
+efem_status read_flags(Plan& p, cudaStream_t s) {
+    EFEM_CUDA_TRY(cudaMemcpyAsync(p.h_hdr, p.hdr, sizeof(WsHeader), cudaMemcpyDeviceToHost, s));
+    EFEM_CUDA_TRY(cudaStreamSynchronize(s));
+    const WsHeader& h = *p.h_hdr;
+    if (h.flags[F_INVALID_NODE]) {
+        set_error("an element references a node id outside [0, n_nodes)");
+        return EFEM_EINVAL;
+    }
+    if (h.flags[F_DEGENERATE]) {
+        set_bad_element((int64_t)h.bad_element);
+        set_error("degenerate element (det B_K == 0 or non-finite): " + std::to_string(h.bad_element));
+        return EFEM_EDEGENERATE;
+    }
+    if (h.flags[F_CAPACITY]) {
+        set_error("per-thread capacity exceeded (mesh too irregular for EFEM_MAX_* limits)");
+        return EFEM_ECAPACITY;
+    }
+    if (h.flags[F_ROW_MISMATCH]) {
+        set_error("internal error: numeric row length differs from symbolic row length");
+        return EFEM_ECUDA;
+    }
+    return EFEM_OK;
+}
+
+efem_status reset_header(Plan& p, cudaStream_t s) {
+    static_assert(sizeof(WsHeader) <= 256, "header");
+    // small pinned-free path: memset then set bad_element
+    EFEM_CUDA_TRY(cudaMemsetAsync(p.hdr, 0, sizeof(WsHeader), s));
+    EFEM_CUDA_TRY(cudaMemsetAsync(&p.hdr->bad_element, 0xff, sizeof(unsigned long long), s));
+    return EFEM_OK;
+}
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void set_bad_element(int64_t e) { g_bad_element = e; }
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ------------------------------------------------------------------------------------
+efem_status run_enumerate(Plan& p, cudaStream_t s) {
+    efem_status st;
+    if ((st = reset_header(p, s)) != EFEM_OK) return st;
+    const int64_t N = p.n_nodes;
+    // 1. node -> element incidence (counting sort)
+    EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (N + 1) * 4, s));
+    if ((st = launch_incidence(p, s)) != EFEM_OK) return st;
+    if ((st = scan(p, p.cnt, p.n2e_ptr, N + 1, s)) != EFEM_OK) return st;
+    if ((st = launch_incidence_fill(p, s)) != EFEM_OK) return st;
+    // 2. entities owned by their minimum node: count, scan, fill
+    if ((st = launch_entities_any(p, false, s)) != EFEM_OK) return st;
+    EFEM_CUDA_TRY(cudaMemsetAsync(p.ent_cnt + N, 0, 4, s));
+    if ((st = scan(p, p.ent_cnt, p.ent_ptr, N + 1, s)) != EFEM_OK) return st;
+    if ((st = launch_entities_any(p, true, s)) != EFEM_OK) return st;
+    EFEM_CUDA_TRY(cudaMemcpyAsync(p.h_scalars, p.ent_ptr + N, 4, cudaMemcpyDeviceToHost, s));
+    if ((st = read_flags(p, s)) != EFEM_OK) return st;  // synchronises
+    p.n_dofs = *reinterpret_cast<int32_t*>(p.h_scalars);
+    p.enumerated = true;
+    return EFEM_OK;
+}
+
+efem_status run_symbolic(Plan& p, cudaStream_t s) {
+    efem_status st;
+    if (!p.enumerated) {
+        if ((st = run_enumerate(p, s)) != EFEM_OK) return st;
+    }
+    const int64_t R = p.n_dofs;
+    // the int32 scan below cannot wrap past 2^32 when every row count is
+    // bounded by its scratch capacity (<= 48): then nnz >= 2^31 shows up as a
+    // negative int32 total.
+    if (R * 48 >= (1ll << 32)) {
+        set_error("too many rows for int32 CSR offsets");
+        return EFEM_EOVERFLOW;
+    }
+    if ((st = launch_rows_any(p, false, 0, nullptr, s)) != EFEM_OK) return st;
+    EFEM_CUDA_TRY(cudaMemsetAsync(p.row_cnt + R, 0, 4, s));
+    if ((st = scan(p, p.row_cnt, p.row_ptr, R + 1, s)) != EFEM_OK) return st;
+    EFEM_CUDA_TRY(cudaMemcpyAsync(p.h_scalars, p.row_ptr + R, 4, cudaMemcpyDeviceToHost, s));
+    if ((st = read_flags(p, s)) != EFEM_OK) return st;
+    const int32_t nnz32 = *reinterpret_cast<int32_t*>(p.h_scalars);
+    if (nnz32 < 0) {
+        set_error("nnz >= 2^31 does not fit int32 CSR");
+        return EFEM_EOVERFLOW;
+    }
+    p.nnz = nnz32;
+    p.symbolic = true;
+    return EFEM_OK;
+}
+
+efem_status run_numeric(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) {
+    efem_status st;
+    if (forms & EFEM_PATTERN) {
+        EFEM_CUDA_TRY(cudaMemcpyAsync(out->row_ptr, p.row_ptr, (p.n_dofs + 1) * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    if ((st = launch_rows_any(p, true, forms, out, s)) != EFEM_OK) return st;
+    return EFEM_OK;
+}
+
+}  // namespace efem
+
+using namespace efem;
+
+extern "C" {
+
+const char* efem_status_string(efem_status st) {
+    switch (st) {
+        case EFEM_OK: return "EFEM_OK";
+        case EFEM_EINVAL: return "EFEM_EINVAL";
+        case EFEM_EDEGENERATE: return "EFEM_EDEGENERATE";
+        case EFEM_ENOMEM: return "EFEM_ENOMEM";
+        case EFEM_EWORKSPACE: return "EFEM_EWORKSPACE";
+        case EFEM_EOVERFLOW: return "EFEM_EOVERFLOW";
+        case EFEM_ECUDA: return "EFEM_ECUDA";
+        case EFEM_ENCCL: return "EFEM_ENCCL";
+        case EFEM_ECAPACITY: return "EFEM_ECAPACITY";
+        case EFEM_ESTATE: return "EFEM_ESTATE";
+    }
+    return "unknown efem_status";
+}
+
+const char* efem_last_error(void) { return g_last_error.c_str(); }
+int64_t efem_last_bad_element(void) { return g_bad_element; }
+int64_t efem_launch_count(void) { return g_launches.load(); }
+
+efem_status efem_mesh_sizes(int dim, int n, int64_t* n_nodes, int64_t* n_elems) {
+    if ((dim != 2 && dim != 3) || n < 1 || !n_nodes || !n_elems) {
+        set_error("efem_mesh_sizes: dim must be 2 or 3, n >= 1, outputs non-NULL");
+        return EFEM_EINVAL;
+    }
+    const int64_t n1 = (int64_t)n + 1;
+    *n_nodes = dim == 2 ? n1 * n1 : n1 * n1 * n1;
+    *n_elems = dim == 2 ? 2ll * n * n : 6ll * n * n * n;
+    if (*n_elems * (dim + 1) >= (1ll << 31) || *n_nodes >= (1ll << 31)) {
+        set_error("efem_mesh_sizes: mesh does not fit int32 indices");
+        return EFEM_EOVERFLOW;
+    }
+    return EFEM_OK;
+}
+
+efem_status efem_build_mesh(int dim, int n, double jitter_frac, uint64_t seed, double* coords, int32_t* elems,
+                            efem_stream_t stream) {
+    int64_t N, T;
+    efem_status st = efem_mesh_sizes(dim, n, &N, &T);
+    if (st != EFEM_OK) return st;
+    // interior jitter must keep every element valid: 2 alpha sqrt(d) < 1/sqrt(2)
+    const double lim = 1.0 / (2.0 * std::sqrt(2.0 * dim));
+    if (!coords || !elems || !(jitter_frac >= 0.0) || !(jitter_frac < lim)) {
+        set_error("efem_build_mesh: NULL array or jitter_frac outside [0, 1/(2 sqrt(2 dim)))");
+        return EFEM_EINVAL;
+    }
+    return launch_build_mesh(dim, n, jitter_frac, seed, coords, elems, (cudaStream_t)stream);
+}
+
+efem_status efem_plan_create(efem_plan* plan, const efem_mesh* mesh, efem_element element, size_t* ws_bytes) {
+    if (!plan || !mesh || !ws_bytes) {
+        set_error("efem_plan_create: NULL argument");
+        return EFEM_EINVAL;
+    }
+    if ((mesh->dim != 2 && mesh->dim != 3) || (element != EFEM_RT0 && element != EFEM_NED0) ||
+        mesh->n_nodes < 0 || mesh->n_elems < 0 || (mesh->n_elems > 0 && (!mesh->coords || !mesh->elems))) {
+        set_error("efem_plan_create: bad mesh (dim 2|3, element RT0|NED0, non-negative sizes, device arrays)");
+        return EFEM_EINVAL;
+    }
+    if ((reinterpret_cast<uintptr_t>(mesh->elems) & 15) != 0 && mesh->dim == 3) {
+        set_error("efem_plan_create: 3D elems must be 16-byte aligned (int4 loads)");
+        return EFEM_EINVAL;
+    }
+    Plan* p = new (std::nothrow) Plan;
+    if (!p) return EFEM_ENOMEM;
+    p->dim = mesh->dim;
+    p->element = element;
+    p->nv = mesh->dim + 1;
+    p->m = mesh->dim == 2 ? 3 : (element == EFEM_RT0 ? 4 : 6);
+    p->ek = (mesh->dim == 3 && element == EFEM_RT0) ? 3 : 2;
+    p->n_nodes = mesh->n_nodes;
+    p->n_elems = mesh->n_elems;
+    p->coords = mesh->coords;
+    p->elems = mesh->elems;
+    p->r_max = p->n_elems * p->m;
+    if (p->n_elems >= (1ll << 29) || p->n_nodes >= (1ll << 31) - 1 || p->r_max * p->ek >= (1ll << 31)) {
+        delete p;
+        set_error("efem_plan_create: mesh too large for int32 indexing (n_elems < 2^29)");
+        return EFEM_EOVERFLOW;
+    }
+    size_t cub_bytes = 0;
+    int64_t scan_n = std::max<int64_t>(p->n_nodes + 1, p->r_max + 1);
+    cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (const int32_t*)nullptr, (int32_t*)nullptr, (int)scan_n);
+    p->cub_bytes = cub_bytes;
+    p->ws_need = layout(*p, cub_bytes).total;
+    if (cudaMallocHost(&p->h_scalars, 64) != cudaSuccess || cudaMallocHost(&p->h_hdr, sizeof(WsHeader)) != cudaSuccess) {
+        delete p;
+        set_error("efem_plan_create: cudaMallocHost failed");
+        return EFEM_ECUDA;
+    }
+    *ws_bytes = p->ws_need;
+    *plan = reinterpret_cast<efem_plan>(p);
+    return EFEM_OK;
+}
+
+efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p) return EFEM_EINVAL;
+    if (!ws || ws_bytes < p->ws_need || (reinterpret_cast<uintptr_t>(ws) & 255)) {
+        set_error("efem_plan_set_workspace: workspace NULL, too small or not 256-byte aligned");
+        return EFEM_EWORKSPACE;
+    }
+    const Layout L = layout(*p, p->cub_bytes);
+    char* b = static_cast<char*>(ws);
+    p->ws = b;
+    p->ws_bytes = ws_bytes;
+    p->hdr = reinterpret_cast<WsHeader*>(b + L.hdr);
+    p->cnt = reinterpret_cast<int32_t*>(b + L.cnt);
+    p->n2e_ptr = reinterpret_cast<int32_t*>(b + L.n2e_ptr);
+    p->n2e = reinterpret_cast<int32_t*>(b + L.n2e);
+    p->ent_cnt = reinterpret_cast<int32_t*>(b + L.ent_cnt);
+    p->ent_ptr = reinterpret_cast<int32_t*>(b + L.ent_ptr);
+    p->d2n = reinterpret_cast<int32_t*>(b + L.d2n);
+    p->e2d = reinterpret_cast<int32_t*>(b + L.e2d);
+    p->row_cnt = reinterpret_cast<int32_t*>(b + L.row_cnt);
+    p->row_ptr = reinterpret_cast<int32_t*>(b + L.row_ptr);
+    p->cub_tmp = b + L.cub;
+    p->enumerated = p->symbolic = false;
+    return EFEM_OK;
+}
+
+efem_status efem_plan_destroy(efem_plan plan) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p) return EFEM_OK;
+    if (p->h_scalars) cudaFreeHost(p->h_scalars);
+    if (p->h_hdr) cudaFreeHost(p->h_hdr);
+    delete p;
+    return EFEM_OK;
+}
+
+static efem_status need_ws(Plan* p) {
+    if (!p) {
+        set_error("NULL plan");
+        return EFEM_EINVAL;
+    }
+    if (!p->ws) {
+        set_error("plan has no workspace (efem_plan_set_workspace)");
+        return EFEM_EWORKSPACE;
+    }
+    return EFEM_OK;
+}
+
+efem_status efem_enumerate_dofs(efem_plan plan, efem_dofs* out, efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    efem_status st = need_ws(p);
+    if (st != EFEM_OK) return st;
+    if (!out) {
+        set_error("efem_enumerate_dofs: NULL out");
+        return EFEM_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    p->symbolic = false;
+    p->enumerated = false;
+    if ((st = run_enumerate(*p, s)) != EFEM_OK) return st;
+    out->n_dofs = p->n_dofs;
+    if (out->dofs2nodes && p->n_dofs)
+        EFEM_CUDA_TRY(cudaMemcpyAsync(out->dofs2nodes, p->d2n, p->n_dofs * p->ek * 4, cudaMemcpyDeviceToDevice, s));
+    if (out->elems2dofs && p->n_elems)
+        EFEM_CUDA_TRY(cudaMemcpyAsync(out->elems2dofs, p->e2d, p->n_elems * p->m * 4, cudaMemcpyDeviceToDevice, s));
+    if (out->signs && (st = launch_signs(*p, out->signs, s)) != EFEM_OK) return st;
+    return EFEM_OK;
+}
+
+efem_status efem_assemble_symbolic(efem_plan plan, int64_t* n_rows, int64_t* nnz, int32_t* row_ptr,
+                                   efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    efem_status st = need_ws(p);
+    if (st != EFEM_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    p->enumerated = false;  // the end-to-end path always re-enumerates
+    p->symbolic = false;
+    if ((st = run_symbolic(*p, s)) != EFEM_OK) return st;
+    if (n_rows) *n_rows = p->n_dofs;
+    if (nnz) *nnz = p->nnz;
+    if (row_ptr) EFEM_CUDA_TRY(cudaMemcpyAsync(row_ptr, p->row_ptr, (p->n_dofs + 1) * 4, cudaMemcpyDeviceToDevice, s));
+    return EFEM_OK;
+}
+
+efem_status efem_assemble_numeric(efem_plan plan, unsigned forms, efem_csr* out, efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    efem_status st = need_ws(p);
+    if (st != EFEM_OK) return st;
+    if (!p->symbolic) {
+        set_error("efem_assemble_numeric before efem_assemble_symbolic");
+        return EFEM_ESTATE;
+    }
+    const bool has_nz = p->nnz > 0;
+    if (!out || out->n_rows != p->n_dofs || out->nnz != p->nnz || (has_nz && !out->col_idx) ||
+        ((forms & EFEM_PATTERN) && !out->row_ptr) || (has_nz && (forms & EFEM_MASS) && !out->vals_mass) ||
+        (has_nz && (forms & EFEM_STIFF) && !out->vals_stiff) || (forms & ~7u)) {
+        set_error("efem_assemble_numeric: out sizes must equal symbolic n_rows/nnz; arrays for every form bit; "
+                  "col_idx always required");
+        return EFEM_EINVAL;
+    }
+    return run_numeric(*p, forms, out, (cudaStream_t)stream);
+}
+
+efem_status efem_plan_check(efem_plan plan, efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    efem_status st = need_ws(p);
+    if (st != EFEM_OK) return st;
+    return read_flags(*p, (cudaStream_t)stream);
+}
+
+efem_status efem_assemble_host(efem_plan plan, const double* h_coords, const int32_t* h_elems, efem_csr* d_out,
+                               efem_csr* h_out, efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    efem_status st = need_ws(p);
+    if (st != EFEM_OK) return st;
+    if (!h_coords || !h_elems || !d_out || !h_out) {
+        set_error("efem_assemble_host: NULL argument");
+        return EFEM_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    EFEM_CUDA_TRY(cudaMemcpyAsync(const_cast<double*>(p->coords), h_coords, p->n_nodes * p->dim * 8,
+                                  cudaMemcpyHostToDevice, s));
+    EFEM_CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(p->elems), h_elems, p->n_elems * p->nv * 4,
+                                  cudaMemcpyHostToDevice, s));
+    int64_t R, nnz;
+    if ((st = efem_assemble_symbolic(plan, &R, &nnz, nullptr, stream)) != EFEM_OK) return st;
+    if (d_out->nnz < nnz || d_out->n_rows < R || h_out->nnz < nnz || h_out->n_rows < R) {
+        set_error("efem_assemble_host: output capacity smaller than the pattern");
+        return EFEM_EINVAL;
+    }
+    efem_csr d = *d_out;
+    d.n_rows = R;
+    d.nnz = nnz;
+    if ((st = efem_assemble_numeric(plan, EFEM_ALL, &d, stream)) != EFEM_OK) return st;
+    EFEM_CUDA_TRY(cudaMemcpyAsync(h_out->row_ptr, d.row_ptr, (R + 1) * 4, cudaMemcpyDeviceToHost, s));
+    EFEM_CUDA_TRY(cudaMemcpyAsync(h_out->col_idx, d.col_idx, nnz * 4, cudaMemcpyDeviceToHost, s));
+    EFEM_CUDA_TRY(cudaMemcpyAsync(h_out->vals_mass, d.vals_mass, nnz * 8, cudaMemcpyDeviceToHost, s));
+    EFEM_CUDA_TRY(cudaMemcpyAsync(h_out->vals_stiff, d.vals_stiff, nnz * 8, cudaMemcpyDeviceToHost, s));
+    if ((st = read_flags(*p, s)) != EFEM_OK) return st;
+    h_out->n_rows = R;
+    h_out->nnz = nnz;
+    return EFEM_OK;
+}
+
+}  // extern "C"

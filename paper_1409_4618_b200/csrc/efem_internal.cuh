@@ -1,0 +1,123 @@
+// efem_internal.cuh -- shared internals of libefem.so (product path only).
+// Nothing here is shared with oracle/; the two implementations are
+// independent.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/efem.h"
+
+namespace efem {
+
+// ---- flags written by kernels (workspace header) ---------------------------
+enum : int {
+    F_INVALID_NODE = 0,  // element references a node id outside [0, n_nodes)
+    F_CAPACITY = 1,      // a per-thread list overflowed
+    F_ROW_MISMATCH = 2,  // numeric row length != symbolic row length (internal error)
+    F_DEGENERATE = 3,    // det B_K == 0 or non-finite
+    F_NFLAGS = 8
+};
+
+struct WsHeader {
+    int flags[F_NFLAGS];
+    unsigned long long bad_element;  // atomicMin of the first degenerate element
+    long long pad[3];
+};
+
+// ---- element kinds ------------------------------------------------------------
+// Local numbering follows PAPER.md Fig. 1 (lines 54-157), 0-based:
+//   2D edges (start->end): e0 = 1->2, e1 = 2->0, e2 = 0->1  (edge k opposite vertex k)
+//   3D edges: e0 = 0->1, e1 = 0->2, e2 = 0->3, e3 = 1->2, e4 = 2->3, e5 = 3->1
+//   3D faces: f_k = all vertices but vertex 3-k  ({0,1,2},{0,1,3},{0,2,3},{1,2,3})
+template <int DIM, int ELEM>
+struct Kind {
+    static constexpr int D = DIM;
+    static constexpr int NV = DIM + 1;
+    static constexpr bool FACES = (DIM == 3 && ELEM == EFEM_RT0);
+    static constexpr int M = DIM == 2 ? 3 : (ELEM == EFEM_RT0 ? 4 : 6);
+    static constexpr int EK = FACES ? 3 : 2;  // nodes per entity
+    static constexpr int ELEMENT = ELEM;
+};
+
+__host__ __device__ constexpr int edge_start(int dim, int k) {
+    return dim == 2 ? (k == 0 ? 1 : k == 1 ? 2 : 0)
+                    : (k == 0 ? 0 : k == 1 ? 0 : k == 2 ? 0 : k == 3 ? 1 : k == 4 ? 2 : 3);
+}
+__host__ __device__ constexpr int edge_end(int dim, int k) {
+    return dim == 2 ? (k == 0 ? 2 : k == 1 ? 0 : 1)
+                    : (k == 0 ? 1 : k == 1 ? 2 : k == 2 ? 3 : k == 3 ? 2 : k == 4 ? 3 : 1);
+}
+
+// ---- host-side plan -------------------------------------------------------------
+struct Plan {
+    int dim = 0, element = 0, m = 0, nv = 0, ek = 0;
+    int64_t n_nodes = 0, n_elems = 0;
+    const double* coords = nullptr;
+    const int32_t* elems = nullptr;
+    int64_t r_max = 0;  // upper bound of n_dofs (n_elems * m)
+
+    // workspace
+    char* ws = nullptr;
+    size_t ws_bytes = 0, ws_need = 0;
+    WsHeader* hdr = nullptr;
+    int32_t* cnt = nullptr;      // N+1 node incidence counts
+    int32_t* n2e_ptr = nullptr;  // N+1
+    int32_t* n2e = nullptr;      // T*NV entries (e << 2 | local vertex)
+    int32_t* ent_cnt = nullptr;  // N+1 entities owned per node (min vertex)
+    int32_t* ent_ptr = nullptr;  // N+1
+    int32_t* d2n = nullptr;      // r_max * ek
+    int32_t* e2d = nullptr;      // T * m
+    int8_t* sgn = nullptr;       // T * m
+    int32_t* row_cnt = nullptr;  // r_max + 1
+    int32_t* row_ptr = nullptr;  // r_max + 1
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+
+    // host pinned readback
+    int64_t* h_scalars = nullptr;  // [0] n_dofs [1] nnz
+    WsHeader* h_hdr = nullptr;
+
+    // state
+    bool enumerated = false, symbolic = false;
+    int64_t n_dofs = 0, nnz = 0;
+};
+
+// ---- error plumbing --------------------------------------------------------------
+void set_error(const std::string& msg);
+void set_bad_element(int64_t e);
+void count_launch(int n = 1);
+
+#define EFEM_CUDA_TRY(expr)                                                          \
+    do {                                                                             \
+        cudaError_t _e = (expr);                                                     \
+        if (_e != cudaSuccess) {                                                     \
+            ::efem::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+            return EFEM_ECUDA;                                                       \
+        }                                                                            \
+    } while (0)
+
+#define EFEM_LAUNCH_CHECK()                                                          \
+    do {                                                                             \
+        ::efem::count_launch();                                                      \
+        cudaError_t _e = cudaGetLastError();                                         \
+        if (_e != cudaSuccess) {                                                     \
+            ::efem::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+            return EFEM_ECUDA;                                                       \
+        }                                                                            \
+    } while (0)
+
+// kernel-launch entry points (defined in the .cu files)
+efem_status launch_build_mesh(int dim, int n, double alpha, uint64_t seed, double* coords, int32_t* elems,
+                              cudaStream_t s);
+efem_status run_enumerate(Plan& p, cudaStream_t s);
+efem_status run_symbolic(Plan& p, cudaStream_t s);
+efem_status run_numeric(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s);
+efem_status run_signs(Plan& p, cudaStream_t s);
+
+inline unsigned grid_for(int64_t n, int tpb) { return (unsigned)((n + tpb - 1) / tpb); }
+
+}  // namespace efem
