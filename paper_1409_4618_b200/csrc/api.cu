@@ -12,11 +12,9 @@
 namespace efem {
 
 // launchers defined in dofs.cu / assemble.cu
-efem_status launch_incidence(Plan& p, cudaStream_t s);
-efem_status launch_incidence_fill(Plan& p, cudaStream_t s);
-efem_status launch_entities_any(Plan& p, bool fill, cudaStream_t s);
+efem_status launch_enumerate(Plan& p, cudaStream_t s);
 efem_status launch_signs(Plan& p, int8_t* out, cudaStream_t s);
-efem_status launch_rows_any(Plan& p, bool fill, unsigned forms, efem_csr* out, cudaStream_t s);
+efem_status launch_rows_any(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s);
 
 namespace {
 thread_local std::string g_last_error;
@@ -26,7 +24,7 @@ std::atomic<int64_t> g_launches{0};
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-    size_t hdr, cnt, n2e_ptr, n2e, ent_cnt, ent_ptr, d2n, e2d, row_cnt, row_ptr, cub, total;
+    size_t hdr, cnt, bucket_ptr, bucket, e2d, inc_ptr, row_ptr, d2n, lb, totals, cub, total;
 };
 
 Layout layout(const Plan& p, size_t cub_bytes) {
@@ -38,26 +36,20 @@ Layout layout(const Plan& p, size_t cub_bytes) {
         return o;
     };
     const size_t N1 = (size_t)p.n_nodes + 1;
+    const size_t Tm = (size_t)p.n_elems * p.m;
     L.hdr = take(sizeof(WsHeader));
     L.cnt = take(N1 * 4);
-    L.n2e_ptr = take(N1 * 4);
-    L.n2e = take((size_t)p.n_elems * p.nv * 4);
-    L.ent_cnt = take(N1 * 4);
-    L.ent_ptr = take(N1 * 4);
-    L.d2n = take((size_t)p.r_max * p.ek * 4);
-    L.e2d = take((size_t)p.n_elems * p.m * 4);
-    L.row_cnt = take(((size_t)p.r_max + 1) * 4);
+    L.bucket_ptr = take(N1 * 4);
+    L.bucket = take(Tm * 4);
+    L.e2d = take(Tm * 4);
+    L.inc_ptr = take(((size_t)p.r_max + 1) * 4);
     L.row_ptr = take(((size_t)p.r_max + 1) * 4);
+    L.d2n = take((size_t)p.r_max * p.ek * 4);
+    L.lb = take(((size_t)p.n_nodes / 32 + 2) * 8 + 64);
+    L.totals = take(16);
     L.cub = take(cub_bytes);
     L.total = off;
     return L;
-}
-
-efem_status scan(Plan& p, const int32_t* in, int32_t* out, int64_t n, cudaStream_t s) {
-    size_t bytes = p.cub_bytes;
-    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, in, out, (int)n, s));
-    count_launch();
-    return EFEM_OK;
 }
 
 efem_status read_flags(Plan& p, cudaStream_t s) {
@@ -101,48 +93,22 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 efem_status run_enumerate(Plan& p, cudaStream_t s) {
     efem_status st;
     if ((st = reset_header(p, s)) != EFEM_OK) return st;
-    const int64_t N = p.n_nodes;
-    // 1. node -> element incidence (counting sort)
-    EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (N + 1) * 4, s));
-    if ((st = launch_incidence(p, s)) != EFEM_OK) return st;
-    if ((st = scan(p, p.cnt, p.n2e_ptr, N + 1, s)) != EFEM_OK) return st;
-    if ((st = launch_incidence_fill(p, s)) != EFEM_OK) return st;
-    // 2. entities owned by their minimum node: count, scan, fill
-    if ((st = launch_entities_any(p, false, s)) != EFEM_OK) return st;
-    EFEM_CUDA_TRY(cudaMemsetAsync(p.ent_cnt + N, 0, 4, s));
-    if ((st = scan(p, p.ent_cnt, p.ent_ptr, N + 1, s)) != EFEM_OK) return st;
-    if ((st = launch_entities_any(p, true, s)) != EFEM_OK) return st;
-    EFEM_CUDA_TRY(cudaMemcpyAsync(p.h_scalars, p.ent_ptr + N, 4, cudaMemcpyDeviceToHost, s));
+    if ((st = launch_enumerate(p, s)) != EFEM_OK) return st;
+    EFEM_CUDA_TRY(cudaMemcpyAsync(p.h_scalars, p.d_totals, 16, cudaMemcpyDeviceToHost, s));
     if ((st = read_flags(p, s)) != EFEM_OK) return st;  // synchronises
-    p.n_dofs = *reinterpret_cast<int32_t*>(p.h_scalars);
+    p.n_dofs = p.h_scalars[0];
+    p.nnz = p.h_scalars[1];
     p.enumerated = true;
     return EFEM_OK;
 }
 
+// Enumeration already yields the exact row lengths and row_ptr (closed-form
+// counts, dofs.cu); symbolic = enumeration + the int32 overflow guard.
 efem_status run_symbolic(Plan& p, cudaStream_t s) {
     efem_status st;
     if (!p.enumerated) {
         if ((st = run_enumerate(p, s)) != EFEM_OK) return st;
     }
-    const int64_t R = p.n_dofs;
-    // the int32 scan below cannot wrap past 2^32 when every row count is
-    // bounded by its scratch capacity (<= 48): then nnz >= 2^31 shows up as a
-    // negative int32 total.
-    if (R * 48 >= (1ll << 32)) {
-        set_error("too many rows for int32 CSR offsets");
-        return EFEM_EOVERFLOW;
-    }
-    if ((st = launch_rows_any(p, false, 0, nullptr, s)) != EFEM_OK) return st;
-    EFEM_CUDA_TRY(cudaMemsetAsync(p.row_cnt + R, 0, 4, s));
-    if ((st = scan(p, p.row_cnt, p.row_ptr, R + 1, s)) != EFEM_OK) return st;
-    EFEM_CUDA_TRY(cudaMemcpyAsync(p.h_scalars, p.row_ptr + R, 4, cudaMemcpyDeviceToHost, s));
-    if ((st = read_flags(p, s)) != EFEM_OK) return st;
-    const int32_t nnz32 = *reinterpret_cast<int32_t*>(p.h_scalars);
-    if (nnz32 < 0) {
-        set_error("nnz >= 2^31 does not fit int32 CSR");
-        return EFEM_EOVERFLOW;
-    }
-    p.nnz = nnz32;
     p.symbolic = true;
     return EFEM_OK;
 }
@@ -152,7 +118,7 @@ efem_status run_numeric(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) 
     if (forms & EFEM_PATTERN) {
         EFEM_CUDA_TRY(cudaMemcpyAsync(out->row_ptr, p.row_ptr, (p.n_dofs + 1) * 4, cudaMemcpyDeviceToDevice, s));
     }
-    if ((st = launch_rows_any(p, true, forms, out, s)) != EFEM_OK) return st;
+    if ((st = launch_rows_any(p, forms, out, s)) != EFEM_OK) return st;
     return EFEM_OK;
 }
 
@@ -237,14 +203,16 @@ efem_status efem_plan_create(efem_plan* plan, const efem_mesh* mesh, efem_elemen
     p->coords = mesh->coords;
     p->elems = mesh->elems;
     p->r_max = p->n_elems * p->m;
-    if (p->n_elems >= (1ll << 29) || p->n_nodes >= (1ll << 31) - 1 || p->r_max * p->ek >= (1ll << 31)) {
+    const int64_t nnz_c = (p->dim == 3 && element == EFEM_NED0) ? 5 : p->m - 1;
+    if (p->n_elems >= (1ll << 28) || p->n_nodes >= (1ll << 31) - 1 || p->r_max * p->ek >= (1ll << 31) ||
+        p->r_max + nnz_c * p->n_elems * p->m >= (1ll << 31)) {
         delete p;
-        set_error("efem_plan_create: mesh too large for int32 indexing (n_elems < 2^29)");
+        set_error("efem_plan_create: mesh too large for int32 indexing (n_elems < 2^28)");
         return EFEM_EOVERFLOW;
     }
     size_t cub_bytes = 0;
-    int64_t scan_n = std::max<int64_t>(p->n_nodes + 1, p->r_max + 1);
-    cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (const int32_t*)nullptr, (int32_t*)nullptr, (int)scan_n);
+    cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (int)(p->n_nodes + 1));
     p->cub_bytes = cub_bytes;
     p->ws_need = layout(*p, cub_bytes).total;
     if (cudaMallocHost(&p->h_scalars, 64) != cudaSuccess || cudaMallocHost(&p->h_hdr, sizeof(WsHeader)) != cudaSuccess) {
@@ -270,14 +238,14 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     p->ws_bytes = ws_bytes;
     p->hdr = reinterpret_cast<WsHeader*>(b + L.hdr);
     p->cnt = reinterpret_cast<int32_t*>(b + L.cnt);
-    p->n2e_ptr = reinterpret_cast<int32_t*>(b + L.n2e_ptr);
-    p->n2e = reinterpret_cast<int32_t*>(b + L.n2e);
-    p->ent_cnt = reinterpret_cast<int32_t*>(b + L.ent_cnt);
-    p->ent_ptr = reinterpret_cast<int32_t*>(b + L.ent_ptr);
-    p->d2n = reinterpret_cast<int32_t*>(b + L.d2n);
+    p->bucket_ptr = reinterpret_cast<int32_t*>(b + L.bucket_ptr);
+    p->bucket = reinterpret_cast<int32_t*>(b + L.bucket);
     p->e2d = reinterpret_cast<int32_t*>(b + L.e2d);
-    p->row_cnt = reinterpret_cast<int32_t*>(b + L.row_cnt);
+    p->inc_ptr = reinterpret_cast<int32_t*>(b + L.inc_ptr);
     p->row_ptr = reinterpret_cast<int32_t*>(b + L.row_ptr);
+    p->d2n = reinterpret_cast<int32_t*>(b + L.d2n);
+    p->lb_status = reinterpret_cast<unsigned long long*>(b + L.lb);
+    p->d_totals = reinterpret_cast<int64_t*>(b + L.totals);
     p->cub_tmp = b + L.cub;
     p->enumerated = p->symbolic = false;
     return EFEM_OK;
@@ -315,7 +283,10 @@ efem_status efem_enumerate_dofs(efem_plan plan, efem_dofs* out, efem_stream_t st
     cudaStream_t s = (cudaStream_t)stream;
     p->symbolic = false;
     p->enumerated = false;
-    if ((st = run_enumerate(*p, s)) != EFEM_OK) return st;
+    p->want_d2n = true;
+    st = run_enumerate(*p, s);
+    p->want_d2n = false;
+    if (st != EFEM_OK) return st;
     out->n_dofs = p->n_dofs;
     if (out->dofs2nodes && p->n_dofs)
         EFEM_CUDA_TRY(cudaMemcpyAsync(out->dofs2nodes, p->d2n, p->n_dofs * p->ek * 4, cudaMemcpyDeviceToDevice, s));

@@ -44,31 +44,6 @@ __device__ __forceinline__ double sign_d(const int (&g)[KT::NV], int k) {
     }
 }
 
-// Entity of row i inside element g: returns local index k or -1.
-template <class KT>
-__device__ __forceinline__ int local_index(const int (&g)[KT::NV], int lv, int b, int c) {
-    int q = -1, r = -1;
-#pragma unroll
-    for (int v = 0; v < KT::NV; ++v) {
-        if (g[v] == b) q = v;
-        if constexpr (KT::FACES) {
-            if (g[v] == c) r = v;
-        }
-    }
-    if (q < 0) return -1;
-    if constexpr (KT::FACES) {
-        if (r < 0) return -1;
-        const int o = 6 - lv - q - r;  // vertex opposite the face
-        return 3 - o;
-    } else if constexpr (KT::D == 2) {
-        return 3 - lv - q;  // 2D edge k is opposite vertex k
-    } else {
-        const int lo = min(lv, q), hi = max(lv, q);
-        // {0,1}->0 {0,2}->1 {0,3}->2 {1,2}->3 {2,3}->4 {1,3}->5
-        return lo == 0 ? hi - 1 : (hi == 2 ? 3 : (lo == 2 ? 4 : 5));
-    }
-}
-
 // Row k of the local mass and stiffness matrices of one element, including
 // the sign data s_k s_l (PAPER.md:344-363 with reading C2).  Closed forms:
 //  RT (2D, 3D) and NE (2D): the Piola-mapped local functions are
@@ -197,99 +172,89 @@ __device__ __forceinline__ double local_row(const double (&X)[KT::NV][KT::D], co
 }
 
 // ---------------------------------------------------------------------------------
-// Row kernels.  Thread per row; TPB rows per CTA.
+// Numeric kernel.  Thread per row; ROW_TPB rows per CTA.
+//
+// Slot of a contribution without sorting: every column of row i is an entity
+// whose nodes lie in W = the sorted set of vertices of the elements containing
+// entity i (|W| <= 2 + t in 2D, 3 + t for faces, 2 + 2t for 3D edges).
+// Since DOF ids are lexicographic in node ids, and W is sorted by node id,
+// the column order equals the lexicographic order of the entities' position
+// tuples in W.  Each present column sets one bit of a 256-bit mask at its
+// lexicographic pair / triple index; its CSR slot is the popcount of the mask
+// below that bit.
 // ---------------------------------------------------------------------------------
 constexpr int ROW_TPB = 128;
+constexpr int WCAP_EDGE = 23;  // C(23, 2) = 253 <= 256 mask bits
+constexpr int WCAP_FACE = 6;   // 6^3 = 216 <= 256
 
 template <class KT>
 struct RowCaps {
-    // expected max nnz per row for the smem staging budget (falls back to
-    // direct global writes when a tile's segment does not fit)
+    // smem staging budget per row (a tile that does not fit writes directly
+    // to global memory -- slower, same result)
     static constexpr int STAGE_PER_ROW = KT::D == 2 ? 6 : (KT::FACES ? 8 : 18);
     static constexpr int STAGE = ROW_TPB * STAGE_PER_ROW;
-    static constexpr int SCRATCH_PER_ROW = KT::D == 2 ? 16 : (KT::FACES ? 16 : 48);
+    static constexpr int WCAP = KT::FACES ? WCAP_FACE : WCAP_EDGE;
 };
 
-// Collect the elements containing entity (a,b[,c]) from a's incidence list,
-// sorted ascending by element id.  Returns count (or -1 on overflow).
+// lexicographic index of local entity l of an element whose vertex positions
+// in W are pos[0..NV)
 template <class KT>
-__device__ __forceinline__ int row_elements(const int32_t* __restrict__ elems, const int32_t* __restrict__ n2e,
-                                            int beg, int end, int b, int c, int* el, int* ek) {
-    int ne = 0;
-    for (int p = beg; p < end; ++p) {
-        const int ent = __ldg(n2e + p);
-        const int e = ent >> 2, lv = ent & 3;
-        int g[KT::NV];
-        load_g<KT>(elems, e, g);
-        const int k = local_index<KT>(g, lv, b, c);
-        if (k < 0) continue;
-        if (ne >= EFEM_MAX_ROW_ELEMS) return -1;
-        int j = ne;
-        while (j > 0 && el[j - 1] > e) {
-            el[j] = el[j - 1];
-            ek[j] = ek[j - 1];
-            --j;
-        }
-        el[j] = e;
-        ek[j] = k;
-        ++ne;
+__device__ __forceinline__ int entity_index(const int (&pos)[KT::NV], int l, int nw) {
+    if constexpr (KT::FACES) {
+        const int o = 3 - l;
+        int f[3], t = 0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+            if (v != o) f[t++] = pos[v];
+        const int lo = min(f[0], min(f[1], f[2])), hi = max(f[0], max(f[1], f[2]));
+        const int mid = f[0] + f[1] + f[2] - lo - hi;
+        return (lo * WCAP_FACE + mid) * WCAP_FACE + hi;
+    } else {
+        const int u = pos[edge_start(KT::D, l)], v = pos[edge_end(KT::D, l)];
+        const int p = min(u, v), q = max(u, v);
+        return p * nw - ((p * (p + 1)) >> 1) + (q - p - 1);
     }
-    return ne;
 }
 
-template <class KT>
-__global__ void __launch_bounds__(ROW_TPB) k_row_count(const int32_t* __restrict__ elems,
-                                                       const int32_t* __restrict__ n2e_ptr,
-                                                       const int32_t* __restrict__ n2e,
-                                                       const int32_t* __restrict__ d2n,
-                                                       const int32_t* __restrict__ e2d, int64_t n_rows,
-                                                       int32_t* __restrict__ row_cnt, WsHeader* hdr) {
-    constexpr int SC = RowCaps<KT>::SCRATCH_PER_ROW;
-    __shared__ int scratch[ROW_TPB * SC];
-    const int64_t i = blockIdx.x * (int64_t)ROW_TPB + threadIdx.x;
-    if (i >= n_rows) return;
-    const int a = __ldg(d2n + i * KT::EK), b = __ldg(d2n + i * KT::EK + 1);
-    const int c = KT::FACES ? __ldg(d2n + i * KT::EK + 2) : -1;
-    int el[EFEM_MAX_ROW_ELEMS], ek[EFEM_MAX_ROW_ELEMS];
-    const int ne = row_elements<KT>(elems, n2e, __ldg(n2e_ptr + a), __ldg(n2e_ptr + a + 1), b, c, el, ek);
-    if (ne < 0) {
-        atomicOr(&hdr->flags[F_CAPACITY], 1);
-        row_cnt[i] = 0;
-        return;
+struct Mask256 {
+    unsigned long long w[4];
+    int pc[4];
+    __device__ __forceinline__ void clear() { w[0] = w[1] = w[2] = w[3] = 0ull; }
+    __device__ __forceinline__ void set(int idx) {
+        const unsigned long long b = 1ull << (idx & 63);
+        const int q = idx >> 6;
+        w[0] |= q == 0 ? b : 0ull;
+        w[1] |= q == 1 ? b : 0ull;
+        w[2] |= q == 2 ? b : 0ull;
+        w[3] |= q == 3 ? b : 0ull;
     }
-    int* sc = scratch + threadIdx.x;  // strided by ROW_TPB: conflict-free
-    int n = 0;
-    bool ok = true;
-    for (int t = 0; t < ne; ++t) {
-        const int32_t* dofs = e2d + (int64_t)el[t] * KT::M;
-#pragma unroll
-        for (int l = 0; l < KT::M; ++l) {
-            const int col = __ldg(dofs + l);
-            int j = n;
-            while (j > 0 && sc[(j - 1) * ROW_TPB] > col) --j;
-            if (j > 0 && sc[(j - 1) * ROW_TPB] == col) continue;
-            if (n >= SC) { ok = false; continue; }
-            for (int u = n; u > j; --u) sc[u * ROW_TPB] = sc[(u - 1) * ROW_TPB];
-            sc[j * ROW_TPB] = col;
-            ++n;
-        }
+    __device__ __forceinline__ int finish() {
+        pc[0] = 0;
+        pc[1] = __popcll(w[0]);
+        pc[2] = pc[1] + __popcll(w[1]);
+        pc[3] = pc[2] + __popcll(w[2]);
+        return pc[3] + __popcll(w[3]);
     }
-    if (!ok) atomicOr(&hdr->flags[F_CAPACITY], 1);
-    row_cnt[i] = n;
-}
+    __device__ __forceinline__ int rank(int idx) const {
+        const int q = idx >> 6;
+        const unsigned long long word = q == 0 ? w[0] : (q == 1 ? w[1] : (q == 2 ? w[2] : w[3]));
+        const int base = q == 0 ? pc[0] : (q == 1 ? pc[1] : (q == 2 ? pc[2] : pc[3]));
+        return base + __popcll(word & ((1ull << (idx & 63)) - 1ull));
+    }
+};
 
 template <class KT>
 __global__ void __launch_bounds__(ROW_TPB) k_row_fill(const double* __restrict__ coords,
                                                       const int32_t* __restrict__ elems,
-                                                      const int32_t* __restrict__ n2e_ptr,
-                                                      const int32_t* __restrict__ n2e,
-                                                      const int32_t* __restrict__ d2n,
+                                                      const int32_t* __restrict__ inc_ptr,
+                                                      const int32_t* __restrict__ inc,
                                                       const int32_t* __restrict__ e2d,
                                                       const int32_t* __restrict__ row_ptr, int64_t n_rows,
                                                       unsigned forms, int32_t* __restrict__ col_idx,
                                                       double* __restrict__ vals_m, double* __restrict__ vals_k,
                                                       WsHeader* hdr) {
     constexpr int STAGE = RowCaps<KT>::STAGE;
+    constexpr int WCAP = RowCaps<KT>::WCAP;
     constexpr int D = KT::D, NV = KT::NV, M = KT::M;
     __shared__ int s_col[STAGE];
     __shared__ double s_vm[STAGE];
@@ -303,11 +268,8 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill(const double* __restrict__
     const int64_t i = r0 + threadIdx.x;
 
     if (i < n_rows) {
-        const int a = __ldg(d2n + i * KT::EK), b = __ldg(d2n + i * KT::EK + 1);
-        const int c = KT::FACES ? __ldg(d2n + i * KT::EK + 2) : -1;
+        const int ib = __ldg(inc_ptr + i), ie = __ldg(inc_ptr + i + 1);
         const int rbeg = __ldg(row_ptr + i), rlen = __ldg(row_ptr + i + 1) - rbeg;
-        int el[EFEM_MAX_ROW_ELEMS], ek[EFEM_MAX_ROW_ELEMS];
-        const int ne = row_elements<KT>(elems, n2e, __ldg(n2e_ptr + a), __ldg(n2e_ptr + a + 1), b, c, el, ek);
         int* cols;
         double *vm, *vk;
         if (staged) {
@@ -315,53 +277,98 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill(const double* __restrict__
             vm = s_vm + (rbeg - seg0);
             vk = s_vk + (rbeg - seg0);
         } else {
-            cols = col_idx + rbeg;  // slow path: in-place in global memory
-            vm = vals_m;
-            vk = vals_k;
-            vm = vm ? vm + rbeg : nullptr;
-            vk = vk ? vk + rbeg : nullptr;
+            cols = col_idx + rbeg;  // slow path: accumulate in place in global memory
+            vm = vals_m ? vals_m + rbeg : s_vm;
+            vk = vals_k ? vals_k + rbeg : s_vk;
         }
-        int n = 0;
-        bool ok = ne >= 0;
-        for (int t = 0; ok && t < ne; ++t) {
-            const int e = el[t];
+        const int t = ie - ib;
+        bool ok = t <= EFEM_MAX_ROW_ELEMS;
+        const int nt = ok ? t : EFEM_MAX_ROW_ELEMS;
+
+        // pass 1: W = sorted distinct vertices of the row's elements
+        int W[WCAP + 1];
+        int nw = 0;
+        for (int j = 0; j < nt; ++j) {
+            const int e = __ldg(inc + ib + j) >> 3;
             int g[NV];
             load_g<KT>(elems, e, g);
-            double X[NV][D];
 #pragma unroll
-            for (int v = 0; v < NV; ++v)
-#pragma unroll
-                for (int cc = 0; cc < D; ++cc) X[v][cc] = __ldg(coords + (int64_t)g[v] * D + cc);
-            double Mr[M], Kr[M];
-            const double det = local_row<KT>(X, g, ek[t], Mr, Kr);
-            if (!(det != 0.0) || !isfinite(det)) {
-                atomicOr(&hdr->flags[F_DEGENERATE], 1);
-                atomicMin(&hdr->bad_element, (unsigned long long)e);
-            }
-            const int32_t* dofs = e2d + (int64_t)e * M;
-#pragma unroll
-            for (int l = 0; l < M; ++l) {
-                const int col = __ldg(dofs + l);
-                int j = n;
-                while (j > 0 && cols[j - 1] > col) --j;
-                if (j > 0 && cols[j - 1] == col) {
-                    if (vm) vm[j - 1] += Mr[l];
-                    if (vk) vk[j - 1] += Kr[l];
-                    continue;
-                }
-                if (n >= rlen) { ok = false; break; }
-                for (int u = n; u > j; --u) {
-                    cols[u] = cols[u - 1];
-                    if (vm) vm[u] = vm[u - 1];
-                    if (vk) vk[u] = vk[u - 1];
-                }
-                cols[j] = col;
-                if (vm) vm[j] = Mr[l];
-                if (vk) vk[j] = Kr[l];
-                ++n;
+            for (int v = 0; v < NV; ++v) {
+                const int x = g[v];
+                int q = nw;
+                while (q > 0 && W[q - 1] > x) --q;
+                if (q > 0 && W[q - 1] == x) continue;
+                if (nw >= WCAP) { ok = false; continue; }
+                for (int u = nw; u > q; --u) W[u] = W[u - 1];
+                W[q] = x;
+                ++nw;
             }
         }
-        if (!ok || n != rlen) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
+        // pass 2: column mask
+        Mask256 mk;
+        mk.clear();
+        int pk[EFEM_MAX_ROW_ELEMS];
+        for (int j = 0; j < nt; ++j) {
+            const int e = __ldg(inc + ib + j) >> 3;
+            int g[NV];
+            load_g<KT>(elems, e, g);
+            int pos[NV];
+            int packed = 0;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                int lo = 0, hi = nw;  // first index with W >= g[v]
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (W[mid] < g[v]) lo = mid + 1; else hi = mid;
+                }
+                pos[v] = lo;
+                packed |= lo << (5 * v);
+            }
+            pk[j] = packed;
+#pragma unroll
+            for (int l = 0; l < M; ++l) mk.set(entity_index<KT>(pos, l, nw));
+        }
+        const int ncol = mk.finish();
+        ok &= ncol == rlen;
+        if (!ok) {
+            atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
+        } else {
+            for (int q = 0; q < rlen; ++q) {
+                vm[q] = 0.0;
+                vk[q] = 0.0;
+            }
+            // pass 3: values, ascending element id (the incidence list order)
+            for (int j = 0; j < nt; ++j) {
+                const int pe = __ldg(inc + ib + j);
+                const int e = pe >> 3, k = pe & 7;
+                int g[NV];
+                load_g<KT>(elems, e, g);
+                double X[NV][D];
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+#pragma unroll
+                    for (int cc = 0; cc < D; ++cc) X[v][cc] = __ldg(coords + (int64_t)g[v] * D + cc);
+                int dofs[M];
+#pragma unroll
+                for (int l = 0; l < M; ++l) dofs[l] = __ldg(e2d + (int64_t)e * M + l);
+                double Mr[M], Kr[M];
+                const double det = local_row<KT>(X, g, k, Mr, Kr);
+                if (!(det != 0.0) || !isfinite(det)) {
+                    atomicOr(&hdr->flags[F_DEGENERATE], 1);
+                    atomicMin(&hdr->bad_element, (unsigned long long)e);
+                }
+                int pos[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) pos[v] = (pk[j] >> (5 * v)) & 31;
+#pragma unroll
+                for (int l = 0; l < M; ++l) {
+                    const int slot = mk.rank(entity_index<KT>(pos, l, nw));
+                    cols[slot] = dofs[l];
+                    vm[slot] += Mr[l];
+                    vk[slot] += Kr[l];
+                }
+            }
+        }
     }
     if (!staged) return;
     __syncthreads();
@@ -374,29 +381,159 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill(const double* __restrict__
         for (int t = threadIdx.x; t < segn; t += ROW_TPB) vals_k[seg0 + t] = s_vk[t];
 }
 
+
+// ---------------------------------------------------------------------------------
+// 2D edges and 3D faces: an entity lies in t <= 2 elements of a conforming
+// mesh and its row is {own DOF} + the (m-1) other DOFs of each element, all
+// distinct (two elements share at most this entity).  So a row has
+// 1 + (m-1) t <= 5 (2D) or 7 (3D faces) entries: gather them in registers,
+// sum the own entry over the elements (ascending element id), and order the
+// columns with a fixed odd-even transposition network.  No search, no merge.
 // ---------------------------------------------------------------------------------
 template <class KT>
-efem_status launch_rows(Plan& p, bool fill, unsigned forms, efem_csr* out, cudaStream_t s) {
+__global__ void __launch_bounds__(ROW_TPB) k_row_fill_net(const double* __restrict__ coords,
+                                                          const int32_t* __restrict__ elems,
+                                                          const int32_t* __restrict__ inc_ptr,
+                                                          const int32_t* __restrict__ inc,
+                                                          const int32_t* __restrict__ e2d,
+                                                          const int32_t* __restrict__ row_ptr, int64_t n_rows,
+                                                          unsigned forms, int32_t* __restrict__ col_idx,
+                                                          double* __restrict__ vals_m, double* __restrict__ vals_k,
+                                                          WsHeader* hdr) {
+    constexpr int D = KT::D, NV = KT::NV, M = KT::M;
+    constexpr int NS = 1 + 2 * (M - 1);
+    constexpr int STAGE = ROW_TPB * NS;
+    __shared__ int s_col[STAGE];
+    __shared__ double s_vm[STAGE];
+    __shared__ double s_vk[STAGE];
+
+    const int64_t r0 = blockIdx.x * (int64_t)ROW_TPB;
+    const int64_t r1 = (r0 + ROW_TPB < n_rows) ? r0 + ROW_TPB : n_rows;
+    const int seg0 = __ldg(row_ptr + r0);
+    const int segn = __ldg(row_ptr + r1) - seg0;
+    const int64_t i = r0 + threadIdx.x;
+
+    if (i < n_rows) {
+        const int ib = __ldg(inc_ptr + i);
+        const int t = __ldg(inc_ptr + i + 1) - ib;
+        const int rbeg = __ldg(row_ptr + i);
+        const int rlen = __ldg(row_ptr + i + 1) - rbeg;
+        if (t < 1 || t > 2 || rlen != 1 + (M - 1) * t) {
+            atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
+        } else {
+            int cols[NS];
+            double vm[NS], vk[NS];
+            cols[0] = (int)i;
+            vm[0] = 0.0;
+            vk[0] = 0.0;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (j < t) {
+                    const int pe = __ldg(inc + ib + j);
+                    const int e = pe >> 3, k = pe & 7;
+                    int g[NV];
+                    load_g<KT>(elems, e, g);
+                    double X[NV][D];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v)
+#pragma unroll
+                        for (int cc = 0; cc < D; ++cc) X[v][cc] = __ldg(coords + (int64_t)g[v] * D + cc);
+                    int dofs[M];
+#pragma unroll
+                    for (int l = 0; l < M; ++l) dofs[l] = __ldg(e2d + (int64_t)e * M + l);
+                    double Mr[M], Kr[M];
+                    const double det = local_row<KT>(X, g, k, Mr, Kr);
+                    if (!(det != 0.0) || !isfinite(det)) {
+                        atomicOr(&hdr->flags[F_DEGENERATE], 1);
+                        atomicMin(&hdr->bad_element, (unsigned long long)e);
+                    }
+                    double om = Mr[0], ok = Kr[0];
+#pragma unroll
+                    for (int l = 1; l < M; ++l) {
+                        om = (k == l) ? Mr[l] : om;
+                        ok = (k == l) ? Kr[l] : ok;
+                    }
+                    vm[0] += om;
+                    vk[0] += ok;
+#pragma unroll
+                    for (int q = 0; q < M - 1; ++q) {  // the other local DOFs, l = q + (q >= k)
+                        int c = dofs[q];
+                        double a = Mr[q], b = Kr[q];
+#pragma unroll
+                        for (int l = q + 1; l <= q + 1 && l < M; ++l) {
+                            c = (q >= k) ? dofs[l] : c;
+                            a = (q >= k) ? Mr[l] : a;
+                            b = (q >= k) ? Kr[l] : b;
+                        }
+                        cols[1 + j * (M - 1) + q] = c;
+                        vm[1 + j * (M - 1) + q] = a;
+                        vk[1 + j * (M - 1) + q] = b;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < M - 1; ++q) {
+                        cols[1 + j * (M - 1) + q] = INT_MAX;
+                        vm[1 + j * (M - 1) + q] = 0.0;
+                        vk[1 + j * (M - 1) + q] = 0.0;
+                    }
+                }
+            }
+            // odd-even transposition sort (NS rounds) by column
+#pragma unroll
+            for (int r = 0; r < NS; ++r) {
+#pragma unroll
+                for (int q = (r & 1); q + 1 < NS; q += 2) {
+                    const bool sw = cols[q] > cols[q + 1];
+                    const int c0 = sw ? cols[q + 1] : cols[q], c1 = sw ? cols[q] : cols[q + 1];
+                    const double m0 = sw ? vm[q + 1] : vm[q], m1 = sw ? vm[q] : vm[q + 1];
+                    const double k0 = sw ? vk[q + 1] : vk[q], k1 = sw ? vk[q] : vk[q + 1];
+                    cols[q] = c0; cols[q + 1] = c1;
+                    vm[q] = m0; vm[q + 1] = m1;
+                    vk[q] = k0; vk[q + 1] = k1;
+                }
+            }
+            const int o = rbeg - seg0;
+#pragma unroll
+            for (int q = 0; q < NS; ++q)
+                if (q < rlen) {
+                    s_col[o + q] = cols[q];
+                    s_vm[o + q] = vm[q];
+                    s_vk[o + q] = vk[q];
+                }
+        }
+    }
+    __syncthreads();
+    if (forms & EFEM_PATTERN)
+        for (int q = threadIdx.x; q < segn; q += ROW_TPB) col_idx[seg0 + q] = s_col[q];
+    if (forms & EFEM_MASS)
+        for (int q = threadIdx.x; q < segn; q += ROW_TPB) vals_m[seg0 + q] = s_vm[q];
+    if (forms & EFEM_STIFF)
+        for (int q = threadIdx.x; q < segn; q += ROW_TPB) vals_k[seg0 + q] = s_vk[q];
+}
+
+// ---------------------------------------------------------------------------------
+template <class KT>
+efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) {
     if (p.n_dofs == 0) return EFEM_OK;
     const unsigned grid = grid_for(p.n_dofs, ROW_TPB);
-    if (!fill) {
-        k_row_count<KT><<<grid, ROW_TPB, 0, s>>>(p.elems, p.n2e_ptr, p.n2e, p.d2n, p.e2d, p.n_dofs, p.row_cnt,
-                                                 p.hdr);
+    double* vm = (forms & EFEM_MASS) ? out->vals_mass : nullptr;
+    double* vk = (forms & EFEM_STIFF) ? out->vals_stiff : nullptr;
+    if constexpr (KT::D == 2 || KT::FACES) {
+        k_row_fill_net<KT><<<grid, ROW_TPB, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr,
+                                                    p.n_dofs, forms, out->col_idx, vm, vk, p.hdr);
     } else {
-        k_row_fill<KT><<<grid, ROW_TPB, 0, s>>>(p.coords, p.elems, p.n2e_ptr, p.n2e, p.d2n, p.e2d, p.row_ptr,
-                                                p.n_dofs, forms, out->col_idx,
-                                                (forms & EFEM_MASS) ? out->vals_mass : nullptr,
-                                                (forms & EFEM_STIFF) ? out->vals_stiff : nullptr, p.hdr);
+        k_row_fill<KT><<<grid, ROW_TPB, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr, p.n_dofs,
+                                                forms, out->col_idx, vm, vk, p.hdr);
     }
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;
 }
 
-efem_status launch_rows_any(Plan& p, bool fill, unsigned forms, efem_csr* out, cudaStream_t s) {
-    if (p.dim == 2) return p.element == EFEM_RT0 ? launch_rows<Kind<2, EFEM_RT0>>(p, fill, forms, out, s)
-                                                 : launch_rows<Kind<2, EFEM_NED0>>(p, fill, forms, out, s);
-    return p.element == EFEM_RT0 ? launch_rows<Kind<3, EFEM_RT0>>(p, fill, forms, out, s)
-                                 : launch_rows<Kind<3, EFEM_NED0>>(p, fill, forms, out, s);
+efem_status launch_rows_any(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) {
+    if (p.dim == 2) return p.element == EFEM_RT0 ? launch_rows<Kind<2, EFEM_RT0>>(p, forms, out, s)
+                                                 : launch_rows<Kind<2, EFEM_NED0>>(p, forms, out, s);
+    return p.element == EFEM_RT0 ? launch_rows<Kind<3, EFEM_RT0>>(p, forms, out, s)
+                                 : launch_rows<Kind<3, EFEM_NED0>>(p, forms, out, s);
 }
 
 }  // namespace efem

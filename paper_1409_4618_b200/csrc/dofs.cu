@@ -1,46 +1,34 @@
-// dofs.cu -- DOF enumeration and orientation (
-// get_edges / get_faces / signs_edges / signs_faces of Sec. 3).
+// dofs.cu -- DOF enumeration, orientation and CSR row lengths
+// (get_edges / get_faces / signs_edges /
+// signs_faces of Sec. 3; PAPER.md:696 for the sparse pattern).
 //
 // Global DOF = edge (2D, 3D NE0) or face (3D RT0), numbered by the
 // lexicographic rank of its ascending node tuple (reading C10).  Instead of a
-// global radix sort of T*m keys, each entity is owned
-// by its minimum node a:
-//   1. node -> element incidence by a counting sort (atomic histogram + scan
-//      + atomic scatter);
-//   2. per node a: collect the entities of its incident elements whose minimum
-//      node is a, sort/unique them in registers  -> count (pass 1) -> exclusive
-//      scan gives ent_ptr[a], the id of a's first entity -> (pass 2) write
-//      dofs2nodes rows and elems2dofs / signs of the entities a owns.
-// Since ids are ent_ptr[a] + rank among a's entities, this equals the
-// lexicographic rank of (a, b[, c]) over all entities: byte-identical to a
-// sort + unique.
+// global radix sort of T*m keys, every (element,
+// local entity) INSTANCE is bucketed by the entity's minimum node a with one
+// counting sort:
+//   k_bucket<count>  instances per minimum node          (warp-aggregated atomics)
+//   CUB scan         -> bucket_ptr
+//   k_bucket<fill>   scatter (e << 3 | k) into the buckets
+//   k_node_entities  per node: sort its bucket by (other nodes, element id);
+//                    runs of equal keys are its entities, numbered
+//                    ent_ptr[a] + run index, which IS the lexicographic rank.
+//                    The sorted bucket is the entity -> element incidence
+//                    (ascending element id per entity), inc_ptr = run starts.
+//                    Row lengths (exact, no union needed):
+//                      2D edges / 3D faces: 1 + (m-1) t   (two elements share
+//                        at most one entity of that kind),
+//                      3D edges: 1 + 2 L + t   (L distinct link vertices c give
+//                        edges a-c and b-c; each tet adds one link edge),
+//                    t = elements containing the entity.  Node offsets of both
+//                    entities and row entries come from one decoupled
+//                    look-back scan inside the same kernel.
+#include <cub/cub.cuh>
+
 #include "efem_internal.cuh"
+#include "scan.cuh"
 
 namespace efem {
-
-__global__ void k_incidence_count(const int32_t* __restrict__ elems, int64_t n_entries, int64_t n_nodes,
-                                  int32_t* __restrict__ cnt, WsHeader* hdr) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n_entries) return;
-    const int v = elems[i];
-    if ((unsigned)v >= (unsigned long long)n_nodes) {
-        atomicOr(&hdr->flags[F_INVALID_NODE], 1);
-        return;
-    }
-    atomicAdd(&cnt[v], 1);
-}
-
-template <int NV>
-__global__ void k_incidence_fill(const int32_t* __restrict__ elems, int64_t n_entries, int64_t n_nodes,
-                                 const int32_t* __restrict__ n2e_ptr, int32_t* __restrict__ cnt,
-                                 int32_t* __restrict__ n2e) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n_entries) return;
-    const int v = elems[i];
-    if ((unsigned)v >= (unsigned long long)n_nodes) return;
-    const int pos = n2e_ptr[v] + atomicSub(&cnt[v], 1) - 1;
-    n2e[pos] = (int)(((i / NV) << 2) | (i % NV));
-}
 
 template <class KT>
 __device__ __forceinline__ void load_elem(const int32_t* __restrict__ elems, int e, int (&g)[KT::NV]) {
@@ -53,16 +41,37 @@ __device__ __forceinline__ void load_elem(const int32_t* __restrict__ elems, int
     }
 }
 
-// sorted insert with dedupe into a per-thread list; returns false on overflow
-__device__ __forceinline__ bool insert_key(uint64_t* keys, int& nk, uint64_t key) {
-    int j = nk;
-    while (j > 0 && keys[j - 1] > key) --j;
-    if (j > 0 && keys[j - 1] == key) return true;
-    if (nk >= EFEM_MAX_NODE_ENTITIES) return false;
-    for (int t = nk; t > j; --t) keys[t] = keys[t - 1];
-    keys[j] = key;
-    ++nk;
-    return true;
+// minimum node of local entity k: edges (start, end), faces the three
+// vertices other than 3-k
+template <class KT>
+__device__ __forceinline__ int entity_min_node(const int (&g)[KT::NV], int k) {
+    if constexpr (KT::FACES) {
+        const int o = 3 - k;
+        int mn = INT_MAX;
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+            if (v != o) mn = min(mn, g[v]);
+        return mn;
+    } else {
+        return min(g[edge_start(KT::D, k)], g[edge_end(KT::D, k)]);
+    }
+}
+
+// key of local entity k = its other (non-minimum) nodes, ascending
+template <class KT>
+__device__ __forceinline__ uint64_t entity_key(const int (&g)[KT::NV], int k) {
+    if constexpr (KT::FACES) {
+        const int o = 3 - k;
+        int f[3], t = 0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+            if (v != o) f[t++] = g[v];
+        const int lo = min(f[0], min(f[1], f[2])), hi = max(f[0], max(f[1], f[2]));
+        const int mid = f[0] + f[1] + f[2] - lo - hi;
+        return ((uint64_t)(uint32_t)mid << 32) | (uint32_t)hi;
+    } else {
+        return (uint64_t)(uint32_t)max(g[edge_start(KT::D, k)], g[edge_end(KT::D, k)]);
+    }
 }
 
 // Sign data (2D rule PAPER.md:528, 3D readings C3/C5/C6):
@@ -74,7 +83,6 @@ __device__ __forceinline__ bool insert_key(uint64_t* keys, int& nk, uint64_t key
 template <class KT>
 __device__ __forceinline__ int local_sign(const int (&g)[KT::NV], int k) {
     if constexpr (KT::FACES) {
-        // face k = vertices {0,1,2,3} \ {3-k} in ascending local order, then 3-k.
         // base parity of (f0,f1,f2,opp): k=0 (0,1,2,3) even, k=1 (0,1,3,2) odd,
         // k=2 (0,2,3,1) even, k=3 (1,2,3,0) odd.
         const int o = 3 - k;
@@ -83,108 +91,242 @@ __device__ __forceinline__ int local_sign(const int (&g)[KT::NV], int k) {
         for (int v = 0; v < 4; ++v)
             if (v != o) f[t++] = g[v];
         const int inv = (f[0] > f[1]) + (f[0] > f[2]) + (f[1] > f[2]);
-        const int base_odd = k & 1;
-        const int odd = (inv + base_odd) & 1;
-        return odd ? 1 : -1;  // s = -sgn(pi)
+        return ((inv + (k & 1)) & 1) ? 1 : -1;  // s = -sgn(pi)
     } else {
         return g[edge_start(KT::D, k)] < g[edge_end(KT::D, k)] ? 1 : -1;
     }
 }
 
+// ---------------------------------------------------------------------------------
+// counting sort of instances by minimum node (warp-aggregated atomics)
+// ---------------------------------------------------------------------------------
 template <class KT, bool FILL>
-__global__ void __launch_bounds__(128) k_node_entities(const int32_t* __restrict__ elems,
-                                                       const int32_t* __restrict__ n2e_ptr,
-                                                       const int32_t* __restrict__ n2e, int64_t n_nodes,
-                                                       int32_t* __restrict__ ent_cnt,
-                                                       const int32_t* __restrict__ ent_ptr,
-                                                       int32_t* __restrict__ d2n, int32_t* __restrict__ e2d,
-                                                       WsHeader* hdr) {
-    const int64_t a64 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (a64 >= n_nodes) return;
-    const int a = (int)a64;
-    const int beg = n2e_ptr[a], end = n2e_ptr[a + 1];
-    uint64_t keys[EFEM_MAX_NODE_ENTITIES];
-    int nk = 0;
-    bool ok = true;
-    for (int p = beg; p < end; ++p) {
-        const int ent = __ldg(n2e + p);
-        const int e = ent >> 2, lv = ent & 3;
-        int g[KT::NV];
-        load_elem<KT>(elems, e, g);
-        if constexpr (!KT::FACES) {
+__global__ void __launch_bounds__(256) k_bucket(const int32_t* __restrict__ elems, int64_t n_elems, int64_t n_nodes,
+                                                int32_t* __restrict__ cnt, const int32_t* __restrict__ bucket_ptr,
+                                                int32_t* __restrict__ bucket, WsHeader* hdr) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool live = e < n_elems;
+    int g[KT::NV];
+    if (live) {
+        load_elem<KT>(elems, (int)e, g);
+        bool bad = false;
 #pragma unroll
-            for (int u = 0; u < KT::NV; ++u)
-                if (u != lv && g[u] > a) ok &= insert_key(keys, nk, (uint64_t)(uint32_t)g[u]);
-        } else {
+        for (int v = 0; v < KT::NV; ++v) bad |= (unsigned)g[v] >= (unsigned long long)n_nodes;
+        if (bad) {
+            atomicOr(&hdr->flags[F_INVALID_NODE], 1);
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int w = u + 1; w < 4; ++w)
-                    if (u != lv && w != lv && g[u] > a && g[w] > a) {
-                        const uint32_t lo = min(g[u], g[w]), hi = max(g[u], g[w]);
-                        ok &= insert_key(keys, nk, ((uint64_t)lo << 32) | hi);
-                    }
+            for (int v = 0; v < KT::NV; ++v) g[v] = 0;
         }
     }
-    if (!ok) atomicOr(&hdr->flags[F_CAPACITY], 1);
-    if constexpr (!FILL) {
-        ent_cnt[a] = nk;
-    } else {
-        const int base = ent_ptr[a];
-        for (int r = 0; r < nk; ++r) {
-            int32_t* row = d2n + (int64_t)(base + r) * KT::EK;
-            row[0] = a;
-            if constexpr (KT::FACES) {
-                row[1] = (int)(keys[r] >> 32);
-                row[2] = (int)(keys[r] & 0xffffffffu);
-            } else {
-                row[1] = (int)keys[r];
-            }
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned active = __ballot_sync(0xffffffffu, live);
+    if (!live) return;
+#pragma unroll
+    for (int k = 0; k < KT::M; ++k) {
+        const int a = entity_min_node<KT>(g, k);
+        const unsigned peers = __match_any_sync(active, a);
+        const int leader = __ffs(peers) - 1;
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        if constexpr (!FILL) {
+            if ((int)lane == leader) atomicAdd(&cnt[a], __popc(peers));
+        } else {
+            int base = 0;
+            if ((int)lane == leader) base = atomicAdd(&cnt[a], __popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            bucket[__ldg(bucket_ptr + a) + base + rank] = (int)((e << 3) | k);
         }
-        // elems2dofs / signs of the entities whose minimum node is a
-        for (int p = beg; p < end; ++p) {
-            const int ent = __ldg(n2e + p);
-            const int e = ent >> 2, lv = ent & 3;
-            int g[KT::NV];
-            load_elem<KT>(elems, e, g);
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// per node: sort bucket, number entities, incidence, row lengths, look-back
+// ---------------------------------------------------------------------------------
+constexpr int NODE_TPB = 64;
+
+template <class KT>
+struct NodeCaps {
+    static constexpr int CAP = KT::D == 2 ? 32 : 56;  // instances per node held in smem
+};
+
+// sort order of instances: (entity key, instance word e << 3 | k)
+__device__ __forceinline__ bool item_less(uint64_t ka, int va, uint64_t kb, int vb) {
+    return ka < kb || (ka == kb && va < vb);
+}
+
+struct NodeOut {
+    int32_t* e2d;
+    int32_t* inc_ptr;
+    int32_t* row_ptr;
+    int32_t* d2n;  // optional
+    int32_t* bucket;
+    int64_t* totals;  // [0] n_dofs, [1] nnz
+    unsigned long long* status;
+    int* ticket;
+};
+
+// number of distinct link vertices of the edge (a, b) over the run [j, q)
+template <class KT, class ValAt>
+__device__ __forceinline__ int link_vertices(const int32_t* __restrict__ elems, int a, int b, int j, int q,
+                                             ValAt val_at) {
+    int L = 0;
+    for (int u = j; u < q; ++u) {
+        int h[4];
+        load_elem<KT>(elems, val_at(u) >> 3, h);
 #pragma unroll
-            for (int k = 0; k < KT::M; ++k) {
-                uint64_t key;
-                bool mine;
-                if constexpr (KT::FACES) {
-                    const int o = 3 - k;
-                    int f[3], t = 0;
-#pragma unroll
-                    for (int v = 0; v < 4; ++v)
-                        if (v != o) f[t++] = v;
-                    const bool has = (f[0] == lv) | (f[1] == lv) | (f[2] == lv);
-                    int lo = INT_MAX, hi = -1, mn = INT_MAX;
-#pragma unroll
-                    for (int q = 0; q < 3; ++q)
-                        if (f[q] != lv) {
-                            lo = min(lo, g[f[q]]);
-                            hi = max(hi, g[f[q]]);
-                        }
-#pragma unroll
-                    for (int q = 0; q < 3; ++q) mn = min(mn, g[f[q]]);
-                    mine = has && mn == a && lo > a;
-                    key = ((uint64_t)(uint32_t)lo << 32) | (uint32_t)hi;
-                } else {
-                    const int s0 = edge_start(KT::D, k), s1 = edge_end(KT::D, k);
-                    const int other = s0 == lv ? s1 : s0;
-                    mine = (s0 == lv || s1 == lv) && g[other] > a;
-                    key = (uint64_t)(uint32_t)g[other];
-                }
-                if (!mine) continue;
-                int lo = 0, hi = nk - 1, r = -1;
-                while (lo <= hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (keys[mid] == key) { r = mid; break; }
-                    if (keys[mid] < key) lo = mid + 1; else hi = mid - 1;
-                }
-                if (r < 0) { atomicOr(&hdr->flags[F_CAPACITY], 1); continue; }
-                e2d[(int64_t)e * KT::M + k] = base + r;
+        for (int v = 0; v < 4; ++v) {
+            const int c = h[v];
+            if (c == a || c == b) continue;
+            bool seen = false;
+            for (int u2 = j; u2 < u && !seen; ++u2) {
+                int h2[4];
+                load_elem<KT>(elems, val_at(u2) >> 3, h2);
+                seen |= (h2[0] == c) | (h2[1] == c) | (h2[2] == c) | (h2[3] == c);
             }
+            L += !seen;
+        }
+    }
+    return L;
+}
+
+template <class KT>
+__global__ void __launch_bounds__(NODE_TPB) k_node_entities(const int32_t* __restrict__ elems,
+                                                            const int32_t* __restrict__ bucket_ptr, int64_t n_nodes,
+                                                            NodeOut out, WsHeader* hdr) {
+    constexpr int CAP = NodeCaps<KT>::CAP;
+    __shared__ uint64_t s_key[CAP * NODE_TPB];
+    __shared__ int s_val[CAP * NODE_TPB];
+    __shared__ unsigned long long s_scan[NODE_TPB / 32 + 2];
+    __shared__ int s_tile;
+
+    if (threadIdx.x == 0) s_tile = atomicAdd(out.ticket, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t a64 = (int64_t)tile * NODE_TPB + threadIdx.x;
+    const bool live = a64 < n_nodes;
+    const int a = (int)a64;
+    int beg = 0, n = 0;
+    if (live) {
+        beg = __ldg(bucket_ptr + a);
+        n = __ldg(bucket_ptr + a + 1) - beg;
+    }
+    const bool in_smem = n <= CAP;
+    // strided per-thread lists: item j of this thread at [j * NODE_TPB + tid]
+    uint64_t* K = s_key + threadIdx.x;
+    int* V = s_val + threadIdx.x;
+    int32_t* gb = out.bucket + beg;
+    // ---- load + insertion sort by (key, instance) -----------------------------
+    if (in_smem) {
+        for (int j = 0; j < n; ++j) {
+            const int v = __ldg(gb + j);
+            int g[KT::NV];
+            load_elem<KT>(elems, v >> 3, g);
+            const uint64_t key = entity_key<KT>(g, v & 7);
+            int q = j;
+            while (q > 0 && item_less(key, v, K[(q - 1) * NODE_TPB], V[(q - 1) * NODE_TPB])) {
+                K[q * NODE_TPB] = K[(q - 1) * NODE_TPB];
+                V[q * NODE_TPB] = V[(q - 1) * NODE_TPB];
+                --q;
+            }
+            K[q * NODE_TPB] = key;
+            V[q * NODE_TPB] = v;
+        }
+    } else {
+        // rare slow path (very high valence): insertion sort in global memory,
+        // keys recomputed from the elements
+        for (int j = 1; j < n; ++j) {
+            const int v = gb[j];
+            int g[KT::NV];
+            load_elem<KT>(elems, v >> 3, g);
+            const uint64_t key = entity_key<KT>(g, v & 7);
+            int q = j;
+            while (q > 0) {
+                const int w = gb[q - 1];
+                int h[KT::NV];
+                load_elem<KT>(elems, w >> 3, h);
+                if (!item_less(key, v, entity_key<KT>(h, w & 7), w)) break;
+                gb[q] = w;
+                --q;
+            }
+            gb[q] = v;
+        }
+    }
+    auto key_at = [&](int j) -> uint64_t {
+        if (in_smem) return K[j * NODE_TPB];
+        const int w = gb[j];
+        int h[KT::NV];
+        load_elem<KT>(elems, w >> 3, h);
+        return entity_key<KT>(h, w & 7);
+    };
+    auto val_at = [&](int j) -> int { return in_smem ? V[j * NODE_TPB] : gb[j]; };
+
+    // ---- count entities and row entries -----------------------------------------
+    int n_ent = 0, n_nnz = 0;
+    for (int j = 0; j < n;) {
+        const uint64_t key = key_at(j);
+        int q = j + 1;
+        while (q < n && key_at(q) == key) ++q;
+        const int t = q - j;
+        if constexpr (KT::D == 3 && !KT::FACES) {
+            n_nnz += 1 + 2 * link_vertices<KT>(elems, a, (int)key, j, q, val_at) + t;
+        } else {
+            n_nnz += 1 + (KT::M - 1) * t;
+        }
+        ++n_ent;
+        j = q;
+    }
+
+    // ---- offsets: block scan + decoupled look-back over tiles -------------------
+    const unsigned long long mine = ((unsigned long long)n_ent << 31) | (unsigned long long)n_nnz;
+    unsigned long long tile_total;
+    const unsigned long long excl = block_exclusive_scan<NODE_TPB>(mine, &tile_total, s_scan);
+    if (threadIdx.x < 32) {
+        const unsigned long long pre = lookback(out.status, tile, tile_total);
+        if (threadIdx.x == 0) s_scan[NODE_TPB / 32 + 1] = pre;
+    }
+    __syncthreads();
+    const unsigned long long off = s_scan[NODE_TPB / 32 + 1] + excl;
+    const int ent0 = (int)(off >> 31);
+    int nnz_run = (int)(off & 0x7fffffffull);
+
+    // ---- write: DOF ids (elems2dofs), incidence offsets, row_ptr, dofs2nodes ----
+    if (live) {
+        int id = ent0;
+        for (int j = 0; j < n;) {
+            const uint64_t key = key_at(j);
+            int q = j;
+            while (q < n && key_at(q) == key) {
+                const int v = val_at(q);
+                out.e2d[(int64_t)(v >> 3) * KT::M + (v & 7)] = id;
+                if (in_smem) gb[q] = v;  // sorted bucket = entity -> element incidence
+                ++q;
+            }
+            const int t = q - j;
+            out.inc_ptr[id] = beg + j;
+            out.row_ptr[id] = nnz_run;
+            if (out.d2n) {
+                int32_t* row = out.d2n + (int64_t)id * KT::EK;
+                row[0] = a;
+                if constexpr (KT::FACES) {
+                    row[1] = (int)(key >> 32);
+                    row[2] = (int)(key & 0xffffffffu);
+                } else {
+                    row[1] = (int)key;
+                }
+            }
+            if constexpr (KT::D == 3 && !KT::FACES) {
+                nnz_run += 1 + 2 * link_vertices<KT>(elems, a, (int)key, j, q, val_at) + t;
+            } else {
+                nnz_run += 1 + (KT::M - 1) * t;
+            }
+            ++id;
+            j = q;
+        }
+        if (a == n_nodes - 1) {
+            const int R = id;
+            out.inc_ptr[R] = beg + n;
+            out.row_ptr[R] = nnz_run;
+            out.totals[0] = R;
+            out.totals[1] = nnz_run;
         }
     }
 }
@@ -199,6 +341,47 @@ __global__ void k_signs(const int32_t* __restrict__ elems, int64_t n_elems, int8
     for (int k = 0; k < KT::M; ++k) sgn[e * KT::M + k] = (int8_t)local_sign<KT>(g, k);
 }
 
+// ---------------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------------
+template <class KT>
+efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
+    const int64_t N = p.n_nodes, T = p.n_elems;
+    EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (N + 1) * 4, s));
+    if (T > 0) {
+        k_bucket<KT, false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, nullptr, nullptr, p.hdr);
+        EFEM_LAUNCH_CHECK();
+    }
+    size_t bytes = p.cub_bytes;
+    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.bucket_ptr, (int)(N + 1), s));
+    count_launch(2);
+    EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (N + 1) * 4, s));
+    if (T > 0) {
+        k_bucket<KT, true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, p.bucket_ptr, p.bucket, p.hdr);
+        EFEM_LAUNCH_CHECK();
+    }
+    const int64_t tiles = (N + NODE_TPB - 1) / NODE_TPB;
+    EFEM_CUDA_TRY(cudaMemsetAsync(p.lb_status, 0, (tiles + 1) * sizeof(unsigned long long) + 64, s));
+    if (N > 0) {
+        NodeOut o{p.e2d, p.inc_ptr, p.row_ptr, p.want_d2n ? p.d2n : nullptr, p.bucket, p.d_totals, p.lb_status,
+                  reinterpret_cast<int*>(p.lb_status + tiles + 1)};
+        k_node_entities<KT><<<(unsigned)tiles, NODE_TPB, 0, s>>>(p.elems, p.bucket_ptr, N, o, p.hdr);
+        EFEM_LAUNCH_CHECK();
+    } else {
+        EFEM_CUDA_TRY(cudaMemsetAsync(p.d_totals, 0, 16, s));
+        EFEM_CUDA_TRY(cudaMemsetAsync(p.inc_ptr, 0, 4, s));
+        EFEM_CUDA_TRY(cudaMemsetAsync(p.row_ptr, 0, 4, s));
+    }
+    return EFEM_OK;
+}
+
+efem_status launch_enumerate(Plan& p, cudaStream_t s) {
+    if (p.dim == 2) return p.element == EFEM_RT0 ? run_enumerate_kt<Kind<2, EFEM_RT0>>(p, s)
+                                                 : run_enumerate_kt<Kind<2, EFEM_NED0>>(p, s);
+    return p.element == EFEM_RT0 ? run_enumerate_kt<Kind<3, EFEM_RT0>>(p, s)
+                                 : run_enumerate_kt<Kind<3, EFEM_NED0>>(p, s);
+}
+
 efem_status launch_signs(Plan& p, int8_t* out, cudaStream_t s) {
     if (p.n_elems == 0) return EFEM_OK;
     const int tpb = 256;
@@ -209,52 +392,6 @@ efem_status launch_signs(Plan& p, int8_t* out, cudaStream_t s) {
     else k_signs<Kind<3, EFEM_NED0>><<<grid, tpb, 0, s>>>(p.elems, p.n_elems, out);
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;
-}
-
-// explicit launchers -----------------------------------------------------------------
-template <class KT>
-efem_status launch_entities(Plan& p, bool fill, cudaStream_t s) {
-    const int tpb = 128;
-    const unsigned grid = grid_for(p.n_nodes, tpb);
-    if (!fill)
-        k_node_entities<KT, false><<<grid, tpb, 0, s>>>(p.elems, p.n2e_ptr, p.n2e, p.n_nodes, p.ent_cnt, nullptr,
-                                                        nullptr, nullptr, p.hdr);
-    else
-        k_node_entities<KT, true><<<grid, tpb, 0, s>>>(p.elems, p.n2e_ptr, p.n2e, p.n_nodes, nullptr, p.ent_ptr,
-                                                       p.d2n, p.e2d, p.hdr);
-    EFEM_LAUNCH_CHECK();
-    return EFEM_OK;
-}
-
-efem_status launch_incidence(Plan& p, cudaStream_t s) {
-    const int64_t n_entries = p.n_elems * p.nv;
-    const int tpb = 256;
-    if (n_entries == 0) return EFEM_OK;
-    k_incidence_count<<<grid_for(n_entries, tpb), tpb, 0, s>>>(p.elems, n_entries, p.n_nodes, p.cnt, p.hdr);
-    EFEM_LAUNCH_CHECK();
-    return EFEM_OK;
-}
-
-efem_status launch_incidence_fill(Plan& p, cudaStream_t s) {
-    const int64_t n_entries = p.n_elems * p.nv;
-    const int tpb = 256;
-    if (n_entries == 0) return EFEM_OK;
-    if (p.nv == 3)
-        k_incidence_fill<3><<<grid_for(n_entries, tpb), tpb, 0, s>>>(p.elems, n_entries, p.n_nodes, p.n2e_ptr,
-                                                                     p.cnt, p.n2e);
-    else
-        k_incidence_fill<4><<<grid_for(n_entries, tpb), tpb, 0, s>>>(p.elems, n_entries, p.n_nodes, p.n2e_ptr,
-                                                                     p.cnt, p.n2e);
-    EFEM_LAUNCH_CHECK();
-    return EFEM_OK;
-}
-
-efem_status launch_entities_any(Plan& p, bool fill, cudaStream_t s) {
-    if (p.n_nodes == 0) return EFEM_OK;
-    if (p.dim == 2) return p.element == EFEM_RT0 ? launch_entities<Kind<2, EFEM_RT0>>(p, fill, s)
-                                                 : launch_entities<Kind<2, EFEM_NED0>>(p, fill, s);
-    return p.element == EFEM_RT0 ? launch_entities<Kind<3, EFEM_RT0>>(p, fill, s)
-                                 : launch_entities<Kind<3, EFEM_NED0>>(p, fill, s);
 }
 
 }  // namespace efem

@@ -64,16 +64,17 @@ struct Plan {
     char* ws = nullptr;
     size_t ws_bytes = 0, ws_need = 0;
     WsHeader* hdr = nullptr;
-    int32_t* cnt = nullptr;      // N+1 node incidence counts
-    int32_t* n2e_ptr = nullptr;  // N+1
-    int32_t* n2e = nullptr;      // T*NV entries (e << 2 | local vertex)
-    int32_t* ent_cnt = nullptr;  // N+1 entities owned per node (min vertex)
-    int32_t* ent_ptr = nullptr;  // N+1
-    int32_t* d2n = nullptr;      // r_max * ek
-    int32_t* e2d = nullptr;      // T * m
-    int8_t* sgn = nullptr;       // T * m
-    int32_t* row_cnt = nullptr;  // r_max + 1
-    int32_t* row_ptr = nullptr;  // r_max + 1
+    int32_t* cnt = nullptr;         // N+1 instances per minimum node (counting sort)
+    int32_t* bucket_ptr = nullptr;  // N+1
+    int32_t* bucket = nullptr;      // T*m instances (e << 3 | k); after enumeration sorted by
+                                    // (entity, element): the entity -> element incidence
+    int32_t* e2d = nullptr;         // T*m elems2dofs
+    int32_t* inc_ptr = nullptr;     // r_max+1 entity -> first incidence in bucket
+    int32_t* row_ptr = nullptr;     // r_max+1 CSR row offsets
+    int32_t* d2n = nullptr;         // r_max*ek (written only when want_d2n)
+    unsigned long long* lb_status = nullptr;  // look-back tile status + ticket
+    int64_t* d_totals = nullptr;    // [0] n_dofs [1] nnz
+    bool want_d2n = false;
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
 

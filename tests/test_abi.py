@@ -57,6 +57,6 @@ def test_plan_create_rejects_bad_mesh_before_cuda():
     assert L.efem_plan_create(ctypes.byref(plan), ctypes.byref(m), 7, ctypes.byref(ws)) == -1
     misaligned = _lib.efem_mesh(3, 10, 10, 16, 20)
     assert L.efem_plan_create(ctypes.byref(plan), ctypes.byref(misaligned), 1, ctypes.byref(ws)) == -1
-    huge = _lib.efem_mesh(3, 10, 1 << 29, 16, 16)
+    huge = _lib.efem_mesh(3, 10, 1 << 28, 16, 16)
     assert L.efem_plan_create(ctypes.byref(plan), ctypes.byref(huge), 1, ctypes.byref(ws)) == -5
     assert L.efem_plan_create(None, ctypes.byref(m), 0, ctypes.byref(ws)) == -1
