@@ -243,22 +243,128 @@ struct Mask256 {
     }
 };
 
+// Generic row: any t <= EFEM_MAX_ROW_ELEMS, |W| <= WCAP.  Accumulates into
+// cols / vm / vk (shared staging or global), returns false on a capacity or
+// row-length mismatch.
 template <class KT>
-__global__ void __launch_bounds__(ROW_TPB) k_row_fill(const double* __restrict__ coords,
-                                                      const int32_t* __restrict__ elems,
-                                                      const int32_t* __restrict__ inc_ptr,
-                                                      const int32_t* __restrict__ inc,
-                                                      const int32_t* __restrict__ e2d,
-                                                      const int32_t* __restrict__ row_ptr, int64_t n_rows,
-                                                      unsigned forms, int32_t* __restrict__ col_idx,
-                                                      double* __restrict__ vals_m, double* __restrict__ vals_k,
-                                                      WsHeader* hdr) {
-    constexpr int STAGE = RowCaps<KT>::STAGE;
+__device__ __noinline__ bool row_generic(const double* __restrict__ coords, const int32_t* __restrict__ elems,
+                                         const int32_t* __restrict__ inc, const int32_t* __restrict__ e2d, int ib,
+                                         int t, int rlen, int* cols, double* vm, double* vk, WsHeader* hdr) {
     constexpr int WCAP = RowCaps<KT>::WCAP;
     constexpr int D = KT::D, NV = KT::NV, M = KT::M;
+    bool ok = t <= EFEM_MAX_ROW_ELEMS;
+    const int nt = ok ? t : EFEM_MAX_ROW_ELEMS;
+    // pass 1: W = sorted distinct vertices of the row's elements
+    int W[WCAP + 1];
+    int nw = 0;
+    for (int j = 0; j < nt; ++j) {
+        const int e = __ldg(inc + ib + j) >> 3;
+        int g[NV];
+        load_g<KT>(elems, e, g);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const int x = g[v];
+            int q = nw;
+            while (q > 0 && W[q - 1] > x) --q;
+            if (q > 0 && W[q - 1] == x) continue;
+            if (nw >= WCAP) { ok = false; continue; }
+            for (int u = nw; u > q; --u) W[u] = W[u - 1];
+            W[q] = x;
+            ++nw;
+        }
+    }
+    // pass 2: column mask
+    Mask256 mk;
+    mk.clear();
+    int pk[EFEM_MAX_ROW_ELEMS];
+    for (int j = 0; j < nt; ++j) {
+        const int e = __ldg(inc + ib + j) >> 3;
+        int g[NV];
+        load_g<KT>(elems, e, g);
+        int pos[NV];
+        int packed = 0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            int lo = 0, hi = nw;  // first index with W >= g[v]
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (W[mid] < g[v]) lo = mid + 1; else hi = mid;
+            }
+            pos[v] = lo;
+            packed |= lo << (5 * v);
+        }
+        pk[j] = packed;
+#pragma unroll
+        for (int l = 0; l < M; ++l) mk.set(entity_index<KT>(pos, l, nw));
+    }
+    const int ncol = mk.finish();
+    ok &= ncol == rlen;
+    if (!ok) return false;
+    for (int q = 0; q < rlen; ++q) {
+        vm[q] = 0.0;
+        vk[q] = 0.0;
+    }
+    // pass 3: values, ascending element id (the incidence list order)
+    for (int j = 0; j < nt; ++j) {
+        const int pe = __ldg(inc + ib + j);
+        const int e = pe >> 3, k = pe & 7;
+        int g[NV];
+        load_g<KT>(elems, e, g);
+        double X[NV][D];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int cc = 0; cc < D; ++cc) X[v][cc] = __ldg(coords + (int64_t)g[v] * D + cc);
+        int dofs[M];
+#pragma unroll
+        for (int l = 0; l < M; ++l) dofs[l] = __ldg(e2d + (int64_t)e * M + l);
+        double Mr[M], Kr[M];
+        const double det = local_row<KT>(X, g, k, Mr, Kr);
+        if (!(det != 0.0) || !isfinite(det)) {
+            atomicOr(&hdr->flags[F_DEGENERATE], 1);
+            atomicMin(&hdr->bad_element, (unsigned long long)e);
+        }
+        int pos[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) pos[v] = (pk[j] >> (5 * v)) & 31;
+#pragma unroll
+        for (int l = 0; l < M; ++l) {
+            const int slot = mk.rank(entity_index<KT>(pos, l, nw));
+            cols[slot] = dofs[l];
+            vm[slot] += Mr[l];
+            vk[slot] += Kr[l];
+        }
+    }
+    return true;
+}
+
+__device__ __forceinline__ int sel4(const int (&g)[4], int i) {
+    return i == 0 ? g[0] : (i == 1 ? g[1] : (i == 2 ? g[2] : g[3]));
+}
+
+// 3D edges (NE0).  Row (a, b) with t tets around the edge: the columns are
+// the edges among W = {a, b} U link vertices.  Fast path (t <= 7, node ids
+// < 2^27): W comes from one 16-key bitonic network in registers
+// (key = node << 5 | source), positions go through a per-thread shared
+// scratch, the column mask / ranks are as in row_generic.  Other rows use
+// row_generic.
+template <class KT>
+__global__ void __launch_bounds__(ROW_TPB) k_row_fill_ne3(const double* __restrict__ coords,
+                                                          const int32_t* __restrict__ elems,
+                                                          const int32_t* __restrict__ inc_ptr,
+                                                          const int32_t* __restrict__ inc,
+                                                          const int32_t* __restrict__ e2d,
+                                                          const int32_t* __restrict__ row_ptr, int64_t n_rows,
+                                                          unsigned forms, int fast_ids, int32_t* __restrict__ col_idx,
+                                                          double* __restrict__ vals_m, double* __restrict__ vals_k,
+                                                          WsHeader* hdr) {
+    static_assert(KT::D == 3 && !KT::FACES, "NE0 3D only");
+    constexpr int STAGE = RowCaps<KT>::STAGE;
+    constexpr int TMAX = 7;
     __shared__ int s_col[STAGE];
     __shared__ double s_vm[STAGE];
     __shared__ double s_vk[STAGE];
+    __shared__ unsigned char s_pos[16 * ROW_TPB];
 
     const int64_t r0 = blockIdx.x * (int64_t)ROW_TPB;
     const int64_t r1 = (r0 + ROW_TPB < n_rows) ? r0 + ROW_TPB : n_rows;
@@ -268,7 +374,8 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill(const double* __restrict__
     const int64_t i = r0 + threadIdx.x;
 
     if (i < n_rows) {
-        const int ib = __ldg(inc_ptr + i), ie = __ldg(inc_ptr + i + 1);
+        const int ib = __ldg(inc_ptr + i);
+        const int t = __ldg(inc_ptr + i + 1) - ib;
         const int rbeg = __ldg(row_ptr + i), rlen = __ldg(row_ptr + i + 1) - rbeg;
         int* cols;
         double *vm, *vk;
@@ -277,110 +384,142 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill(const double* __restrict__
             vm = s_vm + (rbeg - seg0);
             vk = s_vk + (rbeg - seg0);
         } else {
-            cols = col_idx + rbeg;  // slow path: accumulate in place in global memory
+            cols = col_idx + rbeg;
             vm = vals_m ? vals_m + rbeg : s_vm;
             vk = vals_k ? vals_k + rbeg : s_vk;
         }
-        const int t = ie - ib;
-        bool ok = t <= EFEM_MAX_ROW_ELEMS;
-        const int nt = ok ? t : EFEM_MAX_ROW_ELEMS;
-
-        // pass 1: W = sorted distinct vertices of the row's elements
-        int W[WCAP + 1];
-        int nw = 0;
-        for (int j = 0; j < nt; ++j) {
-            const int e = __ldg(inc + ib + j) >> 3;
-            int g[NV];
-            load_g<KT>(elems, e, g);
+        bool ok;
+        if (fast_ids && t >= 1 && t <= TMAX) {
+            unsigned char* P = s_pos + threadIdx.x;  // P[src * ROW_TPB]
+            uint32_t key[16];
+            int inst[TMAX], roles[TMAX];
+            int a = 0, b = 0;
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const int x = g[v];
-                int q = nw;
-                while (q > 0 && W[q - 1] > x) --q;
-                if (q > 0 && W[q - 1] == x) continue;
-                if (nw >= WCAP) { ok = false; continue; }
-                for (int u = nw; u > q; --u) W[u] = W[u - 1];
-                W[q] = x;
-                ++nw;
-            }
-        }
-        // pass 2: column mask
-        Mask256 mk;
-        mk.clear();
-        int pk[EFEM_MAX_ROW_ELEMS];
-        for (int j = 0; j < nt; ++j) {
-            const int e = __ldg(inc + ib + j) >> 3;
-            int g[NV];
-            load_g<KT>(elems, e, g);
-            int pos[NV];
-            int packed = 0;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                int lo = 0, hi = nw;  // first index with W >= g[v]
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (W[mid] < g[v]) lo = mid + 1; else hi = mid;
+            for (int j = 0; j < TMAX; ++j) {
+                if (j < t) {
+                    const int pe = __ldg(inc + ib + j);
+                    inst[j] = pe;
+                    const int k = pe & 7;
+                    int g[4];
+                    load_g<KT>(elems, pe >> 3, g);
+                    const int s0 = k < 3 ? 0 : (k == 3 ? 1 : (k == 4 ? 2 : 3));
+                    const int s1 = k < 3 ? k + 1 : (k == 3 ? 2 : (k == 4 ? 3 : 1));
+                    // complement of {s0, s1}: (2,3) (1,3) (1,2) (0,3) (0,1) (0,2)
+                    const int lc = k == 0 ? 2 : (k == 1 ? 1 : (k == 2 ? 1 : 0));
+                    const int ld = k == 0 ? 3 : (k == 1 ? 3 : (k == 2 ? 2 : (k == 3 ? 3 : (k == 4 ? 1 : 2))));
+                    const int g0 = sel4(g, s0), g1 = sel4(g, s1);
+                    const int la = g0 < g1 ? s0 : s1, lb = g0 < g1 ? s1 : s0;
+                    a = min(g0, g1);
+                    b = max(g0, g1);
+                    roles[j] = la | (lb << 2) | (lc << 4) | (ld << 6);
+                    key[2 * j] = ((uint32_t)sel4(g, lc) << 5) | (2 * j);
+                    key[2 * j + 1] = ((uint32_t)sel4(g, ld) << 5) | (2 * j + 1);
+                } else {
+                    key[2 * j] = 0xffffffffu;
+                    key[2 * j + 1] = 0xffffffffu;
                 }
-                pos[v] = lo;
-                packed |= lo << (5 * v);
             }
-            pk[j] = packed;
+            key[14] = ((uint32_t)a << 5) | 14u;
+            key[15] = ((uint32_t)b << 5) | 15u;
+            // bitonic sort of 16 keys
 #pragma unroll
-            for (int l = 0; l < M; ++l) mk.set(entity_index<KT>(pos, l, nw));
-        }
-        const int ncol = mk.finish();
-        ok &= ncol == rlen;
-        if (!ok) {
-            atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
+            for (int kk = 2; kk <= 16; kk <<= 1)
+#pragma unroll
+                for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) {
+                        const int y = x ^ jj;
+                        if (y > x) {
+                            const uint32_t lo = min(key[x], key[y]), hi = max(key[x], key[y]);
+                            const bool asc = (x & kk) == 0;
+                            key[x] = asc ? lo : hi;
+                            key[y] = asc ? hi : lo;
+                        }
+                    }
+            // distinct ranks -> positions per source
+            int r = -1;
+            uint32_t prev = 0xffffffffu;
+#pragma unroll
+            for (int x = 0; x < 16; ++x) {
+                if (key[x] != 0xffffffffu) {
+                    const uint32_t v = key[x] >> 5;
+                    r += v != prev;
+                    prev = v;
+                    P[(key[x] & 31u) * ROW_TPB] = (unsigned char)r;
+                }
+            }
+            const int nw = r + 1;
+            const int pa = P[14 * ROW_TPB], pb = P[15 * ROW_TPB];
+            Mask256 mk;
+            mk.clear();
+            int pk[TMAX];
+#pragma unroll
+            for (int j = 0; j < TMAX; ++j) {
+                if (j < t) {
+                    const int pc = P[(2 * j) * ROW_TPB], pd = P[(2 * j + 1) * ROW_TPB];
+                    const int rl = roles[j];
+                    int pos[4];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+                        pos[v] = v == (rl & 3) ? pa : (v == ((rl >> 2) & 3) ? pb : (v == ((rl >> 4) & 3) ? pc : pd));
+                    pk[j] = pos[0] | (pos[1] << 5) | (pos[2] << 10) | (pos[3] << 15);
+#pragma unroll
+                    for (int l = 0; l < 6; ++l) mk.set(entity_index<KT>(pos, l, nw));
+                }
+            }
+            ok = mk.finish() == rlen;
+            if (ok) {
+                for (int q = 0; q < rlen; ++q) {
+                    vm[q] = 0.0;
+                    vk[q] = 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < TMAX; ++j) {
+                    if (j < t) {
+                        const int e = inst[j] >> 3, k = inst[j] & 7;
+                        int g[4];
+                        load_g<KT>(elems, e, g);
+                        double X[4][3];
+#pragma unroll
+                        for (int v = 0; v < 4; ++v)
+#pragma unroll
+                            for (int cc = 0; cc < 3; ++cc) X[v][cc] = __ldg(coords + (int64_t)g[v] * 3 + cc);
+                        const int2* dp = reinterpret_cast<const int2*>(e2d + (int64_t)e * 6);
+                        const int2 d01 = __ldg(dp), d23 = __ldg(dp + 1), d45 = __ldg(dp + 2);
+                        const int dofs[6] = {d01.x, d01.y, d23.x, d23.y, d45.x, d45.y};
+                        double Mr[6], Kr[6];
+                        const double det = local_row<KT>(X, g, k, Mr, Kr);
+                        if (!(det != 0.0) || !isfinite(det)) {
+                            atomicOr(&hdr->flags[F_DEGENERATE], 1);
+                            atomicMin(&hdr->bad_element, (unsigned long long)e);
+                        }
+                        int pos[4];
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) pos[v] = (pk[j] >> (5 * v)) & 31;
+#pragma unroll
+                        for (int l = 0; l < 6; ++l) {
+                            const int slot = mk.rank(entity_index<KT>(pos, l, nw));
+                            cols[slot] = dofs[l];
+                            vm[slot] += Mr[l];
+                            vk[slot] += Kr[l];
+                        }
+                    }
+                }
+            }
         } else {
-            for (int q = 0; q < rlen; ++q) {
-                vm[q] = 0.0;
-                vk[q] = 0.0;
-            }
-            // pass 3: values, ascending element id (the incidence list order)
-            for (int j = 0; j < nt; ++j) {
-                const int pe = __ldg(inc + ib + j);
-                const int e = pe >> 3, k = pe & 7;
-                int g[NV];
-                load_g<KT>(elems, e, g);
-                double X[NV][D];
-#pragma unroll
-                for (int v = 0; v < NV; ++v)
-#pragma unroll
-                    for (int cc = 0; cc < D; ++cc) X[v][cc] = __ldg(coords + (int64_t)g[v] * D + cc);
-                int dofs[M];
-#pragma unroll
-                for (int l = 0; l < M; ++l) dofs[l] = __ldg(e2d + (int64_t)e * M + l);
-                double Mr[M], Kr[M];
-                const double det = local_row<KT>(X, g, k, Mr, Kr);
-                if (!(det != 0.0) || !isfinite(det)) {
-                    atomicOr(&hdr->flags[F_DEGENERATE], 1);
-                    atomicMin(&hdr->bad_element, (unsigned long long)e);
-                }
-                int pos[NV];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) pos[v] = (pk[j] >> (5 * v)) & 31;
-#pragma unroll
-                for (int l = 0; l < M; ++l) {
-                    const int slot = mk.rank(entity_index<KT>(pos, l, nw));
-                    cols[slot] = dofs[l];
-                    vm[slot] += Mr[l];
-                    vk[slot] += Kr[l];
-                }
-            }
+            ok = row_generic<KT>(coords, elems, inc, e2d, ib, t, rlen, cols, vm, vk, hdr);
         }
+        if (!ok) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
     }
     if (!staged) return;
     __syncthreads();
-    // coalesced flush of this tile's CSR segment
     if (forms & EFEM_PATTERN)
-        for (int t = threadIdx.x; t < segn; t += ROW_TPB) col_idx[seg0 + t] = s_col[t];
+        for (int q = threadIdx.x; q < segn; q += ROW_TPB) col_idx[seg0 + q] = s_col[q];
     if (forms & EFEM_MASS)
-        for (int t = threadIdx.x; t < segn; t += ROW_TPB) vals_m[seg0 + t] = s_vm[t];
+        for (int q = threadIdx.x; q < segn; q += ROW_TPB) vals_m[seg0 + q] = s_vm[q];
     if (forms & EFEM_STIFF)
-        for (int t = threadIdx.x; t < segn; t += ROW_TPB) vals_k[seg0 + t] = s_vk[t];
+        for (int q = threadIdx.x; q < segn; q += ROW_TPB) vals_k[seg0 + q] = s_vk[q];
 }
-
 
 // ---------------------------------------------------------------------------------
 // 2D edges and 3D faces: an entity lies in t <= 2 elements of a conforming
@@ -522,8 +661,9 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) 
         k_row_fill_net<KT><<<grid, ROW_TPB, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr,
                                                     p.n_dofs, forms, out->col_idx, vm, vk, p.hdr);
     } else {
-        k_row_fill<KT><<<grid, ROW_TPB, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr, p.n_dofs,
-                                                forms, out->col_idx, vm, vk, p.hdr);
+        const int fast_ids = p.n_nodes < (1ll << 27);
+        k_row_fill_ne3<KT><<<grid, ROW_TPB, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr,
+                                                    p.n_dofs, forms, fast_ids, out->col_idx, vm, vk, p.hdr);
     }
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;

@@ -118,22 +118,15 @@ __global__ void __launch_bounds__(256) k_bucket(const int32_t* __restrict__ elem
             for (int v = 0; v < KT::NV; ++v) g[v] = 0;
         }
     }
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned active = __ballot_sync(0xffffffffu, live);
     if (!live) return;
 #pragma unroll
     for (int k = 0; k < KT::M; ++k) {
         const int a = entity_min_node<KT>(g, k);
-        const unsigned peers = __match_any_sync(active, a);
-        const int leader = __ffs(peers) - 1;
-        const int rank = __popc(peers & ((1u << lane) - 1u));
         if constexpr (!FILL) {
-            if ((int)lane == leader) atomicAdd(&cnt[a], __popc(peers));
+            atomicAdd(&cnt[a], 1);
         } else {
-            int base = 0;
-            if ((int)lane == leader) base = atomicAdd(&cnt[a], __popc(peers));
-            base = __shfl_sync(peers, base, leader);
-            bucket[__ldg(bucket_ptr + a) + base + rank] = (int)((e << 3) | k);
+            const int pos = atomicAdd(&cnt[a], 1);
+            bucket[__ldg(bucket_ptr + a) + pos] = (int)((e << 3) | k);
         }
     }
 }
@@ -141,17 +134,14 @@ __global__ void __launch_bounds__(256) k_bucket(const int32_t* __restrict__ elem
 // ---------------------------------------------------------------------------------
 // per node: sort bucket, number entities, incidence, row lengths, look-back
 // ---------------------------------------------------------------------------------
-constexpr int NODE_TPB = 64;
-
 template <class KT>
 struct NodeCaps {
-    static constexpr int CAP = KT::D == 2 ? 32 : 56;  // instances per node held in smem
+    // instances per node held in shared memory (one 64-bit sort key each;
+    // faces add a 32-bit instance word); larger buckets take a global-memory
+    // slow path
+    static constexpr int CAP = KT::D == 2 ? 24 : (KT::FACES ? 32 : 48);
+    static constexpr int TPB = KT::D == 2 ? 128 : 64;
 };
-
-// sort order of instances: (entity key, instance word e << 3 | k)
-__device__ __forceinline__ bool item_less(uint64_t ka, int va, uint64_t kb, int vb) {
-    return ka < kb || (ka == kb && va < vb);
-}
 
 struct NodeOut {
     int32_t* e2d;
@@ -164,44 +154,79 @@ struct NodeOut {
     int* ticket;
 };
 
-// number of distinct link vertices of the edge (a, b) over the run [j, q)
-template <class KT, class ValAt>
-__device__ __forceinline__ int link_vertices(const int32_t* __restrict__ elems, int a, int b, int j, int q,
-                                             ValAt val_at) {
-    int L = 0;
+// Sort item of an instance.  Edges: one u64 (other node << 32 | e << 3 | k),
+// so sorting the word sorts by (entity, element).  Faces: u64 (mid << 32 | hi)
+// plus the instance word as tie-break.
+template <class KT>
+struct Item {
+    uint64_t key;
+    int inst;
+    __device__ __forceinline__ bool operator<(const Item& o) const {
+        if constexpr (KT::FACES) return key < o.key || (key == o.key && inst < o.inst);
+        else return key < o.key;
+    }
+    __device__ __forceinline__ uint64_t entity() const {  // entity key only
+        if constexpr (KT::FACES) return key;
+        else return key >> 32;
+    }
+};
+
+template <class KT>
+__device__ __forceinline__ Item<KT> make_item(const int32_t* __restrict__ elems, int inst) {
+    int g[KT::NV];
+    load_elem<KT>(elems, inst >> 3, g);
+    Item<KT> it;
+    if constexpr (KT::FACES) {
+        it.key = entity_key<KT>(g, inst & 7);
+        it.inst = inst;
+    } else {
+        it.key = (entity_key<KT>(g, inst & 7) << 32) | (uint32_t)inst;
+        it.inst = inst;
+    }
+    return it;
+}
+
+// number of distinct link vertices (nodes other than a, b) over the tets of
+// one edge run; every tet contributes exactly two
+template <class KT, class InstAt>
+__device__ __forceinline__ int link_count(const int32_t* __restrict__ elems, int a, int b, int j, int q,
+                                          InstAt inst_at) {
+    constexpr int CAPL = 2 * EFEM_MAX_ROW_ELEMS;
+    int lk[CAPL];
+    int nl = 0, L = 0;
     for (int u = j; u < q; ++u) {
         int h[4];
-        load_elem<KT>(elems, val_at(u) >> 3, h);
+        load_elem<KT>(elems, inst_at(u) >> 3, h);
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int c = h[v];
             if (c == a || c == b) continue;
             bool seen = false;
-            for (int u2 = j; u2 < u && !seen; ++u2) {
-                int h2[4];
-                load_elem<KT>(elems, val_at(u2) >> 3, h2);
-                seen |= (h2[0] == c) | (h2[1] == c) | (h2[2] == c) | (h2[3] == c);
+            for (int w = 0; w < nl; ++w) seen |= lk[w] == c;
+            if (!seen) {
+                ++L;
+                if (nl < CAPL) lk[nl++] = c;
             }
-            L += !seen;
         }
     }
     return L;
 }
 
 template <class KT>
-__global__ void __launch_bounds__(NODE_TPB) k_node_entities(const int32_t* __restrict__ elems,
-                                                            const int32_t* __restrict__ bucket_ptr, int64_t n_nodes,
-                                                            NodeOut out, WsHeader* hdr) {
+__global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_entities(const int32_t* __restrict__ elems,
+                                                                     const int32_t* __restrict__ bucket_ptr,
+                                                                     int64_t n_nodes, NodeOut out, WsHeader* hdr) {
     constexpr int CAP = NodeCaps<KT>::CAP;
-    __shared__ uint64_t s_key[CAP * NODE_TPB];
-    __shared__ int s_val[CAP * NODE_TPB];
-    __shared__ unsigned long long s_scan[NODE_TPB / 32 + 2];
+    constexpr int TPB = NodeCaps<KT>::TPB;
+    __shared__ uint64_t s_key[CAP * TPB];
+    __shared__ int s_inst[KT::FACES ? CAP * TPB : 1];
+    __shared__ unsigned long long s_scan[TPB / 32 + 2];
     __shared__ int s_tile;
 
     if (threadIdx.x == 0) s_tile = atomicAdd(out.ticket, 1);
     __syncthreads();
     const int tile = s_tile;
-    const int64_t a64 = (int64_t)tile * NODE_TPB + threadIdx.x;
+    const int64_t a64 = (int64_t)tile * TPB + threadIdx.x;
     const bool live = a64 < n_nodes;
     const int a = (int)a64;
     int beg = 0, n = 0;
@@ -210,64 +235,51 @@ __global__ void __launch_bounds__(NODE_TPB) k_node_entities(const int32_t* __res
         n = __ldg(bucket_ptr + a + 1) - beg;
     }
     const bool in_smem = n <= CAP;
-    // strided per-thread lists: item j of this thread at [j * NODE_TPB + tid]
+    // strided per-thread lists: item j of this thread at [j * TPB + tid]
     uint64_t* K = s_key + threadIdx.x;
-    int* V = s_val + threadIdx.x;
+    int* V = s_inst + (KT::FACES ? threadIdx.x : 0);
     int32_t* gb = out.bucket + beg;
-    // ---- load + insertion sort by (key, instance) -----------------------------
-    if (in_smem) {
-        for (int j = 0; j < n; ++j) {
-            const int v = __ldg(gb + j);
-            int g[KT::NV];
-            load_elem<KT>(elems, v >> 3, g);
-            const uint64_t key = entity_key<KT>(g, v & 7);
-            int q = j;
-            while (q > 0 && item_less(key, v, K[(q - 1) * NODE_TPB], V[(q - 1) * NODE_TPB])) {
-                K[q * NODE_TPB] = K[(q - 1) * NODE_TPB];
-                V[q * NODE_TPB] = V[(q - 1) * NODE_TPB];
-                --q;
-            }
-            K[q * NODE_TPB] = key;
-            V[q * NODE_TPB] = v;
+    auto get = [&](int j) -> Item<KT> {
+        if (in_smem) {
+            Item<KT> it;
+            it.key = K[j * TPB];
+            if constexpr (KT::FACES) it.inst = V[j * TPB];
+            else it.inst = (int)(uint32_t)it.key;
+            return it;
         }
-    } else {
-        // rare slow path (very high valence): insertion sort in global memory,
-        // keys recomputed from the elements
-        for (int j = 1; j < n; ++j) {
-            const int v = gb[j];
-            int g[KT::NV];
-            load_elem<KT>(elems, v >> 3, g);
-            const uint64_t key = entity_key<KT>(g, v & 7);
-            int q = j;
-            while (q > 0) {
-                const int w = gb[q - 1];
-                int h[KT::NV];
-                load_elem<KT>(elems, w >> 3, h);
-                if (!item_less(key, v, entity_key<KT>(h, w & 7), w)) break;
-                gb[q] = w;
-                --q;
-            }
-            gb[q] = v;
-        }
-    }
-    auto key_at = [&](int j) -> uint64_t {
-        if (in_smem) return K[j * NODE_TPB];
-        const int w = gb[j];
-        int h[KT::NV];
-        load_elem<KT>(elems, w >> 3, h);
-        return entity_key<KT>(h, w & 7);
+        return make_item<KT>(elems, gb[j]);
     };
-    auto val_at = [&](int j) -> int { return in_smem ? V[j * NODE_TPB] : gb[j]; };
+    auto put = [&](int j, const Item<KT>& it) {
+        if (in_smem) {
+            K[j * TPB] = it.key;
+            if constexpr (KT::FACES) V[j * TPB] = it.inst;
+        } else {
+            gb[j] = it.inst;
+        }
+    };
+    // ---- load + insertion sort by (entity, element) -----------------------------
+    for (int j = 0; j < n; ++j) {
+        const Item<KT> it = make_item<KT>(elems, in_smem ? __ldg(gb + j) : gb[j]);
+        int q = j;
+        while (q > 0) {
+            const Item<KT> prev = get(q - 1);
+            if (!(it < prev)) break;
+            put(q, prev);
+            --q;
+        }
+        put(q, it);
+    }
+    auto inst_at = [&](int j) -> int { return get(j).inst; };
 
     // ---- count entities and row entries -----------------------------------------
     int n_ent = 0, n_nnz = 0;
     for (int j = 0; j < n;) {
-        const uint64_t key = key_at(j);
+        const uint64_t ek = get(j).entity();
         int q = j + 1;
-        while (q < n && key_at(q) == key) ++q;
+        while (q < n && get(q).entity() == ek) ++q;
         const int t = q - j;
         if constexpr (KT::D == 3 && !KT::FACES) {
-            n_nnz += 1 + 2 * link_vertices<KT>(elems, a, (int)key, j, q, val_at) + t;
+            n_nnz += 1 + 2 * link_count<KT>(elems, a, (int)ek, j, q, inst_at) + t;
         } else {
             n_nnz += 1 + (KT::M - 1) * t;
         }
@@ -278,26 +290,27 @@ __global__ void __launch_bounds__(NODE_TPB) k_node_entities(const int32_t* __res
     // ---- offsets: block scan + decoupled look-back over tiles -------------------
     const unsigned long long mine = ((unsigned long long)n_ent << 31) | (unsigned long long)n_nnz;
     unsigned long long tile_total;
-    const unsigned long long excl = block_exclusive_scan<NODE_TPB>(mine, &tile_total, s_scan);
+    const unsigned long long excl = block_exclusive_scan<TPB>(mine, &tile_total, s_scan);
     if (threadIdx.x < 32) {
         const unsigned long long pre = lookback(out.status, tile, tile_total);
-        if (threadIdx.x == 0) s_scan[NODE_TPB / 32 + 1] = pre;
+        if (threadIdx.x == 0) s_scan[TPB / 32 + 1] = pre;
     }
     __syncthreads();
-    const unsigned long long off = s_scan[NODE_TPB / 32 + 1] + excl;
+    const unsigned long long off = s_scan[TPB / 32 + 1] + excl;
     const int ent0 = (int)(off >> 31);
     int nnz_run = (int)(off & 0x7fffffffull);
 
-    // ---- write: DOF ids (elems2dofs), incidence offsets, row_ptr, dofs2nodes ----
+    // ---- write: DOF ids (elems2dofs), incidence, row_ptr, dofs2nodes ------------
     if (live) {
         int id = ent0;
         for (int j = 0; j < n;) {
-            const uint64_t key = key_at(j);
+            const uint64_t ek = get(j).entity();
             int q = j;
-            while (q < n && key_at(q) == key) {
-                const int v = val_at(q);
-                out.e2d[(int64_t)(v >> 3) * KT::M + (v & 7)] = id;
-                if (in_smem) gb[q] = v;  // sorted bucket = entity -> element incidence
+            while (q < n) {
+                const Item<KT> it = get(q);
+                if (it.entity() != ek) break;
+                out.e2d[(int64_t)(it.inst >> 3) * KT::M + (it.inst & 7)] = id;
+                if (in_smem) gb[q] = it.inst;  // sorted bucket = entity -> element incidence
                 ++q;
             }
             const int t = q - j;
@@ -307,14 +320,14 @@ __global__ void __launch_bounds__(NODE_TPB) k_node_entities(const int32_t* __res
                 int32_t* row = out.d2n + (int64_t)id * KT::EK;
                 row[0] = a;
                 if constexpr (KT::FACES) {
-                    row[1] = (int)(key >> 32);
-                    row[2] = (int)(key & 0xffffffffu);
+                    row[1] = (int)(ek >> 32);
+                    row[2] = (int)(ek & 0xffffffffu);
                 } else {
-                    row[1] = (int)key;
+                    row[1] = (int)ek;
                 }
             }
             if constexpr (KT::D == 3 && !KT::FACES) {
-                nnz_run += 1 + 2 * link_vertices<KT>(elems, a, (int)key, j, q, val_at) + t;
+                nnz_run += 1 + 2 * link_count<KT>(elems, a, (int)ek, j, q, inst_at) + t;
             } else {
                 nnz_run += 1 + (KT::M - 1) * t;
             }
@@ -360,6 +373,7 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
         k_bucket<KT, true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, p.bucket_ptr, p.bucket, p.hdr);
         EFEM_LAUNCH_CHECK();
     }
+    constexpr int NODE_TPB = NodeCaps<KT>::TPB;
     const int64_t tiles = (N + NODE_TPB - 1) / NODE_TPB;
     EFEM_CUDA_TRY(cudaMemsetAsync(p.lb_status, 0, (tiles + 1) * sizeof(unsigned long long) + 64, s));
     if (N > 0) {
