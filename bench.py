@@ -37,6 +37,15 @@ def algorithmic_bytes(cfg):
     return mesh_in + csr_out, T
 
 
+def traffic_bytes(cfg):
+    """DRAM bytes per launch of the numeric kernel from a committed ncu capture."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return t[cfg["name"]]["dram_bytes"]
+    except Exception:
+        return None
+
+
 def measured_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -246,7 +255,8 @@ def run_efem(args, cfg):
                    "n_rows": asm.n_rows, "nnz": asm.nnz, "l2": "flushed between timed steps (512 MiB write)"},
         "phase_ms": {"symbolic": sym_ms, "numeric": num_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "k_row_fill (numeric)",
+                     "frac": achieved / peak, "traffic": traffic_bytes(cfg),
+                     "kernel": "numeric row kernel (k_row_fill_net / k_row_fill_ne3)",
                      "peak_source": peak_src, "algorithmic_bytes": alg_bytes,
                      "e2e_achieved": e2e_gbs, "e2e_frac": e2e_gbs / peak},
         "e2e": {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -262,7 +272,7 @@ def run_efem(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="efem", choices=["efem", "reference"])

@@ -70,8 +70,9 @@ efem_status read_flags(Plan& p, cudaStream_t s) {
         return EFEM_ECAPACITY;
     }
     if (h.flags[F_ROW_MISMATCH]) {
-        set_error("internal error: numeric row length differs from symbolic row length");
-        return EFEM_ECUDA;
+        set_error("row structure differs from the closed-form row length: the mesh is not conforming "
+                  "(duplicate elements, or an entity shared by more elements than a conforming mesh allows)");
+        return EFEM_EINVAL;
     }
     return EFEM_OK;
 }
