@@ -184,6 +184,8 @@ __device__ __forceinline__ double local_row(const double (&X)[KT::NV][KT::D], co
 // below that bit.
 // ---------------------------------------------------------------------------------
 constexpr int ROW_TPB = 128;
+constexpr int NE3_SLOTS = 20;  // staged row length cap of the NE0 3D kernel
+constexpr size_t NE3_SMEM = (size_t)NE3_SLOTS * ROW_TPB * (8 + 8 + 4) + (ROW_TPB + 1) * 4 + 16 * ROW_TPB;
 constexpr int WCAP_EDGE = 23;  // C(23, 2) = 253 <= 256 mask bits
 constexpr int WCAP_FACE = 6;   // 6^3 = 216 <= 256
 
@@ -243,13 +245,39 @@ struct Mask256 {
     }
 };
 
+
+// Coalesced, vectorised copy of a CTA's staged CSR segment to global memory.
+// The staging buffers hold element x of the segment at src[sh + x] where
+// sh = seg0 mod W, so global and shared addresses have the same alignment
+// mod W and the body moves W elements per 16-byte access.
+template <class T, class V, int W, int TPB>
+__device__ __forceinline__ void flush_vec(T* __restrict__ dst, const T* src, int sh, int n) {
+    int head = (W - sh) % W;
+    head = head < n ? head : n;
+    for (int x = threadIdx.x; x < head; x += TPB) dst[x] = src[sh + x];
+    const int nv = (n - head) / W;
+    V* dv = reinterpret_cast<V*>(dst + head);
+    const V* sv = reinterpret_cast<const V*>(src + sh + head);
+    for (int v = threadIdx.x; v < nv; v += TPB) dv[v] = sv[v];
+    for (int x = head + nv * W + threadIdx.x; x < n; x += TPB) dst[x] = src[sh + x];
+}
+
+__device__ __forceinline__ void flush_segment(unsigned forms, int seg0, int segn, const int* s_col,
+                                              const double* s_vm, const double* s_vk, int32_t* col_idx,
+                                              double* vals_m, double* vals_k) {
+    if (forms & EFEM_PATTERN) flush_vec<int, int4, 4, 128>(col_idx + seg0, s_col, seg0 & 3, segn);
+    if (forms & EFEM_MASS) flush_vec<double, double2, 2, 128>(vals_m + seg0, s_vm, seg0 & 1, segn);
+    if (forms & EFEM_STIFF) flush_vec<double, double2, 2, 128>(vals_k + seg0, s_vk, seg0 & 1, segn);
+}
+
 // Generic row: any t <= EFEM_MAX_ROW_ELEMS, |W| <= WCAP.  Accumulates into
 // cols / vm / vk (shared staging or global), returns false on a capacity or
 // row-length mismatch.
 template <class KT>
 __device__ __noinline__ bool row_generic(const double* __restrict__ coords, const int32_t* __restrict__ elems,
                                          const int32_t* __restrict__ inc, const int32_t* __restrict__ e2d, int ib,
-                                         int t, int rlen, int* cols, double* vm, double* vk, WsHeader* hdr) {
+                                         int t, int rlen, int* cols, double* vm, double* vk, int st,
+                                         WsHeader* hdr) {
     constexpr int WCAP = RowCaps<KT>::WCAP;
     constexpr int D = KT::D, NV = KT::NV, M = KT::M;
     bool ok = t <= EFEM_MAX_ROW_ELEMS;
@@ -301,8 +329,8 @@ __device__ __noinline__ bool row_generic(const double* __restrict__ coords, cons
     ok &= ncol == rlen;
     if (!ok) return false;
     for (int q = 0; q < rlen; ++q) {
-        vm[q] = 0.0;
-        vk[q] = 0.0;
+        vm[q * st] = 0.0;
+        vk[q * st] = 0.0;
     }
     // pass 3: values, ascending element id (the incidence list order)
     for (int j = 0; j < nt; ++j) {
@@ -330,9 +358,9 @@ __device__ __noinline__ bool row_generic(const double* __restrict__ coords, cons
 #pragma unroll
         for (int l = 0; l < M; ++l) {
             const int slot = mk.rank(entity_index<KT>(pos, l, nw));
-            cols[slot] = dofs[l];
-            vm[slot] += Mr[l];
-            vk[slot] += Kr[l];
+            cols[slot * st] = dofs[l];
+            vm[slot * st] += Mr[l];
+            vk[slot * st] += Kr[l];
         }
     }
     return true;
@@ -359,34 +387,45 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill_ne3(const double* __restri
                                                           double* __restrict__ vals_m, double* __restrict__ vals_k,
                                                           WsHeader* hdr) {
     static_assert(KT::D == 3 && !KT::FACES, "NE0 3D only");
-    constexpr int STAGE = RowCaps<KT>::STAGE;
     constexpr int TMAX = 7;
-    __shared__ int s_col[STAGE];
-    __shared__ double s_vm[STAGE];
-    __shared__ double s_vk[STAGE];
-    __shared__ unsigned char s_pos[16 * ROW_TPB];
+    // column-major per-thread accumulators (slot q of row tid at [q * ROW_TPB +
+    // tid]: conflict-free), flushed in CSR order through the row offset table
+    extern __shared__ __align__(16) unsigned char ne3_smem[];
+    double* s_vm = reinterpret_cast<double*>(ne3_smem);
+    double* s_vk = s_vm + NE3_SLOTS * ROW_TPB;
+    int* s_col = reinterpret_cast<int*>(s_vk + NE3_SLOTS * ROW_TPB);
+    int* s_off = s_col + NE3_SLOTS * ROW_TPB;
+    unsigned char* s_pos = reinterpret_cast<unsigned char*>(s_off + ROW_TPB + 1);
 
     const int64_t r0 = blockIdx.x * (int64_t)ROW_TPB;
     const int64_t r1 = (r0 + ROW_TPB < n_rows) ? r0 + ROW_TPB : n_rows;
     const int seg0 = __ldg(row_ptr + r0);
     const int segn = __ldg(row_ptr + r1) - seg0;
-    const bool staged = segn <= STAGE;
     const int64_t i = r0 + threadIdx.x;
+    int rbeg = 0, rlen = 0;
+    if (i < n_rows) {
+        rbeg = __ldg(row_ptr + i);
+        rlen = __ldg(row_ptr + i + 1) - rbeg;
+        s_off[threadIdx.x] = rbeg - seg0;
+    }
+    const bool staged = __syncthreads_and(rlen <= NE3_SLOTS);
 
     if (i < n_rows) {
         const int ib = __ldg(inc_ptr + i);
         const int t = __ldg(inc_ptr + i + 1) - ib;
-        const int rbeg = __ldg(row_ptr + i), rlen = __ldg(row_ptr + i + 1) - rbeg;
         int* cols;
         double *vm, *vk;
+        int st;
         if (staged) {
-            cols = s_col + (rbeg - seg0);
-            vm = s_vm + (rbeg - seg0);
-            vk = s_vk + (rbeg - seg0);
+            cols = s_col + threadIdx.x;
+            vm = s_vm + threadIdx.x;
+            vk = s_vk + threadIdx.x;
+            st = ROW_TPB;
         } else {
-            cols = col_idx + rbeg;
-            vm = vals_m ? vals_m + rbeg : s_vm;
-            vk = vals_k ? vals_k + rbeg : s_vk;
+            cols = col_idx + rbeg;  // slow path: accumulate in place in global memory
+            vm = vals_m ? vals_m + rbeg : s_vm + threadIdx.x;
+            vk = vals_k ? vals_k + rbeg : s_vk + threadIdx.x;
+            st = 1;
         }
         bool ok;
         if (fast_ids && t >= 1 && t <= TMAX) {
@@ -470,8 +509,8 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill_ne3(const double* __restri
             ok = mk.finish() == rlen;
             if (ok) {
                 for (int q = 0; q < rlen; ++q) {
-                    vm[q] = 0.0;
-                    vk[q] = 0.0;
+                    vm[q * st] = 0.0;
+                    vk[q * st] = 0.0;
                 }
 #pragma unroll
                 for (int j = 0; j < TMAX; ++j) {
@@ -499,26 +538,34 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill_ne3(const double* __restri
 #pragma unroll
                         for (int l = 0; l < 6; ++l) {
                             const int slot = mk.rank(entity_index<KT>(pos, l, nw));
-                            cols[slot] = dofs[l];
-                            vm[slot] += Mr[l];
-                            vk[slot] += Kr[l];
+                            cols[slot * st] = dofs[l];
+                            vm[slot * st] += Mr[l];
+                            vk[slot * st] += Kr[l];
                         }
                     }
                 }
             }
         } else {
-            ok = row_generic<KT>(coords, elems, inc, e2d, ib, t, rlen, cols, vm, vk, hdr);
+            ok = row_generic<KT>(coords, elems, inc, e2d, ib, t, rlen, cols, vm, vk, st, hdr);
         }
         if (!ok) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
     }
     if (!staged) return;
     __syncthreads();
-    if (forms & EFEM_PATTERN)
-        for (int q = threadIdx.x; q < segn; q += ROW_TPB) col_idx[seg0 + q] = s_col[q];
-    if (forms & EFEM_MASS)
-        for (int q = threadIdx.x; q < segn; q += ROW_TPB) vals_m[seg0 + q] = s_vm[q];
-    if (forms & EFEM_STIFF)
-        for (int q = threadIdx.x; q < segn; q += ROW_TPB) vals_k[seg0 + q] = s_vk[q];
+    // CSR-order flush: element x of the segment belongs to the last row r with
+    // s_off[r] <= x, slot x - s_off[r]
+    const int nr = (int)(r1 - r0);
+    for (int x = threadIdx.x; x < segn; x += ROW_TPB) {
+        int lo = 0, hi = nr - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_off[mid] <= x) lo = mid; else hi = mid - 1;
+        }
+        const int src = (x - s_off[lo]) * ROW_TPB + lo;
+        if (forms & EFEM_PATTERN) col_idx[seg0 + x] = s_col[src];
+        if (forms & EFEM_MASS) vals_m[seg0 + x] = s_vm[src];
+        if (forms & EFEM_STIFF) vals_k[seg0 + x] = s_vk[src];
+    }
 }
 
 // ---------------------------------------------------------------------------------
@@ -542,9 +589,9 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill_net(const double* __restri
     constexpr int D = KT::D, NV = KT::NV, M = KT::M;
     constexpr int NS = 1 + 2 * (M - 1);
     constexpr int STAGE = ROW_TPB * NS;
-    __shared__ int s_col[STAGE];
-    __shared__ double s_vm[STAGE];
-    __shared__ double s_vk[STAGE];
+    __shared__ __align__(16) int s_col[STAGE + 4];
+    __shared__ __align__(16) double s_vm[STAGE + 2];
+    __shared__ __align__(16) double s_vk[STAGE + 2];
 
     const int64_t r0 = blockIdx.x * (int64_t)ROW_TPB;
     const int64_t r1 = (r0 + ROW_TPB < n_rows) ? r0 + ROW_TPB : n_rows;
@@ -617,37 +664,24 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill_net(const double* __restri
                     }
                 }
             }
-            // odd-even transposition sort (NS rounds) by column
-#pragma unroll
-            for (int r = 0; r < NS; ++r) {
-#pragma unroll
-                for (int q = (r & 1); q + 1 < NS; q += 2) {
-                    const bool sw = cols[q] > cols[q + 1];
-                    const int c0 = sw ? cols[q + 1] : cols[q], c1 = sw ? cols[q] : cols[q + 1];
-                    const double m0 = sw ? vm[q + 1] : vm[q], m1 = sw ? vm[q] : vm[q + 1];
-                    const double k0 = sw ? vk[q + 1] : vk[q], k1 = sw ? vk[q] : vk[q + 1];
-                    cols[q] = c0; cols[q + 1] = c1;
-                    vm[q] = m0; vm[q + 1] = m1;
-                    vk[q] = k0; vk[q + 1] = k1;
-                }
-            }
+            // place by rank: the valid columns are distinct, sentinels (INT_MAX)
+            // rank last and are not written
             const int o = rbeg - seg0;
 #pragma unroll
-            for (int q = 0; q < NS; ++q)
-                if (q < rlen) {
-                    s_col[o + q] = cols[q];
-                    s_vm[o + q] = vm[q];
-                    s_vk[o + q] = vk[q];
+            for (int x = 0; x < NS; ++x) {
+                int r = 0;
+#pragma unroll
+                for (int y = 0; y < NS; ++y) r += (y != x) & (cols[y] < cols[x]);
+                if (cols[x] != INT_MAX) {
+                    s_col[(seg0 & 3) + o + r] = cols[x];
+                    s_vm[(seg0 & 1) + o + r] = vm[x];
+                    s_vk[(seg0 & 1) + o + r] = vk[x];
                 }
+            }
         }
     }
     __syncthreads();
-    if (forms & EFEM_PATTERN)
-        for (int q = threadIdx.x; q < segn; q += ROW_TPB) col_idx[seg0 + q] = s_col[q];
-    if (forms & EFEM_MASS)
-        for (int q = threadIdx.x; q < segn; q += ROW_TPB) vals_m[seg0 + q] = s_vm[q];
-    if (forms & EFEM_STIFF)
-        for (int q = threadIdx.x; q < segn; q += ROW_TPB) vals_k[seg0 + q] = s_vk[q];
+    flush_segment(forms, seg0, segn, s_col, s_vm, s_vk, col_idx, vals_m, vals_k);
 }
 
 // ---------------------------------------------------------------------------------
@@ -662,7 +696,13 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) 
                                                     p.n_dofs, forms, out->col_idx, vm, vk, p.hdr);
     } else {
         const int fast_ids = p.n_nodes < (1ll << 27);
-        k_row_fill_ne3<KT><<<grid, ROW_TPB, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr,
+        static bool attr = false;
+        if (!attr) {
+            EFEM_CUDA_TRY(cudaFuncSetAttribute(k_row_fill_ne3<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)NE3_SMEM));
+            attr = true;
+        }
+        k_row_fill_ne3<KT><<<grid, ROW_TPB, NE3_SMEM, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr,
                                                     p.n_dofs, forms, fast_ids, out->col_idx, vm, vk, p.hdr);
     }
     EFEM_LAUNCH_CHECK();

@@ -139,7 +139,7 @@ struct NodeCaps {
     // instances per node held in shared memory (one 64-bit sort key each;
     // faces add a 32-bit instance word); larger buckets take a global-memory
     // slow path
-    static constexpr int CAP = KT::D == 2 ? 24 : (KT::FACES ? 32 : 48);
+    static constexpr int CAP = KT::D == 2 ? 16 : (KT::FACES ? 32 : 48);
     static constexpr int TPB = KT::D == 2 ? 128 : 64;
 };
 
@@ -212,6 +212,44 @@ __device__ __forceinline__ int link_count(const int32_t* __restrict__ elems, int
     return L;
 }
 
+// t <= 8: the 2t link values in registers, distinct count by pairwise compares
+template <class KT, class InstAt>
+__device__ __forceinline__ int link_count_fast(const int32_t* __restrict__ elems, int a, int b, int j, int q,
+                                               InstAt inst_at) {
+    const int t = q - j;
+    if (t > 8) return link_count<KT>(elems, a, b, j, q, inst_at);
+    int lk[16];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        if (u < t) {
+            int h[4];
+            load_elem<KT>(elems, inst_at(j + u) >> 3, h);
+            // the two vertices other than a and b, in local order
+            int c = -1, d = -1;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const bool link = h[v] != a && h[v] != b;
+                d = (link && c >= 0 && d < 0) ? h[v] : d;
+                c = (link && c < 0) ? h[v] : c;
+            }
+            lk[2 * u] = c;
+            lk[2 * u + 1] = d;
+        } else {
+            lk[2 * u] = -1 - 2 * u;  // distinct sentinels never counted
+            lk[2 * u + 1] = -2 - 2 * u;
+        }
+    }
+    int L = 0;
+#pragma unroll
+    for (int x = 0; x < 16; ++x) {
+        bool dup = false;
+#pragma unroll
+        for (int y = 0; y < x; ++y) dup |= lk[y] == lk[x];
+        L += (x < 2 * t) && !dup;
+    }
+    return L;
+}
+
 template <class KT>
 __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_entities(const int32_t* __restrict__ elems,
                                                                      const int32_t* __restrict__ bucket_ptr,
@@ -222,6 +260,8 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_entities(const int32
     __shared__ int s_inst[KT::FACES ? CAP * TPB : 1];
     __shared__ unsigned long long s_scan[TPB / 32 + 2];
     __shared__ int s_tile;
+    constexpr int RL_CAP = (KT::D == 3 && !KT::FACES) ? 16 : 1;
+    __shared__ unsigned char s_rl[RL_CAP * TPB];
 
     if (threadIdx.x == 0) s_tile = atomicAdd(out.ticket, 1);
     __syncthreads();
@@ -257,34 +297,86 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_entities(const int32
             gb[j] = it.inst;
         }
     };
-    // ---- load + insertion sort by (entity, element) -----------------------------
-    for (int j = 0; j < n; ++j) {
-        const Item<KT> it = make_item<KT>(elems, in_smem ? __ldg(gb + j) : gb[j]);
-        int q = j;
-        while (q > 0) {
-            const Item<KT> prev = get(q - 1);
-            if (!(it < prev)) break;
-            put(q, prev);
-            --q;
-        }
-        put(q, it);
-    }
     auto inst_at = [&](int j) -> int { return get(j).inst; };
-
-    // ---- count entities and row entries -----------------------------------------
+    // 2D fast path: a node owns <= 8 instances in practice (3 edges x 2
+    // triangles on the structured mesh) -> sort 8 keys in registers with a
+    // bitonic network; larger buckets take the shared-memory path.
+    constexpr int NREG = 8;
+    const bool fast = KT::D == 2 && n <= NREG;
+    uint64_t rk[NREG];
+    int rlen[NREG];
     int n_ent = 0, n_nnz = 0;
-    for (int j = 0; j < n;) {
-        const uint64_t ek = get(j).entity();
-        int q = j + 1;
-        while (q < n && get(q).entity() == ek) ++q;
-        const int t = q - j;
-        if constexpr (KT::D == 3 && !KT::FACES) {
-            n_nnz += 1 + 2 * link_count<KT>(elems, a, (int)ek, j, q, inst_at) + t;
-        } else {
-            n_nnz += 1 + (KT::M - 1) * t;
+    if constexpr (KT::D == 2) {
+        if (fast) {
+#pragma unroll
+            for (int j = 0; j < NREG; ++j) rk[j] = j < n ? make_item<KT>(elems, __ldg(gb + j)).key : ~0ull;
+#pragma unroll
+            for (int kk = 2; kk <= NREG; kk <<= 1)
+#pragma unroll
+                for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+                    for (int x = 0; x < NREG; ++x) {
+                        const int y = x ^ jj;
+                        if (y > x) {
+                            const uint64_t lo = rk[x] < rk[y] ? rk[x] : rk[y];
+                            const uint64_t hi = rk[x] < rk[y] ? rk[y] : rk[x];
+                            const bool asc = (x & kk) == 0;
+                            rk[x] = asc ? lo : hi;
+                            rk[y] = asc ? hi : lo;
+                        }
+                    }
+            // run lengths (backwards) and distinct count
+#pragma unroll
+            for (int x = NREG - 1; x >= 0; --x) {
+                const bool cont = x + 1 < n && (rk[x + 1] >> 32) == (rk[x] >> 32);
+                rlen[x] = cont ? rlen[x + 1 < NREG ? x + 1 : x] + 1 : 1;
+            }
+#pragma unroll
+            for (int x = 0; x < NREG; ++x) n_ent += x < n && (x == 0 || (rk[x] >> 32) != (rk[x - 1] >> 32));
+            n_nnz = n_ent + (KT::M - 1) * n;
         }
-        ++n_ent;
-        j = q;
+    }
+    if (!fast) {
+        // ---- load (independent gathers) then insertion sort by (entity, element) ----
+        if (in_smem) {
+    #pragma unroll 4
+            for (int j = 0; j < n; ++j) {
+                const Item<KT> it = make_item<KT>(elems, __ldg(gb + j));
+                K[j * TPB] = it.key;
+                if constexpr (KT::FACES) V[j * TPB] = it.inst;
+            }
+        }
+        for (int j = in_smem ? 1 : 0; j < n; ++j) {
+            const Item<KT> it = in_smem ? get(j) : make_item<KT>(elems, gb[j]);
+            int q = j;
+            while (q > 0) {
+                const Item<KT> prev = get(q - 1);
+                if (!(it < prev)) break;
+                put(q, prev);
+                --q;
+            }
+            put(q, it);
+        }
+
+        // ---- count entities and row entries -----------------------------------------
+        // 2D edges / 3D faces: rows have 1 + (m-1) t entries, so the node's total
+        // is n_ent + (m-1) n.  3D edges: 1 + 2 L + t per run, L kept per run in
+        // s_rl for the write pass.
+        for (int j = 0; j < n;) {
+            const uint64_t ek = get(j).entity();
+            int q = j + 1;
+            while (q < n && get(q).entity() == ek) ++q;
+            if constexpr (KT::D == 3 && !KT::FACES) {
+                const int t = q - j;
+                const int rl = 1 + 2 * link_count_fast<KT>(elems, a, (int)ek, j, q, inst_at) + t;
+                if (n_ent < RL_CAP) s_rl[n_ent * TPB + threadIdx.x] = rl;
+                n_nnz += rl;
+            }
+            ++n_ent;
+            j = q;
+        }
+        if constexpr (!(KT::D == 3 && !KT::FACES)) n_nnz = n_ent + (KT::M - 1) * n;
+
     }
 
     // ---- offsets: block scan + decoupled look-back over tiles -------------------
@@ -301,7 +393,38 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_entities(const int32
     int nnz_run = (int)(off & 0x7fffffffull);
 
     // ---- write: DOF ids (elems2dofs), incidence, row_ptr, dofs2nodes ------------
-    if (live) {
+    if (live && fast) {
+        if constexpr (KT::D == 2) {
+            int id = ent0 - 1;
+#pragma unroll
+            for (int x = 0; x < NREG; ++x) {
+                if (x < n) {
+                    const bool first = x == 0 || (rk[x] >> 32) != (rk[x - 1] >> 32);
+                    const int inst = (int)(uint32_t)rk[x];
+                    if (first) {
+                        ++id;
+                        out.inc_ptr[id] = beg + x;
+                        out.row_ptr[id] = nnz_run;
+                        nnz_run += 1 + (KT::M - 1) * rlen[x];
+                        if (out.d2n) {
+                            out.d2n[(int64_t)id * 2] = a;
+                            out.d2n[(int64_t)id * 2 + 1] = (int)(rk[x] >> 32);
+                        }
+                    }
+                    out.e2d[(int64_t)(inst >> 3) * KT::M + (inst & 7)] = id;
+                    gb[x] = inst;
+                }
+            }
+            if (a == n_nodes - 1) {
+                const int R = id + 1;
+                out.inc_ptr[R] = beg + n;
+                out.row_ptr[R] = nnz_run;
+                out.totals[0] = R;
+                out.totals[1] = nnz_run;
+            }
+        }
+    }
+    if (live && !fast) {
         int id = ent0;
         for (int j = 0; j < n;) {
             const uint64_t ek = get(j).entity();
@@ -327,7 +450,9 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_entities(const int32
                 }
             }
             if constexpr (KT::D == 3 && !KT::FACES) {
-                nnz_run += 1 + 2 * link_count<KT>(elems, a, (int)ek, j, q, inst_at) + t;
+                const int r = id - ent0;
+                nnz_run += r < RL_CAP ? (int)s_rl[r * TPB + threadIdx.x]
+                                      : 1 + 2 * link_count_fast<KT>(elems, a, (int)ek, j, q, inst_at) + t;
             } else {
                 nnz_run += 1 + (KT::M - 1) * t;
             }
