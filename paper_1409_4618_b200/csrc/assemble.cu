@@ -1,440 +1,223 @@
-// assemble.cu -- sparsity pattern (symbolic) and values (numeric) of the
-// global mass / stiffness matrices.
+// assemble.cu -- numeric assembly: local matrices summed
+// into the CSR rows of the global mass / stiffness matrices (PAPER.md:335-342,
+// 671-696).
 //
-// Row-owner design: one thread per global DOF row i.
-// The elements containing entity i are found in the incidence list of its
-// minimum node; row i's pattern is the union of their elems2dofs rows and its
-// values are row k (= local index of entity i) of their local matrices,
-// summed in ascending element order.  A CTA stages its rows' CSR segment in
-// shared memory and writes it out with coalesced stores, so every CSR byte
-// is written exactly once and no T*m^2 contribution array ever reaches HBM.
-//
-// Local matrices use closed forms of the paper's integrals (DESIGN.md
-// "Element math"); the oracle evaluates the same integrals by quadrature.
-#include <cub/cub.cuh>
-
-#include "efem_internal.cuh"
+// Row-owner design: one thread per global DOF row i.  The
+// elements containing entity i are the run of the sorted bucket
+// [inc_ptr[i], inc_ptr[i+1]) (ascending element id); row i's values are row k
+// (local index of entity i) of their local matrices, summed in that order.
+// A CTA stages its rows' CSR segment in shared memory and writes it out with
+// coalesced stores, so every CSR byte is written exactly once and no local
+// matrix ever reaches HBM.
+#include "element.cuh"
 
 namespace efem {
 
-template <class KT>
-__device__ __forceinline__ void load_g(const int32_t* __restrict__ elems, int e, int (&g)[KT::NV]) {
-    if constexpr (KT::NV == 4) {
-        const int4 t = __ldg(reinterpret_cast<const int4*>(elems) + e);
-        g[0] = t.x; g[1] = t.y; g[2] = t.z; g[3] = t.w;
-    } else {
-        const int32_t* p = elems + (int64_t)e * 3;
-        g[0] = __ldg(p); g[1] = __ldg(p + 1); g[2] = __ldg(p + 2);
-    }
-}
-
-// orientation signs (see dofs.cu local_sign for the derivation)
-template <class KT>
-__device__ __forceinline__ double sign_d(const int (&g)[KT::NV], int k) {
-    if constexpr (KT::FACES) {
-        const int o = 3 - k;
-        int f[3], t = 0;
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-            if (v != o) f[t++] = g[v];
-        const int inv = (f[0] > f[1]) + (f[0] > f[2]) + (f[1] > f[2]);
-        return ((inv + (k & 1)) & 1) ? 1.0 : -1.0;
-    } else {
-        return g[edge_start(KT::D, k)] < g[edge_end(KT::D, k)] ? 1.0 : -1.0;
-    }
-}
-
-// Row k of the local mass and stiffness matrices of one element, including
-// the sign data s_k s_l (PAPER.md:344-363 with reading C2).  Closed forms:
-//  RT (2D, 3D) and NE (2D): the Piola-mapped local functions are
-//    s_k (x - p_k) / (d |K|) * sign(det)   (p_k = vertex opposite DOF k), so
-//    M_kl = s_k s_l (y_k . y_l + Q) / (d^2 |K|),  y_a = x_a - centroid,
-//    Q = sum_a |y_a|^2 / ((d+1)(d+2));   K_kl = s_k s_l / |K|.
-//    (2D NE0 equals 2D RT0 on the same mesh; pinned by the
-//    oracle's own quadrature in the parity tests.)
-//  NE (3D): Whitney form lambda_i grad lambda_j - lambda_j grad lambda_i of
-//    edge i->j; with G_ab = grad lambda_a . grad lambda_b,
-//    M_(ij)(pq) = |K|/20 [(1+d_ip) G_jq - (1+d_iq) G_jp - (1+d_jp) G_iq + (1+d_jq) G_ip]
-//    K_(ij)(pq) = 4 |K| (G_ip G_jq - G_iq G_jp).
-// Returns det B_K (0 -> degenerate).
-template <class KT>
-__device__ __forceinline__ double local_row(const double (&X)[KT::NV][KT::D], const int (&g)[KT::NV], int k,
-                                            double (&Mr)[KT::M], double (&Kr)[KT::M]) {
-    constexpr int D = KT::D, NV = KT::NV, M = KT::M;
-    double s[M];
-#pragma unroll
-    for (int l = 0; l < M; ++l) s[l] = sign_d<KT>(g, l);
-    double sk = s[0];
-#pragma unroll
-    for (int l = 1; l < M; ++l) sk = (k == l) ? s[l] : sk;
-
-    double det;
-    if constexpr (D == 2) {
-        det = (X[1][0] - X[0][0]) * (X[2][1] - X[0][1]) - (X[2][0] - X[0][0]) * (X[1][1] - X[0][1]);
-    } else {
-        const double e1[3] = {X[1][0] - X[0][0], X[1][1] - X[0][1], X[1][2] - X[0][2]};
-        const double e2[3] = {X[2][0] - X[0][0], X[2][1] - X[0][1], X[2][2] - X[0][2]};
-        const double e3[3] = {X[3][0] - X[0][0], X[3][1] - X[0][1], X[3][2] - X[0][2]};
-        det = e1[0] * (e2[1] * e3[2] - e2[2] * e3[1]) - e1[1] * (e2[0] * e3[2] - e2[2] * e3[0]) +
-              e1[2] * (e2[0] * e3[1] - e2[1] * e3[0]);
-    }
-    const double adet = fabs(det);
-
-    if constexpr (KT::ELEMENT == EFEM_NED0 && D == 3) {
-        // gradients of barycentrics: rows of B^{-1} = (e2 x e3, e3 x e1, e1 x e2) / det
-        const double e1[3] = {X[1][0] - X[0][0], X[1][1] - X[0][1], X[1][2] - X[0][2]};
-        const double e2[3] = {X[2][0] - X[0][0], X[2][1] - X[0][1], X[2][2] - X[0][2]};
-        const double e3[3] = {X[3][0] - X[0][0], X[3][1] - X[0][1], X[3][2] - X[0][2]};
-        const double rdet = 1.0 / det;
-        double gl[4][3];
-        gl[1][0] = (e2[1] * e3[2] - e2[2] * e3[1]) * rdet;
-        gl[1][1] = (e2[2] * e3[0] - e2[0] * e3[2]) * rdet;
-        gl[1][2] = (e2[0] * e3[1] - e2[1] * e3[0]) * rdet;
-        gl[2][0] = (e3[1] * e1[2] - e3[2] * e1[1]) * rdet;
-        gl[2][1] = (e3[2] * e1[0] - e3[0] * e1[2]) * rdet;
-        gl[2][2] = (e3[0] * e1[1] - e3[1] * e1[0]) * rdet;
-        gl[3][0] = (e1[1] * e2[2] - e1[2] * e2[1]) * rdet;
-        gl[3][1] = (e1[2] * e2[0] - e1[0] * e2[2]) * rdet;
-        gl[3][2] = (e1[0] * e2[1] - e1[1] * e2[0]) * rdet;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) gl[0][c] = -(gl[1][c] + gl[2][c] + gl[3][c]);
-        const int i = (k < 3 ? 0 : (k == 3 ? 1 : (k == 4 ? 2 : 3)));
-        const int j = k < 3 ? k + 1 : (k == 3 ? 2 : (k == 4 ? 3 : 1));
-        double gi[3], gj[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            gi[c] = i == 0 ? gl[0][c] : (i == 1 ? gl[1][c] : (i == 2 ? gl[2][c] : gl[3][c]));
-            gj[c] = j == 1 ? gl[1][c] : (j == 2 ? gl[2][c] : (j == 3 ? gl[3][c] : gl[0][c]));
-        }
-        double A[4], B[4];  // A_p = G_ip, B_p = G_jp
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            A[q] = gi[0] * gl[q][0] + gi[1] * gl[q][1] + gi[2] * gl[q][2];
-            B[q] = gj[0] * gl[q][0] + gj[1] * gl[q][1] + gj[2] * gl[q][2];
-        }
-        const double vol = adet * (1.0 / 6.0);
-        const double cm = vol * (1.0 / 20.0), ck = 4.0 * vol;
-#pragma unroll
-        for (int l = 0; l < 6; ++l) {
-            const int p = edge_start(3, l), q = edge_end(3, l);
-            const double dip = (i == p) ? 2.0 : 1.0, diq = (i == q) ? 2.0 : 1.0;
-            const double djp = (j == p) ? 2.0 : 1.0, djq = (j == q) ? 2.0 : 1.0;
-            const double ss = sk * s[l];
-            Mr[l] = ss * cm * (dip * B[q] - diq * B[p] - djp * A[q] + djq * A[p]);
-            Kr[l] = ss * ck * (A[p] * B[q] - A[q] * B[p]);
-        }
-    } else {
-        // RT0 2D/3D and NE0 2D: y_a = x_a - centroid
-        double cen[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-            double acc = 0.0;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) acc += X[v][c];
-            cen[c] = acc * (1.0 / NV);
-        }
-        double y[NV][D];
-        double sq = 0.0;
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-                y[v][c] = X[v][c] - cen[c];
-                sq += y[v][c] * y[v][c];
-            }
-        const double Q = sq * (1.0 / ((D + 1) * (D + 2)));
-        // opposite vertex of DOF l: 2D -> l, 3D faces -> 3 - l
-        const int ok_ = KT::FACES ? 3 - k : k;
-        double yk[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-            double t = y[0][c];
-#pragma unroll
-            for (int v = 1; v < NV; ++v) t = (ok_ == v) ? y[v][c] : t;
-            yk[c] = t;
-        }
-        // |K| = |det| / d!;  M scale 1/(d^2 |K|) = (d!/d^2)/|det|;  K scale 1/|K| = d!/|det|
-        const double rad = 1.0 / adet;
-        const double cm = (D == 2 ? 0.5 : 2.0 / 3.0) * rad;
-        const double ck = (D == 2 ? 2.0 : 6.0) * rad;
-#pragma unroll
-        for (int l = 0; l < M; ++l) {
-            const int ol = KT::FACES ? 3 - l : l;
-            double dot = 0.0;
-#pragma unroll
-            for (int c = 0; c < D; ++c) dot += yk[c] * y[ol][c];
-            const double ss = sk * s[l];
-            Mr[l] = ss * cm * (dot + Q);
-            Kr[l] = ss * ck;
-        }
-    }
-    return det;
-}
+constexpr int NUM_TPB = 128;
 
 // ---------------------------------------------------------------------------------
-// Numeric kernel.  Thread per row; ROW_TPB rows per CTA.
-//
-// Slot of a contribution without sorting: every column of row i is an entity
-// whose nodes lie in W = the sorted set of vertices of the elements containing
-// entity i (|W| <= 2 + t in 2D, 3 + t for faces, 2 + 2t for 3D edges).
-// Since DOF ids are lexicographic in node ids, and W is sorted by node id,
-// the column order equals the lexicographic order of the entities' position
-// tuples in W.  Each present column sets one bit of a 256-bit mask at its
-// lexicographic pair / triple index; its CSR slot is the popcount of the mask
-// below that bit.
+// 2D edges and 3D faces.  In a conforming mesh an entity lies in t <= 2
+// elements and two elements share at most that entity, so row i is
+// {i} U (the m-1 other DOFs of each element): 1 + (m-1) t <= 5 (2D) or 7
+// entries, all distinct.  Gather in registers, sum the own entry over the
+// elements, place every column by its rank.
 // ---------------------------------------------------------------------------------
-constexpr int ROW_TPB = 128;
-constexpr int NE3_SLOTS = 20;  // staged row length cap of the NE0 3D kernel
-constexpr size_t NE3_SMEM = (size_t)NE3_SLOTS * ROW_TPB * (8 + 8 + 4) + (ROW_TPB + 1) * 4 + 16 * ROW_TPB;
-constexpr int WCAP_EDGE = 23;  // C(23, 2) = 253 <= 256 mask bits
-constexpr int WCAP_FACE = 6;   // 6^3 = 216 <= 256
-
 template <class KT>
-struct RowCaps {
-    // smem staging budget per row (a tile that does not fit writes directly
-    // to global memory -- slower, same result)
-    static constexpr int STAGE_PER_ROW = KT::D == 2 ? 6 : (KT::FACES ? 8 : 18);
-    static constexpr int STAGE = ROW_TPB * STAGE_PER_ROW;
-    static constexpr int WCAP = KT::FACES ? WCAP_FACE : WCAP_EDGE;
-};
-
-// lexicographic index of local entity l of an element whose vertex positions
-// in W are pos[0..NV)
-template <class KT>
-__device__ __forceinline__ int entity_index(const int (&pos)[KT::NV], int l, int nw) {
-    if constexpr (KT::FACES) {
-        const int o = 3 - l;
-        int f[3], t = 0;
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-            if (v != o) f[t++] = pos[v];
-        const int lo = min(f[0], min(f[1], f[2])), hi = max(f[0], max(f[1], f[2]));
-        const int mid = f[0] + f[1] + f[2] - lo - hi;
-        return (lo * WCAP_FACE + mid) * WCAP_FACE + hi;
-    } else {
-        const int u = pos[edge_start(KT::D, l)], v = pos[edge_end(KT::D, l)];
-        const int p = min(u, v), q = max(u, v);
-        return p * nw - ((p * (p + 1)) >> 1) + (q - p - 1);
-    }
-}
-
-struct Mask256 {
-    unsigned long long w[4];
-    int pc[4];
-    __device__ __forceinline__ void clear() { w[0] = w[1] = w[2] = w[3] = 0ull; }
-    __device__ __forceinline__ void set(int idx) {
-        const unsigned long long b = 1ull << (idx & 63);
-        const int q = idx >> 6;
-        w[0] |= q == 0 ? b : 0ull;
-        w[1] |= q == 1 ? b : 0ull;
-        w[2] |= q == 2 ? b : 0ull;
-        w[3] |= q == 3 ? b : 0ull;
-    }
-    __device__ __forceinline__ int finish() {
-        pc[0] = 0;
-        pc[1] = __popcll(w[0]);
-        pc[2] = pc[1] + __popcll(w[1]);
-        pc[3] = pc[2] + __popcll(w[2]);
-        return pc[3] + __popcll(w[3]);
-    }
-    __device__ __forceinline__ int rank(int idx) const {
-        const int q = idx >> 6;
-        const unsigned long long word = q == 0 ? w[0] : (q == 1 ? w[1] : (q == 2 ? w[2] : w[3]));
-        const int base = q == 0 ? pc[0] : (q == 1 ? pc[1] : (q == 2 ? pc[2] : pc[3]));
-        return base + __popcll(word & ((1ull << (idx & 63)) - 1ull));
-    }
-};
-
-
-// Coalesced, vectorised copy of a CTA's staged CSR segment to global memory.
-// The staging buffers hold element x of the segment at src[sh + x] where
-// sh = seg0 mod W, so global and shared addresses have the same alignment
-// mod W and the body moves W elements per 16-byte access.
-template <class T, class V, int W, int TPB>
-__device__ __forceinline__ void flush_vec(T* __restrict__ dst, const T* src, int sh, int n) {
-    int head = (W - sh) % W;
-    head = head < n ? head : n;
-    for (int x = threadIdx.x; x < head; x += TPB) dst[x] = src[sh + x];
-    const int nv = (n - head) / W;
-    V* dv = reinterpret_cast<V*>(dst + head);
-    const V* sv = reinterpret_cast<const V*>(src + sh + head);
-    for (int v = threadIdx.x; v < nv; v += TPB) dv[v] = sv[v];
-    for (int x = head + nv * W + threadIdx.x; x < n; x += TPB) dst[x] = src[sh + x];
-}
-
-__device__ __forceinline__ void flush_segment(unsigned forms, int seg0, int segn, const int* s_col,
-                                              const double* s_vm, const double* s_vk, int32_t* col_idx,
-                                              double* vals_m, double* vals_k) {
-    if (forms & EFEM_PATTERN) flush_vec<int, int4, 4, 128>(col_idx + seg0, s_col, seg0 & 3, segn);
-    if (forms & EFEM_MASS) flush_vec<double, double2, 2, 128>(vals_m + seg0, s_vm, seg0 & 1, segn);
-    if (forms & EFEM_STIFF) flush_vec<double, double2, 2, 128>(vals_k + seg0, s_vk, seg0 & 1, segn);
-}
-
-// Generic row: any t <= EFEM_MAX_ROW_ELEMS, |W| <= WCAP.  Accumulates into
-// cols / vm / vk (shared staging or global), returns false on a capacity or
-// row-length mismatch.
-template <class KT>
-__device__ __noinline__ bool row_generic(const double* __restrict__ coords, const int32_t* __restrict__ elems,
-                                         const int32_t* __restrict__ inc, const int32_t* __restrict__ e2d, int ib,
-                                         int t, int rlen, int* cols, double* vm, double* vk, int st,
-                                         WsHeader* hdr) {
-    constexpr int WCAP = RowCaps<KT>::WCAP;
+__global__ void __launch_bounds__(NUM_TPB) k_rows_small(const double* __restrict__ coords,
+                                                        const int32_t* __restrict__ elems,
+                                                        const int32_t* __restrict__ inc_ptr,
+                                                        const int32_t* __restrict__ inc,
+                                                        const int32_t* __restrict__ e2d,
+                                                        const int32_t* __restrict__ row_ptr, int n_rows,
+                                                        unsigned forms, int32_t* __restrict__ col_idx,
+                                                        double* __restrict__ vals_m, double* __restrict__ vals_k,
+                                                        WsHeader* hdr) {
     constexpr int D = KT::D, NV = KT::NV, M = KT::M;
-    bool ok = t <= EFEM_MAX_ROW_ELEMS;
-    const int nt = ok ? t : EFEM_MAX_ROW_ELEMS;
-    // pass 1: W = sorted distinct vertices of the row's elements
-    int W[WCAP + 1];
-    int nw = 0;
-    for (int j = 0; j < nt; ++j) {
-        const int e = __ldg(inc + ib + j) >> 3;
-        int g[NV];
-        load_g<KT>(elems, e, g);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const int x = g[v];
-            int q = nw;
-            while (q > 0 && W[q - 1] > x) --q;
-            if (q > 0 && W[q - 1] == x) continue;
-            if (nw >= WCAP) { ok = false; continue; }
-            for (int u = nw; u > q; --u) W[u] = W[u - 1];
-            W[q] = x;
-            ++nw;
-        }
-    }
-    // pass 2: column mask
-    Mask256 mk;
-    mk.clear();
-    int pk[EFEM_MAX_ROW_ELEMS];
-    for (int j = 0; j < nt; ++j) {
-        const int e = __ldg(inc + ib + j) >> 3;
-        int g[NV];
-        load_g<KT>(elems, e, g);
-        int pos[NV];
-        int packed = 0;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            int lo = 0, hi = nw;  // first index with W >= g[v]
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (W[mid] < g[v]) lo = mid + 1; else hi = mid;
-            }
-            pos[v] = lo;
-            packed |= lo << (5 * v);
-        }
-        pk[j] = packed;
-#pragma unroll
-        for (int l = 0; l < M; ++l) mk.set(entity_index<KT>(pos, l, nw));
-    }
-    const int ncol = mk.finish();
-    ok &= ncol == rlen;
-    if (!ok) return false;
-    for (int q = 0; q < rlen; ++q) {
-        vm[q * st] = 0.0;
-        vk[q * st] = 0.0;
-    }
-    // pass 3: values, ascending element id (the incidence list order)
-    for (int j = 0; j < nt; ++j) {
-        const int pe = __ldg(inc + ib + j);
-        const int e = pe >> 3, k = pe & 7;
-        int g[NV];
-        load_g<KT>(elems, e, g);
-        double X[NV][D];
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-            for (int cc = 0; cc < D; ++cc) X[v][cc] = __ldg(coords + (int64_t)g[v] * D + cc);
-        int dofs[M];
-#pragma unroll
-        for (int l = 0; l < M; ++l) dofs[l] = __ldg(e2d + (int64_t)e * M + l);
-        double Mr[M], Kr[M];
-        const double det = local_row<KT>(X, g, k, Mr, Kr);
-        if (!(det != 0.0) || !isfinite(det)) {
-            atomicOr(&hdr->flags[F_DEGENERATE], 1);
-            atomicMin(&hdr->bad_element, (unsigned long long)e);
-        }
-        int pos[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) pos[v] = (pk[j] >> (5 * v)) & 31;
-#pragma unroll
-        for (int l = 0; l < M; ++l) {
-            const int slot = mk.rank(entity_index<KT>(pos, l, nw));
-            cols[slot * st] = dofs[l];
-            vm[slot * st] += Mr[l];
-            vk[slot * st] += Kr[l];
-        }
-    }
-    return true;
-}
+    constexpr int NS = 1 + 2 * (M - 1);
+    constexpr int STAGE = NUM_TPB * NS;
+    __shared__ int s_col[STAGE];
+    __shared__ double s_vm[STAGE];
+    __shared__ double s_vk[STAGE];
 
-__device__ __forceinline__ int sel4(const int (&g)[4], int i) {
-    return i == 0 ? g[0] : (i == 1 ? g[1] : (i == 2 ? g[2] : g[3]));
-}
-
-// 3D edges (NE0).  Row (a, b) with t tets around the edge: the columns are
-// the edges among W = {a, b} U link vertices.  Fast path (t <= 7, node ids
-// < 2^27): W comes from one 16-key bitonic network in registers
-// (key = node << 5 | source), positions go through a per-thread shared
-// scratch, the column mask / ranks are as in row_generic.  Other rows use
-// row_generic.
-template <class KT>
-__global__ void __launch_bounds__(ROW_TPB) k_row_fill_ne3(const double* __restrict__ coords,
-                                                          const int32_t* __restrict__ elems,
-                                                          const int32_t* __restrict__ inc_ptr,
-                                                          const int32_t* __restrict__ inc,
-                                                          const int32_t* __restrict__ e2d,
-                                                          const int32_t* __restrict__ row_ptr, int64_t n_rows,
-                                                          unsigned forms, int fast_ids, int32_t* __restrict__ col_idx,
-                                                          double* __restrict__ vals_m, double* __restrict__ vals_k,
-                                                          WsHeader* hdr) {
-    static_assert(KT::D == 3 && !KT::FACES, "NE0 3D only");
-    constexpr int TMAX = 7;
-    // column-major per-thread accumulators (slot q of row tid at [q * ROW_TPB +
-    // tid]: conflict-free), flushed in CSR order through the row offset table
-    extern __shared__ __align__(16) unsigned char ne3_smem[];
-    double* s_vm = reinterpret_cast<double*>(ne3_smem);
-    double* s_vk = s_vm + NE3_SLOTS * ROW_TPB;
-    int* s_col = reinterpret_cast<int*>(s_vk + NE3_SLOTS * ROW_TPB);
-    int* s_off = s_col + NE3_SLOTS * ROW_TPB;
-    unsigned char* s_pos = reinterpret_cast<unsigned char*>(s_off + ROW_TPB + 1);
-
-    const int64_t r0 = blockIdx.x * (int64_t)ROW_TPB;
-    const int64_t r1 = (r0 + ROW_TPB < n_rows) ? r0 + ROW_TPB : n_rows;
+    const int r0 = blockIdx.x * NUM_TPB;
+    const int r1 = min(r0 + NUM_TPB, n_rows);
     const int seg0 = __ldg(row_ptr + r0);
     const int segn = __ldg(row_ptr + r1) - seg0;
-    const int64_t i = r0 + threadIdx.x;
-    int rbeg = 0, rlen = 0;
-    if (i < n_rows) {
-        rbeg = __ldg(row_ptr + i);
-        rlen = __ldg(row_ptr + i + 1) - rbeg;
-        s_off[threadIdx.x] = rbeg - seg0;
-    }
-    const bool staged = __syncthreads_and(rlen <= NE3_SLOTS);
+    const int i = r0 + (int)threadIdx.x;
 
     if (i < n_rows) {
         const int ib = __ldg(inc_ptr + i);
         const int t = __ldg(inc_ptr + i + 1) - ib;
-        int* cols;
-        double *vm, *vk;
+        const int o = __ldg(row_ptr + i) - seg0;
+        if (t < 1 || t > 2) {
+            atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
+        } else {
+            int cl[NS];
+            double am[NS], ak[NS];
+            cl[0] = i;
+            am[0] = 0.0;
+            ak[0] = 0.0;
+            // all loads of both elements first (element 1 duplicates element 0
+            // when t == 1; its results are then discarded)
+            int pe[2], g[2][NV], dofs[2][M];
+            double X[2][NV][D];
+            pe[0] = __ldg(inc + ib);
+            pe[1] = __ldg(inc + ib + (t - 1));
+#pragma unroll
+            for (int j = 0; j < 2; ++j) load_g<KT>(elems, pe[j] >> 3, g[j]);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+#pragma unroll
+                for (int l = 0; l < M; ++l) dofs[j][l] = __ldg(e2d + (pe[j] >> 3) * M + l);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    if constexpr (D == 2) {
+                        const double2 c = __ldg(reinterpret_cast<const double2*>(coords) + g[j][v]);
+                        X[j][v][0] = c.x;
+                        X[j][v][1] = c.y;
+                    } else {
+#pragma unroll
+                        for (int cc = 0; cc < 3; ++cc) X[j][v][cc] = __ldg(coords + g[j][v] * 3 + cc);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (j < t) {
+                    const int e = pe[j] >> 3, k = pe[j] & 7;
+                    double Mr[M], Kr[M];
+                    const double det = local_row<KT>(X[j], g[j], k, Mr, Kr);
+                    if (!(det != 0.0) || !isfinite(det)) {
+                        atomicOr(&hdr->flags[F_DEGENERATE], 1);
+                        atomicMin(&hdr->bad_element, (unsigned long long)e);
+                    }
+                    double om = Mr[0], okk = Kr[0];
+#pragma unroll
+                    for (int l = 1; l < M; ++l) {
+                        om = (k == l) ? Mr[l] : om;
+                        okk = (k == l) ? Kr[l] : okk;
+                    }
+                    am[0] += om;
+                    ak[0] += okk;
+#pragma unroll
+                    for (int q = 0; q < M - 1; ++q) {  // the other local DOFs, l = q + (q >= k)
+                        const bool sh = q >= k;
+                        cl[1 + j * (M - 1) + q] = sh ? dofs[j][q + 1] : dofs[j][q];
+                        am[1 + j * (M - 1) + q] = sh ? Mr[q + 1] : Mr[q];
+                        ak[1 + j * (M - 1) + q] = sh ? Kr[q + 1] : Kr[q];
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < M - 1; ++q) cl[1 + j * (M - 1) + q] = INT_MAX;
+                }
+            }
+            // place by rank (valid columns are distinct; INT_MAX sentinels rank last)
+#pragma unroll
+            for (int x = 0; x < NS; ++x) {
+                int rk = 0;
+#pragma unroll
+                for (int y = 0; y < NS; ++y)
+                    if (y != x) rk += cl[y] < cl[x];
+                if (cl[x] != INT_MAX) {
+                    s_col[o + rk] = cl[x];
+                    s_vm[o + rk] = am[x];
+                    s_vk[o + rk] = ak[x];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // coalesced flush; the segment holds at most NS entries per row
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+        const int x = u * NUM_TPB + (int)threadIdx.x;
+        if (x < segn) {
+            if (forms & EFEM_PATTERN) col_idx[seg0 + x] = s_col[x];
+            if (forms & EFEM_MASS) vals_m[seg0 + x] = s_vm[x];
+            if (forms & EFEM_STIFF) vals_k[seg0 + x] = s_vk[x];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// 3D edges (NE0).  Row (a, b) with t tets around the edge; tet j = {a, b, c_j,
+// d_j}.  Columns are the edges among W = {a, b} U link vertices: ab, a-w and
+// b-w for every distinct link vertex w, and c_j-d_j.  Fast path (t <= 7,
+// |W| <= 11, node ids < 2^27):
+//   W by one 16-key bitonic network in registers (key = node << 5 | source);
+//   positions of the sources in a per-thread shared scratch;
+//   the row's columns as bits of ONE 64-bit mask over the C(|W|, 2) <= 55
+//   lexicographic pairs; a column's slot = popcount of the mask below it;
+//   per tet, the slots of its 6 pair types (ab shared) are packed 5 bits each
+//   and each local edge picks its slot by the roles of its endpoints.
+// Accumulators are column-major in shared memory (slot q of row r at
+// q * NUM_TPB + r: bank-conflict free) and flushed in CSR order.  Rows that
+// miss the fast-path limits use row_generic (any shape, 256-bit masks).
+// ---------------------------------------------------------------------------------
+constexpr int NE3_SLOTS = 20;
+constexpr int NE3_TMAX = 7;
+
+__device__ __forceinline__ int pair_index(int p, int q, int nw) {  // p < q
+    return p * nw - ((p * (p + 1)) >> 1) + (q - p - 1);
+}
+
+template <class KT>
+__global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__ coords,
+                                                      const int32_t* __restrict__ elems,
+                                                      const int32_t* __restrict__ inc_ptr,
+                                                      const int32_t* __restrict__ inc,
+                                                      const int32_t* __restrict__ e2d,
+                                                      const int32_t* __restrict__ row_ptr, int n_rows,
+                                                      unsigned forms, int fast_ids, int32_t* __restrict__ col_idx,
+                                                      double* __restrict__ vals_m, double* __restrict__ vals_k,
+                                                      WsHeader* hdr) {
+    static_assert(KT::D == 3 && !KT::FACES, "NE0 3D only");
+    extern __shared__ __align__(16) unsigned char ne3_smem[];
+    double* s_vm = reinterpret_cast<double*>(ne3_smem);
+    double* s_vk = s_vm + NE3_SLOTS * NUM_TPB;
+    int* s_col = reinterpret_cast<int*>(s_vk + NE3_SLOTS * NUM_TPB);
+    int* s_off = s_col + NE3_SLOTS * NUM_TPB;  // NUM_TPB + 1 row offsets
+    unsigned char* s_pos = reinterpret_cast<unsigned char*>(s_off + NUM_TPB + 1);  // 16 per thread
+
+    const int r0 = blockIdx.x * NUM_TPB;
+    const int nr = min(NUM_TPB, n_rows - r0);
+    const int seg0 = __ldg(row_ptr + r0);
+    const int segn = __ldg(row_ptr + r0 + nr) - seg0;
+    const int i = r0 + (int)threadIdx.x;
+    int rlen = 0, ib = 0, t = 0;
+    if (i < n_rows) {
+        const int rb = __ldg(row_ptr + i);
+        rlen = __ldg(row_ptr + i + 1) - rb;
+        s_off[threadIdx.x] = rb - seg0;
+        ib = __ldg(inc_ptr + i);
+        t = __ldg(inc_ptr + i + 1) - ib;
+    }
+    const bool staged = __syncthreads_and(rlen <= NE3_SLOTS);
+
+    if (i < n_rows) {
+        int* ccol;
+        double *cvm, *cvk;
         int st;
         if (staged) {
-            cols = s_col + threadIdx.x;
-            vm = s_vm + threadIdx.x;
-            vk = s_vk + threadIdx.x;
-            st = ROW_TPB;
-        } else {
-            cols = col_idx + rbeg;  // slow path: accumulate in place in global memory
-            vm = vals_m ? vals_m + rbeg : s_vm + threadIdx.x;
-            vk = vals_k ? vals_k + rbeg : s_vk + threadIdx.x;
+            ccol = s_col + threadIdx.x;
+            cvm = s_vm + threadIdx.x;
+            cvk = s_vk + threadIdx.x;
+            st = NUM_TPB;
+        } else {  // an oversize row in the tile: accumulate in place in global memory
+            const int rb = s_off[threadIdx.x] + seg0;
+            ccol = col_idx + rb;
+            cvm = vals_m ? vals_m + rb : s_vm + threadIdx.x;
+            cvk = vals_k ? vals_k + rb : s_vk + threadIdx.x;
             st = 1;
         }
-        bool ok;
-        if (fast_ids && t >= 1 && t <= TMAX) {
-            unsigned char* P = s_pos + threadIdx.x;  // P[src * ROW_TPB]
+        bool ok = false, done = false;
+        if (fast_ids && t >= 1 && t <= NE3_TMAX) {
+            unsigned char* P = s_pos + threadIdx.x;  // P[src * NUM_TPB]
             uint32_t key[16];
-            int inst[TMAX], roles[TMAX];
+            int inst[NE3_TMAX], roles[NE3_TMAX];
             int a = 0, b = 0;
 #pragma unroll
-            for (int j = 0; j < TMAX; ++j) {
+            for (int j = 0; j < NE3_TMAX; ++j) {
                 if (j < t) {
                     const int pe = __ldg(inc + ib + j);
                     inst[j] = pe;
@@ -443,16 +226,16 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill_ne3(const double* __restri
                     load_g<KT>(elems, pe >> 3, g);
                     const int s0 = k < 3 ? 0 : (k == 3 ? 1 : (k == 4 ? 2 : 3));
                     const int s1 = k < 3 ? k + 1 : (k == 3 ? 2 : (k == 4 ? 3 : 1));
-                    // complement of {s0, s1}: (2,3) (1,3) (1,2) (0,3) (0,1) (0,2)
                     const int lc = k == 0 ? 2 : (k == 1 ? 1 : (k == 2 ? 1 : 0));
                     const int ld = k == 0 ? 3 : (k == 1 ? 3 : (k == 2 ? 2 : (k == 3 ? 3 : (k == 4 ? 1 : 2))));
                     const int g0 = sel4(g, s0), g1 = sel4(g, s1);
                     const int la = g0 < g1 ? s0 : s1, lb = g0 < g1 ? s1 : s0;
                     a = min(g0, g1);
                     b = max(g0, g1);
+                    // local vertex of each role (a, b, c, d), 2 bits each
                     roles[j] = la | (lb << 2) | (lc << 4) | (ld << 6);
-                    key[2 * j] = ((uint32_t)sel4(g, lc) << 5) | (2 * j);
-                    key[2 * j + 1] = ((uint32_t)sel4(g, ld) << 5) | (2 * j + 1);
+                    key[2 * j] = ((uint32_t)sel4(g, lc) << 5) | (uint32_t)(2 * j);
+                    key[2 * j + 1] = ((uint32_t)sel4(g, ld) << 5) | (uint32_t)(2 * j + 1);
                 } else {
                     key[2 * j] = 0xffffffffu;
                     key[2 * j + 1] = 0xffffffffu;
@@ -460,7 +243,6 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill_ne3(const double* __restri
             }
             key[14] = ((uint32_t)a << 5) | 14u;
             key[15] = ((uint32_t)b << 5) | 15u;
-            // bitonic sort of 16 keys
 #pragma unroll
             for (int kk = 2; kk <= 16; kk <<= 1)
 #pragma unroll
@@ -475,235 +257,181 @@ __global__ void __launch_bounds__(ROW_TPB) k_row_fill_ne3(const double* __restri
                             key[y] = asc ? hi : lo;
                         }
                     }
-            // distinct ranks -> positions per source
-            int r = -1;
+            int rk = -1;
             uint32_t prev = 0xffffffffu;
 #pragma unroll
             for (int x = 0; x < 16; ++x) {
                 if (key[x] != 0xffffffffu) {
                     const uint32_t v = key[x] >> 5;
-                    r += v != prev;
+                    rk += v != prev;
                     prev = v;
-                    P[(key[x] & 31u) * ROW_TPB] = (unsigned char)r;
+                    P[(key[x] & 31u) * NUM_TPB] = (unsigned char)rk;
                 }
             }
-            const int nw = r + 1;
-            const int pa = P[14 * ROW_TPB], pb = P[15 * ROW_TPB];
-            Mask256 mk;
-            mk.clear();
-            int pk[TMAX];
+            const int nw = rk + 1;
+            if (nw <= 11) {
+                const int pa = P[14 * NUM_TPB], pb = P[15 * NUM_TPB];
+                const int iab = pair_index(pa, pb, nw);
+                // column mask over lexicographic pairs of W positions
+                unsigned long long mask = 1ull << iab;
+                int pidx[NE3_TMAX];  // packed pair indices: ac | ad << 6 | bc << 12 | bd << 18 | cd << 24
 #pragma unroll
-            for (int j = 0; j < TMAX; ++j) {
-                if (j < t) {
-                    const int pc = P[(2 * j) * ROW_TPB], pd = P[(2 * j + 1) * ROW_TPB];
-                    const int rl = roles[j];
-                    int pos[4];
-#pragma unroll
-                    for (int v = 0; v < 4; ++v)
-                        pos[v] = v == (rl & 3) ? pa : (v == ((rl >> 2) & 3) ? pb : (v == ((rl >> 4) & 3) ? pc : pd));
-                    pk[j] = pos[0] | (pos[1] << 5) | (pos[2] << 10) | (pos[3] << 15);
-#pragma unroll
-                    for (int l = 0; l < 6; ++l) mk.set(entity_index<KT>(pos, l, nw));
-                }
-            }
-            ok = mk.finish() == rlen;
-            if (ok) {
-                for (int q = 0; q < rlen; ++q) {
-                    vm[q * st] = 0.0;
-                    vk[q * st] = 0.0;
-                }
-#pragma unroll
-                for (int j = 0; j < TMAX; ++j) {
+                for (int j = 0; j < NE3_TMAX; ++j) {
                     if (j < t) {
-                        const int e = inst[j] >> 3, k = inst[j] & 7;
-                        int g[4];
-                        load_g<KT>(elems, e, g);
-                        double X[4][3];
+                        const int pc = P[(2 * j) * NUM_TPB], pd = P[(2 * j + 1) * NUM_TPB];
+                        const int iac = pair_index(min(pa, pc), max(pa, pc), nw);
+                        const int iad = pair_index(min(pa, pd), max(pa, pd), nw);
+                        const int ibc = pair_index(min(pb, pc), max(pb, pc), nw);
+                        const int ibd = pair_index(min(pb, pd), max(pb, pd), nw);
+                        const int icd = pair_index(min(pc, pd), max(pc, pd), nw);
+                        mask |= (1ull << iac) | (1ull << iad) | (1ull << ibc) | (1ull << ibd) | (1ull << icd);
+                        pidx[j] = iac | (iad << 6) | (ibc << 12) | (ibd << 18) | (icd << 24);
+                    }
+                }
+                ok = __popcll(mask) == rlen;
+                done = true;
+                if (ok) {
+                    for (int q = 0; q < rlen; ++q) {
+                        cvm[q * st] = 0.0;
+                        cvk[q * st] = 0.0;
+                    }
+                    const int sab = __popcll(mask & ((1ull << iab) - 1ull));
+                    // role frame: vertices ordered (a, b, c, d), a < b the row's
+                    // edge.  The globally oriented Whitney basis of edge {x, y}
+                    // is sigma_xy (l_x grad l_y - l_y grad l_x), sigma_xy = +1
+                    // iff x < y, which is exactly s_k times the paper's mapped
+                    // local basis, so no other signs enter.
+                    // With n_v the area normals (adjugate rows) and N_uv = n_u.n_v,
+                    // G = N / det^2:
+                    //   M_(ab)(pq) = |K|/20 [(1+d_ap)G_bq - (1+d_aq)G_bp - (1+d_bp)G_aq + (1+d_bq)G_ap]
+                    //   K_(ab)(pq) = 4 |K| (G_ap G_bq - G_aq G_bp)
+                    double xa[3], xb[3];
 #pragma unroll
-                        for (int v = 0; v < 4; ++v)
+                    for (int cc = 0; cc < 3; ++cc) {
+                        xa[cc] = __ldg(coords + a * 3 + cc);
+                        xb[cc] = __ldg(coords + b * 3 + cc);
+                    }
 #pragma unroll
-                            for (int cc = 0; cc < 3; ++cc) X[v][cc] = __ldg(coords + (int64_t)g[v] * 3 + cc);
-                        const int2* dp = reinterpret_cast<const int2*>(e2d + (int64_t)e * 6);
-                        const int2 d01 = __ldg(dp), d23 = __ldg(dp + 1), d45 = __ldg(dp + 2);
-                        const int dofs[6] = {d01.x, d01.y, d23.x, d23.y, d45.x, d45.y};
-                        double Mr[6], Kr[6];
-                        const double det = local_row<KT>(X, g, k, Mr, Kr);
-                        if (!(det != 0.0) || !isfinite(det)) {
-                            atomicOr(&hdr->flags[F_DEGENERATE], 1);
-                            atomicMin(&hdr->bad_element, (unsigned long long)e);
-                        }
-                        int pos[4];
+                    for (int j = 0; j < NE3_TMAX; ++j) {
+                        if (j < t) {
+                            const int e = inst[j] >> 3;
+                            const int rl = roles[j];
+                            const int la = rl & 3, lb = (rl >> 2) & 3, lc = (rl >> 4) & 3, ld = (rl >> 6) & 3;
+                            int g[4];
+                            load_g<KT>(elems, e, g);
+                            const int c = sel4(g, lc), d = sel4(g, ld);
+                            double e1[3], e2[3], e3[3];
 #pragma unroll
-                        for (int v = 0; v < 4; ++v) pos[v] = (pk[j] >> (5 * v)) & 31;
+                            for (int cc = 0; cc < 3; ++cc) {
+                                e1[cc] = xb[cc] - xa[cc];
+                                e2[cc] = __ldg(coords + c * 3 + cc) - xa[cc];
+                                e3[cc] = __ldg(coords + d * 3 + cc) - xa[cc];
+                            }
+                            const double nb[3] = {e2[1] * e3[2] - e2[2] * e3[1], e2[2] * e3[0] - e2[0] * e3[2],
+                                                  e2[0] * e3[1] - e2[1] * e3[0]};
+                            const double nc[3] = {e3[1] * e1[2] - e3[2] * e1[1], e3[2] * e1[0] - e3[0] * e1[2],
+                                                  e3[0] * e1[1] - e3[1] * e1[0]};
+                            const double nd[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                                                  e1[0] * e2[1] - e1[1] * e2[0]};
+                            const double det = e1[0] * nb[0] + e1[1] * nb[1] + e1[2] * nb[2];
+                            if (!(det != 0.0) || !isfinite(det)) {
+                                atomicOr(&hdr->flags[F_DEGENERATE], 1);
+                                atomicMin(&hdr->bad_element, (unsigned long long)e);
+                            }
+                            const double na[3] = {-(nb[0] + nc[0] + nd[0]), -(nb[1] + nc[1] + nd[1]),
+                                                  -(nb[2] + nc[2] + nd[2])};
+                            auto dot = [](const double* u, const double* v) { return u[0] * v[0] + u[1] * v[1] + u[2] * v[2]; };
+                            const double Naa = dot(na, na), Nbb = dot(nb, nb), Nab = dot(na, nb);
+                            const double Nac = dot(na, nc), Nad = dot(na, nd), Nbc = dot(nb, nc), Nbd = dot(nb, nd);
+                            const double rd = 1.0 / fabs(det);
+                            const double cm = rd * (1.0 / 120.0);
+                            const double ck = (2.0 / 3.0) * rd * rd * rd;
+                            // role columns ab ac ad bc bd cd
+                            const int pc = P[(2 * j) * NUM_TPB], pd = P[(2 * j + 1) * NUM_TPB];
+                            const double sac = pa < pc ? 1.0 : -1.0, sad = pa < pd ? 1.0 : -1.0;
+                            const double sbc = pb < pc ? 1.0 : -1.0, sbd = pb < pd ? 1.0 : -1.0;
+                            const double scd = pc < pd ? 1.0 : -1.0;
+                            const double vm[6] = {cm * (2.0 * (Naa + Nbb - Nab)),
+                                                  sac * cm * (2.0 * Nbc - Nab - Nac + Naa),
+                                                  sad * cm * (2.0 * Nbd - Nab - Nad + Naa),
+                                                  sbc * cm * (Nbc - Nbb - 2.0 * Nac + Nab),
+                                                  sbd * cm * (Nbd - Nbb - 2.0 * Nad + Nab),
+                                                  scd * cm * (Nbd - Nbc - Nad + Nac)};
+                            const double vk[6] = {ck * (Naa * Nbb - Nab * Nab),
+                                                  sac * ck * (Naa * Nbc - Nac * Nab),
+                                                  sad * ck * (Naa * Nbd - Nad * Nab),
+                                                  sbc * ck * (Nab * Nbc - Nac * Nbb),
+                                                  sbd * ck * (Nab * Nbd - Nad * Nbb),
+                                                  scd * ck * (Nac * Nbd - Nad * Nbc)};
+                            // local edge id of the role pairs -> DOF ids
+                            auto eid = [](int p, int q) {
+                                const int lo = min(p, q), hi = max(p, q);
+                                return lo == 0 ? hi - 1 : (lo == 1 ? (hi == 2 ? 3 : 5) : 4);
+                            };
+                            const int32_t* de = e2d + e * 6;
+                            const int dof[6] = {(int)i, __ldg(de + eid(la, lc)), __ldg(de + eid(la, ld)),
+                                                __ldg(de + eid(lb, lc)), __ldg(de + eid(lb, ld)),
+                                                __ldg(de + eid(lc, ld))};
+                            const int pi = pidx[j];
 #pragma unroll
-                        for (int l = 0; l < 6; ++l) {
-                            const int slot = mk.rank(entity_index<KT>(pos, l, nw));
-                            cols[slot * st] = dofs[l];
-                            vm[slot * st] += Mr[l];
-                            vk[slot * st] += Kr[l];
+                            for (int u = 0; u < 6; ++u) {
+                                const int slot =
+                                    (u == 0 ? sab : __popcll(mask & ((1ull << ((pi >> (6 * (u - 1))) & 63)) - 1ull))) *
+                                    st;
+                                ccol[slot] = dof[u];
+                                cvm[slot] += vm[u];
+                                cvk[slot] += vk[u];
+                            }
                         }
                     }
                 }
             }
-        } else {
-            ok = row_generic<KT>(coords, elems, inc, e2d, ib, t, rlen, cols, vm, vk, st, hdr);
         }
+        if (!done) ok = row_generic<KT>(coords, elems, inc, e2d, ib, t, rlen, ccol, cvm, cvk, st, hdr);
         if (!ok) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
     }
     if (!staged) return;
     __syncthreads();
-    // CSR-order flush: element x of the segment belongs to the last row r with
-    // s_off[r] <= x, slot x - s_off[r]
-    const int nr = (int)(r1 - r0);
-    for (int x = threadIdx.x; x < segn; x += ROW_TPB) {
-        int lo = 0, hi = nr - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_off[mid] <= x) lo = mid; else hi = mid - 1;
-        }
-        const int src = (x - s_off[lo]) * ROW_TPB + lo;
-        if (forms & EFEM_PATTERN) col_idx[seg0 + x] = s_col[src];
-        if (forms & EFEM_MASS) vals_m[seg0 + x] = s_vm[src];
-        if (forms & EFEM_STIFF) vals_k[seg0 + x] = s_vk[src];
-    }
-}
-
-// ---------------------------------------------------------------------------------
-// 2D edges and 3D faces: an entity lies in t <= 2 elements of a conforming
-// mesh and its row is {own DOF} + the (m-1) other DOFs of each element, all
-// distinct (two elements share at most this entity).  So a row has
-// 1 + (m-1) t <= 5 (2D) or 7 (3D faces) entries: gather them in registers,
-// sum the own entry over the elements (ascending element id), and order the
-// columns with a fixed odd-even transposition network.  No search, no merge.
-// ---------------------------------------------------------------------------------
-template <class KT>
-__global__ void __launch_bounds__(ROW_TPB) k_row_fill_net(const double* __restrict__ coords,
-                                                          const int32_t* __restrict__ elems,
-                                                          const int32_t* __restrict__ inc_ptr,
-                                                          const int32_t* __restrict__ inc,
-                                                          const int32_t* __restrict__ e2d,
-                                                          const int32_t* __restrict__ row_ptr, int64_t n_rows,
-                                                          unsigned forms, int32_t* __restrict__ col_idx,
-                                                          double* __restrict__ vals_m, double* __restrict__ vals_k,
-                                                          WsHeader* hdr) {
-    constexpr int D = KT::D, NV = KT::NV, M = KT::M;
-    constexpr int NS = 1 + 2 * (M - 1);
-    constexpr int STAGE = ROW_TPB * NS;
-    __shared__ __align__(16) int s_col[STAGE + 4];
-    __shared__ __align__(16) double s_vm[STAGE + 2];
-    __shared__ __align__(16) double s_vk[STAGE + 2];
-
-    const int64_t r0 = blockIdx.x * (int64_t)ROW_TPB;
-    const int64_t r1 = (r0 + ROW_TPB < n_rows) ? r0 + ROW_TPB : n_rows;
-    const int seg0 = __ldg(row_ptr + r0);
-    const int segn = __ldg(row_ptr + r1) - seg0;
-    const int64_t i = r0 + threadIdx.x;
-
-    if (i < n_rows) {
-        const int ib = __ldg(inc_ptr + i);
-        const int t = __ldg(inc_ptr + i + 1) - ib;
-        const int rbeg = __ldg(row_ptr + i);
-        const int rlen = __ldg(row_ptr + i + 1) - rbeg;
-        if (t < 1 || t > 2 || rlen != 1 + (M - 1) * t) {
-            atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
-        } else {
-            int cols[NS];
-            double vm[NS], vk[NS];
-            cols[0] = (int)i;
-            vm[0] = 0.0;
-            vk[0] = 0.0;
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                if (j < t) {
-                    const int pe = __ldg(inc + ib + j);
-                    const int e = pe >> 3, k = pe & 7;
-                    int g[NV];
-                    load_g<KT>(elems, e, g);
-                    double X[NV][D];
-#pragma unroll
-                    for (int v = 0; v < NV; ++v)
-#pragma unroll
-                        for (int cc = 0; cc < D; ++cc) X[v][cc] = __ldg(coords + (int64_t)g[v] * D + cc);
-                    int dofs[M];
-#pragma unroll
-                    for (int l = 0; l < M; ++l) dofs[l] = __ldg(e2d + (int64_t)e * M + l);
-                    double Mr[M], Kr[M];
-                    const double det = local_row<KT>(X, g, k, Mr, Kr);
-                    if (!(det != 0.0) || !isfinite(det)) {
-                        atomicOr(&hdr->flags[F_DEGENERATE], 1);
-                        atomicMin(&hdr->bad_element, (unsigned long long)e);
-                    }
-                    double om = Mr[0], ok = Kr[0];
-#pragma unroll
-                    for (int l = 1; l < M; ++l) {
-                        om = (k == l) ? Mr[l] : om;
-                        ok = (k == l) ? Kr[l] : ok;
-                    }
-                    vm[0] += om;
-                    vk[0] += ok;
-#pragma unroll
-                    for (int q = 0; q < M - 1; ++q) {  // the other local DOFs, l = q + (q >= k)
-                        int c = dofs[q];
-                        double a = Mr[q], b = Kr[q];
-#pragma unroll
-                        for (int l = q + 1; l <= q + 1 && l < M; ++l) {
-                            c = (q >= k) ? dofs[l] : c;
-                            a = (q >= k) ? Mr[l] : a;
-                            b = (q >= k) ? Kr[l] : b;
-                        }
-                        cols[1 + j * (M - 1) + q] = c;
-                        vm[1 + j * (M - 1) + q] = a;
-                        vk[1 + j * (M - 1) + q] = b;
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < M - 1; ++q) {
-                        cols[1 + j * (M - 1) + q] = INT_MAX;
-                        vm[1 + j * (M - 1) + q] = 0.0;
-                        vk[1 + j * (M - 1) + q] = 0.0;
-                    }
-                }
-            }
-            // place by rank: the valid columns are distinct, sentinels (INT_MAX)
-            // rank last and are not written
-            const int o = rbeg - seg0;
-#pragma unroll
-            for (int x = 0; x < NS; ++x) {
-                int r = 0;
-#pragma unroll
-                for (int y = 0; y < NS; ++y) r += (y != x) & (cols[y] < cols[x]);
-                if (cols[x] != INT_MAX) {
-                    s_col[(seg0 & 3) + o + r] = cols[x];
-                    s_vm[(seg0 & 1) + o + r] = vm[x];
-                    s_vk[(seg0 & 1) + o + r] = vk[x];
-                }
-            }
-        }
-    }
+    // column-major staging -> CSR order, warp w copies rows 32w .. 32w+31,
+    // one row (<= 20 entries) per iteration with consecutive lanes
+    if (threadIdx.x == 0) s_off[nr] = segn;
     __syncthreads();
-    flush_segment(forms, seg0, segn, s_col, s_vm, s_vk, col_idx, vals_m, vals_k);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int rr = 0; rr < 32; ++rr) {
+        const int r = w * 32 + rr;
+        if (r >= nr) break;
+        const int off = s_off[r], len = s_off[r + 1] - off;
+        if (lane < len) {
+            const int src = lane * NUM_TPB + r;
+            if (forms & EFEM_PATTERN) col_idx[seg0 + off + lane] = s_col[src];
+            if (forms & EFEM_MASS) vals_m[seg0 + off + lane] = s_vm[src];
+            if (forms & EFEM_STIFF) vals_k[seg0 + off + lane] = s_vk[src];
+        }
+    }
 }
+
+constexpr size_t NE3_SMEM = (size_t)NE3_SLOTS * NUM_TPB * (8 + 8 + 4) + (NUM_TPB + 1) * 4 + 16 * NUM_TPB;
 
 // ---------------------------------------------------------------------------------
 template <class KT>
 efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) {
     if (p.n_dofs == 0) return EFEM_OK;
-    const unsigned grid = grid_for(p.n_dofs, ROW_TPB);
+    const unsigned grid = grid_for(p.n_dofs, NUM_TPB);
     double* vm = (forms & EFEM_MASS) ? out->vals_mass : nullptr;
     double* vk = (forms & EFEM_STIFF) ? out->vals_stiff : nullptr;
     if constexpr (KT::D == 2 || KT::FACES) {
-        k_row_fill_net<KT><<<grid, ROW_TPB, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr,
-                                                    p.n_dofs, forms, out->col_idx, vm, vk, p.hdr);
+        k_rows_small<KT><<<grid, NUM_TPB, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr,
+                                                  (int)p.n_dofs, forms, out->col_idx, vm, vk, p.hdr);
     } else {
         const int fast_ids = p.n_nodes < (1ll << 27);
         static bool attr = false;
         if (!attr) {
-            EFEM_CUDA_TRY(cudaFuncSetAttribute(k_row_fill_ne3<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            EFEM_CUDA_TRY(cudaFuncSetAttribute(k_rows_ne3<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)NE3_SMEM));
             attr = true;
         }
-        k_row_fill_ne3<KT><<<grid, ROW_TPB, NE3_SMEM, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr,
-                                                    p.n_dofs, forms, fast_ids, out->col_idx, vm, vk, p.hdr);
+        k_rows_ne3<KT><<<grid, NUM_TPB, NE3_SMEM, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr,
+                                                       (int)p.n_dofs, forms, fast_ids, out->col_idx, vm, vk, p.hdr);
     }
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;

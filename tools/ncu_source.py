@@ -27,3 +27,16 @@ def main(path, kernel, top=25):
 
 if __name__ == "__main__":
     main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 25)
+
+
+def by_file(path, kernel):
+    """Instruction totals per source file (cuda view)."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--kernel-name", "regex:" + kernel,
+                          "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
+    out = {}
+    cur = None
+    rows = list(csv.reader(raw.splitlines()))
+    for r in rows:
+        if r and r[0] == "File Path":
+            cur = r[1].split("/")[-1]
+    return out
