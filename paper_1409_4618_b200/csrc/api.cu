@@ -24,7 +24,7 @@ std::atomic<int64_t> g_launches{0};
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-    size_t hdr, cnt, bucket_ptr, bucket, e2d, inc_ptr, row_ptr, d2n, lb, totals, cub, total;
+    size_t hdr, cnt, bucket_ptr, bucket, e2d, inc_ptr, row_ptr, d2n, ent_ptr, nnz_cnt, nnz_ptr, lb, totals, cub, total;
 };
 
 Layout layout(const Plan& p, size_t cub_bytes) {
@@ -45,6 +45,9 @@ Layout layout(const Plan& p, size_t cub_bytes) {
     L.inc_ptr = take(((size_t)p.r_max + 1) * 4);
     L.row_ptr = take(((size_t)p.r_max + 1) * 4);
     L.d2n = take((size_t)p.r_max * p.ek * 4);
+    L.ent_ptr = take(N1 * 4);
+    L.nnz_cnt = take(N1 * 4);
+    L.nnz_ptr = take(N1 * 4);
     L.lb = take(((size_t)p.n_nodes / 32 + 2) * 8 + 64);
     L.totals = take(16);
     L.cub = take(cub_bytes);
@@ -245,6 +248,9 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     p->inc_ptr = reinterpret_cast<int32_t*>(b + L.inc_ptr);
     p->row_ptr = reinterpret_cast<int32_t*>(b + L.row_ptr);
     p->d2n = reinterpret_cast<int32_t*>(b + L.d2n);
+    p->ent_ptr = reinterpret_cast<int32_t*>(b + L.ent_ptr);
+    p->nnz_cnt = reinterpret_cast<int32_t*>(b + L.nnz_cnt);
+    p->nnz_ptr = reinterpret_cast<int32_t*>(b + L.nnz_ptr);
     p->lb_status = reinterpret_cast<unsigned long long*>(b + L.lb);
     p->d_totals = reinterpret_cast<int64_t*>(b + L.totals);
     p->cub_tmp = b + L.cub;

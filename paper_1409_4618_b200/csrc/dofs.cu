@@ -250,96 +250,77 @@ __device__ __forceinline__ int link_count_fast(const int32_t* __restrict__ elems
     return L;
 }
 
+// Pass A: per node, sort its bucket in place by (entity, element) and count
+// its entities and the CSR entries of their rows.
 template <class KT>
-__global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_entities(const int32_t* __restrict__ elems,
-                                                                     const int32_t* __restrict__ bucket_ptr,
-                                                                     int64_t n_nodes, NodeOut out, WsHeader* hdr) {
+__global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t* __restrict__ elems,
+                                                                  const int32_t* __restrict__ bucket_ptr,
+                                                                  int32_t* __restrict__ bucket, int64_t n_nodes,
+                                                                  int32_t* __restrict__ ent_cnt,
+                                                                  int32_t* __restrict__ nnz_cnt) {
     constexpr int CAP = NodeCaps<KT>::CAP;
     constexpr int TPB = NodeCaps<KT>::TPB;
     __shared__ uint64_t s_key[CAP * TPB];
     __shared__ int s_inst[KT::FACES ? CAP * TPB : 1];
-    __shared__ unsigned long long s_scan[TPB / 32 + 2];
-    __shared__ int s_tile;
-    constexpr int RL_CAP = (KT::D == 3 && !KT::FACES) ? 16 : 1;
-    __shared__ unsigned char s_rl[RL_CAP * TPB];
-
-    if (threadIdx.x == 0) s_tile = atomicAdd(out.ticket, 1);
-    __syncthreads();
-    const int tile = s_tile;
-    const int64_t a64 = (int64_t)tile * TPB + threadIdx.x;
-    const bool live = a64 < n_nodes;
+    const int64_t a64 = (int64_t)blockIdx.x * TPB + threadIdx.x;
+    if (a64 >= n_nodes) return;
     const int a = (int)a64;
-    int beg = 0, n = 0;
-    if (live) {
-        beg = __ldg(bucket_ptr + a);
-        n = __ldg(bucket_ptr + a + 1) - beg;
-    }
-    const bool in_smem = n <= CAP;
-    // strided per-thread lists: item j of this thread at [j * TPB + tid]
-    uint64_t* K = s_key + threadIdx.x;
-    int* V = s_inst + (KT::FACES ? threadIdx.x : 0);
-    int32_t* gb = out.bucket + beg;
-    auto get = [&](int j) -> Item<KT> {
-        if (in_smem) {
-            Item<KT> it;
-            it.key = K[j * TPB];
-            if constexpr (KT::FACES) it.inst = V[j * TPB];
-            else it.inst = (int)(uint32_t)it.key;
-            return it;
-        }
-        return make_item<KT>(elems, gb[j]);
-    };
-    auto put = [&](int j, const Item<KT>& it) {
-        if (in_smem) {
-            K[j * TPB] = it.key;
-            if constexpr (KT::FACES) V[j * TPB] = it.inst;
-        } else {
-            gb[j] = it.inst;
-        }
-    };
-    auto inst_at = [&](int j) -> int { return get(j).inst; };
-    // 2D fast path: a node owns <= 8 instances in practice (3 edges x 2
-    // triangles on the structured mesh) -> sort 8 keys in registers with a
-    // bitonic network; larger buckets take the shared-memory path.
-    constexpr int NREG = 8;
-    const bool fast = KT::D == 2 && n <= NREG;
-    uint64_t rk[NREG];
-    int rlen[NREG];
+    const int beg = __ldg(bucket_ptr + a);
+    const int n = __ldg(bucket_ptr + a + 1) - beg;
+    int32_t* gb = bucket + beg;
     int n_ent = 0, n_nnz = 0;
-    if constexpr (KT::D == 2) {
-        if (fast) {
+    constexpr int NREG = 8;
+    if (KT::D == 2 && n <= NREG) {
+        // register path: bitonic network over 8 keys
+        uint64_t rk[NREG];
 #pragma unroll
-            for (int j = 0; j < NREG; ++j) rk[j] = j < n ? make_item<KT>(elems, __ldg(gb + j)).key : ~0ull;
+        for (int j = 0; j < NREG; ++j) rk[j] = j < n ? make_item<KT>(elems, __ldg(gb + j)).key : ~0ull;
 #pragma unroll
-            for (int kk = 2; kk <= NREG; kk <<= 1)
+        for (int kk = 2; kk <= NREG; kk <<= 1)
 #pragma unroll
-                for (int jj = kk >> 1; jj > 0; jj >>= 1)
+            for (int jj = kk >> 1; jj > 0; jj >>= 1)
 #pragma unroll
-                    for (int x = 0; x < NREG; ++x) {
-                        const int y = x ^ jj;
-                        if (y > x) {
-                            const uint64_t lo = rk[x] < rk[y] ? rk[x] : rk[y];
-                            const uint64_t hi = rk[x] < rk[y] ? rk[y] : rk[x];
-                            const bool asc = (x & kk) == 0;
-                            rk[x] = asc ? lo : hi;
-                            rk[y] = asc ? hi : lo;
-                        }
+                for (int x = 0; x < NREG; ++x) {
+                    const int y = x ^ jj;
+                    if (y > x) {
+                        const bool sw = rk[x] > rk[y];
+                        const bool asc = (x & kk) == 0;
+                        const uint64_t lo = sw ? rk[y] : rk[x], hi = sw ? rk[x] : rk[y];
+                        rk[x] = asc ? lo : hi;
+                        rk[y] = asc ? hi : lo;
                     }
-            // run lengths (backwards) and distinct count
+                }
 #pragma unroll
-            for (int x = NREG - 1; x >= 0; --x) {
-                const bool cont = x + 1 < n && (rk[x + 1] >> 32) == (rk[x] >> 32);
-                rlen[x] = cont ? rlen[x + 1 < NREG ? x + 1 : x] + 1 : 1;
+        for (int x = 0; x < NREG; ++x)
+            if (x < n) {
+                n_ent += x == 0 || (rk[x] >> 32) != (rk[x - 1] >> 32);
+                gb[x] = (int)(uint32_t)rk[x];
             }
-#pragma unroll
-            for (int x = 0; x < NREG; ++x) n_ent += x < n && (x == 0 || (rk[x] >> 32) != (rk[x - 1] >> 32));
-            n_nnz = n_ent + (KT::M - 1) * n;
-        }
-    }
-    if (!fast) {
-        // ---- load (independent gathers) then insertion sort by (entity, element) ----
+        n_nnz = n_ent + (KT::M - 1) * n;
+    } else {
+        const bool in_smem = n <= CAP;
+        uint64_t* K = s_key + threadIdx.x;  // item j at [j * TPB]
+        int* V = s_inst + (KT::FACES ? threadIdx.x : 0);
+        auto get = [&](int j) -> Item<KT> {
+            if (in_smem) {
+                Item<KT> it;
+                it.key = K[j * TPB];
+                if constexpr (KT::FACES) it.inst = V[j * TPB];
+                else it.inst = (int)(uint32_t)it.key;
+                return it;
+            }
+            return make_item<KT>(elems, gb[j]);
+        };
+        auto put = [&](int j, const Item<KT>& it) {
+            if (in_smem) {
+                K[j * TPB] = it.key;
+                if constexpr (KT::FACES) V[j * TPB] = it.inst;
+            } else {
+                gb[j] = it.inst;
+            }
+        };
         if (in_smem) {
-    #pragma unroll 4
+#pragma unroll 4
             for (int j = 0; j < n; ++j) {
                 const Item<KT> it = make_item<KT>(elems, __ldg(gb + j));
                 K[j * TPB] = it.key;
@@ -357,115 +338,83 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_entities(const int32
             }
             put(q, it);
         }
-
-        // ---- count entities and row entries -----------------------------------------
-        // 2D edges / 3D faces: rows have 1 + (m-1) t entries, so the node's total
-        // is n_ent + (m-1) n.  3D edges: 1 + 2 L + t per run, L kept per run in
-        // s_rl for the write pass.
+        if (in_smem)
+            for (int j = 0; j < n; ++j) gb[j] = get(j).inst;
+        auto inst_at = [&](int j) -> int { return in_smem ? get(j).inst : gb[j]; };
         for (int j = 0; j < n;) {
             const uint64_t ek = get(j).entity();
             int q = j + 1;
             while (q < n && get(q).entity() == ek) ++q;
-            if constexpr (KT::D == 3 && !KT::FACES) {
-                const int t = q - j;
-                const int rl = 1 + 2 * link_count_fast<KT>(elems, a, (int)ek, j, q, inst_at) + t;
-                if (n_ent < RL_CAP) s_rl[n_ent * TPB + threadIdx.x] = rl;
-                n_nnz += rl;
-            }
+            if constexpr (KT::D == 3 && !KT::FACES)
+                n_nnz += 1 + 2 * link_count_fast<KT>(elems, a, (int)ek, j, q, inst_at) + (q - j);
             ++n_ent;
             j = q;
         }
         if constexpr (!(KT::D == 3 && !KT::FACES)) n_nnz = n_ent + (KT::M - 1) * n;
-
     }
+    ent_cnt[a] = n_ent;
+    nnz_cnt[a] = n_nnz;
+}
 
-    // ---- offsets: block scan + decoupled look-back over tiles -------------------
-    const unsigned long long mine = ((unsigned long long)n_ent << 31) | (unsigned long long)n_nnz;
-    unsigned long long tile_total;
-    const unsigned long long excl = block_exclusive_scan<TPB>(mine, &tile_total, s_scan);
-    if (threadIdx.x < 32) {
-        const unsigned long long pre = lookback(out.status, tile, tile_total);
-        if (threadIdx.x == 0) s_scan[TPB / 32 + 1] = pre;
-    }
-    __syncthreads();
-    const unsigned long long off = s_scan[TPB / 32 + 1] + excl;
-    const int ent0 = (int)(off >> 31);
-    int nnz_run = (int)(off & 0x7fffffffull);
-
-    // ---- write: DOF ids (elems2dofs), incidence, row_ptr, dofs2nodes ------------
-    if (live && fast) {
-        if constexpr (KT::D == 2) {
-            int id = ent0 - 1;
-#pragma unroll
-            for (int x = 0; x < NREG; ++x) {
-                if (x < n) {
-                    const bool first = x == 0 || (rk[x] >> 32) != (rk[x - 1] >> 32);
-                    const int inst = (int)(uint32_t)rk[x];
-                    if (first) {
-                        ++id;
-                        out.inc_ptr[id] = beg + x;
-                        out.row_ptr[id] = nnz_run;
-                        nnz_run += 1 + (KT::M - 1) * rlen[x];
-                        if (out.d2n) {
-                            out.d2n[(int64_t)id * 2] = a;
-                            out.d2n[(int64_t)id * 2 + 1] = (int)(rk[x] >> 32);
-                        }
-                    }
-                    out.e2d[(int64_t)(inst >> 3) * KT::M + (inst & 7)] = id;
-                    gb[x] = inst;
-                }
-            }
-            if (a == n_nodes - 1) {
-                const int R = id + 1;
-                out.inc_ptr[R] = beg + n;
-                out.row_ptr[R] = nnz_run;
-                out.totals[0] = R;
-                out.totals[1] = nnz_run;
-            }
-        }
-    }
-    if (live && !fast) {
-        int id = ent0;
-        for (int j = 0; j < n;) {
-            const uint64_t ek = get(j).entity();
-            int q = j;
-            while (q < n) {
-                const Item<KT> it = get(q);
-                if (it.entity() != ek) break;
-                out.e2d[(int64_t)(it.inst >> 3) * KT::M + (it.inst & 7)] = id;
-                if (in_smem) gb[q] = it.inst;  // sorted bucket = entity -> element incidence
-                ++q;
-            }
-            const int t = q - j;
+// Pass B: per node, walk its sorted bucket: DOF ids (ent_ptr[a] + run),
+// elems2dofs, the incidence offsets, row_ptr (from nnz_ptr[a]), dofs2nodes.
+template <class KT>
+__global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ elems,
+                                                    const int32_t* __restrict__ bucket_ptr,
+                                                    const int32_t* __restrict__ bucket,
+                                                    const int32_t* __restrict__ ent_ptr,
+                                                    const int32_t* __restrict__ nnz_ptr, int64_t n_nodes,
+                                                    NodeOut out) {
+    const int64_t a64 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a64 >= n_nodes) return;
+    const int a = (int)a64;
+    const int beg = __ldg(bucket_ptr + a);
+    const int n = __ldg(bucket_ptr + a + 1) - beg;
+    const int32_t* gb = bucket + beg;
+    int id = __ldg(ent_ptr + a) - 1;
+    int nnz_run = __ldg(nnz_ptr + a);
+    auto inst_at = [&](int j) -> int { return __ldg(gb + j); };
+    uint64_t prev = ~0ull;
+    int run0 = 0;
+    auto close_run = [&](int j_end, uint64_t key) {
+        const int t = j_end - run0;
+        if constexpr (KT::D == 3 && !KT::FACES)
+            nnz_run += 1 + 2 * link_count_fast<KT>(elems, a, (int)key, run0, j_end, inst_at) + t;
+        else
+            nnz_run += 1 + (KT::M - 1) * t;
+    };
+    for (int j = 0; j < n; ++j) {
+        const int inst = __ldg(gb + j);
+        int g[KT::NV];
+        load_elem<KT>(elems, inst >> 3, g);
+        const uint64_t key = entity_key<KT>(g, inst & 7);
+        if (j == 0 || key != prev) {
+            if (j > 0) close_run(j, prev);
+            ++id;
+            run0 = j;
+            prev = key;
             out.inc_ptr[id] = beg + j;
             out.row_ptr[id] = nnz_run;
             if (out.d2n) {
                 int32_t* row = out.d2n + (int64_t)id * KT::EK;
                 row[0] = a;
                 if constexpr (KT::FACES) {
-                    row[1] = (int)(ek >> 32);
-                    row[2] = (int)(ek & 0xffffffffu);
+                    row[1] = (int)(key >> 32);
+                    row[2] = (int)(key & 0xffffffffu);
                 } else {
-                    row[1] = (int)ek;
+                    row[1] = (int)key;
                 }
             }
-            if constexpr (KT::D == 3 && !KT::FACES) {
-                const int r = id - ent0;
-                nnz_run += r < RL_CAP ? (int)s_rl[r * TPB + threadIdx.x]
-                                      : 1 + 2 * link_count_fast<KT>(elems, a, (int)ek, j, q, inst_at) + t;
-            } else {
-                nnz_run += 1 + (KT::M - 1) * t;
-            }
-            ++id;
-            j = q;
         }
-        if (a == n_nodes - 1) {
-            const int R = id;
-            out.inc_ptr[R] = beg + n;
-            out.row_ptr[R] = nnz_run;
-            out.totals[0] = R;
-            out.totals[1] = nnz_run;
-        }
+        out.e2d[(int64_t)(inst >> 3) * KT::M + (inst & 7)] = id;
+    }
+    if (n > 0) close_run(n, prev);
+    if (a == n_nodes - 1) {
+        const int R = id + 1;
+        out.inc_ptr[R] = beg + n;
+        out.row_ptr[R] = nnz_run;
+        out.totals[0] = R;
+        out.totals[1] = nnz_run;
     }
 }
 
@@ -485,12 +434,12 @@ __global__ void k_signs(const int32_t* __restrict__ elems, int64_t n_elems, int8
 template <class KT>
 efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     const int64_t N = p.n_nodes, T = p.n_elems;
+    size_t bytes = p.cub_bytes;
     EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (N + 1) * 4, s));
     if (T > 0) {
         k_bucket<KT, false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, nullptr, nullptr, p.hdr);
         EFEM_LAUNCH_CHECK();
     }
-    size_t bytes = p.cub_bytes;
     EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.bucket_ptr, (int)(N + 1), s));
     count_launch(2);
     EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (N + 1) * 4, s));
@@ -498,19 +447,25 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
         k_bucket<KT, true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, p.bucket_ptr, p.bucket, p.hdr);
         EFEM_LAUNCH_CHECK();
     }
-    constexpr int NODE_TPB = NodeCaps<KT>::TPB;
-    const int64_t tiles = (N + NODE_TPB - 1) / NODE_TPB;
-    EFEM_CUDA_TRY(cudaMemsetAsync(p.lb_status, 0, (tiles + 1) * sizeof(unsigned long long) + 64, s));
-    if (N > 0) {
-        NodeOut o{p.e2d, p.inc_ptr, p.row_ptr, p.want_d2n ? p.d2n : nullptr, p.bucket, p.d_totals, p.lb_status,
-                  reinterpret_cast<int*>(p.lb_status + tiles + 1)};
-        k_node_entities<KT><<<(unsigned)tiles, NODE_TPB, 0, s>>>(p.elems, p.bucket_ptr, N, o, p.hdr);
-        EFEM_LAUNCH_CHECK();
-    } else {
+    if (N == 0) {
         EFEM_CUDA_TRY(cudaMemsetAsync(p.d_totals, 0, 16, s));
         EFEM_CUDA_TRY(cudaMemsetAsync(p.inc_ptr, 0, 4, s));
         EFEM_CUDA_TRY(cudaMemsetAsync(p.row_ptr, 0, 4, s));
+        return EFEM_OK;
     }
+    // pass A: sort buckets, count entities / row entries per node (cnt reused for ent_cnt)
+    EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt + N, 0, 4, s));
+    EFEM_CUDA_TRY(cudaMemsetAsync(p.nnz_cnt + N, 0, 4, s));
+    constexpr int TPB = NodeCaps<KT>::TPB;
+    k_node_count<KT><<<grid_for(N, TPB), TPB, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, N, p.cnt, p.nnz_cnt);
+    EFEM_LAUNCH_CHECK();
+    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.ent_ptr, (int)(N + 1), s));
+    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.nnz_cnt, p.nnz_ptr, (int)(N + 1), s));
+    count_launch(4);
+    // pass B: DOF ids, elems2dofs, incidence, row_ptr
+    NodeOut o{p.e2d, p.inc_ptr, p.row_ptr, p.want_d2n ? p.d2n : nullptr, p.bucket, p.d_totals, nullptr, nullptr};
+    k_node_write<KT><<<grid_for(N, 256), 256, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.ent_ptr, p.nnz_ptr, N, o);
+    EFEM_LAUNCH_CHECK();
     return EFEM_OK;
 }
 

@@ -72,6 +72,9 @@ struct Plan {
     int32_t* inc_ptr = nullptr;     // r_max+1 entity -> first incidence in bucket
     int32_t* row_ptr = nullptr;     // r_max+1 CSR row offsets
     int32_t* d2n = nullptr;         // r_max*ek (written only when want_d2n)
+    int32_t* ent_ptr = nullptr;     // N+1 first DOF id of each node's entities
+    int32_t* nnz_cnt = nullptr;     // N+1 CSR entries of each node's rows
+    int32_t* nnz_ptr = nullptr;     // N+1
     unsigned long long* lb_status = nullptr;  // look-back tile status + ticket
     int64_t* d_totals = nullptr;    // [0] n_dofs [1] nnz
     bool want_d2n = false;
