@@ -55,9 +55,7 @@ Layout layout(const Plan& p, size_t cub_bytes) {
     return L;
 }
 
-efem_status read_flags(Plan& p, cudaStream_t s) {
-    EFEM_CUDA_TRY(cudaMemcpyAsync(p.h_hdr, p.hdr, sizeof(WsHeader), cudaMemcpyDeviceToHost, s));
-    EFEM_CUDA_TRY(cudaStreamSynchronize(s));
+efem_status flags_status(const Plan& p) {
     const WsHeader& h = *p.h_hdr;
     if (h.flags[F_INVALID_NODE]) {
         set_error("an element references a node id outside [0, n_nodes)");
@@ -80,13 +78,61 @@ efem_status read_flags(Plan& p, cudaStream_t s) {
     return EFEM_OK;
 }
 
-efem_status reset_header(Plan& p, cudaStream_t s) {
-    static_assert(sizeof(WsHeader) <= 256, "header");
-    // small pinned-free path: memset then set bad_element
-    EFEM_CUDA_TRY(cudaMemsetAsync(p.hdr, 0, sizeof(WsHeader), s));
-    EFEM_CUDA_TRY(cudaMemsetAsync(&p.hdr->bad_element, 0xff, sizeof(unsigned long long), s));
+efem_status read_flags(Plan& p, cudaStream_t s) {
+    EFEM_CUDA_TRY(cudaMemcpyAsync(p.h_hdr, p.hdr, sizeof(WsHeader), cudaMemcpyDeviceToHost, s));
+    EFEM_CUDA_TRY(cudaStreamSynchronize(s));
+    return flags_status(p);
+}
+
+// Enumeration = ~10 dependent launches + one D2H of the header; replayed as a
+// CUDA graph (captured once on the plan's internal stream, handshaking with
+// the caller's stream through events) to cut the launch gaps.
+efem_status enumerate_graph(Plan& p, cudaStream_t s, bool* used) {
+    *used = false;
+    if (p.graph_failed || p.want_d2n) return EFEM_OK;
+    if (!p.g_enum) {
+        if (!p.gstream) {
+            if (cudaStreamCreateWithFlags(&p.gstream, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&p.ev_in, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&p.ev_out, cudaEventDisableTiming) != cudaSuccess) {
+                p.graph_failed = true;
+                cudaGetLastError();
+                return EFEM_OK;
+            }
+        }
+        cudaGraph_t graph = nullptr;
+        if (cudaStreamBeginCapture(p.gstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            p.graph_failed = true;
+            cudaGetLastError();
+            return EFEM_OK;
+        }
+        const int64_t l0 = g_launches.load();
+        efem_status st = launch_enumerate(p, p.gstream);
+        const cudaError_t ce = cudaMemcpyAsync(p.h_hdr, p.hdr, sizeof(WsHeader), cudaMemcpyDeviceToHost, p.gstream);
+        const cudaError_t ee = cudaStreamEndCapture(p.gstream, &graph);
+        p.graph_launches = g_launches.load() - l0;
+        g_launches.fetch_sub(p.graph_launches);  // counted when the graph replays
+        if (st != EFEM_OK || ce != cudaSuccess || ee != cudaSuccess ||
+            cudaGraphInstantiate(&p.g_enum, graph, 0) != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            p.g_enum = nullptr;
+            p.graph_failed = true;
+            cudaGetLastError();
+            return EFEM_OK;
+        }
+        cudaGraphDestroy(graph);
+    }
+    EFEM_CUDA_TRY(cudaEventRecord(p.ev_in, s));
+    EFEM_CUDA_TRY(cudaStreamWaitEvent(p.gstream, p.ev_in, 0));
+    EFEM_CUDA_TRY(cudaGraphLaunch(p.g_enum, p.gstream));
+    count_launch((int)p.graph_launches);
+    EFEM_CUDA_TRY(cudaEventRecord(p.ev_out, p.gstream));
+    EFEM_CUDA_TRY(cudaStreamWaitEvent(s, p.ev_out, 0));
+    EFEM_CUDA_TRY(cudaStreamSynchronize(p.gstream));
+    *used = true;
     return EFEM_OK;
 }
+
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -96,12 +142,17 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 // ------------------------------------------------------------------------------------
 efem_status run_enumerate(Plan& p, cudaStream_t s) {
     efem_status st;
-    if ((st = reset_header(p, s)) != EFEM_OK) return st;
-    if ((st = launch_enumerate(p, s)) != EFEM_OK) return st;
-    EFEM_CUDA_TRY(cudaMemcpyAsync(p.h_scalars, p.d_totals, 16, cudaMemcpyDeviceToHost, s));
-    if ((st = read_flags(p, s)) != EFEM_OK) return st;  // synchronises
-    p.n_dofs = p.h_scalars[0];
-    p.nnz = p.h_scalars[1];
+    bool used = false;
+    if ((st = enumerate_graph(p, s, &used)) != EFEM_OK) return st;
+    if (used) {
+        st = flags_status(p);
+    } else {
+        if ((st = launch_enumerate(p, s)) != EFEM_OK) return st;  // resets the header itself
+        st = read_flags(p, s);                                     // one D2H of flags + totals, synchronises
+    }
+    if (st != EFEM_OK) return st;
+    p.n_dofs = p.h_hdr->totals[0];
+    p.nnz = p.h_hdr->totals[1];
     p.enumerated = true;
     return EFEM_OK;
 }
@@ -252,9 +303,13 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     p->nnz_cnt = reinterpret_cast<int32_t*>(b + L.nnz_cnt);
     p->nnz_ptr = reinterpret_cast<int32_t*>(b + L.nnz_ptr);
     p->lb_status = reinterpret_cast<unsigned long long*>(b + L.lb);
-    p->d_totals = reinterpret_cast<int64_t*>(b + L.totals);
+    p->d_totals = reinterpret_cast<int64_t*>(&p->hdr->totals[0]);
     p->cub_tmp = b + L.cub;
     p->enumerated = p->symbolic = false;
+    if (p->g_enum) {
+        cudaGraphExecDestroy(p->g_enum);
+        p->g_enum = nullptr;
+    }
     return EFEM_OK;
 }
 
@@ -263,6 +318,10 @@ efem_status efem_plan_destroy(efem_plan plan) {
     if (!p) return EFEM_OK;
     if (p->h_scalars) cudaFreeHost(p->h_scalars);
     if (p->h_hdr) cudaFreeHost(p->h_hdr);
+    if (p->g_enum) cudaGraphExecDestroy(p->g_enum);
+    if (p->ev_in) cudaEventDestroy(p->ev_in);
+    if (p->ev_out) cudaEventDestroy(p->ev_out);
+    if (p->gstream) cudaStreamDestroy(p->gstream);
     delete p;
     return EFEM_OK;
 }

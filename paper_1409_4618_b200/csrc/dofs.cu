@@ -431,31 +431,45 @@ __global__ void k_signs(const int32_t* __restrict__ elems, int64_t n_elems, int8
 // ---------------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------------
+// header reset + zero the two counter arrays (bucket counts, fill cursors)
+__global__ void k_init(WsHeader* hdr, int32_t* __restrict__ cnt, int32_t* __restrict__ cursor, int64_t n1) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < F_NFLAGS) hdr->flags[i] = 0;
+    if (i == 0) {
+        hdr->bad_element = ~0ull;
+        hdr->totals[0] = 0;
+        hdr->totals[1] = 0;
+    }
+    if (i < n1) {
+        cnt[i] = 0;
+        cursor[i] = 0;
+    }
+}
+
 template <class KT>
 efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     const int64_t N = p.n_nodes, T = p.n_elems;
     size_t bytes = p.cub_bytes;
-    EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (N + 1) * 4, s));
+    k_init<<<grid_for(N + 1 > F_NFLAGS ? N + 1 : F_NFLAGS, 256), 256, 0, s>>>(p.hdr, p.cnt, p.nnz_cnt, N + 1);
+    EFEM_LAUNCH_CHECK();
     if (T > 0) {
         k_bucket<KT, false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, nullptr, nullptr, p.hdr);
         EFEM_LAUNCH_CHECK();
     }
     EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.bucket_ptr, (int)(N + 1), s));
     count_launch(2);
-    EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (N + 1) * 4, s));
-    if (T > 0) {
-        k_bucket<KT, true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, p.bucket_ptr, p.bucket, p.hdr);
+    if (T > 0) {  // fill cursors: nnz_cnt (zeroed by k_init, overwritten by pass A)
+        k_bucket<KT, true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.nnz_cnt, p.bucket_ptr, p.bucket,
+                                                             p.hdr);
         EFEM_LAUNCH_CHECK();
     }
     if (N == 0) {
-        EFEM_CUDA_TRY(cudaMemsetAsync(p.d_totals, 0, 16, s));
         EFEM_CUDA_TRY(cudaMemsetAsync(p.inc_ptr, 0, 4, s));
         EFEM_CUDA_TRY(cudaMemsetAsync(p.row_ptr, 0, 4, s));
         return EFEM_OK;
     }
-    // pass A: sort buckets, count entities / row entries per node (cnt reused for ent_cnt)
-    EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt + N, 0, 4, s));
-    EFEM_CUDA_TRY(cudaMemsetAsync(p.nnz_cnt + N, 0, 4, s));
+    // pass A: sort buckets, count entities / row entries per node (cnt reused
+    // for the entity counts; cnt[N] = nnz_cnt[N] = 0 from k_init)
     constexpr int TPB = NodeCaps<KT>::TPB;
     k_node_count<KT><<<grid_for(N, TPB), TPB, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, N, p.cnt, p.nnz_cnt);
     EFEM_LAUNCH_CHECK();

@@ -25,7 +25,8 @@ enum : int {
 struct WsHeader {
     int flags[F_NFLAGS];
     unsigned long long bad_element;  // atomicMin of the first degenerate element
-    long long pad[3];
+    long long totals[2];             // n_dofs, nnz (read back with the flags in one copy)
+    long long pad;
 };
 
 // ---- element kinds ------------------------------------------------------------
@@ -76,7 +77,7 @@ struct Plan {
     int32_t* nnz_cnt = nullptr;     // N+1 CSR entries of each node's rows
     int32_t* nnz_ptr = nullptr;     // N+1
     unsigned long long* lb_status = nullptr;  // look-back tile status + ticket
-    int64_t* d_totals = nullptr;    // [0] n_dofs [1] nnz
+    int64_t* d_totals = nullptr;    // == hdr->totals
     bool want_d2n = false;
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
@@ -84,6 +85,14 @@ struct Plan {
     // host pinned readback
     int64_t* h_scalars = nullptr;  // [0] n_dofs [1] nnz
     WsHeader* h_hdr = nullptr;
+
+    // CUDA graph of the enumeration sequence (captured once on an internal
+    // stream; replayed with event handshakes against the caller's stream)
+    cudaStream_t gstream = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    cudaGraphExec_t g_enum = nullptr;
+    bool graph_failed = false;
+    int64_t graph_launches = 0;
 
     // state
     bool enumerated = false, symbolic = false;
