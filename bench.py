@@ -170,7 +170,7 @@ def run_efem(args, cfg):
 
     ws, rank, local = dist_env()
     if ws > 1:
-        raise SystemExit("multi-GPU bench path not built yet (DESIGN.md: next row a6)")
+        return run_efem_dist(args, cfg)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
@@ -269,15 +269,90 @@ def run_efem(args, cfg):
         print(json.dumps(line), flush=True)
 
 
+def run_efem_dist(args, cfg):
+    """N > 1: one process per GPU, row-owned partition.  Each
+    rank builds the full mesh (untimed) and its two-hop sub-mesh (untimed
+    setup); a timed step is the rank's local enumeration, the two all_gathers
+    (per-node entity counts, per-rank nnz), globalisation and the owned-row
+    numeric kernel.  Time = max over ranks of the summed per-step device time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1409_4618_b200 import api
+    from paper_1409_4618_b200 import dist as pdist
+
+    ws, rank, local = dist_env()
+    backend = os.environ.get("EFEM_DIST_BACKEND", "nccl")
+    n_dev = torch.cuda.device_count()
+    torch.cuda.set_device(local % n_dev)
+    dev = torch.device("cuda", local % n_dev)
+    dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
+    stream = torch.cuda.current_stream()
+    coords, elems = api.build_mesh(cfg["dim"], cfg["n"], cfg["alpha"], cfg["seed"], device=dev)
+    ranges = pdist.node_ranges(coords.shape[0], ws)
+    part = pdist.PartAssembler(coords, elems, cfg["element"], *ranges[rank])
+    out = None
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(max(args.warmup, 3)):
+        out, first_row, first_nnz = pdist.assemble_rank(part, ranges, out)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = api.launch_count()
+    with ClockSampler(local % n_dev) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.fill_(k & 0xff)
+            starts[k].record(stream)
+            out, first_row, first_nnz = pdist.assemble_rank(part, ranges, out)
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    launches = api.launch_count() - l0
+    mine = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    t = torch.tensor([mine], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    T = elems.shape[0]
+    value = T * args.steps / (total_ms * 1e-3)
+    alg_bytes, _ = algorithmic_bytes(cfg)
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs") or 6650.0
+    achieved = alg_bytes / (total_ms / args.steps * 1e-3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "element": ELEMENT_NAMES[cfg["element"]], "dim": cfg["dim"],
+                       "n": cfg["n"], "jitter": cfg["alpha"], "seed": cfg["seed"], "n_elems": T,
+                       "parallelism": f"row-owned node ranges x{ws} ({backend})",
+                       "l2": "flushed between timed steps (512 MiB write)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
+                         "frac": achieved / (peak * ws), "traffic": None,
+                         "kernel": "whole step, all ranks (aggregate bandwidth vs N x peak)",
+                         "peak_source": "measured" if peaks.get("hbm_gbs") else "fallback"},
+            "e2e": {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "note": "host-buffer e2e measured at N=1 only"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=None, choices=sorted(CONFIGS),
+                    help="BASELINE config; default: 2 (configs[1]) at N=1, 5 (the scaling sweep) at N>1")
     ap.add_argument("--impl", default="efem", choices=["efem", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = 2 if dist_env()[0] == 1 else 5
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

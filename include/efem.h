@@ -173,6 +173,47 @@ efem_status efem_plan_check(efem_plan plan, efem_stream_t stream);
 efem_status efem_assemble_host(efem_plan plan, const double* h_coords, const int32_t* h_elems, efem_csr* d_out,
                                efem_csr* h_out, efem_stream_t stream);
 
+/* ---- partitioned (multi-GPU) assembly, SURVEY.md §8(e) / DESIGN.md §9 ---------------
+ * Rank r owns the rows of the entities whose minimum node lies in [node_lo,
+ * node_hi); with contiguous node ranges these are contiguous global rows, so
+ * the ranks' CSR slices concatenate to the 1-GPU matrix byte for byte.  Each
+ * rank assembles from a two-hop sub-mesh (elements touching the nodes of the
+ * elements touching its range); the exchange is an allgather of per-node
+ * entity counts (done by the caller, e.g. torch.distributed / NCCL). */
+
+/* Sub-mesh of `full` for the node range.  Call with ws == NULL to get
+ * *ws_bytes; then with ws and sub_coords == NULL (synchronising) for the
+ * sizes; then with caller-allocated sub_coords (n_sub_nodes x dim),
+ * sub_elems (n_sub_elems x (dim+1), local node ids) and sub2global
+ * (n_sub_nodes, ascending global node ids), same ws untouched in between. */
+efem_status efem_partition(const efem_mesh* full, int64_t node_lo, int64_t node_hi, void* ws, size_t* ws_bytes,
+                           int64_t* n_sub_nodes, int64_t* n_sub_elems, double* sub_coords, int32_t* sub_elems,
+                           int32_t* sub2global, efem_stream_t stream);
+
+/* After efem_assemble_symbolic on the sub-mesh plan: owned_cnt[g - node_lo] =
+ * number of entities whose minimum node is global node g (device, node_hi -
+ * node_lo ints, the rank's contribution to the allgather); info (host, 4) =
+ * {first owned local row, owned rows, local CSR offset of that row, owned CSR
+ * entries}.  Synchronising. */
+efem_status efem_part_counts(efem_plan plan, const int32_t* sub2global, int64_t node_lo, int64_t node_hi,
+                             int32_t* owned_cnt, int64_t* info, efem_stream_t stream);
+
+/* Exclusive scan of the allgathered per-node counts (n = global node count)
+ * into global_ent_ptr (n+1): the global id of node g's first entity.  ws ==
+ * NULL returns *ws_bytes. */
+efem_status efem_part_scan(const int32_t* global_cnt, int64_t n, int32_t* global_ent_ptr, void* ws, size_t* ws_bytes,
+                           efem_stream_t stream);
+
+/* elems2dofs of the sub-mesh in global DOF ids (n_sub_elems x m, device). */
+efem_status efem_part_globalize(efem_plan plan, const int32_t* sub2global, const int32_t* global_ent_ptr,
+                                int32_t* e2d_global, efem_stream_t stream);
+
+/* The owned rows as a CSR slice with global column ids: slice->row_ptr
+ * starts at 0 (add the rank's global entry offset to place it); n_rows / nnz
+ * must equal info[1] / info[3]; global_first_row = global_ent_ptr[node_lo]. */
+efem_status efem_part_numeric(efem_plan plan, unsigned forms, const int64_t* info, int64_t global_first_row,
+                              const int32_t* e2d_global, efem_csr* slice, efem_stream_t stream);
+
 /* ---- diagnostics ------------------------------------------------------------- */
 const char* efem_status_string(efem_status status);
 const char* efem_last_error(void);

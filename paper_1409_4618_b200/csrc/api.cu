@@ -14,7 +14,7 @@ namespace efem {
 // launchers defined in dofs.cu / assemble.cu
 efem_status launch_enumerate(Plan& p, cudaStream_t s);
 efem_status launch_signs(Plan& p, int8_t* out, cudaStream_t s);
-efem_status launch_rows_any(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s);
+efem_status launch_rows_any(Plan& p, unsigned forms, efem_csr* out, const RowWindow& w, cudaStream_t s);
 
 namespace {
 thread_local std::string g_last_error;
@@ -173,7 +173,13 @@ efem_status run_numeric(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) 
     if (forms & EFEM_PATTERN) {
         EFEM_CUDA_TRY(cudaMemcpyAsync(out->row_ptr, p.row_ptr, (p.n_dofs + 1) * 4, cudaMemcpyDeviceToDevice, s));
     }
-    if ((st = launch_rows_any(p, forms, out, s)) != EFEM_OK) return st;
+    RowWindow w;
+    w.row0 = 0;
+    w.n_rows = p.n_dofs;
+    w.own_base = 0;
+    w.out_base = 0;
+    w.e2d = p.e2d;
+    if ((st = launch_rows_any(p, forms, out, w, s)) != EFEM_OK) return st;
     return EFEM_OK;
 }
 

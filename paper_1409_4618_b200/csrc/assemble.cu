@@ -29,6 +29,7 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_small(const double* __restrict
                                                         const int32_t* __restrict__ inc,
                                                         const int32_t* __restrict__ e2d,
                                                         const int32_t* __restrict__ row_ptr, int n_rows,
+                                                        int own_base, int out_base,
                                                         unsigned forms, int32_t* __restrict__ col_idx,
                                                         double* __restrict__ vals_m, double* __restrict__ vals_k,
                                                         WsHeader* hdr) {
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_small(const double* __restrict
         } else {
             int cl[NS];
             double am[NS], ak[NS];
-            cl[0] = i;
+            cl[0] = own_base + i;
             am[0] = 0.0;
             ak[0] = 0.0;
             // all loads of both elements first (element 1 duplicates element 0
@@ -132,9 +133,10 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_small(const double* __restrict
     for (int u = 0; u < NS; ++u) {
         const int x = u * NUM_TPB + (int)threadIdx.x;
         if (x < segn) {
-            if (forms & EFEM_PATTERN) col_idx[seg0 + x] = s_col[x];
-            if (forms & EFEM_MASS) vals_m[seg0 + x] = s_vm[x];
-            if (forms & EFEM_STIFF) vals_k[seg0 + x] = s_vk[x];
+            const int gx = seg0 - out_base + x;
+            if (forms & EFEM_PATTERN) col_idx[gx] = s_col[x];
+            if (forms & EFEM_MASS) vals_m[gx] = s_vm[x];
+            if (forms & EFEM_STIFF) vals_k[gx] = s_vk[x];
         }
     }
 }
@@ -168,6 +170,7 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
                                                       const int32_t* __restrict__ inc,
                                                       const int32_t* __restrict__ e2d,
                                                       const int32_t* __restrict__ row_ptr, int n_rows,
+                                                      int own_base, int out_base,
                                                       unsigned forms, int fast_ids, int32_t* __restrict__ col_idx,
                                                       double* __restrict__ vals_m, double* __restrict__ vals_k,
                                                       WsHeader* hdr) {
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
             cvk = s_vk + threadIdx.x;
             st = NUM_TPB;
         } else {  // an oversize row in the tile: accumulate in place in global memory
-            const int rb = s_off[threadIdx.x] + seg0;
+            const int rb = s_off[threadIdx.x] + seg0 - out_base;
             ccol = col_idx + rb;
             cvm = vals_m ? vals_m + rb : s_vm + threadIdx.x;
             cvk = vals_k ? vals_k + rb : s_vk + threadIdx.x;
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
                                 return lo == 0 ? hi - 1 : (lo == 1 ? (hi == 2 ? 3 : 5) : 4);
                             };
                             const int32_t* de = e2d + e * 6;
-                            const int dof[6] = {(int)i, __ldg(de + eid(la, lc)), __ldg(de + eid(la, ld)),
+                            const int dof[6] = {own_base + i, __ldg(de + eid(la, lc)), __ldg(de + eid(la, ld)),
                                                 __ldg(de + eid(lb, lc)), __ldg(de + eid(lb, ld)),
                                                 __ldg(de + eid(lc, ld))};
                             const int pi = pidx[j];
@@ -403,9 +406,10 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
         const int off = s_off[r], len = s_off[r + 1] - off;
         if (lane < len) {
             const int src = lane * NUM_TPB + r;
-            if (forms & EFEM_PATTERN) col_idx[seg0 + off + lane] = s_col[src];
-            if (forms & EFEM_MASS) vals_m[seg0 + off + lane] = s_vm[src];
-            if (forms & EFEM_STIFF) vals_k[seg0 + off + lane] = s_vk[src];
+            const int gx = seg0 - out_base + off + lane;
+            if (forms & EFEM_PATTERN) col_idx[gx] = s_col[src];
+            if (forms & EFEM_MASS) vals_m[gx] = s_vm[src];
+            if (forms & EFEM_STIFF) vals_k[gx] = s_vk[src];
         }
     }
 }
@@ -414,14 +418,16 @@ constexpr size_t NE3_SMEM = (size_t)NE3_SLOTS * NUM_TPB * (8 + 8 + 4) + (NUM_TPB
 
 // ---------------------------------------------------------------------------------
 template <class KT>
-efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) {
-    if (p.n_dofs == 0) return EFEM_OK;
-    const unsigned grid = grid_for(p.n_dofs, NUM_TPB);
+efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow& w, cudaStream_t s) {
+    if (w.n_rows == 0) return EFEM_OK;
+    const unsigned grid = grid_for(w.n_rows, NUM_TPB);
     double* vm = (forms & EFEM_MASS) ? out->vals_mass : nullptr;
     double* vk = (forms & EFEM_STIFF) ? out->vals_stiff : nullptr;
+    const int32_t* inc_ptr = p.inc_ptr + w.row0;
+    const int32_t* row_ptr = p.row_ptr + w.row0;
     if constexpr (KT::D == 2 || KT::FACES) {
-        k_rows_small<KT><<<grid, NUM_TPB, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr,
-                                                  (int)p.n_dofs, forms, out->col_idx, vm, vk, p.hdr);
+        k_rows_small<KT><<<grid, NUM_TPB, 0, s>>>(p.coords, p.elems, inc_ptr, p.bucket, w.e2d, row_ptr, (int)w.n_rows,
+                                                  w.own_base, w.out_base, forms, out->col_idx, vm, vk, p.hdr);
     } else {
         const int fast_ids = p.n_nodes < (1ll << 27);
         static bool attr = false;
@@ -430,18 +436,19 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) 
                                                (int)NE3_SMEM));
             attr = true;
         }
-        k_rows_ne3<KT><<<grid, NUM_TPB, NE3_SMEM, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.e2d, p.row_ptr,
-                                                       (int)p.n_dofs, forms, fast_ids, out->col_idx, vm, vk, p.hdr);
+        k_rows_ne3<KT><<<grid, NUM_TPB, NE3_SMEM, s>>>(p.coords, p.elems, inc_ptr, p.bucket, w.e2d, row_ptr,
+                                                       (int)w.n_rows, w.own_base, w.out_base, forms, fast_ids,
+                                                       out->col_idx, vm, vk, p.hdr);
     }
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;
 }
 
-efem_status launch_rows_any(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) {
-    if (p.dim == 2) return p.element == EFEM_RT0 ? launch_rows<Kind<2, EFEM_RT0>>(p, forms, out, s)
-                                                 : launch_rows<Kind<2, EFEM_NED0>>(p, forms, out, s);
-    return p.element == EFEM_RT0 ? launch_rows<Kind<3, EFEM_RT0>>(p, forms, out, s)
-                                 : launch_rows<Kind<3, EFEM_NED0>>(p, forms, out, s);
+efem_status launch_rows_any(Plan& p, unsigned forms, efem_csr* out, const RowWindow& w, cudaStream_t s) {
+    if (p.dim == 2) return p.element == EFEM_RT0 ? launch_rows<Kind<2, EFEM_RT0>>(p, forms, out, w, s)
+                                                 : launch_rows<Kind<2, EFEM_NED0>>(p, forms, out, w, s);
+    return p.element == EFEM_RT0 ? launch_rows<Kind<3, EFEM_RT0>>(p, forms, out, w, s)
+                                 : launch_rows<Kind<3, EFEM_NED0>>(p, forms, out, w, s);
 }
 
 }  // namespace efem

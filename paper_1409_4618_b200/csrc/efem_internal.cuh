@@ -99,6 +99,15 @@ struct Plan {
     int64_t n_dofs = 0, nnz = 0;
 };
 
+// Rows [row0, row0 + n_rows) of a plan, written to a CSR whose entry 0 is the
+// plan's entry row_ptr[row0] = out_base; own DOF of local row i is
+// own_base + i; column ids from e2d (local or globalised).
+struct RowWindow {
+    int64_t row0 = 0, n_rows = 0;
+    int own_base = 0, out_base = 0;
+    const int32_t* e2d = nullptr;
+};
+
 // ---- error plumbing --------------------------------------------------------------
 void set_error(const std::string& msg);
 void set_bad_element(int64_t e);

@@ -1,0 +1,195 @@
+"""Row-owned partitioned assembly over several GPUs (SURVEY.md §8(e),
+DESIGN.md §9).  Argument marshalling around the efem_part_* C-ABI calls plus
+the two torch.distributed collectives of the method:
+
+  1. all_gather of the per-node entity counts of every rank's node range
+     (-> global DOF offsets), and
+  2. all_gather of every rank's CSR entry count (-> its row-block offset).
+
+No matrix values cross ranks (owner computes): rank r assembles the rows of
+the entities whose minimum node lies in its node range from a two-hop
+sub-mesh.  Concatenating the ranks' slices in rank order gives the 1-GPU CSR
+byte for byte.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .api import ALL, CSR, Assembler, _ptr, _stream
+
+
+def node_ranges(n_nodes: int, world: int):
+    """Contiguous, near-equal node ranges [lo, hi) per rank."""
+    cuts = [(n_nodes * r) // world for r in range(world + 1)]
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def offsets_from_counts(counts):
+    """Exclusive prefix of per-rank counts (host ints)."""
+    out, run = [], 0
+    for c in counts:
+        out.append(run)
+        run += int(c)
+    return out, run
+
+
+class PartAssembler:
+    """One rank's share: sub-mesh plan + globalisation + owned-row numeric."""
+
+    def __init__(self, coords: torch.Tensor, elems: torch.Tensor, element: int, lo: int, hi: int, stream=None):
+        L = _lib.load()
+        self.lo, self.hi = int(lo), int(hi)
+        self.n_global_nodes = int(coords.shape[0])
+        dim = int(coords.shape[1])
+        self.device = coords.device
+        full = _lib.efem_mesh(dim, coords.shape[0], elems.shape[0], coords.data_ptr(), elems.data_ptr())
+        ws_bytes = ctypes.c_size_t()
+        nn, ne = ctypes.c_int64(), ctypes.c_int64()
+        with torch.cuda.device(self.device):
+            _lib.check("efem_partition", L.efem_partition(ctypes.byref(full), self.lo, self.hi, None,
+                                                          ctypes.byref(ws_bytes), None, None, None, None, None,
+                                                          _stream(stream)))
+            ws = torch.empty(max(ws_bytes.value, 256), dtype=torch.uint8, device=self.device)
+            _lib.check("efem_partition", L.efem_partition(ctypes.byref(full), self.lo, self.hi, _ptr(ws),
+                                                          ctypes.byref(ws_bytes), ctypes.byref(nn),
+                                                          ctypes.byref(ne), None, None, None, _stream(stream)))
+            self.sub_coords = torch.empty((nn.value, dim), dtype=torch.float64, device=self.device)
+            self.sub_elems = torch.empty((ne.value, dim + 1), dtype=torch.int32, device=self.device)
+            self.sub2global = torch.empty(nn.value, dtype=torch.int32, device=self.device)
+            _lib.check("efem_partition", L.efem_partition(ctypes.byref(full), self.lo, self.hi, _ptr(ws),
+                                                          ctypes.byref(ws_bytes), ctypes.byref(nn),
+                                                          ctypes.byref(ne), _ptr(self.sub_coords),
+                                                          _ptr(self.sub_elems), _ptr(self.sub2global),
+                                                          _stream(stream)))
+        del ws
+        self.asm = Assembler(self.sub_coords, self.sub_elems, element)
+        self.owned_cnt = torch.empty(max(self.hi - self.lo, 1), dtype=torch.int32, device=self.device)
+        self.info = (ctypes.c_int64 * 4)()
+        self.e2d_global = torch.empty(max(self.sub_elems.shape[0] * self.asm.m, 1), dtype=torch.int32,
+                                      device=self.device)
+        self.global_ent_ptr = torch.empty(self.n_global_nodes + 1, dtype=torch.int32, device=self.device)
+        scan_bytes = ctypes.c_size_t()
+        _lib.check("efem_part_scan", L.efem_part_scan(None, self.n_global_nodes, None, None,
+                                                      ctypes.byref(scan_bytes), None))
+        self.scan_ws = torch.empty(max(scan_bytes.value, 256), dtype=torch.uint8, device=self.device)
+        self.first_row = 0
+
+    @property
+    def owned_rows(self):
+        return int(self.info[1])
+
+    @property
+    def owned_nnz(self):
+        return int(self.info[3])
+
+    def symbolic(self, stream=None):
+        """Local enumeration; returns this rank's per-node entity counts."""
+        L = _lib.load()
+        self.asm.symbolic(stream=stream)
+        with torch.cuda.device(self.device):
+            _lib.check("efem_part_counts", L.efem_part_counts(self.asm._plan, _ptr(self.sub2global), self.lo,
+                                                              self.hi, _ptr(self.owned_cnt), self.info,
+                                                              _stream(stream)))
+        return self.owned_cnt[: self.hi - self.lo]
+
+    def globalize(self, global_cnt: torch.Tensor, stream=None):
+        """global_cnt: per-node entity counts of ALL nodes (device int32)."""
+        L = _lib.load()
+        b = ctypes.c_size_t(self.scan_ws.numel())
+        with torch.cuda.device(self.device):
+            _lib.check("efem_part_scan", L.efem_part_scan(_ptr(global_cnt), self.n_global_nodes,
+                                                          _ptr(self.global_ent_ptr), _ptr(self.scan_ws),
+                                                          ctypes.byref(b), _stream(stream)))
+            _lib.check("efem_part_globalize", L.efem_part_globalize(self.asm._plan, _ptr(self.sub2global),
+                                                                    _ptr(self.global_ent_ptr),
+                                                                    _ptr(self.e2d_global), _stream(stream)))
+        self.first_row = int(self.global_ent_ptr[self.lo].item())
+        return self.first_row
+
+    def alloc_slice(self) -> CSR:
+        dev = self.device
+        return CSR(torch.empty(self.owned_rows + 1, dtype=torch.int32, device=dev),
+                   torch.empty(self.owned_nnz, dtype=torch.int32, device=dev),
+                   torch.empty(self.owned_nnz, dtype=torch.float64, device=dev),
+                   torch.empty(self.owned_nnz, dtype=torch.float64, device=dev))
+
+    def numeric(self, out: CSR, forms: int = ALL, stream=None):
+        L = _lib.load()
+        c = _lib.efem_csr(self.owned_rows, self.owned_nnz, out.row_ptr.data_ptr(), out.col_idx.data_ptr(),
+                          out.vals_M.data_ptr(), out.vals_K.data_ptr())
+        with torch.cuda.device(self.device):
+            _lib.check("efem_part_numeric", L.efem_part_numeric(self.asm._plan, forms, self.info, self.first_row,
+                                                                _ptr(self.e2d_global), ctypes.byref(c),
+                                                                _stream(stream)))
+        return out
+
+    def check(self, stream=None):
+        self.asm.check(stream=stream)
+
+
+def _comm_device(t: torch.Tensor, group=None):
+    """NCCL gathers device tensors directly; gloo (CPU tests, or several
+    ranks sharing one GPU) goes through host copies."""
+    import torch.distributed as dist
+
+    return t.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+
+def allgather_counts(owned: torch.Tensor, ranges, group=None) -> torch.Tensor:
+    """Collective 1: every rank's per-node counts -> counts of all nodes."""
+    import torch.distributed as dist
+
+    dev = _comm_device(owned, group)
+    width = max(hi - lo for lo, hi in ranges)
+    buf = torch.zeros(width, dtype=torch.int32, device=dev)
+    buf[: owned.numel()] = owned.to(dev)
+    parts = [torch.empty_like(buf) for _ in ranges]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([p[: hi - lo] for p, (lo, hi) in zip(parts, ranges)]).to(owned.device)
+
+
+def allgather_nnz(nnz: int, device, group=None):
+    """Collective 2: every rank's CSR entry count."""
+    import torch.distributed as dist
+
+    t = torch.tensor([nnz], dtype=torch.int64, device=device)
+    dev = _comm_device(t, group)
+    t = t.to(dev)
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, t, group=group)
+    return [int(p.item()) for p in parts]
+
+
+def assemble_rank(part: PartAssembler, ranges, out: CSR | None = None, group=None, stream=None):
+    """One rank's full step: local symbolic, the two collectives, numeric.
+    Returns (slice CSR, first global row, first global CSR entry)."""
+    import torch.distributed as dist
+
+    owned = part.symbolic(stream=stream)
+    global_cnt = allgather_counts(owned, ranges, group=group)
+    part.globalize(global_cnt, stream=stream)
+    nnzs = allgather_nnz(part.owned_nnz, owned.device, group=group)
+    offs, _ = offsets_from_counts(nnzs)
+    if out is None or out.nnz != part.owned_nnz or out.n_rows != part.owned_rows:
+        out = part.alloc_slice()
+    part.numeric(out, stream=stream)
+    part.check(stream=stream)
+    return out, part.first_row, offs[dist.get_rank(group)]
+
+
+def concat_slices(slices, entry_offsets):
+    """Host-side concatenation of rank slices (row_ptr shifted by the entry
+    offsets) -> numpy CSR arrays, for checking against the 1-GPU result."""
+    rp = [np.zeros(1, np.int64)]
+    ci, vm, vk = [], [], []
+    for s, off in zip(slices, entry_offsets):
+        r = s.row_ptr.cpu().numpy().astype(np.int64)
+        rp.append(r[1:] + off)
+        ci.append(s.col_idx.cpu().numpy())
+        vm.append(s.vals_M.cpu().numpy())
+        vk.append(s.vals_K.cpu().numpy())
+    return (np.concatenate(rp), np.concatenate(ci), np.concatenate(vm), np.concatenate(vk))

@@ -1,0 +1,87 @@
+"""Partitioned (multi-GPU) path on ONE GPU: the P ranks run one after another
+in this process (no rank waits on another -- the collectives are replaced by
+in-process concatenation, which is what all_gather returns).  The ranks'
+slices must concatenate to the 1-GPU CSR byte for byte (same DOF numbering,
+same per-row summation order)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as ora
+from workloads import NED0, RT0
+
+pytestmark = pytest.mark.gpu
+
+KINDS = [(2, RT0), (2, NED0), (3, RT0), (3, NED0)]
+KIND_IDS = ["rt0_2d", "ne0_2d", "rt0_3d", "ne0_3d"]
+
+
+def _emulate(coords, elems, element, P):
+    from paper_1409_4618_b200 import dist
+
+    ranges = dist.node_ranges(coords.shape[0], P)
+    parts = [dist.PartAssembler(coords, elems, element, lo, hi) for lo, hi in ranges]
+    owned = [p.symbolic() for p in parts]
+    global_cnt = torch.cat(owned)  # == all_gather of the owned counts
+    for p in parts:
+        p.globalize(global_cnt)
+    offs, total = dist.offsets_from_counts([p.owned_nnz for p in parts])
+    slices = []
+    for p in parts:
+        s = p.alloc_slice()
+        p.numeric(s)
+        p.check()
+        slices.append(s)
+    return parts, slices, offs, total
+
+
+@pytest.mark.parametrize("dim,element", KINDS, ids=KIND_IDS)
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_partitioned_equals_single(dim, element, P):
+    from paper_1409_4618_b200 import api, dist
+
+    n = 24 if dim == 2 else 6
+    coords, elems = api.build_mesh(dim, n, 0.2 if dim == 2 else 0.15, 17)
+    one = api.Assembler(coords, elems, element).assemble()
+    parts, slices, offs, total = _emulate(coords, elems, element, P)
+    assert total == one.nnz
+    rp, ci, vm, vk = dist.concat_slices(slices, offs)
+    assert np.array_equal(rp, one.row_ptr.cpu().numpy())
+    assert np.array_equal(ci, one.col_idx.cpu().numpy())
+    assert np.array_equal(vm, one.vals_M.cpu().numpy())  # bitwise: same summation order
+    assert np.array_equal(vk, one.vals_K.cpu().numpy())
+    # the ranks' first rows tile [0, R)
+    firsts = [p.first_row for p in parts]
+    assert firsts[0] == 0 and sorted(firsts) == firsts
+    assert sum(p.owned_rows for p in parts) == one.n_rows
+
+
+def test_partitioned_config5_against_oracle_rows():
+    """BASELINE config 5 (the scaling sweep) split 8 ways; sampled rows of
+    the concatenation against the oracle."""
+    from paper_1409_4618_b200 import api, dist
+    from workloads import CONFIGS
+
+    C = CONFIGS[5]
+    coords, elems = api.build_mesh(C["dim"], C["n"], C["alpha"], C["seed"])
+    parts, slices, offs, total = _emulate(coords, elems, C["element"], 8)
+    one = api.Assembler(coords, elems, C["element"])
+    d2n, _, _ = one.enumerate_dofs()
+    rp, ci, vm, vk = dist.concat_slices(slices, offs)
+    full = one.assemble()
+    assert np.array_equal(rp, full.row_ptr.cpu().numpy())
+    assert np.array_equal(ci, full.col_idx.cpu().numpy())
+    assert np.array_equal(vm, full.vals_M.cpu().numpy()) and np.array_equal(vk, full.vals_K.cpu().numpy())
+    # a few rows at the rank boundaries against the oracle
+    rows = []
+    for p in parts:
+        rows += [p.first_row, max(p.first_row - 1, 0), p.first_row + 1]
+    rows = np.unique(np.array(rows))
+    d2n_h = d2n.cpu().numpy()
+    res = ora.rows_by_entity(2, C["element"], coords.cpu().numpy(), elems.cpu().numpy(), d2n_h[rows])
+    for r, (cols, m, k) in zip(rows, res):
+        lo, hi = rp[r], rp[r + 1]
+        assert np.array_equal(d2n_h[ci[lo:hi]], cols[:, :2])
+        scale = np.abs(m).max()
+        assert np.abs(vm[lo:hi] - m).max() <= 1e-12 * scale
+        assert np.abs(vk[lo:hi] - k).max() <= 1e-12 * np.abs(k).max()
