@@ -114,13 +114,20 @@ __device__ __forceinline__ double local_row(const double (&X)[KT::NV][KT::D], co
             Kr[l] = ss * ck * (A[p] * B[q] - A[q] * B[p]);
         }
     } else {
-        // RT0 2D/3D and NE0 2D: y_a = x_a - centroid
+        // RT0 2D/3D and NE0 2D: y_a = x_a - centroid, formed from the edge
+        // vectors x_a - x_0 (exact differences of neighbouring coordinates) so
+        // that no O(1) coordinate is rounded at the O(h) scale of y
+        double ev[NV][D];
         double cen[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
+            ev[0][c] = 0.0;
             double acc = 0.0;
 #pragma unroll
-            for (int v = 0; v < NV; ++v) acc += X[v][c];
+            for (int v = 1; v < NV; ++v) {
+                ev[v][c] = X[v][c] - X[0][c];
+                acc += ev[v][c];
+            }
             cen[c] = acc * (1.0 / NV);
         }
         double y[NV][D];
@@ -129,7 +136,7 @@ __device__ __forceinline__ double local_row(const double (&X)[KT::NV][KT::D], co
         for (int v = 0; v < NV; ++v)
 #pragma unroll
             for (int c = 0; c < D; ++c) {
-                y[v][c] = X[v][c] - cen[c];
+                y[v][c] = ev[v][c] - cen[c];
                 sq += y[v][c] * y[v][c];
             }
         const double Q = sq * (1.0 / ((D + 1) * (D + 2)));
