@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_small(const double* __restrict
 // q * NUM_TPB + r: bank-conflict free) and flushed in CSR order.  Rows that
 // miss the fast-path limits use row_generic (any shape, 256-bit masks).
 // ---------------------------------------------------------------------------------
-constexpr int NE3_SLOTS = 20;
+constexpr int NE3_SLOTS = 19;  // staged row length cap (Kuhn max: 19)
+constexpr int NE3_LD = NUM_TPB + 1;  // padded column-major stride
 constexpr int NE3_TMAX = 7;
 
 __device__ __forceinline__ int pair_index(int p, int q, int nw) {  // p < q
@@ -177,10 +178,11 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
     static_assert(KT::D == 3 && !KT::FACES, "NE0 3D only");
     extern __shared__ __align__(16) unsigned char ne3_smem[];
     double* s_vm = reinterpret_cast<double*>(ne3_smem);
-    double* s_vk = s_vm + NE3_SLOTS * NUM_TPB;
-    int* s_col = reinterpret_cast<int*>(s_vk + NE3_SLOTS * NUM_TPB);
-    int* s_off = s_col + NE3_SLOTS * NUM_TPB;  // NUM_TPB + 1 row offsets
-    unsigned char* s_pos = reinterpret_cast<unsigned char*>(s_off + NUM_TPB + 1);  // 16 per thread
+    double* s_vk = s_vm + NE3_SLOTS * NE3_LD;
+    int* s_col = reinterpret_cast<int*>(s_vk + NE3_SLOTS * NE3_LD);
+    int* s_off = s_col + NE3_SLOTS * NE3_LD;  // NUM_TPB + 1 row offsets
+    unsigned short* s_map = reinterpret_cast<unsigned short*>(s_off + NUM_TPB + 1);  // CSR position -> slot
+    unsigned char* s_pos = reinterpret_cast<unsigned char*>(s_map + NE3_SLOTS * NUM_TPB);  // 16 per thread
 
     const int r0 = blockIdx.x * NUM_TPB;
     const int nr = min(NUM_TPB, n_rows - r0);
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
             ccol = s_col + threadIdx.x;
             cvm = s_vm + threadIdx.x;
             cvk = s_vk + threadIdx.x;
-            st = NUM_TPB;
+            st = NE3_LD;
         } else {  // an oversize row in the tile: accumulate in place in global memory
             const int rb = s_off[threadIdx.x] + seg0 - out_base;
             ccol = col_idx + rb;
@@ -392,29 +394,25 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
         }
         if (!done) ok = row_generic<KT>(coords, elems, inc, e2d, ib, t, rlen, ccol, cvm, cvk, st, hdr);
         if (!ok) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
+        if (staged) {
+            const int off = s_off[threadIdx.x];
+            for (int q = 0; q < rlen; ++q) s_map[off + q] = (unsigned short)(q * NE3_LD + threadIdx.x);
+        }
     }
     if (!staged) return;
     __syncthreads();
-    // column-major staging -> CSR order, warp w copies rows 32w .. 32w+31,
-    // one row (<= 20 entries) per iteration with consecutive lanes
-    if (threadIdx.x == 0) s_off[nr] = segn;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int rr = 0; rr < 32; ++rr) {
-        const int r = w * 32 + rr;
-        if (r >= nr) break;
-        const int off = s_off[r], len = s_off[r + 1] - off;
-        if (lane < len) {
-            const int src = lane * NUM_TPB + r;
-            const int gx = seg0 - out_base + off + lane;
-            if (forms & EFEM_PATTERN) col_idx[gx] = s_col[src];
-            if (forms & EFEM_MASS) vals_m[gx] = s_vm[src];
-            if (forms & EFEM_STIFF) vals_k[gx] = s_vk[src];
-        }
+    // coalesced flush in CSR order through the position -> slot map
+    for (int x = threadIdx.x; x < segn; x += NUM_TPB) {
+        const int src = s_map[x];
+        const int gx = seg0 - out_base + x;
+        if (forms & EFEM_PATTERN) col_idx[gx] = s_col[src];
+        if (forms & EFEM_MASS) vals_m[gx] = s_vm[src];
+        if (forms & EFEM_STIFF) vals_k[gx] = s_vk[src];
     }
 }
 
-constexpr size_t NE3_SMEM = (size_t)NE3_SLOTS * NUM_TPB * (8 + 8 + 4) + (NUM_TPB + 1) * 4 + 16 * NUM_TPB;
+constexpr size_t NE3_SMEM = (size_t)NE3_SLOTS * NE3_LD * (8 + 8 + 4) + (NUM_TPB + 1) * 4 +
+                            (size_t)NE3_SLOTS * NUM_TPB * 2 + 16 * NUM_TPB;
 
 // ---------------------------------------------------------------------------------
 template <class KT>
