@@ -221,30 +221,33 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
             uint32_t key[16];
             int inst[NE3_TMAX], roles[NE3_TMAX];
             int a = 0, b = 0;
+            // all index loads first, then all element loads: two round trips
+            // (slots j >= t repeat the last incidence and are masked below)
+#pragma unroll
+            for (int j = 0; j < NE3_TMAX; ++j) inst[j] = __ldg(inc + ib + min(j, t - 1));
+            int4 gq[NE3_TMAX];
+#pragma unroll
+            for (int j = 0; j < NE3_TMAX; ++j) gq[j] = __ldg(reinterpret_cast<const int4*>(elems) + (inst[j] >> 3));
 #pragma unroll
             for (int j = 0; j < NE3_TMAX; ++j) {
-                if (j < t) {
-                    const int pe = __ldg(inc + ib + j);
-                    inst[j] = pe;
-                    const int k = pe & 7;
-                    int g[4];
-                    load_g<KT>(elems, pe >> 3, g);
-                    const int s0 = k < 3 ? 0 : (k == 3 ? 1 : (k == 4 ? 2 : 3));
-                    const int s1 = k < 3 ? k + 1 : (k == 3 ? 2 : (k == 4 ? 3 : 1));
-                    const int lc = k == 0 ? 2 : (k == 1 ? 1 : (k == 2 ? 1 : 0));
-                    const int ld = k == 0 ? 3 : (k == 1 ? 3 : (k == 2 ? 2 : (k == 3 ? 3 : (k == 4 ? 1 : 2))));
-                    const int g0 = sel4(g, s0), g1 = sel4(g, s1);
-                    const int la = g0 < g1 ? s0 : s1, lb = g0 < g1 ? s1 : s0;
+                const int pe = inst[j];
+                const int k = pe & 7;
+                const int g[4] = {gq[j].x, gq[j].y, gq[j].z, gq[j].w};
+                const int s0 = k < 3 ? 0 : (k == 3 ? 1 : (k == 4 ? 2 : 3));
+                const int s1 = k < 3 ? k + 1 : (k == 3 ? 2 : (k == 4 ? 3 : 1));
+                const int lc = k == 0 ? 2 : (k == 1 ? 1 : (k == 2 ? 1 : 0));
+                const int ld = k == 0 ? 3 : (k == 1 ? 3 : (k == 2 ? 2 : (k == 3 ? 3 : (k == 4 ? 1 : 2))));
+                const int g0 = sel4(g, s0), g1 = sel4(g, s1);
+                const int la = g0 < g1 ? s0 : s1, lb = g0 < g1 ? s1 : s0;
+                if (j == 0) {
                     a = min(g0, g1);
                     b = max(g0, g1);
-                    // local vertex of each role (a, b, c, d), 2 bits each
-                    roles[j] = la | (lb << 2) | (lc << 4) | (ld << 6);
-                    key[2 * j] = ((uint32_t)sel4(g, lc) << 5) | (uint32_t)(2 * j);
-                    key[2 * j + 1] = ((uint32_t)sel4(g, ld) << 5) | (uint32_t)(2 * j + 1);
-                } else {
-                    key[2 * j] = 0xffffffffu;
-                    key[2 * j + 1] = 0xffffffffu;
                 }
+                // local vertex of each role (a, b, c, d), 2 bits each
+                roles[j] = la | (lb << 2) | (lc << 4) | (ld << 6);
+                const bool live = j < t;
+                key[2 * j] = live ? (((uint32_t)sel4(g, lc) << 5) | (uint32_t)(2 * j)) : 0xffffffffu;
+                key[2 * j + 1] = live ? (((uint32_t)sel4(g, ld) << 5) | (uint32_t)(2 * j + 1)) : 0xffffffffu;
             }
             key[14] = ((uint32_t)a << 5) | 14u;
             key[15] = ((uint32_t)b << 5) | 15u;
