@@ -3,6 +3,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -89,7 +90,7 @@ efem_status read_flags(Plan& p, cudaStream_t s) {
 // the caller's stream through events) to cut the launch gaps.
 efem_status enumerate_graph(Plan& p, cudaStream_t s, bool* used) {
     *used = false;
-    if (p.graph_failed || p.want_d2n) return EFEM_OK;
+    if (p.graph_failed || p.want_d2n || debug_sync()) return EFEM_OK;
     if (!p.g_enum) {
         if (!p.gstream) {
             if (cudaStreamCreateWithFlags(&p.gstream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -133,9 +134,45 @@ efem_status enumerate_graph(Plan& p, cudaStream_t s, bool* used) {
     return EFEM_OK;
 }
 
+// row_ptr of rows [r0, r0 + n] (n + 1 entries), relative to row r0's start.
+// 2D edges / 3D faces: closed form r + (m-1) inc_ptr[r]; 3D edges: stored.
+__global__ void k_row_ptr(const int32_t* __restrict__ inc_ptr, const int32_t* __restrict__ row_ptr, int64_t r0,
+                          int64_t n, int c, int32_t* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    const int64_t r = r0 + i;
+    const int64_t v = row_ptr ? (int64_t)row_ptr[r] - row_ptr[r0]
+                              : (r + (int64_t)c * inc_ptr[r]) - (r0 + (int64_t)c * inc_ptr[r0]);
+    out[i] = (int32_t)v;
+}
+
 }  // namespace
 
+bool row_ptr_stored(const Plan& p) { return p.dim == 3 && p.element == EFEM_NED0; }
+
+efem_status write_row_ptr(Plan& p, int64_t r0, int64_t n, int32_t* out, cudaStream_t s) {
+    k_row_ptr<<<grid_for(n + 1, 256), 256, 0, s>>>(p.inc_ptr, row_ptr_stored(p) ? p.row_ptr : nullptr, r0, n, p.m - 1,
+                                                   out);
+    EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
+
+efem_status row_start_host(Plan& p, int64_t r, int64_t* start, cudaStream_t s) {
+    int32_t v = 0;
+    EFEM_CUDA_TRY(cudaMemcpyAsync(&v, (row_ptr_stored(p) ? p.row_ptr : p.inc_ptr) + r, 4, cudaMemcpyDeviceToHost, s));
+    EFEM_CUDA_TRY(cudaStreamSynchronize(s));
+    *start = row_ptr_stored(p) ? (int64_t)v : r + (int64_t)(p.m - 1) * v;
+    return EFEM_OK;
+}
+
 void set_error(const std::string& msg) { g_last_error = msg; }
+bool debug_sync() {
+    static const bool on = [] {
+        const char* v = std::getenv("EFEM_DEBUG_SYNC");
+        return v && v[0] && v[0] != '0';
+    }();
+    return on;
+}
 void set_bad_element(int64_t e) { g_bad_element = e; }
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
@@ -168,10 +205,12 @@ efem_status run_symbolic(Plan& p, cudaStream_t s) {
     return EFEM_OK;
 }
 
+// The numeric row kernels write row_ptr themselves (EFEM_PATTERN).
 efem_status run_numeric(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) {
     efem_status st;
-    if (forms & EFEM_PATTERN) {
-        EFEM_CUDA_TRY(cudaMemcpyAsync(out->row_ptr, p.row_ptr, (p.n_dofs + 1) * 4, cudaMemcpyDeviceToDevice, s));
+    if (p.n_dofs == 0) {
+        if (forms & EFEM_PATTERN) EFEM_CUDA_TRY(cudaMemsetAsync(out->row_ptr, 0, 4, s));
+        return EFEM_OK;
     }
     RowWindow w;
     w.row0 = 0;
@@ -379,7 +418,7 @@ efem_status efem_assemble_symbolic(efem_plan plan, int64_t* n_rows, int64_t* nnz
     if ((st = run_symbolic(*p, s)) != EFEM_OK) return st;
     if (n_rows) *n_rows = p->n_dofs;
     if (nnz) *nnz = p->nnz;
-    if (row_ptr) EFEM_CUDA_TRY(cudaMemcpyAsync(row_ptr, p->row_ptr, (p->n_dofs + 1) * 4, cudaMemcpyDeviceToDevice, s));
+    if (row_ptr) return write_row_ptr(*p, 0, p->n_dofs, row_ptr, s);
     return EFEM_OK;
 }
 

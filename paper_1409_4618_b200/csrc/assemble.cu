@@ -19,68 +19,170 @@ constexpr int NUM_TPB = 128;
 // 2D edges and 3D faces.  In a conforming mesh an entity lies in t <= 2
 // elements and two elements share at most that entity, so row i is
 // {i} U (the m-1 other DOFs of each element): 1 + (m-1) t <= 5 (2D) or 7
-// entries, all distinct.  Gather in registers, sum the own entry over the
-// elements, place every column by its rank.
+// entries, all distinct, and row i starts at i + (m-1) inc_ptr[i] (closed
+// form; this kernel also writes row_ptr).  One thread per row; each warp
+// stages its 32 rows' CSR segment in shared memory (no block barrier) and
+// flushes it with coalesced stores, so every CSR byte is written once.
 // ---------------------------------------------------------------------------------
+constexpr int PAIR_TPB = 256;
+
+// 2D: local row k of one triangle in the frame rotated so that vertex k (the
+// vertex opposite edge k) comes first.  Edge l runs from vertex l+1 to l+2
+// (Fig. 1, reading C4), so with q0 = g[k], q1 = g[k+1], q2 = g[k+2]
+// the row's edge is q1 -> q2 and the other two are q2 -> q0 (local k+1,
+// opposite q1) and q0 -> q1 (local k+2, opposite q2).  Closed form of
+// PAPER.md:344-363 (see local_row): M_kl = s_k s_l (y_k.y_l + Q) / (2|det|),
+// K_kl = 2 s_k s_l / |det|, y = vertex - centroid, Q = sum |y|^2 / 12.
+struct Tri {
+    int q0, q1, q2;  // global vertex ids, rotated
+    int d1, d2;      // DOF ids of local edges k+1, k+2
+    double2 x0, x1, x2;
+};
+
+__device__ __forceinline__ int mod3_next(int k) { return k == 2 ? 0 : k + 1; }
+__device__ __forceinline__ int mod3_prev(int k) { return k == 0 ? 2 : k - 1; }
+
+__device__ __forceinline__ void tri_load_ids(const int32_t* __restrict__ elems, const int32_t* __restrict__ e2d,
+                                             int inst, Tri& T) {
+    const int e = inst >> 3, k = inst & 7;
+    const int k1 = mod3_next(k), k2 = mod3_prev(k);
+    const int32_t* ge = elems + (int64_t)e * 3;
+    const int32_t* de = e2d + (int64_t)e * 3;
+    T.q0 = __ldg(ge + k);
+    T.q1 = __ldg(ge + k1);
+    T.q2 = __ldg(ge + k2);
+    T.d1 = __ldg(de + k1);
+    T.d2 = __ldg(de + k2);
+}
+
+__device__ __forceinline__ void tri_load_x(const double* __restrict__ coords, Tri& T) {
+    const double2* c2 = reinterpret_cast<const double2*>(coords);
+    T.x0 = __ldg(c2 + T.q0);
+    T.x1 = __ldg(c2 + T.q1);
+    T.x2 = __ldg(c2 + T.q2);
+}
+
+// returns det; m0/k0 own entry, m1,k1 / m2,k2 the entries of columns d1, d2
+__device__ __forceinline__ double tri_row(const Tri& T, double& m0, double& k0, double& m1, double& k1,
+                                          double& m2, double& k2) {
+    const double ax = T.x1.x - T.x0.x, ay = T.x1.y - T.x0.y;  // q1 - q0
+    const double bx = T.x2.x - T.x0.x, by = T.x2.y - T.x0.y;  // q2 - q0
+    const double det = ax * by - bx * ay;
+    const double cx = (ax + bx) * (1.0 / 3.0), cy = (ay + by) * (1.0 / 3.0);
+    const double y0x = -cx, y0y = -cy;
+    const double y1x = ax - cx, y1y = ay - cy;
+    const double y2x = bx - cx, y2y = by - cy;
+    const double n0 = y0x * y0x + y0y * y0y;
+    const double Q = (n0 + (y1x * y1x + y1y * y1y) + (y2x * y2x + y2y * y2y)) * (1.0 / 12.0);
+    const double rad = 1.0 / fabs(det);
+    const double cm = 0.5 * rad, ck = 2.0 * rad;
+    const bool so = T.q1 < T.q2;  // s_own
+    const bool sg1 = so == (T.q2 < T.q0), sg2 = so == (T.q0 < T.q1);  // s_own s_l > 0
+    m0 = cm * (n0 + Q);
+    k0 = ck;
+    const double v1 = cm * ((y0x * y1x + y0y * y1y) + Q), v2 = cm * ((y0x * y2x + y0y * y2y) + Q);
+    m1 = sg1 ? v1 : -v1;
+    m2 = sg2 ? v2 : -v2;
+    k1 = sg1 ? ck : -ck;
+    k2 = sg2 ? ck : -ck;
+    return det;
+}
+
 template <class KT>
-__global__ void __launch_bounds__(NUM_TPB) k_rows_small(const double* __restrict__ coords,
+__global__ void __launch_bounds__(PAIR_TPB, KT::D == 2 ? 5 : 2) k_rows_pair(const double* __restrict__ coords,
                                                         const int32_t* __restrict__ elems,
                                                         const int32_t* __restrict__ inc_ptr,
                                                         const int32_t* __restrict__ inc,
-                                                        const int32_t* __restrict__ e2d,
-                                                        const int32_t* __restrict__ row_ptr, int n_rows,
-                                                        int own_base, int out_base,
-                                                        unsigned forms, int32_t* __restrict__ col_idx,
-                                                        double* __restrict__ vals_m, double* __restrict__ vals_k,
-                                                        WsHeader* hdr) {
+                                                        const int32_t* __restrict__ e2d, int row0, int n_rows,
+                                                        int own_base, int out_base, unsigned forms,
+                                                        int32_t* __restrict__ row_ptr_out,
+                                                        int32_t* __restrict__ col_idx, double* __restrict__ vals_m,
+                                                        double* __restrict__ vals_k, WsHeader* hdr) {
     constexpr int D = KT::D, NV = KT::NV, M = KT::M;
-    constexpr int NS = 1 + 2 * (M - 1);
-    constexpr int STAGE = NUM_TPB * NS;
-    __shared__ int s_col[STAGE];
-    __shared__ double s_vm[STAGE];
-    __shared__ double s_vk[STAGE];
+    constexpr int NS = 1 + 2 * (M - 1);  // max entries per row
+    constexpr int WSEG = 32 * NS;         // per-warp staging capacity
+    constexpr int NW = PAIR_TPB / 32;
+    __shared__ int s_col[NW][WSEG];
+    __shared__ double s_vm[NW][WSEG];
+    __shared__ double s_vk[NW][WSEG];
 
-    const int r0 = blockIdx.x * NUM_TPB;
-    const int r1 = min(r0 + NUM_TPB, n_rows);
-    const int seg0 = __ldg(row_ptr + r0);
-    const int segn = __ldg(row_ptr + r1) - seg0;
-    const int i = r0 + (int)threadIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int w0 = blockIdx.x * PAIR_TPB + wid * 32;  // first row of the warp (window-local)
+    if (w0 >= n_rows) return;
+    const int li = w0 + lane;
+    const bool live = li < n_rows;
+    const int lc = live ? li : n_rows - 1;
+    const int ib = __ldg(inc_ptr + lc);
+    const int ie = __ldg(inc_ptr + lc + 1);
+    const int t = live ? ie - ib : 0;
+    const int ib0 = __shfl_sync(0xffffffffu, ib, 0);
+    const int nlast = min(32, n_rows - w0) - 1;
+    const int ie_last = __shfl_sync(0xffffffffu, ie, nlast);
+    // CSR offsets (window-local, relative to out_base)
+    const int gbase = row0 + w0 + (M - 1) * ib0 - out_base;  // warp segment start
+    const int segn = (nlast + 1) + (M - 1) * (ie_last - ib0);
+    const int o = (li - w0) + (M - 1) * (ib - ib0);
+    if (forms & EFEM_PATTERN) {
+        if (live) row_ptr_out[li] = gbase + o;
+        if (li == n_rows - 1) row_ptr_out[n_rows] = gbase + segn;
+    }
+    const bool bad = live && (t < 1 || t > 2);
+    if (bad) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
+    if (__any_sync(0xffffffffu, bad) || segn > WSEG) return;  // non-conforming: flagged, no output
 
-    if (i < n_rows) {
-        const int ib = __ldg(inc_ptr + i);
-        const int t = __ldg(inc_ptr + i + 1) - ib;
-        const int o = __ldg(row_ptr + i) - seg0;
-        if (t < 1 || t > 2) {
-            atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
-        } else {
-            int cl[NS];
-            double am[NS], ak[NS];
-            cl[0] = own_base + i;
-            am[0] = 0.0;
-            ak[0] = 0.0;
-            // all loads of both elements first (element 1 duplicates element 0
-            // when t == 1; its results are then discarded)
-            int pe[2], g[2][NV], dofs[2][M];
+    int* sc = s_col[wid];
+    double* sm = s_vm[wid];
+    double* sk = s_vk[wid];
+    if (live) {
+        const int p0 = __ldg(inc + ib) & 0x7fffffff;
+        const int p1 = __ldg(inc + ib + (t - 1)) & 0x7fffffff;  // == p0 when t == 1
+        int cl[NS];
+        double am[NS], ak[NS];
+        cl[0] = own_base + li;
+        am[0] = 0.0;
+        ak[0] = 0.0;
+        if constexpr (D == 2) {
+            Tri T[2];
+            tri_load_ids(elems, e2d, p0, T[0]);
+            tri_load_ids(elems, e2d, p1, T[1]);
+            tri_load_x(coords, T[0]);
+            tri_load_x(coords, T[1]);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                double m0, k0, m1, k1, m2, k2;
+                const double det = tri_row(T[j], m0, k0, m1, k1, m2, k2);
+                if (j < t) {
+                    if (!(det != 0.0) || !isfinite(det)) {
+                        atomicOr(&hdr->flags[F_DEGENERATE], 1);
+                        atomicMin(&hdr->bad_element, (unsigned long long)((j ? p1 : p0) >> 3));
+                    }
+                    am[0] += m0;
+                    ak[0] += k0;
+                    cl[1 + 2 * j] = T[j].d1;
+                    am[1 + 2 * j] = m1;
+                    ak[1 + 2 * j] = k1;
+                    cl[2 + 2 * j] = T[j].d2;
+                    am[2 + 2 * j] = m2;
+                    ak[2 + 2 * j] = k2;
+                } else {
+                    cl[1 + 2 * j] = INT_MAX;
+                    cl[2 + 2 * j] = INT_MAX;
+                }
+            }
+        } else {  // 3D faces (RT0): general local row
+            const int pe[2] = {p0, p1};
+            int g[2][NV], dofs[2][M];
             double X[2][NV][D];
-            pe[0] = __ldg(inc + ib);
-            pe[1] = __ldg(inc + ib + (t - 1));
 #pragma unroll
             for (int j = 0; j < 2; ++j) load_g<KT>(elems, pe[j] >> 3, g[j]);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
 #pragma unroll
-                for (int l = 0; l < M; ++l) dofs[j][l] = __ldg(e2d + (pe[j] >> 3) * M + l);
+                for (int l = 0; l < M; ++l) dofs[j][l] = __ldg(e2d + (int64_t)(pe[j] >> 3) * M + l);
 #pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    if constexpr (D == 2) {
-                        const double2 c = __ldg(reinterpret_cast<const double2*>(coords) + g[j][v]);
-                        X[j][v][0] = c.x;
-                        X[j][v][1] = c.y;
-                    } else {
+                for (int v = 0; v < NV; ++v)
 #pragma unroll
-                        for (int cc = 0; cc < 3; ++cc) X[j][v][cc] = __ldg(coords + g[j][v] * 3 + cc);
-                    }
-                }
+                    for (int cc = 0; cc < 3; ++cc) X[j][v][cc] = __ldg(coords + (int64_t)g[j][v] * 3 + cc);
             }
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
@@ -112,31 +214,31 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_small(const double* __restrict
                     for (int q = 0; q < M - 1; ++q) cl[1 + j * (M - 1) + q] = INT_MAX;
                 }
             }
-            // place by rank (valid columns are distinct; INT_MAX sentinels rank last)
+        }
+        // place by rank (valid columns are distinct; INT_MAX sentinels rank last)
 #pragma unroll
-            for (int x = 0; x < NS; ++x) {
-                int rk = 0;
+        for (int x = 0; x < NS; ++x) {
+            int rk = 0;
 #pragma unroll
-                for (int y = 0; y < NS; ++y)
-                    if (y != x) rk += cl[y] < cl[x];
-                if (cl[x] != INT_MAX) {
-                    s_col[o + rk] = cl[x];
-                    s_vm[o + rk] = am[x];
-                    s_vk[o + rk] = ak[x];
-                }
+            for (int y = 0; y < NS; ++y)
+                if (y != x) rk += cl[y] < cl[x];
+            if (cl[x] != INT_MAX) {
+                sc[o + rk] = cl[x];
+                sm[o + rk] = am[x];
+                sk[o + rk] = ak[x];
             }
         }
     }
-    __syncthreads();
-    // coalesced flush; the segment holds at most NS entries per row
+    __syncwarp();
+    // coalesced flush of the warp's segment
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
-        const int x = u * NUM_TPB + (int)threadIdx.x;
+        const int x = u * 32 + lane;
         if (x < segn) {
-            const int gx = seg0 - out_base + x;
-            if (forms & EFEM_PATTERN) col_idx[gx] = s_col[x];
-            if (forms & EFEM_MASS) vals_m[gx] = s_vm[x];
-            if (forms & EFEM_STIFF) vals_k[gx] = s_vk[x];
+            const int gx = gbase + x;
+            if (forms & EFEM_PATTERN) col_idx[gx] = sc[x];
+            if (forms & EFEM_MASS) vals_m[gx] = sm[x];
+            if (forms & EFEM_STIFF) vals_k[gx] = sk[x];
         }
     }
 }
@@ -172,7 +274,8 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
                                                       const int32_t* __restrict__ e2d,
                                                       const int32_t* __restrict__ row_ptr, int n_rows,
                                                       int own_base, int out_base,
-                                                      unsigned forms, int fast_ids, int32_t* __restrict__ col_idx,
+                                                      unsigned forms, int fast_ids, int32_t* __restrict__ row_ptr_out,
+                                                      int32_t* __restrict__ col_idx,
                                                       double* __restrict__ vals_m, double* __restrict__ vals_k,
                                                       WsHeader* hdr) {
     static_assert(KT::D == 3 && !KT::FACES, "NE0 3D only");
@@ -193,6 +296,10 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
     if (i < n_rows) {
         const int rb = __ldg(row_ptr + i);
         rlen = __ldg(row_ptr + i + 1) - rb;
+        if (forms & EFEM_PATTERN) {
+            row_ptr_out[i] = rb - out_base;
+            if (i == n_rows - 1) row_ptr_out[n_rows] = rb + rlen - out_base;
+        }
         s_off[threadIdx.x] = rb - seg0;
         ib = __ldg(inc_ptr + i);
         t = __ldg(inc_ptr + i + 1) - ib;
@@ -224,7 +331,7 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
             // all index loads first, then all element loads: two round trips
             // (slots j >= t repeat the last incidence and are masked below)
 #pragma unroll
-            for (int j = 0; j < NE3_TMAX; ++j) inst[j] = __ldg(inc + ib + min(j, t - 1));
+            for (int j = 0; j < NE3_TMAX; ++j) inst[j] = __ldg(inc + ib + min(j, t - 1)) & 0x7fffffff;
             int4 gq[NE3_TMAX];
 #pragma unroll
             for (int j = 0; j < NE3_TMAX; ++j) gq[j] = __ldg(reinterpret_cast<const int4*>(elems) + (inst[j] >> 3));
@@ -421,14 +528,14 @@ constexpr size_t NE3_SMEM = (size_t)NE3_SLOTS * NE3_LD * (8 + 8 + 4) + (NUM_TPB 
 template <class KT>
 efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow& w, cudaStream_t s) {
     if (w.n_rows == 0) return EFEM_OK;
-    const unsigned grid = grid_for(w.n_rows, NUM_TPB);
     double* vm = (forms & EFEM_MASS) ? out->vals_mass : nullptr;
     double* vk = (forms & EFEM_STIFF) ? out->vals_stiff : nullptr;
     const int32_t* inc_ptr = p.inc_ptr + w.row0;
     const int32_t* row_ptr = p.row_ptr + w.row0;
     if constexpr (KT::D == 2 || KT::FACES) {
-        k_rows_small<KT><<<grid, NUM_TPB, 0, s>>>(p.coords, p.elems, inc_ptr, p.bucket, w.e2d, row_ptr, (int)w.n_rows,
-                                                  w.own_base, w.out_base, forms, out->col_idx, vm, vk, p.hdr);
+        k_rows_pair<KT><<<grid_for(w.n_rows, PAIR_TPB), PAIR_TPB, 0, s>>>(
+            p.coords, p.elems, inc_ptr, p.bucket, w.e2d, (int)w.row0, (int)w.n_rows, w.own_base, w.out_base, forms,
+            out->row_ptr, out->col_idx, vm, vk, p.hdr);
     } else {
         const int fast_ids = p.n_nodes < (1ll << 27);
         static bool attr = false;
@@ -437,9 +544,9 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
                                                (int)NE3_SMEM));
             attr = true;
         }
-        k_rows_ne3<KT><<<grid, NUM_TPB, NE3_SMEM, s>>>(p.coords, p.elems, inc_ptr, p.bucket, w.e2d, row_ptr,
+        k_rows_ne3<KT><<<grid_for(w.n_rows, NUM_TPB), NUM_TPB, NE3_SMEM, s>>>(p.coords, p.elems, inc_ptr, p.bucket, w.e2d, row_ptr,
                                                        (int)w.n_rows, w.own_base, w.out_base, forms, fast_ids,
-                                                       out->col_idx, vm, vk, p.hdr);
+                                                       out->row_ptr, out->col_idx, vm, vk, p.hdr);
     }
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;

@@ -157,6 +157,11 @@ struct NodeOut {
 // Sort item of an instance.  Edges: one u64 (other node << 32 | e << 3 | k),
 // so sorting the word sorts by (entity, element).  Faces: u64 (mid << 32 | hi)
 // plus the instance word as tie-break.
+// Bucket words are instances e << 3 | k; k_node_count sets bit 31 on the
+// first instance of every entity run (consumers mask with INST_MASK).
+constexpr int INST_MASK = 0x7fffffff;
+constexpr unsigned RUN_FLAG = 0x80000000u;
+
 template <class KT>
 struct Item {
     uint64_t key;
@@ -173,6 +178,7 @@ struct Item {
 
 template <class KT>
 __device__ __forceinline__ Item<KT> make_item(const int32_t* __restrict__ elems, int inst) {
+    inst &= INST_MASK;
     int g[KT::NV];
     load_elem<KT>(elems, inst >> 3, g);
     Item<KT> it;
@@ -293,8 +299,9 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
 #pragma unroll
         for (int x = 0; x < NREG; ++x)
             if (x < n) {
-                n_ent += x == 0 || (rk[x] >> 32) != (rk[x - 1] >> 32);
-                gb[x] = (int)(uint32_t)rk[x];
+                const bool st = x == 0 || (rk[x] >> 32) != (rk[x - 1] >> 32);
+                n_ent += st;
+                gb[x] = (int)((uint32_t)rk[x] | (st ? RUN_FLAG : 0u));
             }
         n_nnz = n_ent + (KT::M - 1) * n;
     } else {
@@ -338,9 +345,7 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
             }
             put(q, it);
         }
-        if (in_smem)
-            for (int j = 0; j < n; ++j) gb[j] = get(j).inst;
-        auto inst_at = [&](int j) -> int { return in_smem ? get(j).inst : gb[j]; };
+        auto inst_at = [&](int j) -> int { return (in_smem ? get(j).inst : gb[j]) & INST_MASK; };
         for (int j = 0; j < n;) {
             const uint64_t ek = get(j).entity();
             int q = j + 1;
@@ -348,16 +353,24 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
             if constexpr (KT::D == 3 && !KT::FACES)
                 n_nnz += 1 + 2 * link_count_fast<KT>(elems, a, (int)ek, j, q, inst_at) + (q - j);
             ++n_ent;
+            if (in_smem)
+                for (int u = j; u < q; ++u) gb[u] = (int)((uint32_t)get(u).inst | (u == j ? RUN_FLAG : 0u));
+            else
+                gb[j] = (int)((uint32_t)gb[j] | RUN_FLAG);
             j = q;
         }
         if constexpr (!(KT::D == 3 && !KT::FACES)) n_nnz = n_ent + (KT::M - 1) * n;
     }
     ent_cnt[a] = n_ent;
-    nnz_cnt[a] = n_nnz;
+    if constexpr (KT::D == 3 && !KT::FACES) nnz_cnt[a] = n_nnz;
 }
 
 // Pass B: per node, walk its sorted bucket: DOF ids (ent_ptr[a] + run),
-// elems2dofs, the incidence offsets, row_ptr (from nnz_ptr[a]), dofs2nodes.
+// elems2dofs, the incidence offsets, dofs2nodes (on request).  Runs are read
+// from the RUN_FLAG bits pass A left, so no element is gathered except for
+// NE0 3D row lengths (link vertices) and dofs2nodes.  Only NE0 3D writes
+// row_ptr here; for 2D edges and 3D faces row i starts at
+// i + (m-1) inc_ptr[i] (closed form, written by the numeric kernel).
 template <class KT>
 __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ elems,
                                                     const int32_t* __restrict__ bucket_ptr,
@@ -365,6 +378,7 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
                                                     const int32_t* __restrict__ ent_ptr,
                                                     const int32_t* __restrict__ nnz_ptr, int64_t n_nodes,
                                                     NodeOut out) {
+    constexpr bool NE3 = KT::D == 3 && !KT::FACES;
     const int64_t a64 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (a64 >= n_nodes) return;
     const int a = (int)a64;
@@ -372,49 +386,49 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
     const int n = __ldg(bucket_ptr + a + 1) - beg;
     const int32_t* gb = bucket + beg;
     int id = __ldg(ent_ptr + a) - 1;
-    int nnz_run = __ldg(nnz_ptr + a);
-    auto inst_at = [&](int j) -> int { return __ldg(gb + j); };
-    uint64_t prev = ~0ull;
-    int run0 = 0;
-    auto close_run = [&](int j_end, uint64_t key) {
-        const int t = j_end - run0;
-        if constexpr (KT::D == 3 && !KT::FACES)
-            nnz_run += 1 + 2 * link_count_fast<KT>(elems, a, (int)key, run0, j_end, inst_at) + t;
-        else
-            nnz_run += 1 + (KT::M - 1) * t;
-    };
+    int nnz_run = NE3 ? __ldg(nnz_ptr + a) : 0;
+    auto inst_at = [&](int j) -> int { return __ldg(gb + j) & INST_MASK; };
+    int run0 = 0, run_b = 0;
     for (int j = 0; j < n; ++j) {
-        const int inst = __ldg(gb + j);
-        int g[KT::NV];
-        load_elem<KT>(elems, inst >> 3, g);
-        const uint64_t key = entity_key<KT>(g, inst & 7);
-        if (j == 0 || key != prev) {
-            if (j > 0) close_run(j, prev);
+        const int w = __ldg(gb + j);
+        const int inst = w & INST_MASK;
+        if (w < 0) {  // RUN_FLAG: first instance of a new entity
+            if constexpr (NE3) {
+                if (j > 0) nnz_run += 1 + 2 * link_count_fast<KT>(elems, a, run_b, run0, j, inst_at) + (j - run0);
+            }
             ++id;
             run0 = j;
-            prev = key;
             out.inc_ptr[id] = beg + j;
-            out.row_ptr[id] = nnz_run;
-            if (out.d2n) {
-                int32_t* row = out.d2n + (int64_t)id * KT::EK;
-                row[0] = a;
-                if constexpr (KT::FACES) {
-                    row[1] = (int)(key >> 32);
-                    row[2] = (int)(key & 0xffffffffu);
-                } else {
-                    row[1] = (int)key;
+            if (NE3 || out.d2n) {
+                int g[KT::NV];
+                load_elem<KT>(elems, inst >> 3, g);
+                const uint64_t key = entity_key<KT>(g, inst & 7);
+                run_b = (int)key;
+                if (NE3) out.row_ptr[id] = nnz_run;
+                if (out.d2n) {
+                    int32_t* row = out.d2n + (int64_t)id * KT::EK;
+                    row[0] = a;
+                    if constexpr (KT::FACES) {
+                        row[1] = (int)(key >> 32);
+                        row[2] = (int)(key & 0xffffffffu);
+                    } else {
+                        row[1] = (int)key;
+                    }
                 }
             }
         }
         out.e2d[(int64_t)(inst >> 3) * KT::M + (inst & 7)] = id;
     }
-    if (n > 0) close_run(n, prev);
+    if constexpr (NE3) {
+        if (n > 0) nnz_run += 1 + 2 * link_count_fast<KT>(elems, a, run_b, run0, n, inst_at) + (n - run0);
+    }
     if (a == n_nodes - 1) {
         const int R = id + 1;
         out.inc_ptr[R] = beg + n;
-        out.row_ptr[R] = nnz_run;
+        if (NE3) out.row_ptr[R] = nnz_run;
         out.totals[0] = R;
-        out.totals[1] = nnz_run;
+        // 2D edges / 3D faces: nnz = sum_i (1 + (m-1) t_i) = R + (m-1) (T m)
+        out.totals[1] = NE3 ? (int64_t)nnz_run : (int64_t)R + (int64_t)(KT::M - 1) * (beg + n);
     }
 }
 
@@ -474,9 +488,12 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     k_node_count<KT><<<grid_for(N, TPB), TPB, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, N, p.cnt, p.nnz_cnt);
     EFEM_LAUNCH_CHECK();
     EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.ent_ptr, (int)(N + 1), s));
-    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.nnz_cnt, p.nnz_ptr, (int)(N + 1), s));
-    count_launch(4);
-    // pass B: DOF ids, elems2dofs, incidence, row_ptr
+    count_launch(2);
+    if constexpr (KT::D == 3 && !KT::FACES) {  // row lengths need a union only for 3D edges
+        EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.nnz_cnt, p.nnz_ptr, (int)(N + 1), s));
+        count_launch(2);
+    }
+    // pass B: DOF ids, elems2dofs, incidence (+ row_ptr for 3D edges)
     NodeOut o{p.e2d, p.inc_ptr, p.row_ptr, p.want_d2n ? p.d2n : nullptr, p.bucket, p.d_totals, nullptr, nullptr};
     k_node_write<KT><<<grid_for(N, 256), 256, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.ent_ptr, p.nnz_ptr, N, o);
     EFEM_LAUNCH_CHECK();

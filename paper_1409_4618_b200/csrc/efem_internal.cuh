@@ -122,12 +122,18 @@ void count_launch(int n = 1);
         }                                                                            \
     } while (0)
 
+// EFEM_DEBUG_SYNC=1 in the environment: synchronise after every launch and
+// report the failing launch site (debugging aid; off by default, graphs off).
+bool debug_sync();
+
 #define EFEM_LAUNCH_CHECK()                                                          \
     do {                                                                             \
         ::efem::count_launch();                                                      \
         cudaError_t _e = cudaGetLastError();                                         \
+        if (_e == cudaSuccess && ::efem::debug_sync()) _e = cudaDeviceSynchronize();  \
         if (_e != cudaSuccess) {                                                     \
-            ::efem::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+            ::efem::set_error(std::string("kernel launch (") + __FILE__ + ":" +       \
+                              std::to_string(__LINE__) + "): " + cudaGetErrorString(_e)); \
             return EFEM_ECUDA;                                                       \
         }                                                                            \
     } while (0)
@@ -139,6 +145,11 @@ efem_status run_enumerate(Plan& p, cudaStream_t s);
 efem_status run_symbolic(Plan& p, cudaStream_t s);
 efem_status run_numeric(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s);
 efem_status run_signs(Plan& p, cudaStream_t s);
+// row_ptr helpers (api.cu): 2D edges / 3D faces keep no row_ptr array, row r
+// starts at r + (m-1) inc_ptr[r]; 3D edges store it (plan row_ptr).
+bool row_ptr_stored(const Plan& p);
+efem_status write_row_ptr(Plan& p, int64_t r0, int64_t n, int32_t* out, cudaStream_t s);
+efem_status row_start_host(Plan& p, int64_t r, int64_t* start, cudaStream_t s);
 
 inline unsigned grid_for(int64_t n, int tpb) { return (unsigned)((n + tpb - 1) / tpb); }
 

@@ -254,7 +254,7 @@ __device__ __noinline__ bool row_generic(const double* __restrict__ coords, cons
     int W[WCAP + 1];
     int nw = 0;
     for (int j = 0; j < nt; ++j) {
-        const int e = __ldg(inc + ib + j) >> 3;
+        const int e = (__ldg(inc + ib + j) & 0x7fffffff) >> 3;
         int g[NV];
         load_g<KT>(elems, e, g);
 #pragma unroll
@@ -274,7 +274,7 @@ __device__ __noinline__ bool row_generic(const double* __restrict__ coords, cons
     mk.clear();
     int pk[EFEM_MAX_ROW_ELEMS];
     for (int j = 0; j < nt; ++j) {
-        const int e = __ldg(inc + ib + j) >> 3;
+        const int e = (__ldg(inc + ib + j) & 0x7fffffff) >> 3;
         int g[NV];
         load_g<KT>(elems, e, g);
         int pos[NV];
@@ -302,7 +302,7 @@ __device__ __noinline__ bool row_generic(const double* __restrict__ coords, cons
     }
     // pass 3: values, ascending element id (the incidence list order)
     for (int j = 0; j < nt; ++j) {
-        const int pe = __ldg(inc + ib + j);
+        const int pe = __ldg(inc + ib + j) & 0x7fffffff;
         const int e = pe >> 3, k = pe & 7;
         int g[NV];
         load_g<KT>(elems, e, g);

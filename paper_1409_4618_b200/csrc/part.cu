@@ -146,10 +146,6 @@ __global__ void k_globalize(const int32_t* __restrict__ elems, int64_t n_elems, 
     }
 }
 
-__global__ void k_shift(const int32_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) out[i] = in[i] - in[0];
-}
 
 }  // namespace
 
@@ -254,13 +250,14 @@ efem_status efem_part_counts(efem_plan plan, const int32_t* sub2global, int64_t 
                                                                     owned_cnt);
         EFEM_LAUNCH_CHECK();
     }
-    int32_t rows[2], nz[2];
+    int32_t rows[2];
+    int64_t nz[2];
     EFEM_CUDA_TRY(cudaMemcpyAsync(&rows[0], p->ent_ptr + lr[0], 4, cudaMemcpyDeviceToHost, s));
     EFEM_CUDA_TRY(cudaMemcpyAsync(&rows[1], p->ent_ptr + lr[1], 4, cudaMemcpyDeviceToHost, s));
     EFEM_CUDA_TRY(cudaStreamSynchronize(s));
-    EFEM_CUDA_TRY(cudaMemcpyAsync(&nz[0], p->row_ptr + rows[0], 4, cudaMemcpyDeviceToHost, s));
-    EFEM_CUDA_TRY(cudaMemcpyAsync(&nz[1], p->row_ptr + rows[1], 4, cudaMemcpyDeviceToHost, s));
-    EFEM_CUDA_TRY(cudaStreamSynchronize(s));
+    efem_status st;
+    if ((st = row_start_host(*p, rows[0], &nz[0], s)) != EFEM_OK) return st;
+    if ((st = row_start_host(*p, rows[1], &nz[1], s)) != EFEM_OK) return st;
     info[0] = rows[0];          // first owned local row
     info[1] = rows[1] - rows[0];  // owned rows
     info[2] = nz[0];            // local CSR offset of the first owned row
@@ -331,9 +328,9 @@ efem_status efem_part_numeric(efem_plan plan, unsigned forms, const int64_t* inf
         return EFEM_EINVAL;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    if (forms & EFEM_PATTERN) {
-        k_shift<<<grid_for(info[1] + 1, 256), 256, 0, s>>>(p->row_ptr + info[0], info[1] + 1, slice->row_ptr);
-        EFEM_LAUNCH_CHECK();
+    if (info[1] == 0) {  // the row kernels write row_ptr; an empty slice still needs its 0
+        if (forms & EFEM_PATTERN) EFEM_CUDA_TRY(cudaMemsetAsync(slice->row_ptr, 0, 4, s));
+        return EFEM_OK;
     }
     RowWindow w;
     w.row0 = info[0];
