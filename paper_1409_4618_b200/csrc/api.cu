@@ -25,7 +25,7 @@ std::atomic<int64_t> g_launches{0};
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-    size_t hdr, cnt, bucket_ptr, bucket, e2d, inc_ptr, row_ptr, d2n, ent_ptr, nnz_cnt, nnz_ptr, lb, totals, cub, total;
+    size_t hdr, cnt, bucket_ptr, bucket, e2d, inc_ptr, row_ptr, rec, d2n, ent_ptr, nnz_cnt, nnz_ptr, lb, totals, cub, total;
 };
 
 Layout layout(const Plan& p, size_t cub_bytes) {
@@ -44,7 +44,9 @@ Layout layout(const Plan& p, size_t cub_bytes) {
     L.bucket = take(Tm * 4);
     L.e2d = take(Tm * 4);
     L.inc_ptr = take(((size_t)p.r_max + 1) * 4);
-    L.row_ptr = take(((size_t)p.r_max + 1) * 4);
+    const bool ne3 = p.dim == 3 && p.element == EFEM_NED0;
+    L.row_ptr = take(ne3 ? ((size_t)p.r_max + 1) * 4 : 4);
+    L.rec = take(ne3 ? 8 : (size_t)p.r_max * 8);
     L.d2n = take((size_t)p.r_max * p.ek * 4);
     L.ent_ptr = take(N1 * 4);
     L.nnz_cnt = take(N1 * 4);
@@ -343,6 +345,7 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     p->e2d = reinterpret_cast<int32_t*>(b + L.e2d);
     p->inc_ptr = reinterpret_cast<int32_t*>(b + L.inc_ptr);
     p->row_ptr = reinterpret_cast<int32_t*>(b + L.row_ptr);
+    p->rec = reinterpret_cast<int2*>(b + L.rec);
     p->d2n = reinterpret_cast<int32_t*>(b + L.d2n);
     p->ent_ptr = reinterpret_cast<int32_t*>(b + L.ent_ptr);
     p->nnz_cnt = reinterpret_cast<int32_t*>(b + L.nnz_cnt);

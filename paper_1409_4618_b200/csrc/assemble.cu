@@ -88,11 +88,153 @@ __device__ __forceinline__ double tri_row(const Tri& T, double& m0, double& k0, 
     return det;
 }
 
+// 2D, persistent and software-pipelined: every warp walks 32-row batches
+// (grid-stride, so concurrently running warps work on neighbouring rows and
+// share element data in L2).  The gather chain per row is
+//   L1 inc_ptr[i], inc_ptr[i+1], rec[i]  ->  L2 elems / elems2dofs  ->  L3 coords
+// and is overlapped across batches: while batch b is computed, the L2 loads
+// of batch b+1 and the L1 loads of batch b+2 are in flight.
+constexpr int TRI_TPB = 256;
+
+struct TriL1 {
+    int ib, ie;
+    int2 rr;
+};
+
+__device__ __forceinline__ TriL1 tri_l1(const int32_t* __restrict__ inc_ptr, const int2* __restrict__ rec, int batch,
+                                        int nbatch, int n_rows, int lane) {
+    TriL1 a;
+    const int li = min(batch * 32 + lane, n_rows - 1);
+    if (batch < nbatch) {
+        a.ib = __ldg(inc_ptr + li);
+        a.ie = __ldg(inc_ptr + li + 1);
+        a.rr = __ldg(rec + li);
+    } else {
+        a.ib = a.ie = 0;
+        a.rr = make_int2(0, 0);
+    }
+    return a;
+}
+
 template <class KT>
-__global__ void __launch_bounds__(PAIR_TPB, KT::D == 2 ? 5 : 2) k_rows_pair(const double* __restrict__ coords,
+__global__ void __launch_bounds__(TRI_TPB, 3) k_rows_tri(const double* __restrict__ coords,
                                                         const int32_t* __restrict__ elems,
                                                         const int32_t* __restrict__ inc_ptr,
-                                                        const int32_t* __restrict__ inc,
+                                                        const int2* __restrict__ rec,
+                                                        const int32_t* __restrict__ e2d, int row0, int n_rows,
+                                                        int own_base, int out_base, unsigned forms,
+                                                        int32_t* __restrict__ row_ptr_out,
+                                                        int32_t* __restrict__ col_idx, double* __restrict__ vals_m,
+                                                        double* __restrict__ vals_k, WsHeader* hdr) {
+    constexpr int NS = 5, WSEG = 32 * NS, NW = TRI_TPB / 32;
+    __shared__ int s_col[NW][WSEG];
+    __shared__ double s_vm[NW][WSEG];
+    __shared__ double s_vk[NW][WSEG];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int* sc = s_col[wid];
+    double* sm = s_vm[wid];
+    double* sk = s_vk[wid];
+    const int nbatch = (n_rows + 31) >> 5;
+    const int stride = gridDim.x * NW;
+    int batch = blockIdx.x * NW + wid;
+    if (batch >= nbatch) return;
+
+    // prologue: L1 of batches b and b+1, L2 of batch b
+    TriL1 c1 = tri_l1(inc_ptr, rec, batch, nbatch, n_rows, lane);
+    TriL1 n1 = tri_l1(inc_ptr, rec, batch + stride, nbatch, n_rows, lane);
+    Tri T0, T1;
+    tri_load_ids(elems, e2d, c1.rr.x, T0);
+    tri_load_ids(elems, e2d, c1.rr.y, T1);
+
+    for (; batch < nbatch; batch += stride) {
+        // L3 of batch b
+        tri_load_x(coords, T0);
+        tri_load_x(coords, T1);
+        // L2 of batch b+1, L1 of batch b+2
+        Tri U0, U1;
+        const bool has_next = batch + stride < nbatch;
+        if (has_next) {
+            tri_load_ids(elems, e2d, n1.rr.x, U0);
+            tri_load_ids(elems, e2d, n1.rr.y, U1);
+        }
+        const TriL1 n2 = tri_l1(inc_ptr, rec, batch + 2 * stride, nbatch, n_rows, lane);
+
+        // ---- batch b
+        const int w0 = batch * 32;
+        const int li = w0 + lane;
+        const bool live = li < n_rows;
+        const int t = live ? c1.ie - c1.ib : 0;
+        const int ib0 = __shfl_sync(0xffffffffu, c1.ib, 0);
+        const int nlast = min(32, n_rows - w0) - 1;
+        const int ie_last = __shfl_sync(0xffffffffu, c1.ie, nlast);
+        const int gbase = row0 + w0 + 2 * ib0 - out_base;
+        const int segn = (nlast + 1) + 2 * (ie_last - ib0);
+        const int o = lane + 2 * (c1.ib - ib0);
+        if (forms & EFEM_PATTERN) {
+            if (live) row_ptr_out[li] = gbase + o;
+            if (li == n_rows - 1) row_ptr_out[n_rows] = gbase + segn;
+        }
+        const bool bad = live && (t < 1 || t > 2);
+        if (bad) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
+        if (!__any_sync(0xffffffffu, bad) && segn <= WSEG) {
+            if (live) {
+                double m0a, k0a, m1a, k1a, m2a, k2a, m0b, k0b, m1b, k1b, m2b, k2b;
+                const double da = tri_row(T0, m0a, k0a, m1a, k1a, m2a, k2a);
+                const double db = tri_row(T1, m0b, k0b, m1b, k1b, m2b, k2b);
+                const bool two = t == 2;
+                const bool bad_a = !(fabs(da) > 0.0 && fabs(da) < INFINITY);
+                const bool bad_b = two && !(fabs(db) > 0.0 && fabs(db) < INFINITY);
+                if (bad_a || bad_b) {
+                    atomicOr(&hdr->flags[F_DEGENERATE], 1);
+                    atomicMin(&hdr->bad_element, (unsigned long long)((bad_a ? c1.rr.x : c1.rr.y) >> 3));
+                }
+                int cl[NS] = {own_base + li, T0.d1, T0.d2, two ? T1.d1 : INT_MAX, two ? T1.d2 : INT_MAX};
+                const double am[NS] = {two ? m0a + m0b : m0a, m1a, m2a, m1b, m2b};
+                const double ak[NS] = {two ? k0a + k0b : k0a, k1a, k2a, k1b, k2b};
+                int rk[NS] = {0, 0, 0, 0, 0};
+#pragma unroll
+                for (int x = 0; x < NS; ++x)
+#pragma unroll
+                    for (int y = x + 1; y < NS; ++y) {
+                        const bool lt = cl[x] < cl[y];
+                        rk[y] += lt;
+                        rk[x] += !lt;
+                    }
+#pragma unroll
+                for (int x = 0; x < NS; ++x) {
+                    if (x < 3 || two) {
+                        sc[o + rk[x]] = cl[x];
+                        sm[o + rk[x]] = am[x];
+                        sk[o + rk[x]] = ak[x];
+                    }
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < NS; ++u) {
+                const int x = u * 32 + lane;
+                if (x < segn) {
+                    const int gx = gbase + x;
+                    if (forms & EFEM_PATTERN) col_idx[gx] = sc[x];
+                    if (forms & EFEM_MASS) vals_m[gx] = sm[x];
+                    if (forms & EFEM_STIFF) vals_k[gx] = sk[x];
+                }
+            }
+            __syncwarp();
+        }
+        // rotate the pipeline
+        c1 = n1;
+        n1 = n2;
+        T0 = U0;
+        T1 = U1;
+    }
+}
+
+template <class KT>
+__global__ void __launch_bounds__(PAIR_TPB, 2) k_rows_pair(const double* __restrict__ coords,
+                                                        const int32_t* __restrict__ elems,
+                                                        const int32_t* __restrict__ inc_ptr,
+                                                        const int2* __restrict__ rec,
                                                         const int32_t* __restrict__ e2d, int row0, int n_rows,
                                                         int own_base, int out_base, unsigned forms,
                                                         int32_t* __restrict__ row_ptr_out,
@@ -114,6 +256,7 @@ __global__ void __launch_bounds__(PAIR_TPB, KT::D == 2 ? 5 : 2) k_rows_pair(cons
     const int lc = live ? li : n_rows - 1;
     const int ib = __ldg(inc_ptr + lc);
     const int ie = __ldg(inc_ptr + lc + 1);
+    const int2 rr = __ldg(rec + lc);  // {first, last} instance: same level as inc_ptr
     const int t = live ? ie - ib : 0;
     const int ib0 = __shfl_sync(0xffffffffu, ib, 0);
     const int nlast = min(32, n_rows - w0) - 1;
@@ -134,8 +277,8 @@ __global__ void __launch_bounds__(PAIR_TPB, KT::D == 2 ? 5 : 2) k_rows_pair(cons
     double* sm = s_vm[wid];
     double* sk = s_vk[wid];
     if (live) {
-        const int p0 = __ldg(inc + ib) & 0x7fffffff;
-        const int p1 = __ldg(inc + ib + (t - 1)) & 0x7fffffff;  // == p0 when t == 1
+        const int p0 = rr.x;
+        const int p1 = rr.y;  // == p0 when t == 1
         int cl[NS];
         double am[NS], ak[NS];
         cl[0] = own_base + li;
@@ -532,9 +675,22 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
     double* vk = (forms & EFEM_STIFF) ? out->vals_stiff : nullptr;
     const int32_t* inc_ptr = p.inc_ptr + w.row0;
     const int32_t* row_ptr = p.row_ptr + w.row0;
-    if constexpr (KT::D == 2 || KT::FACES) {
+    if constexpr (KT::D == 2) {
+        static int grid = 0;
+        if (!grid) {
+            int dev = 0, sms = 0, per_sm = 0;
+            EFEM_CUDA_TRY(cudaGetDevice(&dev));
+            EFEM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            EFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_tri<KT>, TRI_TPB, 0));
+            grid = sms * (per_sm > 0 ? per_sm : 1);
+        }
+        const int64_t need = (w.n_rows + TRI_TPB - 1) / TRI_TPB;
+        k_rows_tri<KT><<<(unsigned)(need < grid ? need : grid), TRI_TPB, 0, s>>>(
+            p.coords, p.elems, inc_ptr, p.rec + w.row0, w.e2d, (int)w.row0, (int)w.n_rows, w.own_base, w.out_base,
+            forms, out->row_ptr, out->col_idx, vm, vk, p.hdr);
+    } else if constexpr (KT::FACES) {
         k_rows_pair<KT><<<grid_for(w.n_rows, PAIR_TPB), PAIR_TPB, 0, s>>>(
-            p.coords, p.elems, inc_ptr, p.bucket, w.e2d, (int)w.row0, (int)w.n_rows, w.own_base, w.out_base, forms,
+            p.coords, p.elems, inc_ptr, p.rec + w.row0, w.e2d, (int)w.row0, (int)w.n_rows, w.own_base, w.out_base, forms,
             out->row_ptr, out->col_idx, vm, vk, p.hdr);
     } else {
         const int fast_ids = p.n_nodes < (1ll << 27);

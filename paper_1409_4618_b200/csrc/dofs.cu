@@ -148,6 +148,7 @@ struct NodeOut {
     int32_t* inc_ptr;
     int32_t* row_ptr;
     int32_t* d2n;  // optional
+    int2* rec;     // 2D edges / 3D faces: {first, last} instance of each row
     int32_t* bucket;
     int64_t* totals;  // [0] n_dofs, [1] nnz
     unsigned long long* status;
@@ -388,13 +389,16 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
     int id = __ldg(ent_ptr + a) - 1;
     int nnz_run = NE3 ? __ldg(nnz_ptr + a) : 0;
     auto inst_at = [&](int j) -> int { return __ldg(gb + j) & INST_MASK; };
-    int run0 = 0, run_b = 0;
+    int run0 = 0, run_b = 0, first = 0, prev = 0;
     for (int j = 0; j < n; ++j) {
         const int w = __ldg(gb + j);
         const int inst = w & INST_MASK;
         if (w < 0) {  // RUN_FLAG: first instance of a new entity
             if constexpr (NE3) {
                 if (j > 0) nnz_run += 1 + 2 * link_count_fast<KT>(elems, a, run_b, run0, j, inst_at) + (j - run0);
+            } else {
+                if (j > 0) out.rec[id] = make_int2(first, prev);
+                first = inst;
             }
             ++id;
             run0 = j;
@@ -418,9 +422,12 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
             }
         }
         out.e2d[(int64_t)(inst >> 3) * KT::M + (inst & 7)] = id;
+        prev = inst;
     }
     if constexpr (NE3) {
         if (n > 0) nnz_run += 1 + 2 * link_count_fast<KT>(elems, a, run_b, run0, n, inst_at) + (n - run0);
+    } else {
+        if (n > 0) out.rec[id] = make_int2(first, prev);
     }
     if (a == n_nodes - 1) {
         const int R = id + 1;
@@ -494,7 +501,7 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
         count_launch(2);
     }
     // pass B: DOF ids, elems2dofs, incidence (+ row_ptr for 3D edges)
-    NodeOut o{p.e2d, p.inc_ptr, p.row_ptr, p.want_d2n ? p.d2n : nullptr, p.bucket, p.d_totals, nullptr, nullptr};
+    NodeOut o{p.e2d, p.inc_ptr, p.row_ptr, p.want_d2n ? p.d2n : nullptr, p.rec, p.bucket, p.d_totals, nullptr, nullptr};
     k_node_write<KT><<<grid_for(N, 256), 256, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.ent_ptr, p.nnz_ptr, N, o);
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;

@@ -71,7 +71,8 @@ struct Plan {
                                     // (entity, element): the entity -> element incidence
     int32_t* e2d = nullptr;         // T*m elems2dofs
     int32_t* inc_ptr = nullptr;     // r_max+1 entity -> first incidence in bucket
-    int32_t* row_ptr = nullptr;     // r_max+1 CSR row offsets
+    int32_t* row_ptr = nullptr;     // r_max+1 CSR row offsets (3D edges only; others: closed form)
+    int2* rec = nullptr;            // r_max row records {first, last instance} (2D edges, 3D faces)
     int32_t* d2n = nullptr;         // r_max*ek (written only when want_d2n)
     int32_t* ent_ptr = nullptr;     // N+1 first DOF id of each node's entities
     int32_t* nnz_cnt = nullptr;     // N+1 CSR entries of each node's rows
