@@ -96,22 +96,23 @@ __device__ __forceinline__ double tri_row(const Tri& T, double& m0, double& k0, 
 // of batch b+1 and the L1 loads of batch b+2 are in flight.
 constexpr int TRI_TPB = 256;
 
+// L1 of a batch: the lane's row record; lane 0 also the batch's first
+// incidence offset (row offsets follow from t = 1 + (first != last) by a
+// warp scan, so inc_ptr is read once per batch, not per row)
 struct TriL1 {
-    int ib, ie;
     int2 rr;
+    int ib0;
 };
 
 __device__ __forceinline__ TriL1 tri_l1(const int32_t* __restrict__ inc_ptr, const int2* __restrict__ rec, int batch,
                                         int nbatch, int n_rows, int lane) {
     TriL1 a;
-    const int li = min(batch * 32 + lane, n_rows - 1);
+    a.ib0 = 0;
+    a.rr = make_int2(0, 0);
     if (batch < nbatch) {
-        a.ib = __ldg(inc_ptr + li);
-        a.ie = __ldg(inc_ptr + li + 1);
+        const int li = min(batch * 32 + lane, n_rows - 1);
         a.rr = __ldg(rec + li);
-    } else {
-        a.ib = a.ie = 0;
-        a.rr = make_int2(0, 0);
+        if (lane == 0) a.ib0 = __ldg(inc_ptr + batch * 32);
     }
     return a;
 }
@@ -163,25 +164,31 @@ __global__ void __launch_bounds__(TRI_TPB, 3) k_rows_tri(const double* __restric
         const int w0 = batch * 32;
         const int li = w0 + lane;
         const bool live = li < n_rows;
-        const int t = live ? c1.ie - c1.ib : 0;
-        const int ib0 = __shfl_sync(0xffffffffu, c1.ib, 0);
-        const int nlast = min(32, n_rows - w0) - 1;
-        const int ie_last = __shfl_sync(0xffffffffu, c1.ie, nlast);
+        const bool two = c1.rr.x != c1.rr.y;
+        const int t = live ? 1 + two : 0;
+        int incl = t;  // warp inclusive scan of t
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        const int ib0 = __shfl_sync(0xffffffffu, c1.ib0, 0);
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        const int nr = min(32, n_rows - w0);
         const int gbase = row0 + w0 + 2 * ib0 - out_base;
-        const int segn = (nlast + 1) + 2 * (ie_last - ib0);
-        const int o = lane + 2 * (c1.ib - ib0);
+        const int segn = nr + 2 * tot;
+        const int o = lane + 2 * (incl - t);
         if (forms & EFEM_PATTERN) {
             if (live) row_ptr_out[li] = gbase + o;
             if (li == n_rows - 1) row_ptr_out[n_rows] = gbase + segn;
         }
-        const bool bad = live && (t < 1 || t > 2);
-        if (bad) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
+        // (rows of more than two elements are flagged by the symbolic pass)
+        const bool bad = false;
         if (!__any_sync(0xffffffffu, bad) && segn <= WSEG) {
             if (live) {
                 double m0a, k0a, m1a, k1a, m2a, k2a, m0b, k0b, m1b, k1b, m2b, k2b;
                 const double da = tri_row(T0, m0a, k0a, m1a, k1a, m2a, k2a);
                 const double db = tri_row(T1, m0b, k0b, m1b, k1b, m2b, k2b);
-                const bool two = t == 2;
                 const bool bad_a = !(fabs(da) > 0.0 && fabs(da) < INFINITY);
                 const bool bad_b = two && !(fabs(db) > 0.0 && fabs(db) < INFINITY);
                 if (bad_a || bad_b) {

@@ -149,6 +149,7 @@ struct NodeOut {
     int32_t* row_ptr;
     int32_t* d2n;  // optional
     int2* rec;     // 2D edges / 3D faces: {first, last} instance of each row
+    int* flags;    // WsHeader flags
     int32_t* bucket;
     int64_t* totals;  // [0] n_dofs, [1] nnz
     unsigned long long* status;
@@ -397,7 +398,11 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
             if constexpr (NE3) {
                 if (j > 0) nnz_run += 1 + 2 * link_count_fast<KT>(elems, a, run_b, run0, j, inst_at) + (j - run0);
             } else {
-                if (j > 0) out.rec[id] = make_int2(first, prev);
+                if (j > 0) {
+                    out.rec[id] = make_int2(first, prev);
+                    // a conforming mesh has <= 2 elements per edge (2D) / face (3D)
+                    if (j - run0 > 2) atomicOr(&out.flags[F_ROW_MISMATCH], 1);
+                }
                 first = inst;
             }
             ++id;
@@ -427,7 +432,10 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
     if constexpr (NE3) {
         if (n > 0) nnz_run += 1 + 2 * link_count_fast<KT>(elems, a, run_b, run0, n, inst_at) + (n - run0);
     } else {
-        if (n > 0) out.rec[id] = make_int2(first, prev);
+        if (n > 0) {
+            out.rec[id] = make_int2(first, prev);
+            if (n - run0 > 2) atomicOr(&out.flags[F_ROW_MISMATCH], 1);
+        }
     }
     if (a == n_nodes - 1) {
         const int R = id + 1;
@@ -501,7 +509,8 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
         count_launch(2);
     }
     // pass B: DOF ids, elems2dofs, incidence (+ row_ptr for 3D edges)
-    NodeOut o{p.e2d, p.inc_ptr, p.row_ptr, p.want_d2n ? p.d2n : nullptr, p.rec, p.bucket, p.d_totals, nullptr, nullptr};
+    NodeOut o{p.e2d,    p.inc_ptr, p.row_ptr,  p.want_d2n ? p.d2n : nullptr, p.rec, reinterpret_cast<int*>(reinterpret_cast<char*>(p.hdr) + offsetof(WsHeader, flags)),
+              p.bucket, p.d_totals, nullptr,    nullptr};
     k_node_write<KT><<<grid_for(N, 256), 256, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.ent_ptr, p.nnz_ptr, N, o);
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;
