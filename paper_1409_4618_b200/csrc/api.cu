@@ -25,7 +25,7 @@ std::atomic<int64_t> g_launches{0};
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-    size_t hdr, cnt, bucket_ptr, bucket, e2d, inc_ptr, row_ptr, rec, d2n, ent_ptr, nnz_cnt, nnz_ptr, lb, totals, cub, total;
+    size_t hdr, cnt, bucket_ptr, bucket, bkey, binst, bx, nbr, e2d, inc_ptr, row_ptr, rec, d2n, ent_ptr, nnz_cnt, nnz_ptr, lb, totals, cub, total;
 };
 
 Layout layout(const Plan& p, size_t cub_bytes) {
@@ -42,6 +42,11 @@ Layout layout(const Plan& p, size_t cub_bytes) {
     L.cnt = take(N1 * 4);
     L.bucket_ptr = take(N1 * 4);
     L.bucket = take(Tm * 4);
+    const bool faces = p.dim == 3 && p.element == EFEM_RT0;
+    L.bkey = take(Tm * 8);
+    L.binst = take(faces ? Tm * 4 : 4);
+    L.bx = take(p.dim == 3 && !faces ? Tm * 4 : 4);
+    L.nbr = take(p.dim == 3 && !faces ? (size_t)p.r_max * 4 : 4);
     L.e2d = take(Tm * 4);
     L.inc_ptr = take(((size_t)p.r_max + 1) * 4);
     const bool ne3 = p.dim == 3 && p.element == EFEM_NED0;
@@ -306,10 +311,10 @@ efem_status efem_plan_create(efem_plan* plan, const efem_mesh* mesh, efem_elemen
     p->elems = mesh->elems;
     p->r_max = p->n_elems * p->m;
     const int64_t nnz_c = (p->dim == 3 && element == EFEM_NED0) ? 5 : p->m - 1;
-    if (p->n_elems >= (1ll << 28) || p->n_nodes >= (1ll << 31) - 1 || p->r_max * p->ek >= (1ll << 31) ||
+    if (p->n_elems >= (1ll << 27) || p->n_nodes >= (1ll << 31) - 1 || p->r_max * p->ek >= (1ll << 31) ||
         p->r_max + nnz_c * p->n_elems * p->m >= (1ll << 31)) {
         delete p;
-        set_error("efem_plan_create: mesh too large for int32 indexing (n_elems < 2^28)");
+        set_error("efem_plan_create: mesh too large for int32 indexing (n_elems < 2^27)");
         return EFEM_EOVERFLOW;
     }
     size_t cub_bytes = 0;
@@ -342,6 +347,10 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     p->cnt = reinterpret_cast<int32_t*>(b + L.cnt);
     p->bucket_ptr = reinterpret_cast<int32_t*>(b + L.bucket_ptr);
     p->bucket = reinterpret_cast<int32_t*>(b + L.bucket);
+    p->bkey = reinterpret_cast<uint64_t*>(b + L.bkey);
+    p->binst = reinterpret_cast<int32_t*>(b + L.binst);
+    p->bx = reinterpret_cast<int32_t*>(b + L.bx);
+    p->nbr = reinterpret_cast<int32_t*>(b + L.nbr);
     p->e2d = reinterpret_cast<int32_t*>(b + L.e2d);
     p->inc_ptr = reinterpret_cast<int32_t*>(b + L.inc_ptr);
     p->row_ptr = reinterpret_cast<int32_t*>(b + L.row_ptr);

@@ -481,7 +481,30 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
             // all index loads first, then all element loads: two round trips
             // (slots j >= t repeat the last incidence and are masked below)
 #pragma unroll
-            for (int j = 0; j < NE3_TMAX; ++j) inst[j] = __ldg(inc + ib + min(j, t - 1)) & 0x7fffffff;
+            for (int j = 0; j < NE3_TMAX; ++j) inst[j] = __ldg(inc + ib + min(j, t - 1)) & INST_MASK;
+            {   // ascending element id (the symbolic pass groups a node's tets
+                // by edge without ordering them): a fixed summation order
+                int srt[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) srt[j] = j < t && j < NE3_TMAX ? inst[j] : INT_MAX;
+#pragma unroll
+                for (int kk = 2; kk <= 8; kk <<= 1)
+#pragma unroll
+                    for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) {
+                            const int y = x ^ jj;
+                            if (y > x) {
+                                const int lo = min(srt[x], srt[y]), hi = max(srt[x], srt[y]);
+                                const bool asc = (x & kk) == 0;
+                                srt[x] = asc ? lo : hi;
+                                srt[y] = asc ? hi : lo;
+                            }
+                        }
+                const int last = srt[max(min(t, NE3_TMAX) - 1, 0)];
+#pragma unroll
+                for (int j = 0; j < NE3_TMAX; ++j) inst[j] = j < t ? srt[j] : last;
+            }
             int4 gq[NE3_TMAX];
 #pragma unroll
             for (int j = 0; j < NE3_TMAX; ++j) gq[j] = __ldg(reinterpret_cast<const int4*>(elems) + (inst[j] >> 3));

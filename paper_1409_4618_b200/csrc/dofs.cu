@@ -6,27 +6,34 @@
 // lexicographic rank of its ascending node tuple (reading C10).  Instead of a
 // global radix sort of T*m keys, every (element,
 // local entity) INSTANCE is bucketed by the entity's minimum node a with one
-// counting sort:
-//   k_bucket<count>  instances per minimum node          (warp-aggregated atomics)
+// counting sort, then sorted inside its bucket:
+//   k_bucket<count>  instances per minimum node (one atomic per distinct
+//                    minimum node of an element, not per instance)
 //   CUB scan         -> bucket_ptr
-//   k_bucket<fill>   scatter (e << 3 | k) into the buckets
-//   k_node_entities  per node: sort its bucket by (other nodes, element id);
+//   k_bucket<fill>   scatter each instance's sort key (its other nodes, and
+//                    e << 3 | k) into the buckets -- no later pass gathers
+//                    elements again
+//   k_node_count     per node: sort its bucket by (other nodes, element id);
 //                    runs of equal keys are its entities, numbered
 //                    ent_ptr[a] + run index, which IS the lexicographic rank.
-//                    The sorted bucket is the entity -> element incidence
-//                    (ascending element id per entity), inc_ptr = run starts.
-//                    Row lengths (exact, no union needed):
+//                    Writes the sorted instances (the entity -> element
+//                    incidence, ascending element id per entity) with a
+//                    RUN_FLAG on each run start.  Row lengths (no union):
 //                      2D edges / 3D faces: 1 + (m-1) t   (two elements share
 //                        at most one entity of that kind),
-//                      3D edges: 1 + 2 L + t   (L distinct link vertices c give
-//                        edges a-c and b-c; each tet adds one link edge),
-//                    t = elements containing the entity.  Node offsets of both
-//                    entities and row entries come from one decoupled
-//                    look-back scan inside the same kernel.
+//                      3D edges: 1 + 2 L + t, L the distinct link vertices
+//                        (each gives edges a-c, b-c; each tet adds its link
+//                        edge).  The link of an edge is a cycle (interior:
+//                        L = t) or a path (boundary: L = t + 1); the XOR of
+//                        all link-vertex occurrences is 0 exactly for the
+//                        cycle, so L = t + [xor != 0] (BND_FLAG).  The numeric
+//                        kernel re-derives every row's column set and flags
+//                        a mismatch (non-manifold fans) as non-conforming.
+//   CUB scan(s)      -> ent_ptr (+ nnz_ptr for 3D edges)
+//   k_node_write     DOF ids, elems2dofs, inc_ptr, row records / row_ptr
 #include <cub/cub.cuh>
 
 #include "efem_internal.cuh"
-#include "scan.cuh"
 
 namespace efem {
 
@@ -98,49 +105,86 @@ __device__ __forceinline__ int local_sign(const int (&g)[KT::NV], int k) {
 }
 
 // ---------------------------------------------------------------------------------
-// counting sort of instances by minimum node (warp-aggregated atomics)
+// counting sort of instances by minimum node
 // ---------------------------------------------------------------------------------
+struct BucketArrays {
+    uint64_t* key;  // edges: other node << 32 | inst; faces: mid << 32 | hi
+    int32_t* inst;  // faces only: e << 3 | k
+    int32_t* x;     // 3D edges only: xor of the tet's four vertex ids
+};
+
 template <class KT, bool FILL>
 __global__ void __launch_bounds__(256) k_bucket(const int32_t* __restrict__ elems, int64_t n_elems, int64_t n_nodes,
                                                 int32_t* __restrict__ cnt, const int32_t* __restrict__ bucket_ptr,
-                                                int32_t* __restrict__ bucket, WsHeader* hdr) {
+                                                BucketArrays B, WsHeader* hdr) {
+    constexpr int M = KT::M;
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool live = e < n_elems;
+    if (e >= n_elems) return;
     int g[KT::NV];
-    if (live) {
-        load_elem<KT>(elems, (int)e, g);
-        bool bad = false;
+    load_elem<KT>(elems, (int)e, g);
+    bool bad = false;
 #pragma unroll
-        for (int v = 0; v < KT::NV; ++v) bad |= (unsigned)g[v] >= (unsigned long long)n_nodes;
-        if (bad) {
-            atomicOr(&hdr->flags[F_INVALID_NODE], 1);
+    for (int v = 0; v < KT::NV; ++v) bad |= (unsigned)g[v] >= (unsigned long long)n_nodes;
+    if (bad) {
+        if (!FILL) atomicOr(&hdr->flags[F_INVALID_NODE], 1);
 #pragma unroll
-            for (int v = 0; v < KT::NV; ++v) g[v] = 0;
-        }
+        for (int v = 0; v < KT::NV; ++v) g[v] = 0;
     }
-    if (!live) return;
+    int amin[M];
 #pragma unroll
-    for (int k = 0; k < KT::M; ++k) {
-        const int a = entity_min_node<KT>(g, k);
-        if constexpr (!FILL) {
-            atomicAdd(&cnt[a], 1);
-        } else {
-            const int pos = atomicAdd(&cnt[a], 1);
-            bucket[__ldg(bucket_ptr + a) + pos] = (int)((e << 3) | k);
+    for (int k = 0; k < M; ++k) amin[k] = entity_min_node<KT>(g, k);
+    // one atomic per distinct minimum node of the element; its instances take
+    // consecutive slots in local order
+    int slot[M];
+    bool owner[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        bool first = true;
+        int before = 0, total = 0;
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+            const bool same = amin[q] == amin[k];
+            if (q < k) {
+                first &= !same;
+                before += same;
+            }
+            total += same;
+        }
+        owner[k] = first;
+        slot[k] = first ? atomicAdd(&cnt[amin[k]], total) : before;
+    }
+    if constexpr (FILL) {
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            int base = slot[k];
+            if (!owner[k]) {
+#pragma unroll
+                for (int q = 0; q < M; ++q)
+                    if (q < k && owner[q] && amin[q] == amin[k]) base = slot[q] + slot[k];
+            }
+            const int64_t pos = (int64_t)__ldg(bucket_ptr + amin[k]) + base;
+            const int inst = (int)((e << 3) | k);
+            if constexpr (KT::FACES) {
+                B.key[pos] = entity_key<KT>(g, k);
+                B.inst[pos] = inst;
+            } else {
+                B.key[pos] = (entity_key<KT>(g, k) << 32) | (uint32_t)inst;
+                if constexpr (KT::D == 3) B.x[pos] = g[0] ^ g[1] ^ g[2] ^ g[3];
+            }
         }
     }
 }
 
 // ---------------------------------------------------------------------------------
-// per node: sort bucket, number entities, incidence, row lengths, look-back
+// per node: sort the bucket, count entities and row entries
 // ---------------------------------------------------------------------------------
 template <class KT>
 struct NodeCaps {
-    // instances per node held in shared memory (one 64-bit sort key each;
-    // faces add a 32-bit instance word); larger buckets take a global-memory
-    // slow path
+    // instances per node held in shared memory; larger buckets take a
+    // global-memory slow path
     static constexpr int CAP = KT::D == 2 ? 16 : (KT::FACES ? 32 : 48);
     static constexpr int TPB = KT::D == 2 ? 128 : 64;
+    static constexpr int DCAP = 16;  // 3D edges: distinct larger neighbours held in shared memory
 };
 
 struct NodeOut {
@@ -148,22 +192,22 @@ struct NodeOut {
     int32_t* inc_ptr;
     int32_t* row_ptr;
     int32_t* d2n;  // optional
+    int32_t* nbr;  // 3D edges: larger endpoint b of every edge (DOF id order)
     int2* rec;     // 2D edges / 3D faces: {first, last} instance of each row
     int* flags;    // WsHeader flags
     int32_t* bucket;
     int64_t* totals;  // [0] n_dofs, [1] nnz
-    unsigned long long* status;
-    int* ticket;
 };
+
+// Bucket words after k_node_count: instances e << 3 | k (INST_MASK); bit 31
+// marks the first instance of every entity run, bit 30 (3D edges, on run
+// starts) a boundary edge (open link path).
+constexpr unsigned RUN_FLAG = 0x80000000u;
+constexpr unsigned BND_FLAG = 0x40000000u;
 
 // Sort item of an instance.  Edges: one u64 (other node << 32 | e << 3 | k),
 // so sorting the word sorts by (entity, element).  Faces: u64 (mid << 32 | hi)
 // plus the instance word as tie-break.
-// Bucket words are instances e << 3 | k; k_node_count sets bit 31 on the
-// first instance of every entity run (consumers mask with INST_MASK).
-constexpr int INST_MASK = 0x7fffffff;
-constexpr unsigned RUN_FLAG = 0x80000000u;
-
 template <class KT>
 struct Item {
     uint64_t key;
@@ -179,204 +223,281 @@ struct Item {
 };
 
 template <class KT>
-__device__ __forceinline__ Item<KT> make_item(const int32_t* __restrict__ elems, int inst) {
-    inst &= INST_MASK;
-    int g[KT::NV];
-    load_elem<KT>(elems, inst >> 3, g);
+__device__ __forceinline__ Item<KT> load_item(const BucketArrays& B, int64_t pos) {
     Item<KT> it;
-    if constexpr (KT::FACES) {
-        it.key = entity_key<KT>(g, inst & 7);
-        it.inst = inst;
-    } else {
-        it.key = (entity_key<KT>(g, inst & 7) << 32) | (uint32_t)inst;
-        it.inst = inst;
-    }
+    it.key = B.key[pos];
+    if constexpr (KT::FACES) it.inst = B.inst[pos];
+    else it.inst = (int)(uint32_t)it.key;
     return it;
 }
 
-// number of distinct link vertices (nodes other than a, b) over the tets of
-// one edge run; every tet contributes exactly two
-template <class KT, class InstAt>
-__device__ __forceinline__ int link_count(const int32_t* __restrict__ elems, int a, int b, int j, int q,
-                                          InstAt inst_at) {
-    constexpr int CAPL = 2 * EFEM_MAX_ROW_ELEMS;
-    int lk[CAPL];
-    int nl = 0, L = 0;
-    for (int u = j; u < q; ++u) {
-        int h[4];
-        load_elem<KT>(elems, inst_at(u) >> 3, h);
+// 2D edges, 3D faces: sort by (entity, element), flag runs.
+template <class KT, bool SMEM>
+__device__ __forceinline__ void node_sort_generic(const BucketArrays& B, int32_t* __restrict__ gb, int64_t beg,
+                                                  int n, uint64_t* s_key, int* s_inst, int& n_ent) {
+    constexpr int CAP = NodeCaps<KT>::CAP;
+    constexpr int TPB = NodeCaps<KT>::TPB;
+    const bool in_smem = SMEM && n <= CAP;
+    uint64_t* K = s_key + threadIdx.x;  // item j at [j * TPB]
+    int* V = s_inst + (KT::FACES ? threadIdx.x : 0);
+    // slow path (n > CAP): sort in place in the bucket-key arrays (global)
+    auto get = [&](int j) -> Item<KT> {
+        if (in_smem) {
+            Item<KT> it;
+            it.key = K[j * TPB];
+            if constexpr (KT::FACES) it.inst = V[j * TPB];
+            else it.inst = (int)(uint32_t)it.key;
+            return it;
+        }
+        return load_item<KT>(B, beg + j);
+    };
+    auto put = [&](int j, const Item<KT>& it) {
+        if (in_smem) {
+            K[j * TPB] = it.key;
+            if constexpr (KT::FACES) V[j * TPB] = it.inst;
+        } else {
+            B.key[beg + j] = it.key;
+            if constexpr (KT::FACES) B.inst[beg + j] = it.inst;
+        }
+    };
+    if (in_smem) {
+#pragma unroll 4
+        for (int j = 0; j < n; ++j) put(j, load_item<KT>(B, beg + j));
+    }
+    for (int j = 1; j < n; ++j) {
+        const Item<KT> it = get(j);
+        int q = j;
+        while (q > 0) {
+            const Item<KT> prev = get(q - 1);
+            if (!(it < prev)) break;
+            put(q, prev);
+            --q;
+        }
+        put(q, it);
+    }
+    uint64_t prev = 0;
+    for (int j = 0; j < n; ++j) {
+        const Item<KT> it = get(j);
+        const bool st = j == 0 || it.entity() != prev;
+        prev = it.entity();
+        n_ent += st;
+        gb[j] = (int)((uint32_t)it.inst | (st ? RUN_FLAG : 0u));
+    }
+}
+
+// 3D edges: group the node's instances by the other node b -- sorted
+// distinct list D (<= DCAP) in shared memory, then a counting scatter.  The
+// order inside a group (the tets of one edge) is left as the fill produced
+// it; the numeric kernel sorts each row's tets by element id, so sums stay
+// in a fixed order.  Also per group: t, and the xor of its link edges
+// (BND_FLAG, see the file comment).  Writes the grouped instance words (RUN
+// flag on group starts) and b << 32 at every group start of the key array
+// (read by k_node_write).  Returns false when the node has more than DCAP
+// distinct larger neighbours (caller falls back to the generic sort).
+template <class KT>
+__device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* __restrict__ gb, int64_t beg, int n,
+                                               int a, int* s_grp, int& n_ent, int& n_nnz) {
+    constexpr int TPB = NodeCaps<KT>::TPB;
+    constexpr int DCAP = NodeCaps<KT>::DCAP;
+    int* D = s_grp + threadIdx.x;  // [p * TPB]: distinct b, ascending
+    int* C = D + DCAP * TPB;       // counts, then running cursors
+    int* S = C + DCAP * TPB;       // group starts
+    int* X = S + DCAP * TPB;       // xor of link edges
+    const uint64_t* __restrict__ key = B.key + beg;
+    const int32_t* __restrict__ xr = B.x + beg;
+    int nd = 0;
+    bool over = false;
+    constexpr int U = 4;  // keys loaded ahead of use
+    for (int j0 = 0; j0 < n; j0 += U) {
+        int bb[U];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int c = h[v];
-            if (c == a || c == b) continue;
-            bool seen = false;
-            for (int w = 0; w < nl; ++w) seen |= lk[w] == c;
-            if (!seen) {
-                ++L;
-                if (nl < CAPL) lk[nl++] = c;
+        for (int u = 0; u < U; ++u) bb[u] = j0 + u < n ? (int)(__ldg(key + j0 + u) >> 32) : -1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int b = bb[u];
+            if (b < 0) continue;
+            int p = 0;
+            while (p < nd && D[p * TPB] < b) ++p;
+            if (p < nd && D[p * TPB] == b) {
+                C[p * TPB] += 1;
+            } else if (nd == DCAP) {
+                over = true;
+            } else {
+                for (int q = nd; q > p; --q) {
+                    D[q * TPB] = D[(q - 1) * TPB];
+                    C[q * TPB] = C[(q - 1) * TPB];
+                }
+                D[p * TPB] = b;
+                C[p * TPB] = 1;
+                ++nd;
             }
         }
     }
-    return L;
+    if (over) return false;
+    int off = 0;
+    for (int p = 0; p < nd; ++p) {
+        const int c = C[p * TPB];
+        C[p * TPB] = off;
+        S[p * TPB] = off;
+        X[p * TPB] = 0;
+        off += c;
+    }
+    for (int j0 = 0; j0 < n; j0 += U) {
+        uint64_t kk[U];
+        int xx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            kk[u] = j0 + u < n ? __ldg(key + j0 + u) : 0ull;
+            xx[u] = j0 + u < n ? __ldg(xr + j0 + u) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (j0 + u >= n) continue;
+            const int b = (int)(kk[u] >> 32);
+            int lo = 0, hi = nd - 1;  // D sorted, b present
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (D[mid * TPB] < b) lo = mid + 1; else hi = mid;
+            }
+            const int pos = C[lo * TPB];
+            C[lo * TPB] = pos + 1;
+            X[lo * TPB] ^= xx[u] ^ a ^ b;  // c ^ d of this tet
+            gb[pos] = (int)((uint32_t)kk[u] | (pos == S[lo * TPB] ? RUN_FLAG : 0u));
+        }
+    }
+    int nnz = 0;
+    for (int p = 0; p < nd; ++p) {
+        const int st = S[p * TPB];
+        const int t = C[p * TPB] - st;
+        const bool bnd = X[p * TPB] != 0;  // open link path: L = t + 1
+        if (bnd) atomicOr(gb + st, (int)BND_FLAG);
+        B.key[beg + st] = (uint64_t)(uint32_t)D[p * TPB] << 32;
+        nnz += 1 + 3 * t + 2 * (int)bnd;
+    }
+    n_ent = nd;
+    n_nnz = nnz;
+    return true;
 }
 
-// t <= 8: the 2t link values in registers, distinct count by pairwise compares
-template <class KT, class InstAt>
-__device__ __forceinline__ int link_count_fast(const int32_t* __restrict__ elems, int a, int b, int j, int q,
-                                               InstAt inst_at) {
-    const int t = q - j;
-    if (t > 8) return link_count<KT>(elems, a, b, j, q, inst_at);
-    int lk[16];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        if (u < t) {
+// 3D edges, fallback: after node_sort_generic, per run count the distinct
+// link vertices exactly and set BND_FLAG = (L > t)
+template <class KT>
+__device__ __forceinline__ void ne3_runs_exact(const int32_t* __restrict__ elems, int32_t* __restrict__ gb, int n,
+                                               int a, int& n_nnz) {
+    int j = 0;
+    while (j < n) {
+        int q = j + 1;
+        while (q < n && !(gb[q] < 0)) ++q;
+        // edge (a, b): b from the first tet of the run
+        const int i0 = gb[j] & INST_MASK;
+        int g[4];
+        load_elem<KT>(elems, i0 >> 3, g);
+        const int b = (int)entity_key<KT>(g, i0 & 7);
+        int L = 0;
+        for (int u = j; u < q; ++u) {
             int h[4];
-            load_elem<KT>(elems, inst_at(j + u) >> 3, h);
-            // the two vertices other than a and b, in local order
-            int c = -1, d = -1;
+            load_elem<KT>(elems, (gb[u] & INST_MASK) >> 3, h);
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                const bool link = h[v] != a && h[v] != b;
-                d = (link && c >= 0 && d < 0) ? h[v] : d;
-                c = (link && c < 0) ? h[v] : c;
+                const int c = h[v];
+                if (c == a || c == b) continue;
+                bool seen = false;  // seen in an earlier tet of the run (or earlier in this one)
+                for (int w = j; w < u && !seen; ++w) {
+                    int f[4];
+                    load_elem<KT>(elems, (gb[w] & INST_MASK) >> 3, f);
+                    seen = f[0] == c || f[1] == c || f[2] == c || f[3] == c;
+                }
+                L += !seen;
             }
-            lk[2 * u] = c;
-            lk[2 * u + 1] = d;
-        } else {
-            lk[2 * u] = -1 - 2 * u;  // distinct sentinels never counted
-            lk[2 * u + 1] = -2 - 2 * u;
         }
+        // rows are sized 1 + 3t + 2 [L > t]; any other L (non-manifold fan)
+        // makes the numeric kernel's exact column count disagree -> flagged
+        const int t = q - j;
+        const bool bnd = L > t;
+        if (bnd) gb[j] = (int)((uint32_t)gb[j] | BND_FLAG);
+        n_nnz += 1 + 3 * t + 2 * (int)bnd;
+        j = q;
     }
-    int L = 0;
-#pragma unroll
-    for (int x = 0; x < 16; ++x) {
-        bool dup = false;
-#pragma unroll
-        for (int y = 0; y < x; ++y) dup |= lk[y] == lk[x];
-        L += (x < 2 * t) && !dup;
-    }
-    return L;
 }
 
-// Pass A: per node, sort its bucket in place by (entity, element) and count
-// its entities and the CSR entries of their rows.
 template <class KT>
 __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t* __restrict__ elems,
                                                                   const int32_t* __restrict__ bucket_ptr,
-                                                                  int32_t* __restrict__ bucket, int64_t n_nodes,
-                                                                  int32_t* __restrict__ ent_cnt,
+                                                                  BucketArrays B, int32_t* __restrict__ bucket,
+                                                                  int64_t n_nodes, int32_t* __restrict__ ent_cnt,
                                                                   int32_t* __restrict__ nnz_cnt) {
+    constexpr bool NE3 = KT::D == 3 && !KT::FACES;
     constexpr int CAP = NodeCaps<KT>::CAP;
     constexpr int TPB = NodeCaps<KT>::TPB;
-    __shared__ uint64_t s_key[CAP * TPB];
+    constexpr int DCAP = NodeCaps<KT>::DCAP;
+    __shared__ uint64_t s_key[NE3 ? 1 : CAP * TPB];
     __shared__ int s_inst[KT::FACES ? CAP * TPB : 1];
+    __shared__ int s_grp[NE3 ? 4 * DCAP * TPB : 1];
     const int64_t a64 = (int64_t)blockIdx.x * TPB + threadIdx.x;
     if (a64 >= n_nodes) return;
     const int a = (int)a64;
-    const int beg = __ldg(bucket_ptr + a);
-    const int n = __ldg(bucket_ptr + a + 1) - beg;
+    const int64_t beg = __ldg(bucket_ptr + a);
+    const int n = __ldg(bucket_ptr + a + 1) - (int)beg;
     int32_t* gb = bucket + beg;
     int n_ent = 0, n_nnz = 0;
     constexpr int NREG = 8;
-    if (KT::D == 2 && n <= NREG) {
-        // register path: bitonic network over 8 keys
-        uint64_t rk[NREG];
+    if constexpr (KT::D == 2) {
+        if (n <= NREG) {
+            // register path: bitonic network over 8 keys
+            uint64_t rk[NREG];
 #pragma unroll
-        for (int j = 0; j < NREG; ++j) rk[j] = j < n ? make_item<KT>(elems, __ldg(gb + j)).key : ~0ull;
+            for (int j = 0; j < NREG; ++j) rk[j] = j < n ? B.key[beg + j] : ~0ull;
 #pragma unroll
-        for (int kk = 2; kk <= NREG; kk <<= 1)
+            for (int kk = 2; kk <= NREG; kk <<= 1)
 #pragma unroll
-            for (int jj = kk >> 1; jj > 0; jj >>= 1)
+                for (int jj = kk >> 1; jj > 0; jj >>= 1)
 #pragma unroll
-                for (int x = 0; x < NREG; ++x) {
-                    const int y = x ^ jj;
-                    if (y > x) {
-                        const bool sw = rk[x] > rk[y];
-                        const bool asc = (x & kk) == 0;
-                        const uint64_t lo = sw ? rk[y] : rk[x], hi = sw ? rk[x] : rk[y];
-                        rk[x] = asc ? lo : hi;
-                        rk[y] = asc ? hi : lo;
+                    for (int x = 0; x < NREG; ++x) {
+                        const int y = x ^ jj;
+                        if (y > x) {
+                            const bool sw = rk[x] > rk[y];
+                            const bool asc = (x & kk) == 0;
+                            const uint64_t lo = sw ? rk[y] : rk[x], hi = sw ? rk[x] : rk[y];
+                            rk[x] = asc ? lo : hi;
+                            rk[y] = asc ? hi : lo;
+                        }
                     }
-                }
 #pragma unroll
-        for (int x = 0; x < NREG; ++x)
-            if (x < n) {
-                const bool st = x == 0 || (rk[x] >> 32) != (rk[x - 1] >> 32);
-                n_ent += st;
-                gb[x] = (int)((uint32_t)rk[x] | (st ? RUN_FLAG : 0u));
-            }
-        n_nnz = n_ent + (KT::M - 1) * n;
+            for (int x = 0; x < NREG; ++x)
+                if (x < n) {
+                    const bool st = x == 0 || (rk[x] >> 32) != (rk[x - 1] >> 32);
+                    n_ent += st;
+                    gb[x] = (int)((uint32_t)rk[x] | (st ? RUN_FLAG : 0u));
+                }
+        } else {
+            node_sort_generic<KT, true>(B, gb, beg, n, s_key, s_inst, n_ent);
+        }
+    } else if constexpr (KT::FACES) {
+        node_sort_generic<KT, true>(B, gb, beg, n, s_key, s_inst, n_ent);
     } else {
-        const bool in_smem = n <= CAP;
-        uint64_t* K = s_key + threadIdx.x;  // item j at [j * TPB]
-        int* V = s_inst + (KT::FACES ? threadIdx.x : 0);
-        auto get = [&](int j) -> Item<KT> {
-            if (in_smem) {
-                Item<KT> it;
-                it.key = K[j * TPB];
-                if constexpr (KT::FACES) it.inst = V[j * TPB];
-                else it.inst = (int)(uint32_t)it.key;
-                return it;
-            }
-            return make_item<KT>(elems, gb[j]);
-        };
-        auto put = [&](int j, const Item<KT>& it) {
-            if (in_smem) {
-                K[j * TPB] = it.key;
-                if constexpr (KT::FACES) V[j * TPB] = it.inst;
-            } else {
-                gb[j] = it.inst;
-            }
-        };
-        if (in_smem) {
-#pragma unroll 4
-            for (int j = 0; j < n; ++j) {
-                const Item<KT> it = make_item<KT>(elems, __ldg(gb + j));
-                K[j * TPB] = it.key;
-                if constexpr (KT::FACES) V[j * TPB] = it.inst;
-            }
+        if (!node_group_ne3<KT>(B, gb, beg, n, a, s_grp, n_ent, n_nnz)) {
+            n_ent = 0;
+            n_nnz = 0;
+            // (the NE3 instantiation has no key smem: sort in global memory)
+            node_sort_generic<KT, false>(B, gb, beg, n, s_key, s_inst, n_ent);
+            ne3_runs_exact<KT>(elems, gb, n, a, n_nnz);
         }
-        for (int j = in_smem ? 1 : 0; j < n; ++j) {
-            const Item<KT> it = in_smem ? get(j) : make_item<KT>(elems, gb[j]);
-            int q = j;
-            while (q > 0) {
-                const Item<KT> prev = get(q - 1);
-                if (!(it < prev)) break;
-                put(q, prev);
-                --q;
-            }
-            put(q, it);
-        }
-        auto inst_at = [&](int j) -> int { return (in_smem ? get(j).inst : gb[j]) & INST_MASK; };
-        for (int j = 0; j < n;) {
-            const uint64_t ek = get(j).entity();
-            int q = j + 1;
-            while (q < n && get(q).entity() == ek) ++q;
-            if constexpr (KT::D == 3 && !KT::FACES)
-                n_nnz += 1 + 2 * link_count_fast<KT>(elems, a, (int)ek, j, q, inst_at) + (q - j);
-            ++n_ent;
-            if (in_smem)
-                for (int u = j; u < q; ++u) gb[u] = (int)((uint32_t)get(u).inst | (u == j ? RUN_FLAG : 0u));
-            else
-                gb[j] = (int)((uint32_t)gb[j] | RUN_FLAG);
-            j = q;
-        }
-        if constexpr (!(KT::D == 3 && !KT::FACES)) n_nnz = n_ent + (KT::M - 1) * n;
     }
     ent_cnt[a] = n_ent;
-    if constexpr (KT::D == 3 && !KT::FACES) nnz_cnt[a] = n_nnz;
+    if constexpr (NE3) nnz_cnt[a] = n_nnz;
 }
 
 // Pass B: per node, walk its sorted bucket: DOF ids (ent_ptr[a] + run),
-// elems2dofs, the incidence offsets, dofs2nodes (on request).  Runs are read
-// from the RUN_FLAG bits pass A left, so no element is gathered except for
-// NE0 3D row lengths (link vertices) and dofs2nodes.  Only NE0 3D writes
-// row_ptr here; for 2D edges and 3D faces row i starts at
-// i + (m-1) inc_ptr[i] (closed form, written by the numeric kernel).
+// elems2dofs, the incidence offsets, dofs2nodes (on request).  Runs and row
+// lengths come from the flags pass A left, so no element is gathered except
+// for dofs2nodes.  2D edges / 3D faces write row records {first, last}
+// instance (row i starts at i + (m-1) inc_ptr[i], closed form); 3D edges
+// write row_ptr.
 template <class KT>
 __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ elems,
                                                     const int32_t* __restrict__ bucket_ptr,
                                                     const int32_t* __restrict__ bucket,
+                                                    const uint64_t* __restrict__ bkey,
                                                     const int32_t* __restrict__ ent_ptr,
                                                     const int32_t* __restrict__ nnz_ptr, int64_t n_nodes,
                                                     NodeOut out) {
@@ -389,54 +510,54 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
     const int32_t* gb = bucket + beg;
     int id = __ldg(ent_ptr + a) - 1;
     int nnz_run = NE3 ? __ldg(nnz_ptr + a) : 0;
-    auto inst_at = [&](int j) -> int { return __ldg(gb + j) & INST_MASK; };
-    int run0 = 0, run_b = 0, first = 0, prev = 0;
+    int run0 = 0, first = 0, prev = 0;
+    bool bnd = false;
+    auto close_run = [&](int j_end) {
+        const int t = j_end - run0;
+        if constexpr (NE3) {
+            nnz_run += 1 + 3 * t + 2 * (int)bnd;
+        } else {
+            out.rec[id] = make_int2(first, prev);
+            // a conforming mesh has <= 2 elements per edge (2D) / face (3D)
+            if (t > 2) atomicOr(&out.flags[F_ROW_MISMATCH], 1);
+        }
+    };
     for (int j = 0; j < n; ++j) {
         const int w = __ldg(gb + j);
         const int inst = w & INST_MASK;
         if (w < 0) {  // RUN_FLAG: first instance of a new entity
-            if constexpr (NE3) {
-                if (j > 0) nnz_run += 1 + 2 * link_count_fast<KT>(elems, a, run_b, run0, j, inst_at) + (j - run0);
-            } else {
-                if (j > 0) {
-                    out.rec[id] = make_int2(first, prev);
-                    // a conforming mesh has <= 2 elements per edge (2D) / face (3D)
-                    if (j - run0 > 2) atomicOr(&out.flags[F_ROW_MISMATCH], 1);
-                }
-                first = inst;
-            }
+            if (j > 0) close_run(j);
             ++id;
             run0 = j;
+            first = inst;
+            bnd = (w & BND_FLAG) != 0;
             out.inc_ptr[id] = beg + j;
-            if (NE3 || out.d2n) {
+            if constexpr (NE3) {
+                out.row_ptr[id] = nnz_run;
+                const int b = (int)(__ldg(bkey + beg + j) >> 32);
+                out.nbr[id] = b;
+                if (out.d2n) {
+                    out.d2n[(int64_t)id * 2] = a;
+                    out.d2n[(int64_t)id * 2 + 1] = b;
+                }
+            } else if (out.d2n) {
                 int g[KT::NV];
                 load_elem<KT>(elems, inst >> 3, g);
                 const uint64_t key = entity_key<KT>(g, inst & 7);
-                run_b = (int)key;
-                if (NE3) out.row_ptr[id] = nnz_run;
-                if (out.d2n) {
-                    int32_t* row = out.d2n + (int64_t)id * KT::EK;
-                    row[0] = a;
-                    if constexpr (KT::FACES) {
-                        row[1] = (int)(key >> 32);
-                        row[2] = (int)(key & 0xffffffffu);
-                    } else {
-                        row[1] = (int)key;
-                    }
+                int32_t* row = out.d2n + (int64_t)id * KT::EK;
+                row[0] = a;
+                if constexpr (KT::FACES) {
+                    row[1] = (int)(key >> 32);
+                    row[2] = (int)(key & 0xffffffffu);
+                } else {
+                    row[1] = (int)key;
                 }
             }
         }
-        out.e2d[(int64_t)(inst >> 3) * KT::M + (inst & 7)] = id;
+        if constexpr (!NE3) out.e2d[(int64_t)(inst >> 3) * KT::M + (inst & 7)] = id;  // 3D edges: k_elem_dofs
         prev = inst;
     }
-    if constexpr (NE3) {
-        if (n > 0) nnz_run += 1 + 2 * link_count_fast<KT>(elems, a, run_b, run0, n, inst_at) + (n - run0);
-    } else {
-        if (n > 0) {
-            out.rec[id] = make_int2(first, prev);
-            if (n - run0 > 2) atomicOr(&out.flags[F_ROW_MISMATCH], 1);
-        }
-    }
+    if (n > 0) close_run(n);
     if (a == n_nodes - 1) {
         const int R = id + 1;
         out.inc_ptr[R] = beg + n;
@@ -445,6 +566,35 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
         // 2D edges / 3D faces: nnz = sum_i (1 + (m-1) t_i) = R + (m-1) (T m)
         out.totals[1] = NE3 ? (int64_t)nnz_run : (int64_t)R + (int64_t)(KT::M - 1) * (beg + n);
     }
+}
+
+// 3D edges: elems2dofs per element (coalesced writes): the DOF of edge (a, b)
+// is ent_ptr[a] + the rank of b among a's larger neighbours nbr[ent_ptr[a] ..
+// ent_ptr[a+1]) (ascending: they are the lexicographic ranks).
+template <class KT>
+__global__ void __launch_bounds__(256) k_elem_dofs(const int32_t* __restrict__ elems, int64_t n_elems,
+                                                   const int32_t* __restrict__ ent_ptr,
+                                                   const int32_t* __restrict__ nbr, int32_t* __restrict__ e2d) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n_elems) return;
+    int g[4];
+    load_elem<KT>(elems, (int)e, g);
+    int id[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const int u = g[edge_start(3, k)], v = g[edge_end(3, k)];
+        const int a = min(u, v), b = max(u, v);
+        int lo = __ldg(ent_ptr + a), hi = __ldg(ent_ptr + a + 1) - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(nbr + mid) < b) lo = mid + 1; else hi = mid;
+        }
+        id[k] = lo;
+    }
+    int2* o = reinterpret_cast<int2*>(e2d + e * 6);  // 8-byte aligned: 6 ints per element
+    o[0] = make_int2(id[0], id[1]);
+    o[1] = make_int2(id[2], id[3]);
+    o[2] = make_int2(id[4], id[5]);
 }
 
 template <class KT>
@@ -479,17 +629,17 @@ template <class KT>
 efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     const int64_t N = p.n_nodes, T = p.n_elems;
     size_t bytes = p.cub_bytes;
+    const BucketArrays barr{p.bkey, p.binst, p.bx};
     k_init<<<grid_for(N + 1 > F_NFLAGS ? N + 1 : F_NFLAGS, 256), 256, 0, s>>>(p.hdr, p.cnt, p.nnz_cnt, N + 1);
     EFEM_LAUNCH_CHECK();
     if (T > 0) {
-        k_bucket<KT, false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, nullptr, nullptr, p.hdr);
+        k_bucket<KT, false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, nullptr, BucketArrays{}, p.hdr);
         EFEM_LAUNCH_CHECK();
     }
     EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.bucket_ptr, (int)(N + 1), s));
     count_launch(2);
     if (T > 0) {  // fill cursors: nnz_cnt (zeroed by k_init, overwritten by pass A)
-        k_bucket<KT, true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.nnz_cnt, p.bucket_ptr, p.bucket,
-                                                             p.hdr);
+        k_bucket<KT, true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.nnz_cnt, p.bucket_ptr, barr, p.hdr);
         EFEM_LAUNCH_CHECK();
     }
     if (N == 0) {
@@ -500,7 +650,7 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     // pass A: sort buckets, count entities / row entries per node (cnt reused
     // for the entity counts; cnt[N] = nnz_cnt[N] = 0 from k_init)
     constexpr int TPB = NodeCaps<KT>::TPB;
-    k_node_count<KT><<<grid_for(N, TPB), TPB, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, N, p.cnt, p.nnz_cnt);
+    k_node_count<KT><<<grid_for(N, TPB), TPB, 0, s>>>(p.elems, p.bucket_ptr, barr, p.bucket, N, p.cnt, p.nnz_cnt);
     EFEM_LAUNCH_CHECK();
     EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.ent_ptr, (int)(N + 1), s));
     count_launch(2);
@@ -509,10 +659,18 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
         count_launch(2);
     }
     // pass B: DOF ids, elems2dofs, incidence (+ row_ptr for 3D edges)
-    NodeOut o{p.e2d,    p.inc_ptr, p.row_ptr,  p.want_d2n ? p.d2n : nullptr, p.rec, reinterpret_cast<int*>(reinterpret_cast<char*>(p.hdr) + offsetof(WsHeader, flags)),
-              p.bucket, p.d_totals, nullptr,    nullptr};
-    k_node_write<KT><<<grid_for(N, 256), 256, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.ent_ptr, p.nnz_ptr, N, o);
+    int* d_flags = reinterpret_cast<int*>(reinterpret_cast<char*>(p.hdr) + offsetof(WsHeader, flags));
+    NodeOut o{p.e2d, p.inc_ptr, p.row_ptr, p.want_d2n ? p.d2n : nullptr, p.nbr, p.rec, d_flags, p.bucket,
+              p.d_totals};
+    k_node_write<KT><<<grid_for(N, 256), 256, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.bkey, p.ent_ptr, p.nnz_ptr,
+                                                       N, o);
     EFEM_LAUNCH_CHECK();
+    if constexpr (KT::D == 3 && !KT::FACES) {
+        if (T > 0) {
+            k_elem_dofs<KT><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, p.ent_ptr, p.nbr, p.e2d);
+            EFEM_LAUNCH_CHECK();
+        }
+    }
     return EFEM_OK;
 }
 

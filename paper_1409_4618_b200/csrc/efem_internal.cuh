@@ -29,6 +29,10 @@ struct WsHeader {
     long long pad;
 };
 
+// Instance words e << 3 | k (element e < 2^27, local entity k); the two top
+// bits of bucket words carry run / boundary flags (dofs.cu).
+constexpr int INST_MASK = 0x3fffffff;
+
 // ---- element kinds ------------------------------------------------------------
 // Local numbering follows PAPER.md Fig. 1 (lines 54-157), 0-based:
 //   2D edges (start->end): e0 = 1->2, e1 = 2->0, e2 = 0->1  (edge k opposite vertex k)
@@ -69,6 +73,10 @@ struct Plan {
     int32_t* bucket_ptr = nullptr;  // N+1
     int32_t* bucket = nullptr;      // T*m instances (e << 3 | k); after enumeration sorted by
                                     // (entity, element): the entity -> element incidence
+    uint64_t* bkey = nullptr;       // T*m bucket sort keys (filled by k_bucket<fill>)
+    int32_t* binst = nullptr;       // T*m instance words (3D faces only)
+    int32_t* bx = nullptr;          // T*m xor of the tet's vertices (3D edges only)
+    int32_t* nbr = nullptr;         // r_max larger endpoint of each edge (3D edges only)
     int32_t* e2d = nullptr;         // T*m elems2dofs
     int32_t* inc_ptr = nullptr;     // r_max+1 entity -> first incidence in bucket
     int32_t* row_ptr = nullptr;     // r_max+1 CSR row offsets (3D edges only; others: closed form)

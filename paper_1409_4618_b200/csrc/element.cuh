@@ -250,11 +250,22 @@ __device__ __noinline__ bool row_generic(const double* __restrict__ coords, cons
     constexpr int D = KT::D, NV = KT::NV, M = KT::M;
     bool ok = t <= EFEM_MAX_ROW_ELEMS;
     const int nt = ok ? t : EFEM_MAX_ROW_ELEMS;
+    // the row's instances in ascending element order (fixed summation order)
+    int ord[EFEM_MAX_ROW_ELEMS];
+    for (int j = 0; j < nt; ++j) {
+        const int v = __ldg(inc + ib + j) & INST_MASK;
+        int q = j;
+        while (q > 0 && ord[q - 1] > v) {
+            ord[q] = ord[q - 1];
+            --q;
+        }
+        ord[q] = v;
+    }
     // pass 1: W = sorted distinct vertices of the row's elements
     int W[WCAP + 1];
     int nw = 0;
     for (int j = 0; j < nt; ++j) {
-        const int e = (__ldg(inc + ib + j) & 0x7fffffff) >> 3;
+        const int e = ord[j] >> 3;
         int g[NV];
         load_g<KT>(elems, e, g);
 #pragma unroll
@@ -274,7 +285,7 @@ __device__ __noinline__ bool row_generic(const double* __restrict__ coords, cons
     mk.clear();
     int pk[EFEM_MAX_ROW_ELEMS];
     for (int j = 0; j < nt; ++j) {
-        const int e = (__ldg(inc + ib + j) & 0x7fffffff) >> 3;
+        const int e = ord[j] >> 3;
         int g[NV];
         load_g<KT>(elems, e, g);
         int pos[NV];
@@ -302,7 +313,7 @@ __device__ __noinline__ bool row_generic(const double* __restrict__ coords, cons
     }
     // pass 3: values, ascending element id (the incidence list order)
     for (int j = 0; j < nt; ++j) {
-        const int pe = __ldg(inc + ib + j) & 0x7fffffff;
+        const int pe = ord[j];
         const int e = pe >> 3, k = pe & 7;
         int g[NV];
         load_g<KT>(elems, e, g);
