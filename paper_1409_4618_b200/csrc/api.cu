@@ -25,7 +25,7 @@ std::atomic<int64_t> g_launches{0};
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-    size_t hdr, cnt, bucket_ptr, bucket, bkey, binst, bx, nbr, e2d, inc_ptr, row_ptr, rec, d2n, ent_ptr, nnz_cnt, nnz_ptr, lb, totals, cub, total;
+    size_t hdr, cnt, ent_cnt, bucket_ptr, bucket, bkey, binst, bx, nbr, e2d, inc_ptr, row_ptr, rec, d2n, ent_ptr, nnz_cnt, nnz_ptr, lb, totals, cub, total;
 };
 
 Layout layout(const Plan& p, size_t cub_bytes) {
@@ -40,6 +40,7 @@ Layout layout(const Plan& p, size_t cub_bytes) {
     const size_t Tm = (size_t)p.n_elems * p.m;
     L.hdr = take(sizeof(WsHeader));
     L.cnt = take(N1 * 4);
+    L.ent_cnt = take(N1 * 4);
     L.bucket_ptr = take(N1 * 4);
     L.bucket = take(Tm * 4);
     const bool faces = p.dim == 3 && p.element == EFEM_RT0;
@@ -345,6 +346,7 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     p->ws_bytes = ws_bytes;
     p->hdr = reinterpret_cast<WsHeader*>(b + L.hdr);
     p->cnt = reinterpret_cast<int32_t*>(b + L.cnt);
+    p->ent_cnt = reinterpret_cast<int32_t*>(b + L.ent_cnt);
     p->bucket_ptr = reinterpret_cast<int32_t*>(b + L.bucket_ptr);
     p->bucket = reinterpret_cast<int32_t*>(b + L.bucket);
     p->bkey = reinterpret_cast<uint64_t*>(b + L.bkey);
@@ -363,6 +365,11 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     p->d_totals = reinterpret_cast<int64_t*>(&p->hdr->totals[0]);
     p->cub_tmp = b + L.cub;
     p->enumerated = p->symbolic = false;
+    // counters that must start at zero (the fill pass restores cnt to zero;
+    // entry N of the count arrays is never written)
+    EFEM_CUDA_TRY(cudaMemset(p->cnt, 0, ((size_t)p->n_nodes + 1) * 4));
+    EFEM_CUDA_TRY(cudaMemset(p->ent_cnt, 0, ((size_t)p->n_nodes + 1) * 4));
+    EFEM_CUDA_TRY(cudaMemset(p->nnz_cnt, 0, ((size_t)p->n_nodes + 1) * 4));
     if (p->g_enum) {
         cudaGraphExecDestroy(p->g_enum);
         p->g_enum = nullptr;

@@ -151,7 +151,9 @@ __global__ void __launch_bounds__(256) k_bucket(const int32_t* __restrict__ elem
             total += same;
         }
         owner[k] = first;
-        slot[k] = first ? atomicAdd(&cnt[amin[k]], total) : before;
+        // count: add; fill: take slots from the top of the bucket (the counts
+        // return to zero, which the next enumeration's count pass relies on)
+        slot[k] = first ? (FILL ? atomicSub(&cnt[amin[k]], total) - total : atomicAdd(&cnt[amin[k]], total)) : before;
     }
     if constexpr (FILL) {
 #pragma unroll
@@ -610,18 +612,15 @@ __global__ void k_signs(const int32_t* __restrict__ elems, int64_t n_elems, int8
 // ---------------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------------
-// header reset + zero the two counter arrays (bucket counts, fill cursors)
-__global__ void k_init(WsHeader* hdr, int32_t* __restrict__ cnt, int32_t* __restrict__ cursor, int64_t n1) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// header reset.  The instance counters need no reset: they are zeroed with
+// the workspace and every enumeration's fill pass takes them back to zero.
+__global__ void k_init(WsHeader* hdr) {
+    const int i = threadIdx.x;
     if (i < F_NFLAGS) hdr->flags[i] = 0;
     if (i == 0) {
         hdr->bad_element = ~0ull;
         hdr->totals[0] = 0;
         hdr->totals[1] = 0;
-    }
-    if (i < n1) {
-        cnt[i] = 0;
-        cursor[i] = 0;
     }
 }
 
@@ -630,7 +629,7 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     const int64_t N = p.n_nodes, T = p.n_elems;
     size_t bytes = p.cub_bytes;
     const BucketArrays barr{p.bkey, p.binst, p.bx};
-    k_init<<<grid_for(N + 1 > F_NFLAGS ? N + 1 : F_NFLAGS, 256), 256, 0, s>>>(p.hdr, p.cnt, p.nnz_cnt, N + 1);
+    k_init<<<1, 32, 0, s>>>(p.hdr);
     EFEM_LAUNCH_CHECK();
     if (T > 0) {
         k_bucket<KT, false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, nullptr, BucketArrays{}, p.hdr);
@@ -638,8 +637,8 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     }
     EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.bucket_ptr, (int)(N + 1), s));
     count_launch(2);
-    if (T > 0) {  // fill cursors: nnz_cnt (zeroed by k_init, overwritten by pass A)
-        k_bucket<KT, true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.nnz_cnt, p.bucket_ptr, barr, p.hdr);
+    if (T > 0) {
+        k_bucket<KT, true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, p.bucket_ptr, barr, p.hdr);
         EFEM_LAUNCH_CHECK();
     }
     if (N == 0) {
@@ -648,11 +647,12 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
         return EFEM_OK;
     }
     // pass A: sort buckets, count entities / row entries per node (cnt reused
-    // for the entity counts; cnt[N] = nnz_cnt[N] = 0 from k_init)
+    // entity counts in ent_cnt; ent_cnt[N] = nnz_cnt[N] = 0 since the workspace was set)
     constexpr int TPB = NodeCaps<KT>::TPB;
-    k_node_count<KT><<<grid_for(N, TPB), TPB, 0, s>>>(p.elems, p.bucket_ptr, barr, p.bucket, N, p.cnt, p.nnz_cnt);
+    k_node_count<KT><<<grid_for(N, TPB), TPB, 0, s>>>(p.elems, p.bucket_ptr, barr, p.bucket, N, p.ent_cnt,
+                                                      p.nnz_cnt);
     EFEM_LAUNCH_CHECK();
-    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.ent_ptr, (int)(N + 1), s));
+    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.ent_cnt, p.ent_ptr, (int)(N + 1), s));
     count_launch(2);
     if constexpr (KT::D == 3 && !KT::FACES) {  // row lengths need a union only for 3D edges
         EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.nnz_cnt, p.nnz_ptr, (int)(N + 1), s));

@@ -69,7 +69,8 @@ struct Plan {
     char* ws = nullptr;
     size_t ws_bytes = 0, ws_need = 0;
     WsHeader* hdr = nullptr;
-    int32_t* cnt = nullptr;         // N+1 instances per minimum node (counting sort)
+    int32_t* cnt = nullptr;         // N+1 instances per minimum node (counting sort; zero between calls)
+    int32_t* ent_cnt = nullptr;     // N+1 entities per node
     int32_t* bucket_ptr = nullptr;  // N+1
     int32_t* bucket = nullptr;      // T*m instances (e << 3 | k); after enumeration sorted by
                                     // (entity, element): the entity -> element incidence
