@@ -9,6 +9,8 @@
 // A CTA stages its rows' CSR segment in shared memory and writes it out with
 // coalesced stores, so every CSR byte is written exactly once and no local
 // matrix ever reaches HBM.
+#include <type_traits>
+
 #include "element.cuh"
 
 namespace efem {
@@ -88,6 +90,139 @@ __device__ __forceinline__ double tri_row(const Tri& T, double& m0, double& k0, 
     return det;
 }
 
+// Element policies of the pipelined pair kernel (rows of t <= 2 elements).
+// Ids = the gathers that depend only on the instance (L2), Geo = the
+// coordinates (L3); row() returns det and fills the own entry and the m-1
+// other entries of the element's local row.
+struct TriPolicy {
+    static constexpr int M = 3;
+    using Ids = Tri;
+    struct Geo {};
+    __device__ __forceinline__ static void load_ids(const int32_t* __restrict__ elems,
+                                                    const int32_t* __restrict__ e2d, int inst, Ids& I) {
+        tri_load_ids(elems, e2d, inst, I);
+    }
+    __device__ __forceinline__ static void load_x(const double* __restrict__ coords, Ids& I, Geo&) {
+        tri_load_x(coords, I);
+    }
+    __device__ __forceinline__ static double row(const Ids& I, const Geo&, double& m0, double& k0, int (&c)[2],
+                                                 double (&m)[2], double (&k)[2]) {
+        c[0] = I.d1;
+        c[1] = I.d2;
+        return tri_row(I, m0, k0, m[0], k[0], m[1], k[1]);
+    }
+};
+
+// 3D faces (RT0).  Face k is the face opposite vertex o = 3 - k; with y_v the
+// vertices relative to the centroid, M_kl = s_k s_l (y_o(k).y_o(l) + Q) (2/3)/|det|,
+// Q = sum |y|^2 / 20, K_kl = 6 s_k s_l / |det| (see local_row).
+struct FacePolicy {
+    static constexpr int M = 4;
+    struct Ids {
+        int4 g, d;
+        int k;
+    };
+    struct Geo {
+        double x[4][3];
+    };
+    __device__ __forceinline__ static void load_ids(const int32_t* __restrict__ elems,
+                                                    const int32_t* __restrict__ e2d, int inst, Ids& I) {
+        const int e = inst >> 3;
+        I.k = inst & 7;
+        I.g = __ldg(reinterpret_cast<const int4*>(elems) + e);
+        I.d = __ldg(reinterpret_cast<const int4*>(e2d) + e);
+    }
+    __device__ __forceinline__ static void load_x(const double* __restrict__ coords, Ids& I, Geo& G) {
+        const int g[4] = {I.g.x, I.g.y, I.g.z, I.g.w};
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) G.x[v][c] = __ldg(coords + (int64_t)g[v] * 3 + c);
+    }
+    __device__ __forceinline__ static double row(const Ids& I, const Geo& G, double& m0, double& k0, int (&c)[3],
+                                                 double (&m)[3], double (&kv)[3]) {
+        const int g[4] = {I.g.x, I.g.y, I.g.z, I.g.w};
+        const int d[4] = {I.d.x, I.d.y, I.d.z, I.d.w};
+        double ev[4][3], cen[3];
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+            ev[0][cc] = 0.0;
+            ev[1][cc] = G.x[1][cc] - G.x[0][cc];
+            ev[2][cc] = G.x[2][cc] - G.x[0][cc];
+            ev[3][cc] = G.x[3][cc] - G.x[0][cc];
+            cen[cc] = (ev[1][cc] + ev[2][cc] + ev[3][cc]) * 0.25;
+        }
+        const double det = ev[1][0] * (ev[2][1] * ev[3][2] - ev[2][2] * ev[3][1]) -
+                           ev[1][1] * (ev[2][0] * ev[3][2] - ev[2][2] * ev[3][0]) +
+                           ev[1][2] * (ev[2][0] * ev[3][1] - ev[2][1] * ev[3][0]);
+        double y[4][3], sq = 0.0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                y[v][cc] = ev[v][cc] - cen[cc];
+                sq += y[v][cc] * y[v][cc];
+            }
+        const double Q = sq * (1.0 / 20.0);
+        const double rad = 1.0 / fabs(det);
+        const double cm = (2.0 / 3.0) * rad, ck = 6.0 * rad;
+        // face signs: s_l = -sgn(ascending face vertices, then the opposite one)
+        bool pos[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const int o = 3 - l;
+            int f[3], t = 0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                if (v != o) f[t++] = g[v];
+            const int inv = (f[0] > f[1]) + (f[0] > f[2]) + (f[1] > f[2]);
+            pos[l] = ((inv + (l & 1)) & 1) != 0;
+        }
+        const int k = I.k, ok = 3 - k;
+        bool sk = pos[0];
+        double yo[3];
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) yo[cc] = y[0][cc];
+#pragma unroll
+        for (int v = 1; v < 4; ++v) {
+            if (ok == v) {
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) yo[cc] = y[v][cc];
+            }
+            if (k == v) sk = pos[v];
+        }
+        m0 = cm * ((yo[0] * yo[0] + yo[1] * yo[1] + yo[2] * yo[2]) + Q);
+        k0 = ck;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {  // the other faces l = q + (q >= k), opposite vertex 3 - l
+            const bool sh = q >= k;
+            const int l = q + sh;
+            const int ol = 3 - l;
+            double yl[3];
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                double v = y[0][cc];
+#pragma unroll
+                for (int w = 1; w < 4; ++w) v = (ol == w) ? y[w][cc] : v;
+                yl[cc] = v;
+            }
+            bool sl = pos[0];
+            int dl = d[0];
+#pragma unroll
+            for (int w = 1; w < 4; ++w) {
+                sl = (l == w) ? pos[w] : sl;
+                dl = (l == w) ? d[w] : dl;
+            }
+            const double val = cm * ((yo[0] * yl[0] + yo[1] * yl[1] + yo[2] * yl[2]) + Q);
+            const bool same = sk == sl;
+            c[q] = dl;
+            m[q] = same ? val : -val;
+            kv[q] = same ? ck : -ck;
+        }
+        return det;
+    }
+};
+
 // 2D, persistent and software-pipelined: every warp walks 32-row batches
 // (grid-stride, so concurrently running warps work on neighbouring rows and
 // share element data in L2).  The gather chain per row is
@@ -117,17 +252,19 @@ __device__ __forceinline__ TriL1 tri_l1(const int32_t* __restrict__ inc_ptr, con
     return a;
 }
 
-template <class KT>
-__global__ void __launch_bounds__(TRI_TPB, 3) k_rows_tri(const double* __restrict__ coords,
-                                                        const int32_t* __restrict__ elems,
-                                                        const int32_t* __restrict__ inc_ptr,
-                                                        const int2* __restrict__ rec,
-                                                        const int32_t* __restrict__ e2d, int row0, int n_rows,
-                                                        int own_base, int out_base, unsigned forms,
-                                                        int32_t* __restrict__ row_ptr_out,
-                                                        int32_t* __restrict__ col_idx, double* __restrict__ vals_m,
-                                                        double* __restrict__ vals_k, WsHeader* hdr) {
-    constexpr int NS = 5, WSEG = 32 * NS, NW = TRI_TPB / 32;
+template <class KT, class P, int MINB>
+__global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __restrict__ coords,
+                                                           const int32_t* __restrict__ elems,
+                                                           const int32_t* __restrict__ inc_ptr,
+                                                           const int2* __restrict__ rec,
+                                                           const int32_t* __restrict__ e2d, int row0, int n_rows,
+                                                           int own_base, int out_base, unsigned forms,
+                                                           int32_t* __restrict__ row_ptr_out,
+                                                           int32_t* __restrict__ col_idx,
+                                                           double* __restrict__ vals_m, double* __restrict__ vals_k,
+                                                           WsHeader* hdr) {
+    constexpr int M = P::M, NO = M - 1;
+    constexpr int NS = 1 + 2 * NO, WSEG = 32 * NS, NW = TRI_TPB / 32;
     __shared__ int s_col[NW][WSEG];
     __shared__ double s_vm[NW][WSEG];
     __shared__ double s_vk[NW][WSEG];
@@ -143,20 +280,21 @@ __global__ void __launch_bounds__(TRI_TPB, 3) k_rows_tri(const double* __restric
     // prologue: L1 of batches b and b+1, L2 of batch b
     TriL1 c1 = tri_l1(inc_ptr, rec, batch, nbatch, n_rows, lane);
     TriL1 n1 = tri_l1(inc_ptr, rec, batch + stride, nbatch, n_rows, lane);
-    Tri T0, T1;
-    tri_load_ids(elems, e2d, c1.rr.x, T0);
-    tri_load_ids(elems, e2d, c1.rr.y, T1);
+    typename P::Ids T0, T1;
+    P::load_ids(elems, e2d, c1.rr.x, T0);
+    P::load_ids(elems, e2d, c1.rr.y, T1);
 
     for (; batch < nbatch; batch += stride) {
         // L3 of batch b
-        tri_load_x(coords, T0);
-        tri_load_x(coords, T1);
+        typename P::Geo G0, G1;
+        P::load_x(coords, T0, G0);
+        P::load_x(coords, T1, G1);
         // L2 of batch b+1, L1 of batch b+2
-        Tri U0, U1;
+        typename P::Ids U0, U1;
         const bool has_next = batch + stride < nbatch;
         if (has_next) {
-            tri_load_ids(elems, e2d, n1.rr.x, U0);
-            tri_load_ids(elems, e2d, n1.rr.y, U1);
+            P::load_ids(elems, e2d, n1.rr.x, U0);
+            P::load_ids(elems, e2d, n1.rr.y, U1);
         }
         const TriL1 n2 = tri_l1(inc_ptr, rec, batch + 2 * stride, nbatch, n_rows, lane);
 
@@ -175,9 +313,9 @@ __global__ void __launch_bounds__(TRI_TPB, 3) k_rows_tri(const double* __restric
         const int ib0 = __shfl_sync(0xffffffffu, c1.ib0, 0);
         const int tot = __shfl_sync(0xffffffffu, incl, 31);
         const int nr = min(32, n_rows - w0);
-        const int gbase = row0 + w0 + 2 * ib0 - out_base;
-        const int segn = nr + 2 * tot;
-        const int o = lane + 2 * (incl - t);
+        const int gbase = row0 + w0 + NO * ib0 - out_base;
+        const int segn = nr + NO * tot;
+        const int o = lane + NO * (incl - t);
         if (forms & EFEM_PATTERN) {
             if (live) row_ptr_out[li] = gbase + o;
             if (li == n_rows - 1) row_ptr_out[n_rows] = gbase + segn;
@@ -186,19 +324,33 @@ __global__ void __launch_bounds__(TRI_TPB, 3) k_rows_tri(const double* __restric
         const bool bad = false;
         if (!__any_sync(0xffffffffu, bad) && segn <= WSEG) {
             if (live) {
-                double m0a, k0a, m1a, k1a, m2a, k2a, m0b, k0b, m1b, k1b, m2b, k2b;
-                const double da = tri_row(T0, m0a, k0a, m1a, k1a, m2a, k2a);
-                const double db = tri_row(T1, m0b, k0b, m1b, k1b, m2b, k2b);
+                double m0a, k0a, m0b, k0b, ma[NO], ka[NO], mb[NO], kb[NO];
+                int ca[NO], cb[NO];
+                const double da = P::row(T0, G0, m0a, k0a, ca, ma, ka);
+                const double db = P::row(T1, G1, m0b, k0b, cb, mb, kb);
                 const bool bad_a = !(fabs(da) > 0.0 && fabs(da) < INFINITY);
                 const bool bad_b = two && !(fabs(db) > 0.0 && fabs(db) < INFINITY);
                 if (bad_a || bad_b) {
                     atomicOr(&hdr->flags[F_DEGENERATE], 1);
                     atomicMin(&hdr->bad_element, (unsigned long long)((bad_a ? c1.rr.x : c1.rr.y) >> 3));
                 }
-                int cl[NS] = {own_base + li, T0.d1, T0.d2, two ? T1.d1 : INT_MAX, two ? T1.d2 : INT_MAX};
-                const double am[NS] = {two ? m0a + m0b : m0a, m1a, m2a, m1b, m2b};
-                const double ak[NS] = {two ? k0a + k0b : k0a, k1a, k2a, k1b, k2b};
-                int rk[NS] = {0, 0, 0, 0, 0};
+                int cl[NS];
+                double am[NS], ak[NS];
+                cl[0] = own_base + li;
+                am[0] = two ? m0a + m0b : m0a;
+                ak[0] = two ? k0a + k0b : k0a;
+#pragma unroll
+                for (int q = 0; q < NO; ++q) {
+                    cl[1 + q] = ca[q];
+                    am[1 + q] = ma[q];
+                    ak[1 + q] = ka[q];
+                    cl[1 + NO + q] = two ? cb[q] : INT_MAX;
+                    am[1 + NO + q] = mb[q];
+                    ak[1 + NO + q] = kb[q];
+                }
+                int rk[NS];
+#pragma unroll
+                for (int x = 0; x < NS; ++x) rk[x] = 0;
 #pragma unroll
                 for (int x = 0; x < NS; ++x)
 #pragma unroll
@@ -209,7 +361,7 @@ __global__ void __launch_bounds__(TRI_TPB, 3) k_rows_tri(const double* __restric
                     }
 #pragma unroll
                 for (int x = 0; x < NS; ++x) {
-                    if (x < 3 || two) {
+                    if (x <= NO || two) {
                         sc[o + rk[x]] = cl[x];
                         sm[o + rk[x]] = am[x];
                         sk[o + rk[x]] = ak[x];
@@ -234,162 +386,6 @@ __global__ void __launch_bounds__(TRI_TPB, 3) k_rows_tri(const double* __restric
         n1 = n2;
         T0 = U0;
         T1 = U1;
-    }
-}
-
-template <class KT>
-__global__ void __launch_bounds__(PAIR_TPB, 2) k_rows_pair(const double* __restrict__ coords,
-                                                        const int32_t* __restrict__ elems,
-                                                        const int32_t* __restrict__ inc_ptr,
-                                                        const int2* __restrict__ rec,
-                                                        const int32_t* __restrict__ e2d, int row0, int n_rows,
-                                                        int own_base, int out_base, unsigned forms,
-                                                        int32_t* __restrict__ row_ptr_out,
-                                                        int32_t* __restrict__ col_idx, double* __restrict__ vals_m,
-                                                        double* __restrict__ vals_k, WsHeader* hdr) {
-    constexpr int D = KT::D, NV = KT::NV, M = KT::M;
-    constexpr int NS = 1 + 2 * (M - 1);  // max entries per row
-    constexpr int WSEG = 32 * NS;         // per-warp staging capacity
-    constexpr int NW = PAIR_TPB / 32;
-    __shared__ int s_col[NW][WSEG];
-    __shared__ double s_vm[NW][WSEG];
-    __shared__ double s_vk[NW][WSEG];
-
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int w0 = blockIdx.x * PAIR_TPB + wid * 32;  // first row of the warp (window-local)
-    if (w0 >= n_rows) return;
-    const int li = w0 + lane;
-    const bool live = li < n_rows;
-    const int lc = live ? li : n_rows - 1;
-    const int ib = __ldg(inc_ptr + lc);
-    const int ie = __ldg(inc_ptr + lc + 1);
-    const int2 rr = __ldg(rec + lc);  // {first, last} instance: same level as inc_ptr
-    const int t = live ? ie - ib : 0;
-    const int ib0 = __shfl_sync(0xffffffffu, ib, 0);
-    const int nlast = min(32, n_rows - w0) - 1;
-    const int ie_last = __shfl_sync(0xffffffffu, ie, nlast);
-    // CSR offsets (window-local, relative to out_base)
-    const int gbase = row0 + w0 + (M - 1) * ib0 - out_base;  // warp segment start
-    const int segn = (nlast + 1) + (M - 1) * (ie_last - ib0);
-    const int o = (li - w0) + (M - 1) * (ib - ib0);
-    if (forms & EFEM_PATTERN) {
-        if (live) row_ptr_out[li] = gbase + o;
-        if (li == n_rows - 1) row_ptr_out[n_rows] = gbase + segn;
-    }
-    const bool bad = live && (t < 1 || t > 2);
-    if (bad) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
-    if (__any_sync(0xffffffffu, bad) || segn > WSEG) return;  // non-conforming: flagged, no output
-
-    int* sc = s_col[wid];
-    double* sm = s_vm[wid];
-    double* sk = s_vk[wid];
-    if (live) {
-        const int p0 = rr.x;
-        const int p1 = rr.y;  // == p0 when t == 1
-        int cl[NS];
-        double am[NS], ak[NS];
-        cl[0] = own_base + li;
-        am[0] = 0.0;
-        ak[0] = 0.0;
-        if constexpr (D == 2) {
-            Tri T[2];
-            tri_load_ids(elems, e2d, p0, T[0]);
-            tri_load_ids(elems, e2d, p1, T[1]);
-            tri_load_x(coords, T[0]);
-            tri_load_x(coords, T[1]);
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                double m0, k0, m1, k1, m2, k2;
-                const double det = tri_row(T[j], m0, k0, m1, k1, m2, k2);
-                if (j < t) {
-                    if (!(det != 0.0) || !isfinite(det)) {
-                        atomicOr(&hdr->flags[F_DEGENERATE], 1);
-                        atomicMin(&hdr->bad_element, (unsigned long long)((j ? p1 : p0) >> 3));
-                    }
-                    am[0] += m0;
-                    ak[0] += k0;
-                    cl[1 + 2 * j] = T[j].d1;
-                    am[1 + 2 * j] = m1;
-                    ak[1 + 2 * j] = k1;
-                    cl[2 + 2 * j] = T[j].d2;
-                    am[2 + 2 * j] = m2;
-                    ak[2 + 2 * j] = k2;
-                } else {
-                    cl[1 + 2 * j] = INT_MAX;
-                    cl[2 + 2 * j] = INT_MAX;
-                }
-            }
-        } else {  // 3D faces (RT0): general local row
-            const int pe[2] = {p0, p1};
-            int g[2][NV], dofs[2][M];
-            double X[2][NV][D];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) load_g<KT>(elems, pe[j] >> 3, g[j]);
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-#pragma unroll
-                for (int l = 0; l < M; ++l) dofs[j][l] = __ldg(e2d + (int64_t)(pe[j] >> 3) * M + l);
-#pragma unroll
-                for (int v = 0; v < NV; ++v)
-#pragma unroll
-                    for (int cc = 0; cc < 3; ++cc) X[j][v][cc] = __ldg(coords + (int64_t)g[j][v] * 3 + cc);
-            }
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                if (j < t) {
-                    const int e = pe[j] >> 3, k = pe[j] & 7;
-                    double Mr[M], Kr[M];
-                    const double det = local_row<KT>(X[j], g[j], k, Mr, Kr);
-                    if (!(det != 0.0) || !isfinite(det)) {
-                        atomicOr(&hdr->flags[F_DEGENERATE], 1);
-                        atomicMin(&hdr->bad_element, (unsigned long long)e);
-                    }
-                    double om = Mr[0], okk = Kr[0];
-#pragma unroll
-                    for (int l = 1; l < M; ++l) {
-                        om = (k == l) ? Mr[l] : om;
-                        okk = (k == l) ? Kr[l] : okk;
-                    }
-                    am[0] += om;
-                    ak[0] += okk;
-#pragma unroll
-                    for (int q = 0; q < M - 1; ++q) {  // the other local DOFs, l = q + (q >= k)
-                        const bool sh = q >= k;
-                        cl[1 + j * (M - 1) + q] = sh ? dofs[j][q + 1] : dofs[j][q];
-                        am[1 + j * (M - 1) + q] = sh ? Mr[q + 1] : Mr[q];
-                        ak[1 + j * (M - 1) + q] = sh ? Kr[q + 1] : Kr[q];
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < M - 1; ++q) cl[1 + j * (M - 1) + q] = INT_MAX;
-                }
-            }
-        }
-        // place by rank (valid columns are distinct; INT_MAX sentinels rank last)
-#pragma unroll
-        for (int x = 0; x < NS; ++x) {
-            int rk = 0;
-#pragma unroll
-            for (int y = 0; y < NS; ++y)
-                if (y != x) rk += cl[y] < cl[x];
-            if (cl[x] != INT_MAX) {
-                sc[o + rk] = cl[x];
-                sm[o + rk] = am[x];
-                sk[o + rk] = ak[x];
-            }
-        }
-    }
-    __syncwarp();
-    // coalesced flush of the warp's segment
-#pragma unroll
-    for (int u = 0; u < NS; ++u) {
-        const int x = u * 32 + lane;
-        if (x < segn) {
-            const int gx = gbase + x;
-            if (forms & EFEM_PATTERN) col_idx[gx] = sc[x];
-            if (forms & EFEM_MASS) vals_m[gx] = sm[x];
-            if (forms & EFEM_STIFF) vals_k[gx] = sk[x];
-        }
     }
 }
 
@@ -705,23 +701,22 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
     double* vk = (forms & EFEM_STIFF) ? out->vals_stiff : nullptr;
     const int32_t* inc_ptr = p.inc_ptr + w.row0;
     const int32_t* row_ptr = p.row_ptr + w.row0;
-    if constexpr (KT::D == 2) {
+    if constexpr (KT::D == 2 || KT::FACES) {
+        using P = std::conditional_t<KT::D == 2, TriPolicy, FacePolicy>;
+        constexpr int MINB = KT::D == 2 ? 3 : 2;
         static int grid = 0;
         if (!grid) {
             int dev = 0, sms = 0, per_sm = 0;
             EFEM_CUDA_TRY(cudaGetDevice(&dev));
             EFEM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            EFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_tri<KT>, TRI_TPB, 0));
+            EFEM_CUDA_TRY(
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_tri<KT, P, MINB>, TRI_TPB, 0));
             grid = sms * (per_sm > 0 ? per_sm : 1);
         }
         const int64_t need = (w.n_rows + TRI_TPB - 1) / TRI_TPB;
-        k_rows_tri<KT><<<(unsigned)(need < grid ? need : grid), TRI_TPB, 0, s>>>(
+        k_rows_tri<KT, P, MINB><<<(unsigned)(need < grid ? need : grid), TRI_TPB, 0, s>>>(
             p.coords, p.elems, inc_ptr, p.rec + w.row0, w.e2d, (int)w.row0, (int)w.n_rows, w.own_base, w.out_base,
             forms, out->row_ptr, out->col_idx, vm, vk, p.hdr);
-    } else if constexpr (KT::FACES) {
-        k_rows_pair<KT><<<grid_for(w.n_rows, PAIR_TPB), PAIR_TPB, 0, s>>>(
-            p.coords, p.elems, inc_ptr, p.rec + w.row0, w.e2d, (int)w.row0, (int)w.n_rows, w.own_base, w.out_base, forms,
-            out->row_ptr, out->col_idx, vm, vk, p.hdr);
     } else {
         const int fast_ids = p.n_nodes < (1ll << 27);
         static bool attr = false;

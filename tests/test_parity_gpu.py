@@ -164,6 +164,33 @@ def test_invalid_node_id_reported(api):
     assert ei.value.status == -1
 
 
+def _bowtie_tets():
+    """Two tets sharing only the edge (0, 1): a non-manifold fan (its link is
+    two disjoint segments)."""
+    c = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [0, -1, 0], [0, 0, -1]], dtype=np.float64)
+    e = np.array([[0, 1, 2, 3], [0, 1, 4, 5]], dtype=np.int32)
+    return c, e
+
+
+def test_nonmanifold_edge_rt0_3d_exact(api):
+    """Faces need no link count: RT0 3D assembles the bow-tie exactly."""
+    c, e = _bowtie_tets()
+    ref = ora.assemble(3, RT0, c, e)
+    asm = api.Assembler(torch.from_numpy(c).cuda(), torch.from_numpy(e).cuda(), RT0)
+    assert_csr_parity(asm.assemble(), ref, what="bowtie")
+
+
+def test_nonmanifold_edge_ne0_3d_reported(api):
+    """NE0 3D sizes edge rows as 1 + 3t + 2[boundary edge], valid when every
+    edge's tets form one fan (cycle or path).  A non-manifold edge must be
+    reported (EFEM_EINVAL, "non-conforming"), never assembled wrongly."""
+    c, e = _bowtie_tets()
+    asm = api.Assembler(torch.from_numpy(c).cuda(), torch.from_numpy(e).cuda(), NED0)
+    with pytest.raises(api._lib.EfemError) as ei:
+        asm.assemble()
+    assert ei.value.status == -1
+
+
 @pytest.mark.parametrize("dim,element", KINDS, ids=KIND_IDS)
 def test_single_element_and_unused_nodes(api, dim, element):
     rc, re = ora.build_mesh(dim, 2, 0.1, 3)
