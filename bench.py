@@ -67,10 +67,16 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs a moment before its first sample: wait for it,
+            # then keep only samples taken from here on (the timed region)
+            t_end = time.time() + 3.0
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.01)
+            self.lines.clear()
         except Exception:
             self.proc = None
         return self
@@ -256,7 +262,8 @@ def run_efem(args, cfg):
         "phase_ms": {"symbolic": sym_ms, "numeric": num_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_bytes(cfg),
-                     "kernel": "numeric row kernel (k_row_fill_net / k_row_fill_ne3)",
+                     "kernel": ("k_rows_ne3" if (cfg["dim"] == 3 and cfg["element"] == 1) else "k_rows_tri")
+                               + " (the numeric call: one launch)",
                      "peak_source": peak_src, "algorithmic_bytes": alg_bytes,
                      "e2e_achieved": e2e_gbs, "e2e_frac": e2e_gbs / peak},
         "e2e": {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -344,7 +351,7 @@ def run_efem_dist(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=None, choices=sorted(CONFIGS),
                     help="BASELINE config; default: 2 (configs[1]) at N=1, 5 (the scaling sweep) at N>1")

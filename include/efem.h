@@ -40,11 +40,14 @@ typedef struct CUstream_st* efem_stream_t; /* == cudaStream_t; NULL = legacy def
 typedef enum {
     EFEM_OK = 0,
     EFEM_EINVAL = -1,      /* bad argument: dim not in {2,3}, n < 1, NULL pointer, node id out of range,
-                              jitter outside [0, 1/(2 sqrt(2 d))) ... */
+                              jitter outside [0, 1/(2 sqrt(2 d))) ...; or a non-conforming mesh: an
+                              edge (2D) / face (3D RT0) in more than two elements, or (3D NE0) an edge
+                              whose tets do not form one fan (see efem_assemble_numeric) */
     EFEM_EDEGENERATE = -2, /* an element has det B_K == 0 (or non-finite); efem_last_bad_element() names it */
     EFEM_ENOMEM = -3,      /* host allocation failed */
     EFEM_EWORKSPACE = -4,  /* workspace NULL or smaller than efem_plan_create reported */
-    EFEM_EOVERFLOW = -5,   /* a count does not fit int32 (nnz >= 2^31, T*(d+1) >= 2^31 ...) */
+    EFEM_EOVERFLOW = -5,   /* a count does not fit int32 (nnz >= 2^31, T*(d+1) >= 2^31 ...) or
+                              n_elems >= 2^27 (instance words e << 3 | k carry two flag bits) */
     EFEM_ECUDA = -6,       /* CUDA runtime error; message in efem_last_error() */
     EFEM_ENCCL = -7,       /* NCCL error (distributed entry points) */
     EFEM_ECAPACITY = -8,   /* a node touches more elements / owns more entities than the
@@ -153,7 +156,12 @@ efem_status efem_assemble_symbolic(efem_plan plan, int64_t* n_rows, int64_t* nnz
 
 /* Numeric assembly into caller-allocated CSR arrays (sizes from symbolic):
  * local matrices computed in fp64 registers and summed
- * per row in ascending element order.  forms: EFEM_PATTERN writes row_ptr and
+ * per row in ascending element order.  Every row's column set is re-derived
+ * here and compared with the symbolic row length; a mismatch (a mesh the
+ * closed-form row lengths do not describe: 3D NE0 rows are sized
+ * 1 + 3t + 2[edge on the boundary], valid when the tets around every edge
+ * form one fan, a cycle or a path) is reported by efem_plan_check as
+ * EFEM_EINVAL, never as wrong values.  forms: EFEM_PATTERN writes row_ptr and
  * col_idx, EFEM_MASS vals_mass, EFEM_STIFF vals_stiff (NULL allowed for
  * arrays whose bit is clear).  Asynchronous: degenerate elements are
  * reported by efem_plan_check. */
