@@ -563,3 +563,258 @@ int ora_rows_by_entity(int dim, int element, int64_t n_nodes, int64_t n_elems, c
 }
 
 }  // extern "C"
+
+namespace {
+/* ===========================================================================
+ * vectorized integration (Sec. 3.1):
+ * quadrature points F_K(xh_i) for all elements, load vectors against the
+ * global basis, L2 norms and field errors.  Same per-element loop style.
+ * ======================================================================== */
+
+/* Degree-6 rules on the reference element ("integration
+ * quadratures for triangles and tetrahedrons from [Du] and [ZhCuLi]"; the
+ * norm listing uses intquad(6, dim)).  2D: Dunavant's
+ * 12-point rule; 3D: Keast's 24-point rule (reading C7: any exact rule of the
+ * order gives the same integral up to rounding).  Barycentric points,
+ * weights normalised to 1 and scaled by |K_hat| = 1/2 resp. 1/6.  Pinned by
+ * exact integration of all monomials of degree <= 6 (tests). */
+int quad6(int dim, double* pts, double* w) {
+    int n = 0;
+    auto put = [&](double l1, double l2, double l3, double wt) {  // l0 implied
+        pts[dim * n + 0] = l1;
+        pts[dim * n + 1] = l2;
+        if (dim == 3) pts[dim * n + 2] = l3;
+        w[n] = wt;
+        ++n;
+    };
+    if (dim == 2) {
+        const double W[3] = {0.116786275726379, 0.050844906370207, 0.082851075618374};
+        const double a1 = 0.501426509658179, b1 = 0.249286745170910;
+        const double a2 = 0.873821971016996, b2 = 0.063089014491502;
+        const double c0 = 0.053145049844817, c1 = 0.310352451033784, c2 = 0.636502499121399;
+        /* (l0, l1, l2) permutations; the point is (l1, l2) */
+        const double s1[3][3] = {{a1, b1, b1}, {b1, a1, b1}, {b1, b1, a1}};
+        const double s2[3][3] = {{a2, b2, b2}, {b2, a2, b2}, {b2, b2, a2}};
+        for (int i = 0; i < 3; ++i) put(s1[i][1], s1[i][2], 0.0, 0.5 * W[0]);
+        for (int i = 0; i < 3; ++i) put(s2[i][1], s2[i][2], 0.0, 0.5 * W[1]);
+        const double l[3] = {c0, c1, c2};
+        const int perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+        for (int i = 0; i < 6; ++i) put(l[perm[i][1]], l[perm[i][2]], 0.0, 0.5 * W[2]);
+        return n;
+    }
+    const double sixth = 1.0 / 6.0;
+    const double A[3] = {0.214602871259151684, 0.0406739585346113397, 0.322337890142275646};
+    const double WA[3] = {0.0399227502581679, 0.0100772110553207, 0.0553571815436544};
+    for (int c = 0; c < 3; ++c) {
+        const double a = A[c], b = 1.0 - 3.0 * a;
+        /* (l0..l3) = (b,a,a,a) and its 3 other placements */
+        put(a, a, a, sixth * WA[c]);
+        put(b, a, a, sixth * WA[c]);
+        put(a, b, a, sixth * WA[c]);
+        put(a, a, b, sixth * WA[c]);
+    }
+    const double a = 0.0636610018750175299, b = 0.269672331458315867, c = 0.603005664791649076;
+    const double wt = sixth * 0.0482142857142857;
+    /* the 12 placements of (a, a, b, c) over (l0, l1, l2, l3) */
+    const double v[4] = {a, a, b, c};
+    int cnt = 0;
+    for (int i0 = 0; i0 < 4; ++i0)
+        for (int i1 = 0; i1 < 4; ++i1)
+            for (int i2 = 0; i2 < 4; ++i2)
+                for (int i3 = 0; i3 < 4; ++i3) {
+                    if (i0 == i1 || i0 == i2 || i0 == i3 || i1 == i2 || i1 == i3 || i2 == i3) continue;
+                    if (i0 > i1) continue; /* the two a's are interchangeable: keep i0 < i1 */
+                    /* slot i0 and i1 get a, i2 gets b, i3 gets c */
+                    double lam[4];
+                    lam[i0] = v[0];
+                    lam[i1] = v[1];
+                    lam[i2] = v[2];
+                    lam[i3] = v[3];
+                    put(lam[1], lam[2], lam[3], wt);
+                    ++cnt;
+                }
+    (void)cnt;
+    return n;
+}
+
+/* Physical point F_K(xh) = B_K xh + b_K. */
+void map_point(int dim, const double* verts, const double B[3][3], const double* xh, double* x) {
+    for (int r = 0; r < dim; ++r) {
+        double acc = verts[r];
+        for (int c = 0; c < dim; ++c) acc += B[r][c] * xh[c];
+        x[r] = acc;
+    }
+}
+
+/* Values of the global basis on element K at xh: phi[k][r] (value) and
+ * dphi[k][r] (div: nd=1, 2D curl: nd=1, 3D curl: nd=3), sign data included
+ * (PAPER.md:240-245 RT, 291-301 Ned, 323-331 signs):
+ *   RT:  s_k / det B  B eta_hat_k,      div  = s_k / det B  div_hat
+ *   Ned: s_k B^{-T} eta_hat_k,          curl = s_k / det B  curl_hat (2D),
+ *                                              s_k / det B  B curl_hat (3D). */
+void global_basis(int dim, int element, const double* xh, const double B[3][3], double det, const int* s,
+                  double phi[6][3], double dphi[6][3]) {
+    double BiT[3][3];
+    inverse_transpose(dim, B, det, BiT);
+    const int m = n_local_dofs(dim, element);
+    const int nd = (dim == 3 && element == ORA_NED0) ? 3 : 1;
+    double val[18], dc[18];
+    ref_basis(dim, element, xh, val, dc);
+    for (int k = 0; k < m; ++k) {
+        for (int r = 0; r < dim; ++r) {
+            double acc = 0.0;
+            for (int c = 0; c < dim; ++c)
+                acc += (element == ORA_RT0 ? B[r][c] : BiT[r][c]) * val[k * dim + c];
+            phi[k][r] = element == ORA_RT0 ? s[k] * acc / det : s[k] * acc;
+        }
+        if (nd == 3) {
+            for (int r = 0; r < 3; ++r) {
+                double acc = 0.0;
+                for (int c = 0; c < 3; ++c) acc += B[r][c] * dc[3 * k + c];
+                dphi[k][r] = s[k] * acc / det;
+            }
+        } else {
+            dphi[k][0] = s[k] * dc[k] / det;
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int ora_quad6(int dim, double* pts, double* w) {
+    if (dim != 2 && dim != 3) return ORA_EINVAL;
+    return quad6(dim, pts, w);
+}
+
+/* pts[(e*nq + q)*dim + r] = F_K(xh_q) for every element (degree-6 rule). */
+int ora_quad_points(int dim, int64_t n_elems, const double* coords, const int32_t* elems, double* pts) {
+    if (dim != 2 && dim != 3) return ORA_EINVAL;
+    double xh[72], w[24];
+    const int nq = quad6(dim, xh, w), nv = dim + 1;
+    std::vector<double> verts(nv * dim);
+    for (int64_t e = 0; e < n_elems; ++e) {
+        for (int v = 0; v < nv; ++v)
+            for (int c = 0; c < dim; ++c) verts[v * dim + c] = coords[(int64_t)elems[e * nv + v] * dim + c];
+        double B[3][3];
+        affine(dim, verts.data(), B);
+        for (int q = 0; q < nq; ++q) map_point(dim, verts.data(), B, xh + dim * q, pts + (e * nq + q) * dim);
+    }
+    return nq;
+}
+
+/* Load vector b_i = sum_K sum_q w_q |det B_K| f(F_K(xh_q)) . phi_i(xh_q)
+ * (pairing 0, f a d-vector) or  . (div / curl phi_i)(xh_q) (pairing 1, f
+ * with nd components), accumulated in element order.  e2d / signs are the
+ * oracle's own (ora_assemble).  fq[(e*nq + q)*nf + c]. */
+int ora_load(int dim, int element, int pairing, int64_t n_elems, const double* coords, const int32_t* elems,
+             const int32_t* e2d, const int8_t* signs, int64_t n_dofs, const double* fq, double* b) {
+    if ((dim != 2 && dim != 3) || (element != ORA_RT0 && element != ORA_NED0)) return ORA_EINVAL;
+    double xh[72], w[24];
+    const int nq = quad6(dim, xh, w), nv = dim + 1, m = n_local_dofs(dim, element);
+    const int nd = (dim == 3 && element == ORA_NED0) ? 3 : 1;
+    const int nf = pairing == 0 ? dim : nd;
+    for (int64_t i = 0; i < n_dofs; ++i) b[i] = 0.0;
+    std::vector<double> verts(nv * dim);
+    for (int64_t e = 0; e < n_elems; ++e) {
+        for (int v = 0; v < nv; ++v)
+            for (int c = 0; c < dim; ++c) verts[v * dim + c] = coords[(int64_t)elems[e * nv + v] * dim + c];
+        double B[3][3];
+        const double det = affine(dim, verts.data(), B);
+        if (!(det != 0.0)) return ORA_EDEGENERATE;
+        int s[6];
+        for (int k = 0; k < m; ++k) s[k] = signs[e * m + k];
+        double loc[6] = {0, 0, 0, 0, 0, 0};
+        for (int q = 0; q < nq; ++q) {
+            double phi[6][3], dphi[6][3];
+            global_basis(dim, element, xh + dim * q, B, det, s, phi, dphi);
+            const double* f = fq + (e * nq + q) * nf;
+            for (int k = 0; k < m; ++k) {
+                double dot = 0.0;
+                for (int c = 0; c < nf; ++c) dot += f[c] * (pairing == 0 ? phi[k][c] : dphi[k][c]);
+                loc[k] += w[q] * std::fabs(det) * dot;
+            }
+        }
+        for (int k = 0; k < m; ++k) b[e2d[e * m + k]] += loc[k];
+    }
+    return ORA_OK;
+}
+
+/* ||f||^2 = sum_K sum_q w_q |det B_K| |f(F_K(xh_q))|^2 (PAPER.md:633-645,
+ * norm_L2 listing); per_elem[e] = ||f||^2_K; *total = their sum in element
+ * order. */
+int ora_norm_l2(int dim, int64_t n_elems, const double* coords, const int32_t* elems, const double* fq, int nf,
+                double* per_elem, double* total) {
+    if (dim != 2 && dim != 3) return ORA_EINVAL;
+    double xh[72], w[24];
+    const int nq = quad6(dim, xh, w), nv = dim + 1;
+    std::vector<double> verts(nv * dim);
+    double sum = 0.0;
+    for (int64_t e = 0; e < n_elems; ++e) {
+        for (int v = 0; v < nv; ++v)
+            for (int c = 0; c < dim; ++c) verts[v * dim + c] = coords[(int64_t)elems[e * nv + v] * dim + c];
+        double B[3][3];
+        const double adet = std::fabs(affine(dim, verts.data(), B));
+        double acc = 0.0;
+        for (int q = 0; q < nq; ++q) {
+            const double* f = fq + (e * nq + q) * nf;
+            double f2 = 0.0;
+            for (int c = 0; c < nf; ++c) f2 += f[c] * f[c];
+            acc += w[q] * adet * f2;
+        }
+        if (per_elem) per_elem[e] = acc;
+        sum += acc;
+    }
+    *total = sum;
+    return ORA_OK;
+}
+
+/* Error of the discrete field v = sum_i c_i phi_i against exact values at the
+ * quadrature points: err[0] = ||E - v||^2, err[1] = ||D E - D v||^2 with
+ * D = div (RT) or curl (Ned).  Eq[(e*nq+q)*dim + r], Dq[(e*nq+q)*nd + r]. */
+int ora_field_error(int dim, int element, int64_t n_elems, const double* coords, const int32_t* elems,
+                    const int32_t* e2d, const int8_t* signs, const double* coeffs, const double* Eq,
+                    const double* Dq, double* err) {
+    if ((dim != 2 && dim != 3) || (element != ORA_RT0 && element != ORA_NED0)) return ORA_EINVAL;
+    double xh[72], w[24];
+    const int nq = quad6(dim, xh, w), nv = dim + 1, m = n_local_dofs(dim, element);
+    const int nd = (dim == 3 && element == ORA_NED0) ? 3 : 1;
+    std::vector<double> verts(nv * dim);
+    double ev = 0.0, ed = 0.0;
+    for (int64_t e = 0; e < n_elems; ++e) {
+        for (int v = 0; v < nv; ++v)
+            for (int c = 0; c < dim; ++c) verts[v * dim + c] = coords[(int64_t)elems[e * nv + v] * dim + c];
+        double B[3][3];
+        const double det = affine(dim, verts.data(), B);
+        if (!(det != 0.0)) return ORA_EDEGENERATE;
+        int s[6];
+        for (int k = 0; k < m; ++k) s[k] = signs[e * m + k];
+        for (int q = 0; q < nq; ++q) {
+            double phi[6][3], dphi[6][3];
+            global_basis(dim, element, xh + dim * q, B, det, s, phi, dphi);
+            double v[3] = {0, 0, 0}, dv[3] = {0, 0, 0};
+            for (int k = 0; k < m; ++k) {
+                const double ck = coeffs[e2d[e * m + k]];
+                for (int r = 0; r < dim; ++r) v[r] += ck * phi[k][r];
+                for (int r = 0; r < nd; ++r) dv[r] += ck * dphi[k][r];
+            }
+            double a = 0.0, d = 0.0;
+            for (int r = 0; r < dim; ++r) {
+                const double t = Eq[(e * nq + q) * dim + r] - v[r];
+                a += t * t;
+            }
+            for (int r = 0; r < nd; ++r) {
+                const double t = Dq[(e * nq + q) * nd + r] - dv[r];
+                d += t * t;
+            }
+            ev += w[q] * std::fabs(det) * a;
+            ed += w[q] * std::fabs(det) * d;
+        }
+    }
+    err[0] = ev;
+    err[1] = ed;
+    return ORA_OK;
+}
+
+}  // extern "C"

@@ -54,6 +54,12 @@ def lib():
         L.ora_result_copy.argtypes = [vp] + [vp] * 7
         L.ora_free.argtypes = [vp]
         L.ora_free.restype = None
+        L.ora_quad6.argtypes = [ctypes.c_int, vp, vp]
+        L.ora_quad_points.argtypes = [ctypes.c_int, ctypes.c_int64, vp, vp, vp]
+        L.ora_load.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp,
+                               ctypes.c_int64, vp, vp]
+        L.ora_norm_l2.argtypes = [ctypes.c_int, ctypes.c_int64, vp, vp, vp, ctypes.c_int, vp, vp]
+        L.ora_field_error.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp]
         L.ora_rows_by_entity.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, vp, vp,
                                          ctypes.c_int64, vp, ctypes.c_int, vp, vp, vp, vp]
         _lib = L
@@ -190,3 +196,66 @@ def rows_by_entity(dim: int, element: int, coords, elems, query, cap: int = 64):
     if st != 0:
         raise ValueError(f"ora_rows_by_entity failed ({st})")
     return [(cols[i, : count[i]], vm[i, : count[i]], vk[i, : count[i]]) for i in range(nq)]
+
+
+# --------------------------------------------------------------------------- f1: vectorized integration
+VALUE, DERIVATIVE = 0, 1
+
+
+def quad6(dim: int):
+    """Degree-6 rule on the reference element: points (nq, dim), weights (nq,)."""
+    pts = np.zeros((24, dim))
+    w = np.zeros(24)
+    nq = lib().ora_quad6(dim, _p(pts), _p(w))
+    return pts[:nq].copy(), w[:nq].copy()
+
+
+def quad_points(dim: int, coords, elems):
+    """Physical degree-6 quadrature points, shape (T, nq, dim)."""
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    elems = np.ascontiguousarray(elems, dtype=np.int32)
+    nq = 12 if dim == 2 else 24
+    out = np.zeros((elems.shape[0], nq, dim))
+    lib().ora_quad_points(dim, elems.shape[0], _p(coords), _p(elems), _p(out))
+    return out
+
+
+def load(dim: int, element: int, pairing: int, coords, elems, asm: Assembly, fq):
+    """b_i = sum_K sum_q w |det| f . (phi_i or its div / curl) at the points."""
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    elems = np.ascontiguousarray(elems, dtype=np.int32)
+    fq = np.ascontiguousarray(fq, dtype=np.float64)
+    b = np.zeros(asm.n_dofs)
+    st = lib().ora_load(dim, element, pairing, elems.shape[0], _p(coords), _p(elems),
+                        _p(np.ascontiguousarray(asm.elems2dofs)), _p(np.ascontiguousarray(asm.signs)), asm.n_dofs,
+                        _p(fq), _p(b))
+    if st != 0:
+        raise ValueError(f"ora_load failed ({st})")
+    return b
+
+
+def norm_l2(dim: int, coords, elems, fq):
+    """(total, per_element) of sum_K sum_q w |det| |f|^2; fq shape (T, nq[, nf])."""
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    elems = np.ascontiguousarray(elems, dtype=np.int32)
+    fq = np.ascontiguousarray(fq, dtype=np.float64)
+    nf = 1 if fq.ndim == 2 else fq.shape[2]
+    per = np.zeros(elems.shape[0])
+    tot = ctypes.c_double()
+    lib().ora_norm_l2(dim, elems.shape[0], _p(coords), _p(elems), _p(fq), nf, _p(per), ctypes.byref(tot))
+    return tot.value, per
+
+
+def field_error(dim: int, element: int, coords, elems, asm: Assembly, coeffs, Eq, Dq):
+    """(||E - v||^2, ||D E - D v||^2) for v = sum_i coeffs_i phi_i, D = div / curl."""
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    elems = np.ascontiguousarray(elems, dtype=np.int32)
+    err = np.zeros(2)
+    st = lib().ora_field_error(dim, element, elems.shape[0], _p(coords), _p(elems),
+                               _p(np.ascontiguousarray(asm.elems2dofs)), _p(np.ascontiguousarray(asm.signs)),
+                               _p(np.ascontiguousarray(coeffs, dtype=np.float64)),
+                               _p(np.ascontiguousarray(Eq, dtype=np.float64)),
+                               _p(np.ascontiguousarray(Dq, dtype=np.float64)), _p(err))
+    if st != 0:
+        raise ValueError(f"ora_field_error failed ({st})")
+    return err[0], err[1]
