@@ -222,6 +222,57 @@ efem_status efem_part_globalize(efem_plan plan, const int32_t* sub2global, const
 efem_status efem_part_numeric(efem_plan plan, unsigned forms, const int64_t* info, int64_t global_first_row,
                               const int32_t* e2d_global, efem_csr* slice, efem_stream_t stream);
 
+/* ---- vectorized integration (Sec. 3.1)
+ * The paper's recipe: map the quadrature points of the reference element to
+ * every element at once, evaluate the user's function there (the caller does
+ * this, vectorized, on the device), then reduce per element.  Degree-6 rules
+ * (PAPER.md:637, 648): 12 points per triangle (Dunavant), 24 per
+ * tetrahedron (Keast).  Point order within an element (fq rows follow it):
+ * each symmetry orbit in turn -- 2D: (a,b,b) orbits as (l0,l1,l2) = (a,b,b),
+ * (b,a,b), (b,b,a), then the 6-point orbit in lexicographic permutation
+ * order; 3D: the four (a,a,a,b) orbits as (b,a,a,a)..(a,a,a,b) with l0 first,
+ * then the 12-point orbit with a at slots i0 < i1, b at i2, c at i3 in
+ * lexicographic (i0, i1, i2) order; the point is (l1, l2[, l3]). */
+enum { EFEM_PAIR_VALUE = 0, EFEM_PAIR_DERIV = 1 };
+
+/* points per element of the degree-6 rule: 12 (dim 2), 24 (dim 3); 0 otherwise */
+int efem_quad_size(int dim);
+
+/* pts (device, n_elems x nq x dim): F_K(xh_q) = B_K xh_q + b_K. */
+efem_status efem_quad_points(const efem_mesh* mesh, double* pts, efem_stream_t stream);
+
+/* Load vector b (device, n_dofs) after efem_assemble_symbolic:
+ *   b_i = sum_K sum_q w_q |det B_K| f(x_q) . phi_i(x_q)          pairing EFEM_PAIR_VALUE, fq: T x nq x dim
+ *   b_i = sum_K sum_q w_q |det B_K| f(x_q) . (D phi_i)(x_q)      pairing EFEM_PAIR_DERIV, fq: T x nq x nd
+ * phi_i the global, sign-corrected Piola-mapped basis (PAPER.md:240-245,
+ * 291-331), D = div (RT, nd = 1), curl (Ned 2D nd = 1, 3D nd = 3).  Summed
+ * per DOF over its elements in ascending element order (deterministic). */
+efem_status efem_assemble_load(efem_plan plan, int pairing, const double* fq, double* b, efem_stream_t stream);
+
+/* ||f||^2 = sum_K sum_q w_q |det B_K| |f(x_q)|^2 (the norm_L2 listing,
+ * PAPER.md:633-645).  fq: T x nq x nf (device); per_elem (device, T) gets
+ * ||f||^2_K, total (device, 1 double) their fixed-order sum.  ws == NULL
+ * returns *ws_bytes. */
+efem_status efem_norm_l2(const efem_mesh* mesh, const double* fq, int nf, double* per_elem, double* total, void* ws,
+                         size_t* ws_bytes, efem_stream_t stream);
+
+/* Error of v = sum_i coeffs_i phi_i (after symbolic): err2 (device, 2) =
+ * { ||E - v||^2, ||D E - D v||^2 } from exact values Eq (T x nq x dim) and
+ * Dq (T x nq x nd) at the quadrature points.  ws == NULL returns *ws_bytes. */
+efem_status efem_field_error(efem_plan plan, const double* coeffs, const double* Eq, const double* Dq, double* err2,
+                             void* ws, size_t* ws_bytes, efem_stream_t stream);
+
+/* y = alpha K x + beta M x on an assembled CSR (vals_stiff = K, vals_mass = M). */
+efem_status efem_spmv(const efem_csr* A, double alpha, double beta, const double* x, double* y,
+                      efem_stream_t stream);
+
+/* Jacobi-preconditioned conjugate gradients for (alpha K + beta M) x = b
+ * (SPD for alpha, beta > 0): x (device) is the initial guess on entry, the
+ * iterate on return; stops when ||r|| <= rtol ||b|| (checked every 20
+ * iterations) or after maxit.  Synchronising.  ws == NULL returns *ws_bytes. */
+efem_status efem_cg(const efem_csr* A, double alpha, double beta, const double* b, double* x, double rtol, int maxit,
+                    int* iters, double* relres, void* ws, size_t* ws_bytes, efem_stream_t stream);
+
 /* ---- diagnostics ------------------------------------------------------------- */
 const char* efem_status_string(efem_status status);
 const char* efem_last_error(void);

@@ -17,6 +17,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "efem.h")
 EFEM_OK = 0
 EFEM_RT0, EFEM_NED0 = 0, 1
 EFEM_MASS, EFEM_STIFF, EFEM_PATTERN, EFEM_ALL = 1, 2, 4, 7
+EFEM_PAIR_VALUE, EFEM_PAIR_DERIV = 0, 1
 
 
 class efem_mesh(ctypes.Structure):
@@ -79,6 +80,16 @@ def load():
         "efem_part_scan": (st, [vp, i64, vp, vp, ctypes.POINTER(ctypes.c_size_t), vp]),
         "efem_part_globalize": (st, [vp, vp, vp, vp, vp]),
         "efem_part_numeric": (st, [vp, ctypes.c_uint, i64p, i64, vp, ctypes.POINTER(efem_csr), vp]),
+        "efem_quad_size": (ctypes.c_int, [ctypes.c_int]),
+        "efem_quad_points": (st, [ctypes.POINTER(efem_mesh), vp, vp]),
+        "efem_assemble_load": (st, [vp, ctypes.c_int, vp, vp, vp]),
+        "efem_norm_l2": (st, [ctypes.POINTER(efem_mesh), vp, ctypes.c_int, vp, vp, vp,
+                              ctypes.POINTER(ctypes.c_size_t), vp]),
+        "efem_field_error": (st, [vp, vp, vp, vp, vp, vp, ctypes.POINTER(ctypes.c_size_t), vp]),
+        "efem_spmv": (st, [ctypes.POINTER(efem_csr), ctypes.c_double, ctypes.c_double, vp, vp, vp]),
+        "efem_cg": (st, [ctypes.POINTER(efem_csr), ctypes.c_double, ctypes.c_double, vp, vp, ctypes.c_double,
+                         ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), vp,
+                         ctypes.POINTER(ctypes.c_size_t), vp]),
         "efem_status_string": (ctypes.c_char_p, [st]),
         "efem_last_error": (ctypes.c_char_p, []),
         "efem_last_bad_element": (i64, []),

@@ -188,3 +188,109 @@ class Assembler:
                                                                   ctypes.byref(d), ctypes.byref(h), _stream(stream)))
         self.n_rows, self.nnz = h.n_rows, h.nnz
         return h_out
+
+
+# --------------------------------------------------------------------------- f1 / f2: vectorized integration
+VALUE, DERIVATIVE = _lib.EFEM_PAIR_VALUE, _lib.EFEM_PAIR_DERIV
+
+
+def quad_size(dim: int) -> int:
+    """Points per element of the degree-6 rule (12 triangles, 24 tetrahedra)."""
+    return _lib.load().efem_quad_size(dim)
+
+
+def _mesh_struct(coords: torch.Tensor, elems: torch.Tensor):
+    return _lib.efem_mesh(int(coords.shape[1]), coords.shape[0], elems.shape[0], coords.data_ptr(),
+                          elems.data_ptr())
+
+
+def quad_points(coords: torch.Tensor, elems: torch.Tensor, stream=None) -> torch.Tensor:
+    """Physical quadrature points F_K(xh_q) of every element: (T, nq, dim)."""
+    dim = int(coords.shape[1])
+    pts = torch.empty((elems.shape[0], quad_size(dim), dim), dtype=torch.float64, device=coords.device)
+    m = _mesh_struct(coords, elems)
+    with torch.cuda.device(coords.device):
+        _lib.check("efem_quad_points", _lib.load().efem_quad_points(ctypes.byref(m), _ptr(pts), _stream(stream)))
+    return pts
+
+
+def norm_l2(coords: torch.Tensor, elems: torch.Tensor, fq: torch.Tensor, stream=None):
+    """(total, per_element) of sum_K sum_q w |det| |f|^2 for f values (T, nq[, nf])."""
+    fq = fq.contiguous()
+    nf = 1 if fq.dim() == 2 else int(fq.shape[2])
+    L = _lib.load()
+    m = _mesh_struct(coords, elems)
+    ws_bytes = ctypes.c_size_t()
+    per = torch.empty(elems.shape[0], dtype=torch.float64, device=coords.device)
+    tot = torch.empty(1, dtype=torch.float64, device=coords.device)
+    with torch.cuda.device(coords.device):
+        _lib.check("efem_norm_l2", L.efem_norm_l2(ctypes.byref(m), None, nf, None, None, None, ctypes.byref(ws_bytes),
+                                                  _stream(stream)))
+        ws = torch.empty(int(ws_bytes.value), dtype=torch.uint8, device=coords.device)
+        _lib.check("efem_norm_l2", L.efem_norm_l2(ctypes.byref(m), _ptr(fq), nf, _ptr(per), _ptr(tot), _ptr(ws),
+                                                  ctypes.byref(ws_bytes), _stream(stream)))
+    return tot, per
+
+
+def _assembler_load(self, fq: torch.Tensor, pairing: int = VALUE, stream=None) -> torch.Tensor:
+    """Load vector against the global basis (after symbolic): (n_dofs,)."""
+    if self.n_rows is None:
+        self.symbolic(stream=stream)
+    fq = fq.contiguous()
+    b = torch.empty(self.n_rows, dtype=torch.float64, device=self.device)
+    with torch.cuda.device(self.device):
+        _lib.check("efem_assemble_load", _lib.load().efem_assemble_load(self._plan, pairing, _ptr(fq), _ptr(b),
+                                                                        _stream(stream)))
+    return b
+
+
+def _assembler_field_error(self, coeffs: torch.Tensor, Eq: torch.Tensor, Dq: torch.Tensor, stream=None):
+    """Device tensor [||E - v||^2, ||D E - D v||^2] for v = sum_i coeffs_i phi_i."""
+    L = _lib.load()
+    ws_bytes = ctypes.c_size_t()
+    err = torch.empty(2, dtype=torch.float64, device=self.device)
+    Eq, Dq, coeffs = Eq.contiguous(), Dq.contiguous(), coeffs.contiguous()
+    with torch.cuda.device(self.device):
+        _lib.check("efem_field_error", L.efem_field_error(self._plan, None, None, None, None, None,
+                                                          ctypes.byref(ws_bytes), _stream(stream)))
+        ws = torch.empty(max(int(ws_bytes.value), 8), dtype=torch.uint8, device=self.device)
+        _lib.check("efem_field_error", L.efem_field_error(self._plan, _ptr(coeffs), _ptr(Eq), _ptr(Dq), _ptr(err),
+                                                          _ptr(ws), ctypes.byref(ws_bytes), _stream(stream)))
+    return err
+
+
+Assembler.load = _assembler_load
+Assembler.field_error = _assembler_field_error
+
+
+def _csr_ptrs(A: CSR):
+    return _lib.efem_csr(A.n_rows, A.nnz, A.row_ptr.data_ptr(), A.col_idx.data_ptr(), A.vals_M.data_ptr(),
+                         A.vals_K.data_ptr())
+
+
+def spmv(A: CSR, x: torch.Tensor, alpha: float = 1.0, beta: float = 1.0, stream=None) -> torch.Tensor:
+    """y = alpha K x + beta M x."""
+    y = torch.empty_like(x)
+    c = _csr_ptrs(A)
+    with torch.cuda.device(x.device):
+        _lib.check("efem_spmv", _lib.load().efem_spmv(ctypes.byref(c), alpha, beta, _ptr(x), _ptr(y),
+                                                      _stream(stream)))
+    return y
+
+
+def cg(A: CSR, b: torch.Tensor, alpha: float = 1.0, beta: float = 1.0, x0: torch.Tensor | None = None,
+       rtol: float = 1e-12, maxit: int = 100000, stream=None):
+    """Jacobi-preconditioned CG for (alpha K + beta M) x = b; returns (x, iters, relres)."""
+    L = _lib.load()
+    x = torch.zeros_like(b) if x0 is None else x0.clone()
+    c = _csr_ptrs(A)
+    ws_bytes = ctypes.c_size_t()
+    it, rr = ctypes.c_int(), ctypes.c_double()
+    with torch.cuda.device(b.device):
+        _lib.check("efem_cg", L.efem_cg(ctypes.byref(c), alpha, beta, None, None, rtol, maxit, ctypes.byref(it),
+                                        ctypes.byref(rr), None, ctypes.byref(ws_bytes), _stream(stream)))
+        ws = torch.empty(int(ws_bytes.value), dtype=torch.uint8, device=b.device)
+        _lib.check("efem_cg", L.efem_cg(ctypes.byref(c), alpha, beta, _ptr(b), _ptr(x), rtol, maxit,
+                                        ctypes.byref(it), ctypes.byref(rr), _ptr(ws), ctypes.byref(ws_bytes),
+                                        _stream(stream)))
+    return x, it.value, rr.value

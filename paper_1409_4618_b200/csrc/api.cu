@@ -16,6 +16,20 @@ namespace efem {
 efem_status launch_enumerate(Plan& p, cudaStream_t s);
 efem_status launch_signs(Plan& p, int8_t* out, cudaStream_t s);
 efem_status launch_rows_any(Plan& p, unsigned forms, efem_csr* out, const RowWindow& w, cudaStream_t s);
+// integrate.cu (f1 / f2)
+int quad6_size(int dim);
+efem_status launch_quad_points(int dim, const double* coords, const int32_t* elems, int64_t n_elems, double* pts,
+                               cudaStream_t s);
+efem_status launch_load(Plan& p, int pairing, const double* fq, double* b, cudaStream_t s);
+size_t reduce_ws_bytes();
+efem_status launch_norm_l2(int dim, const double* coords, const int32_t* elems, int64_t n_elems, const double* fq,
+                           int nf, double* per_elem, double* total, double* part, cudaStream_t s);
+efem_status launch_field_error(Plan& p, const double* coeffs, const double* Eq, const double* Dq, double* err2,
+                               double* scratch, cudaStream_t s);
+efem_status launch_spmv(const efem_csr* A, double alpha, double beta, const double* x, double* y, cudaStream_t s);
+size_t cg_ws_bytes(int64_t n);
+efem_status run_cg(const efem_csr* A, double alpha, double beta, const double* b, double* x, double rtol, int maxit,
+                   int* iters, double* relres, void* ws, cudaStream_t s);
 
 namespace {
 thread_local std::string g_last_error;
@@ -499,6 +513,105 @@ efem_status efem_assemble_host(efem_plan plan, const double* h_coords, const int
     h_out->n_rows = R;
     h_out->nnz = nnz;
     return EFEM_OK;
+}
+
+// ---- f1 / f2 -------------------------------------------------------------------------
+int efem_quad_size(int dim) { return (dim == 2 || dim == 3) ? quad6_size(dim) : 0; }
+
+efem_status efem_quad_points(const efem_mesh* mesh, double* pts, efem_stream_t stream) {
+    if (!mesh || (mesh->dim != 2 && mesh->dim != 3) || mesh->n_elems < 0 ||
+        (mesh->n_elems > 0 && (!pts || !mesh->coords || !mesh->elems))) {
+        set_error("efem_quad_points: bad mesh or NULL output");
+        return EFEM_EINVAL;
+    }
+    return launch_quad_points(mesh->dim, mesh->coords, mesh->elems, mesh->n_elems, pts, (cudaStream_t)stream);
+}
+
+efem_status efem_assemble_load(efem_plan plan, int pairing, const double* fq, double* b, efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    efem_status st = need_ws(p);
+    if (st != EFEM_OK) return st;
+    if (!p->symbolic) {
+        set_error("efem_assemble_load before efem_assemble_symbolic");
+        return EFEM_ESTATE;
+    }
+    if ((pairing != EFEM_PAIR_VALUE && pairing != EFEM_PAIR_DERIV) || (p->n_dofs > 0 && (!fq || !b))) {
+        set_error("efem_assemble_load: pairing must be EFEM_PAIR_VALUE or EFEM_PAIR_DERIV, arrays non-NULL");
+        return EFEM_EINVAL;
+    }
+    return launch_load(*p, pairing, fq, b, (cudaStream_t)stream);
+}
+
+efem_status efem_norm_l2(const efem_mesh* mesh, const double* fq, int nf, double* per_elem, double* total, void* ws,
+                         size_t* ws_bytes, efem_stream_t stream) {
+    if (!ws_bytes) {
+        set_error("efem_norm_l2: NULL ws_bytes");
+        return EFEM_EINVAL;
+    }
+    if (!ws) {
+        *ws_bytes = reduce_ws_bytes();
+        return EFEM_OK;
+    }
+    if (!mesh || (mesh->dim != 2 && mesh->dim != 3) || nf < 1 || !total || *ws_bytes < reduce_ws_bytes() ||
+        (mesh->n_elems > 0 && (!fq || !per_elem))) {
+        set_error("efem_norm_l2: bad arguments or workspace too small");
+        return EFEM_EINVAL;
+    }
+    return launch_norm_l2(mesh->dim, mesh->coords, mesh->elems, mesh->n_elems, fq, nf, per_elem, total,
+                          static_cast<double*>(ws), (cudaStream_t)stream);
+}
+
+efem_status efem_field_error(efem_plan plan, const double* coeffs, const double* Eq, const double* Dq, double* err2,
+                             void* ws, size_t* ws_bytes, efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    efem_status st = need_ws(p);
+    if (st != EFEM_OK) return st;
+    if (!ws_bytes) {
+        set_error("efem_field_error: NULL ws_bytes");
+        return EFEM_EINVAL;
+    }
+    const size_t need = (size_t)(2 * p->n_elems) * sizeof(double) + reduce_ws_bytes();
+    if (!ws) {
+        *ws_bytes = need;
+        return EFEM_OK;
+    }
+    if (!p->symbolic) {
+        set_error("efem_field_error before efem_assemble_symbolic");
+        return EFEM_ESTATE;
+    }
+    if (*ws_bytes < need || !err2 || (p->n_elems > 0 && (!coeffs || !Eq || !Dq))) {
+        set_error("efem_field_error: bad arguments or workspace too small");
+        return EFEM_EINVAL;
+    }
+    return launch_field_error(*p, coeffs, Eq, Dq, err2, static_cast<double*>(ws), (cudaStream_t)stream);
+}
+
+efem_status efem_spmv(const efem_csr* A, double alpha, double beta, const double* x, double* y,
+                      efem_stream_t stream) {
+    if (!A || A->n_rows < 0 || (A->n_rows > 0 && (!A->row_ptr || !A->col_idx || !A->vals_mass || !A->vals_stiff ||
+                                                  !x || !y))) {
+        set_error("efem_spmv: NULL array");
+        return EFEM_EINVAL;
+    }
+    return launch_spmv(A, alpha, beta, x, y, (cudaStream_t)stream);
+}
+
+efem_status efem_cg(const efem_csr* A, double alpha, double beta, const double* b, double* x, double rtol, int maxit,
+                    int* iters, double* relres, void* ws, size_t* ws_bytes, efem_stream_t stream) {
+    if (!A || !ws_bytes) {
+        set_error("efem_cg: NULL argument");
+        return EFEM_EINVAL;
+    }
+    if (!ws) {
+        *ws_bytes = cg_ws_bytes(A->n_rows);
+        return EFEM_OK;
+    }
+    if (*ws_bytes < cg_ws_bytes(A->n_rows) || !iters || !relres || maxit < 0 || !(rtol >= 0.0) ||
+        (A->n_rows > 0 && (!b || !x || !A->row_ptr || !A->col_idx || !A->vals_mass || !A->vals_stiff))) {
+        set_error("efem_cg: bad arguments or workspace too small");
+        return EFEM_EINVAL;
+    }
+    return run_cg(A, alpha, beta, b, x, rtol, maxit, iters, relres, ws, (cudaStream_t)stream);
 }
 
 }  // extern "C"

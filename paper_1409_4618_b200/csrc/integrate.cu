@@ -1,0 +1,654 @@
+// integrate.cu -- SURVEY.md §8(f) rows f1 / f2 on the GPU: the paper's
+// vectorized integration (Sec. 3.1) -- degree-6
+// quadrature points F_K(xh_i) of all elements, load vectors against the
+// global Piola-mapped basis, L2 norms and field errors -- plus the CSR SpMV
+// and the Jacobi-preconditioned CG used by the eddy-current example
+// (PAPER.md:863-918).  Every reduction runs in a fixed order (per-element
+// values, then a two-level tree), so results are bitwise reproducible.
+// Product path only; shares nothing with oracle/.
+#include <cmath>
+#include <vector>
+
+#include "element.cuh"
+
+namespace efem {
+
+// ---- degree-6 rules: Dunavant 12-point (2D), Keast
+// 24-point (3D); barycentric (l1, l2[, l3]) and weights including |K_hat|.
+struct Quad6 {
+    double l[24][3];
+    double w[24];
+    int nq;
+};
+
+__constant__ Quad6 c_quad[2];  // [0] 2D, [1] 3D
+
+namespace {
+
+Quad6 make_quad6(int dim) {
+    Quad6 Q{};
+    int n = 0;
+    auto put = [&](double a, double b, double c, double wt) {
+        Q.l[n][0] = a;
+        Q.l[n][1] = b;
+        Q.l[n][2] = c;
+        Q.w[n] = wt;
+        ++n;
+    };
+    if (dim == 2) {
+        struct S3 { double w, a, b; };
+        const S3 s3[2] = {{0.116786275726379, 0.501426509658179, 0.249286745170910},
+                          {0.050844906370207, 0.873821971016996, 0.063089014491502}};
+        for (const S3& s : s3) {  // (l0, l1, l2) in {(a,b,b), (b,a,b), (b,b,a)}
+            put(s.b, s.b, 0.0, 0.5 * s.w);
+            put(s.a, s.b, 0.0, 0.5 * s.w);
+            put(s.b, s.a, 0.0, 0.5 * s.w);
+        }
+        // the six placements of (c0, c1, c2) on (l0, l1, l2), permutations in
+        // lexicographic order (the point order is part of the interface: fq
+        // rows follow it)
+        const double v[3] = {0.053145049844817, 0.310352451033784, 0.636502499121399};
+        const int perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+        for (int i = 0; i < 6; ++i) put(v[perm[i][1]], v[perm[i][2]], 0.0, 0.5 * 0.082851075618374);
+    } else {
+        const double a4[3] = {0.214602871259151684, 0.0406739585346113397, 0.322337890142275646};
+        const double w4[3] = {0.0399227502581679, 0.0100772110553207, 0.0553571815436544};
+        for (int c = 0; c < 3; ++c) {
+            const double a = a4[c], b = 1.0 - 3.0 * a, wt = w4[c] / 6.0;
+            put(a, a, a, wt);
+            put(b, a, a, wt);
+            put(a, b, a, wt);
+            put(a, a, b, wt);
+        }
+        const double a = 0.0636610018750175299, b = 0.269672331458315867, c = 0.603005664791649076;
+        const double wt = 0.0482142857142857 / 6.0;
+        // the 12 arrangements of {a, a, b, c} on (l0..l3): a at slots i0 < i1,
+        // b at i2, c at i3, (i0, i1, i2, i3) in lexicographic order
+        for (int i0 = 0; i0 < 4; ++i0)
+            for (int i1 = i0 + 1; i1 < 4; ++i1)
+                for (int i2 = 0; i2 < 4; ++i2) {
+                    if (i2 == i0 || i2 == i1) continue;
+                    const int i3 = 6 - i0 - i1 - i2;
+                    double lam[4];
+                    lam[i0] = a;
+                    lam[i1] = a;
+                    lam[i2] = b;
+                    lam[i3] = c;
+                    put(lam[1], lam[2], lam[3], wt);
+                }
+    }
+    Q.nq = n;
+    return Q;
+}
+
+bool g_quad_ready = false;
+
+efem_status ensure_quad() {
+    if (g_quad_ready) return EFEM_OK;
+    Quad6 q[2] = {make_quad6(2), make_quad6(3)};
+    EFEM_CUDA_TRY(cudaMemcpyToSymbol(c_quad, q, sizeof(q)));
+    g_quad_ready = true;
+    return EFEM_OK;
+}
+
+// ---- element geometry: B = [x1-x0 | x2-x0 (| x3-x0)]
+template <int D>
+struct Geo {
+    double x0[D];
+    double B[D][D];  // B[r][c]
+    double det;
+    double BiT[D][D];  // B^{-T}
+};
+
+template <int D>
+__device__ __forceinline__ void load_geo(const double* __restrict__ coords, const int (&g)[D + 1], Geo<D>& G) {
+    double X[D + 1][D];
+#pragma unroll
+    for (int v = 0; v <= D; ++v)
+#pragma unroll
+        for (int c = 0; c < D; ++c) X[v][c] = __ldg(coords + (int64_t)g[v] * D + c);
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        G.x0[r] = X[0][r];
+#pragma unroll
+        for (int c = 0; c < D; ++c) G.B[r][c] = X[c + 1][r] - X[0][r];
+    }
+    if constexpr (D == 2) {
+        G.det = G.B[0][0] * G.B[1][1] - G.B[0][1] * G.B[1][0];
+        const double id = 1.0 / G.det;
+        G.BiT[0][0] = G.B[1][1] * id;
+        G.BiT[0][1] = -G.B[1][0] * id;
+        G.BiT[1][0] = -G.B[0][1] * id;
+        G.BiT[1][1] = G.B[0][0] * id;
+    } else {
+        double cof[3][3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int r1 = (r + 1) % 3, r2 = (r + 2) % 3, c1 = (c + 1) % 3, c2 = (c + 2) % 3;
+                cof[r][c] = G.B[r1][c1] * G.B[r2][c2] - G.B[r1][c2] * G.B[r2][c1];
+            }
+        G.det = G.B[0][0] * cof[0][0] + G.B[0][1] * cof[0][1] + G.B[0][2] * cof[0][2];
+        const double id = 1.0 / G.det;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) G.BiT[r][c] = cof[r][c] * id;
+    }
+}
+
+// Reference basis value of local DOF k at xh (PAPER.md:228-238 RT with the
+// 3D RT basis doubled (reading C1), 275-289 Ned) and its reference div /
+// curl (constant).
+template <class KT>
+__device__ __forceinline__ void ref_value(int k, const double* xh, double (&v)[KT::D]) {
+    const double x1 = xh[0], x2 = xh[1];
+    if constexpr (KT::D == 2 && KT::ELEMENT == EFEM_RT0) {
+        v[0] = k == 1 ? x1 - 1.0 : x1;
+        v[1] = k == 2 ? x2 - 1.0 : x2;
+    } else if constexpr (KT::D == 2) {
+        v[0] = k == 2 ? 1.0 - x2 : -x2;
+        v[1] = k == 1 ? x1 - 1.0 : x1;
+    } else if constexpr (KT::FACES) {
+        const double x3 = xh[2];
+        v[0] = 2.0 * (k == 2 ? x1 - 1.0 : x1);
+        v[1] = 2.0 * (k == 1 ? x2 - 1.0 : x2);
+        v[2] = 2.0 * (k == 0 ? x3 - 1.0 : x3);
+    } else {
+        const double x3 = xh[2];
+        switch (k) {
+            case 0: v[0] = 1.0 - x3 - x2; v[1] = x1; v[2] = x1; break;
+            case 1: v[0] = x2; v[1] = 1.0 - x3 - x1; v[2] = x2; break;
+            case 2: v[0] = x3; v[1] = x3; v[2] = 1.0 - x2 - x1; break;
+            case 3: v[0] = -x2; v[1] = x1; v[2] = 0.0; break;
+            case 4: v[0] = 0.0; v[1] = -x3; v[2] = x2; break;
+            default: v[0] = x3; v[1] = 0.0; v[2] = -x1; break;
+        }
+    }
+}
+
+template <class KT>
+__host__ __device__ constexpr int n_deriv() { return (KT::D == 3 && KT::ELEMENT == EFEM_NED0) ? 3 : 1; }
+
+template <class KT>
+__device__ __forceinline__ void ref_deriv(int k, double (&d)[n_deriv<KT>()]) {
+    if constexpr (KT::D == 2) {
+        d[0] = 2.0;  // div (RT) and curl (Ned) of every 2D reference function
+    } else if constexpr (KT::FACES) {
+        d[0] = 6.0;
+    } else {  // curl of the 3D Ned reference functions
+        const double c[6][3] = {{0, -2, 2}, {2, 0, -2}, {-2, 2, 0}, {0, 0, 2}, {2, 0, 0}, {0, 2, 0}};
+#pragma unroll
+        for (int r = 0; r < 3; ++r) d[r] = c[0][r];
+#pragma unroll
+        for (int j = 1; j < 6; ++j)
+            if (k == j) {
+#pragma unroll
+                for (int r = 0; r < 3; ++r) d[r] = c[j][r];
+            }
+    }
+}
+
+// Global basis of local DOF k on the element (PAPER.md:240-245, 291-301,
+// 323-331): RT s/det B eta, div s/det div; Ned s B^{-T} eta, curl s/det curl
+// (2D), s/det B curl (3D).
+template <class KT>
+__device__ __forceinline__ void global_value(const Geo<KT::D>& G, double s, int k, const double* xh,
+                                             double (&phi)[KT::D]) {
+    constexpr int D = KT::D;
+    double v[D];
+    ref_value<KT>(k, xh, v);
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc += (KT::ELEMENT == EFEM_RT0 ? G.B[r][c] : G.BiT[r][c]) * v[c];
+        phi[r] = KT::ELEMENT == EFEM_RT0 ? s * acc / G.det : s * acc;
+    }
+}
+
+template <class KT>
+__device__ __forceinline__ void global_deriv(const Geo<KT::D>& G, double s, int k, double (&dphi)[n_deriv<KT>()]) {
+    double d[n_deriv<KT>()];
+    ref_deriv<KT>(k, d);
+    if constexpr (n_deriv<KT>() == 3) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) dphi[r] = s * (G.B[r][0] * d[0] + G.B[r][1] * d[1] + G.B[r][2] * d[2]) / G.det;
+    } else {
+        dphi[0] = s * d[0] / G.det;
+    }
+}
+
+__device__ __forceinline__ const Quad6& quad(int D) { return c_quad[D - 2]; }
+
+// ---- kernels ------------------------------------------------------------------------
+template <int D>
+__global__ void k_quad_points(const double* __restrict__ coords, const int32_t* __restrict__ elems, int64_t n_elems,
+                              double* __restrict__ pts) {
+    const Quad6& Q = quad(D);
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_elems * Q.nq) return;
+    const int64_t e = i / Q.nq;
+    const int q = (int)(i - e * Q.nq);
+    double x[D];
+    double X0[D];
+    const int g0 = __ldg(elems + e * (D + 1));
+#pragma unroll
+    for (int c = 0; c < D; ++c) X0[c] = __ldg(coords + (int64_t)g0 * D + c);
+#pragma unroll
+    for (int c = 0; c < D; ++c) x[c] = X0[c];
+#pragma unroll
+    for (int v = 1; v <= D; ++v) {
+        const int gv = __ldg(elems + e * (D + 1) + v);
+        const double l = Q.l[q][v - 1];
+#pragma unroll
+        for (int c = 0; c < D; ++c) x[c] += (__ldg(coords + (int64_t)gv * D + c) - X0[c]) * l;
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) pts[i * D + c] = x[c];
+}
+
+// b_i = sum over the elements of DOF i (ascending element id) of
+// sum_q w_q |det| f(x_q) . phi_k(x_q)   (pairing 0)  or  . (div/curl phi_k)(x_q)  (pairing 1)
+template <class KT, int PAIR>
+__global__ void __launch_bounds__(128) k_load(const double* __restrict__ coords, const int32_t* __restrict__ elems,
+                                              const int32_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
+                                              int64_t n_dofs, const double* __restrict__ fq, double* __restrict__ b) {
+    constexpr int D = KT::D, NV = KT::NV;
+    constexpr int ND = n_deriv<KT>();
+    constexpr int NF = PAIR == 0 ? D : ND;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_dofs) return;
+    const Quad6& Q = quad(D);
+    const int ib = __ldg(inc_ptr + i), t = min(__ldg(inc_ptr + i + 1) - ib, EFEM_MAX_ROW_ELEMS);
+    int ord[EFEM_MAX_ROW_ELEMS];  // ascending element order
+    for (int j = 0; j < t; ++j) {
+        const int v = __ldg(inc + ib + j) & INST_MASK;
+        int q = j;
+        while (q > 0 && ord[q - 1] > v) {
+            ord[q] = ord[q - 1];
+            --q;
+        }
+        ord[q] = v;
+    }
+    double acc = 0.0;
+    for (int j = 0; j < t; ++j) {
+        const int e = ord[j] >> 3, k = ord[j] & 7;
+        int g[NV];
+        load_g<KT>(elems, e, g);
+        Geo<D> G;
+        load_geo<D>(coords, g, G);
+        const double s = sign_d<KT>(g, k);
+        const double adet = fabs(G.det);
+        const double* f = fq + (int64_t)e * Q.nq * NF;
+        double loc = 0.0;
+        if constexpr (PAIR == 1) {
+            double dphi[ND];
+            global_deriv<KT>(G, s, k, dphi);
+            for (int q = 0; q < Q.nq; ++q) {
+                double dot = 0.0;
+#pragma unroll
+                for (int c = 0; c < NF; ++c) dot += __ldg(f + q * NF + c) * dphi[c];
+                loc += Q.w[q] * adet * dot;
+            }
+        } else {
+            for (int q = 0; q < Q.nq; ++q) {
+                double phi[D];
+                global_value<KT>(G, s, k, Q.l[q], phi);
+                double dot = 0.0;
+#pragma unroll
+                for (int c = 0; c < NF; ++c) dot += __ldg(f + q * NF + c) * phi[c];
+                loc += Q.w[q] * adet * dot;
+            }
+        }
+        acc += loc;
+    }
+    b[i] = acc;
+}
+
+template <int D>
+__global__ void k_norm_elem(const double* __restrict__ coords, const int32_t* __restrict__ elems, int64_t n_elems,
+                            const double* __restrict__ fq, int nf, double* __restrict__ per_elem) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n_elems) return;
+    const Quad6& Q = quad(D);
+    int g[D + 1];
+#pragma unroll
+    for (int v = 0; v <= D; ++v) g[v] = __ldg(elems + e * (D + 1) + v);
+    Geo<D> G;
+    load_geo<D>(coords, g, G);
+    const double adet = fabs(G.det);
+    const double* f = fq + e * Q.nq * nf;
+    double acc = 0.0;
+    for (int q = 0; q < Q.nq; ++q) {
+        double f2 = 0.0;
+        for (int c = 0; c < nf; ++c) {
+            const double v = __ldg(f + q * nf + c);
+            f2 += v * v;
+        }
+        acc += Q.w[q] * adet * f2;
+    }
+    per_elem[e] = acc;
+}
+
+// per element: ||E - v||^2_K and ||D E - D v||^2_K, v = sum_i c_i phi_i
+template <class KT>
+__global__ void k_field_error(const double* __restrict__ coords, const int32_t* __restrict__ elems, int64_t n_elems,
+                              const int32_t* __restrict__ e2d, const double* __restrict__ coeffs,
+                              const double* __restrict__ Eq, const double* __restrict__ Dq,
+                              double* __restrict__ ev, double* __restrict__ ed) {
+    constexpr int D = KT::D, NV = KT::NV, M = KT::M, ND = n_deriv<KT>();
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n_elems) return;
+    const Quad6& Q = quad(D);
+    int g[NV];
+    load_g<KT>(elems, (int)e, g);
+    Geo<D> G;
+    load_geo<D>(coords, g, G);
+    double c[M], s[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        c[k] = __ldg(coeffs + __ldg(e2d + e * M + k));
+        s[k] = sign_d<KT>(g, k);
+    }
+    double dv[ND];
+#pragma unroll
+    for (int r = 0; r < ND; ++r) dv[r] = 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        double d[ND];
+        global_deriv<KT>(G, s[k], k, d);
+#pragma unroll
+        for (int r = 0; r < ND; ++r) dv[r] += c[k] * d[r];
+    }
+    const double adet = fabs(G.det);
+    double a = 0.0, dd = 0.0;
+    for (int q = 0; q < Q.nq; ++q) {
+        double v[D];
+#pragma unroll
+        for (int r = 0; r < D; ++r) v[r] = 0.0;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            double phi[D];
+            global_value<KT>(G, s[k], k, Q.l[q], phi);
+#pragma unroll
+            for (int r = 0; r < D; ++r) v[r] += c[k] * phi[r];
+        }
+        double ta = 0.0, td = 0.0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            const double x = __ldg(Eq + (e * Q.nq + q) * D + r) - v[r];
+            ta += x * x;
+        }
+#pragma unroll
+        for (int r = 0; r < ND; ++r) {
+            const double x = __ldg(Dq + (e * Q.nq + q) * ND + r) - dv[r];
+            td += x * x;
+        }
+        a += Q.w[q] * adet * ta;
+        dd += Q.w[q] * adet * td;
+    }
+    ev[e] = a;
+    ed[e] = dd;
+}
+
+// ---- fixed-order reductions ---------------------------------------------------------
+constexpr int RED_TPB = 256;
+constexpr int RED_PARTS = 1024;
+
+// part p sums v[p*chunk, (p+1)*chunk) with a fixed shared-memory tree
+__global__ void __launch_bounds__(RED_TPB) k_reduce_parts(const double* __restrict__ v, int64_t n, int64_t chunk,
+                                                          double* __restrict__ part) {
+    __shared__ double sm[RED_TPB];
+    const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    double acc = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += RED_TPB) acc += v[i];
+    sm[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = RED_TPB / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) sm[threadIdx.x] += sm[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+
+// out[0] = sum of part[0..np) (fixed tree); optional finalize
+__global__ void __launch_bounds__(RED_TPB) k_reduce_final(const double* __restrict__ part, int np,
+                                                          double* __restrict__ out) {
+    __shared__ double sm[RED_TPB];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < np; i += RED_TPB) acc += part[i];
+    sm[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = RED_TPB / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) sm[threadIdx.x] += sm[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = sm[0];
+}
+
+efem_status reduce_fixed(const double* v, int64_t n, double* part, double* out, cudaStream_t s) {
+    const int64_t chunk = std::max<int64_t>(RED_TPB, (n + RED_PARTS - 1) / RED_PARTS);
+    const int np = (int)((n + chunk - 1) / chunk);
+    if (np > 0) {
+        k_reduce_parts<<<np, RED_TPB, 0, s>>>(v, n, chunk, part);
+        EFEM_LAUNCH_CHECK();
+    }
+    k_reduce_final<<<1, RED_TPB, 0, s>>>(part, np, out);
+    EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
+
+// ---- SpMV and CG ----------------------------------------------------------------------
+// y = alpha K x + beta M x on the shared pattern (one thread per row)
+__global__ void k_spmv(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ vk,
+                       const double* __restrict__ vm, double alpha, double beta, int64_t n, const double* __restrict__ x,
+                       double* __restrict__ y) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = 0.0;
+    for (int j = __ldg(rp + i); j < __ldg(rp + i + 1); ++j)
+        acc += (alpha * __ldg(vk + j) + beta * __ldg(vm + j)) * __ldg(x + __ldg(ci + j));
+    y[i] = acc;
+}
+
+__global__ void k_diag(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ vk,
+                       const double* __restrict__ vm, double alpha, double beta, int64_t n, double* __restrict__ dinv) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double d = 0.0;
+    for (int j = rp[i]; j < rp[i + 1]; ++j)
+        if (ci[j] == i) d = alpha * vk[j] + beta * vm[j];
+    dinv[i] = d != 0.0 ? 1.0 / d : 1.0;
+}
+
+// elementwise product into a scratch vector (then reduced in fixed order)
+__global__ void k_mul(const double* __restrict__ a, const double* __restrict__ b, int64_t n, double* __restrict__ o) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) o[i] = a[i] * b[i];
+}
+
+// x += a p ; r -= a q ; z = dinv r ; t1 = r z ; t2 = r r    (a = sc[0] / sc[1])
+__global__ void k_cg_update(const double* __restrict__ sc, const double* __restrict__ p, const double* __restrict__ q,
+                            const double* __restrict__ dinv, int64_t n, double* __restrict__ x, double* __restrict__ r,
+                            double* __restrict__ z, double* __restrict__ t1, double* __restrict__ t2) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double a = sc[0] / sc[1];
+    x[i] += a * p[i];
+    const double ri = r[i] - a * q[i];
+    r[i] = ri;
+    const double zi = dinv[i] * ri;
+    z[i] = zi;
+    t1[i] = ri * zi;
+    t2[i] = ri * ri;
+}
+
+// p = z + (rz_new / rz_old) p ; then rz_old = rz_new
+__global__ void k_cg_dir(double* __restrict__ sc, const double* __restrict__ z, int64_t n, double* __restrict__ p) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    p[i] = z[i] + (sc[2] / sc[0]) * p[i];
+}
+
+__global__ void k_copy_scalar(const double* __restrict__ src, double* __restrict__ dst) { dst[0] = src[0]; }
+
+}  // namespace
+
+// ---- launchers ------------------------------------------------------------------------
+int quad6_size(int dim) { return dim == 2 ? 12 : 24; }
+
+efem_status launch_quad_points(int dim, const double* coords, const int32_t* elems, int64_t n_elems, double* pts,
+                               cudaStream_t s) {
+    efem_status st;
+    if ((st = ensure_quad()) != EFEM_OK) return st;
+    const int64_t n = n_elems * quad6_size(dim);
+    if (n == 0) return EFEM_OK;
+    if (dim == 2) k_quad_points<2><<<grid_for(n, 256), 256, 0, s>>>(coords, elems, n_elems, pts);
+    else k_quad_points<3><<<grid_for(n, 256), 256, 0, s>>>(coords, elems, n_elems, pts);
+    EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
+
+template <class KT>
+efem_status load_kt(Plan& p, int pairing, const double* fq, double* b, cudaStream_t s) {
+    const unsigned grid = grid_for(p.n_dofs, 128);
+    if (pairing == 0)
+        k_load<KT, 0><<<grid, 128, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.n_dofs, fq, b);
+    else
+        k_load<KT, 1><<<grid, 128, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.n_dofs, fq, b);
+    EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
+
+efem_status launch_load(Plan& p, int pairing, const double* fq, double* b, cudaStream_t s) {
+    efem_status st;
+    if ((st = ensure_quad()) != EFEM_OK) return st;
+    if (p.n_dofs == 0) return EFEM_OK;
+    if (p.dim == 2) return p.element == EFEM_RT0 ? load_kt<Kind<2, EFEM_RT0>>(p, pairing, fq, b, s)
+                                                 : load_kt<Kind<2, EFEM_NED0>>(p, pairing, fq, b, s);
+    return p.element == EFEM_RT0 ? load_kt<Kind<3, EFEM_RT0>>(p, pairing, fq, b, s)
+                                 : load_kt<Kind<3, EFEM_NED0>>(p, pairing, fq, b, s);
+}
+
+size_t reduce_ws_bytes() { return (size_t)(RED_PARTS + 8) * sizeof(double); }
+
+efem_status launch_norm_l2(int dim, const double* coords, const int32_t* elems, int64_t n_elems, const double* fq,
+                           int nf, double* per_elem, double* total, double* part, cudaStream_t s) {
+    efem_status st;
+    if ((st = ensure_quad()) != EFEM_OK) return st;
+    if (n_elems > 0) {
+        if (dim == 2) k_norm_elem<2><<<grid_for(n_elems, 128), 128, 0, s>>>(coords, elems, n_elems, fq, nf, per_elem);
+        else k_norm_elem<3><<<grid_for(n_elems, 128), 128, 0, s>>>(coords, elems, n_elems, fq, nf, per_elem);
+        EFEM_LAUNCH_CHECK();
+    }
+    return reduce_fixed(per_elem, n_elems, part, total, s);
+}
+
+template <class KT>
+efem_status field_error_kt(Plan& p, const double* coeffs, const double* Eq, const double* Dq, double* ev, double* ed,
+                           cudaStream_t s) {
+    k_field_error<KT><<<grid_for(p.n_elems, 128), 128, 0, s>>>(p.coords, p.elems, p.n_elems, p.e2d, coeffs, Eq, Dq,
+                                                               ev, ed);
+    EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
+
+efem_status launch_field_error(Plan& p, const double* coeffs, const double* Eq, const double* Dq, double* err2,
+                               double* scratch, cudaStream_t s) {
+    efem_status st;
+    if ((st = ensure_quad()) != EFEM_OK) return st;
+    double* ev = scratch;
+    double* ed = scratch + p.n_elems;
+    double* part = scratch + 2 * p.n_elems;
+    if (p.n_elems > 0) {
+        if (p.dim == 2)
+            st = p.element == EFEM_RT0 ? field_error_kt<Kind<2, EFEM_RT0>>(p, coeffs, Eq, Dq, ev, ed, s)
+                                       : field_error_kt<Kind<2, EFEM_NED0>>(p, coeffs, Eq, Dq, ev, ed, s);
+        else
+            st = p.element == EFEM_RT0 ? field_error_kt<Kind<3, EFEM_RT0>>(p, coeffs, Eq, Dq, ev, ed, s)
+                                       : field_error_kt<Kind<3, EFEM_NED0>>(p, coeffs, Eq, Dq, ev, ed, s);
+        if (st != EFEM_OK) return st;
+    }
+    if ((st = reduce_fixed(ev, p.n_elems, part, err2, s)) != EFEM_OK) return st;
+    return reduce_fixed(ed, p.n_elems, part, err2 + 1, s);
+}
+
+efem_status launch_spmv(const efem_csr* A, double alpha, double beta, const double* x, double* y, cudaStream_t s) {
+    if (A->n_rows == 0) return EFEM_OK;
+    k_spmv<<<grid_for(A->n_rows, 256), 256, 0, s>>>(A->row_ptr, A->col_idx, A->vals_stiff, A->vals_mass, alpha, beta,
+                                                    A->n_rows, x, y);
+    EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
+
+size_t cg_ws_bytes(int64_t n) { return (size_t)(7 * n + RED_PARTS + 16) * sizeof(double) + 256; }
+
+// Jacobi-preconditioned CG on A = alpha K + beta M (SPD for alpha, beta > 0).
+// Device-side scalars; the host reads the residual every `check` iterations.
+efem_status run_cg(const efem_csr* A, double alpha, double beta, const double* b, double* x, double rtol, int maxit,
+                   int* iters, double* relres, void* ws, cudaStream_t s) {
+    const int64_t n = A->n_rows;
+    double* w = reinterpret_cast<double*>(ws);
+    double *r = w, *z = w + n, *p = w + 2 * n, *q = w + 3 * n, *dinv = w + 4 * n, *t1 = w + 5 * n, *t2 = w + 6 * n;
+    double* part = w + 7 * n;
+    double* sc = part + RED_PARTS;  // [0] rz  [1] pq  [2] rz_new  [3] rr  [4] bb
+    const unsigned g = grid_for(n, 256);
+    efem_status st;
+    *iters = 0;
+    *relres = 0.0;
+    if (n == 0) return EFEM_OK;
+    k_diag<<<g, 256, 0, s>>>(A->row_ptr, A->col_idx, A->vals_stiff, A->vals_mass, alpha, beta, n, dinv);
+    EFEM_LAUNCH_CHECK();
+    // r = b - A x ; z = D^-1 r ; p = z ; rz
+    if ((st = launch_spmv(A, alpha, beta, x, q, s)) != EFEM_OK) return st;
+    {
+        double h[2];
+        // r = b - q via k_cg_update with a = 1: x untouched needs p = 0 -> do it directly
+        cudaMemcpyAsync(r, b, n * 8, cudaMemcpyDeviceToDevice, s);
+        k_mul<<<g, 256, 0, s>>>(b, b, n, t2);
+        EFEM_LAUNCH_CHECK();
+        if ((st = reduce_fixed(t2, n, part, sc + 4, s)) != EFEM_OK) return st;
+        // r -= q
+        EFEM_CUDA_TRY(cudaMemsetAsync(p, 0, n * 8, s));
+        const double one_one[2] = {1.0, 1.0};
+        EFEM_CUDA_TRY(cudaMemcpyAsync(sc, one_one, 16, cudaMemcpyHostToDevice, s));
+        k_cg_update<<<g, 256, 0, s>>>(sc, p, q, dinv, n, x, r, z, t1, t2);  // a = 1, p = 0: x unchanged
+        EFEM_LAUNCH_CHECK();
+        if ((st = reduce_fixed(t1, n, part, sc + 0, s)) != EFEM_OK) return st;
+        if ((st = reduce_fixed(t2, n, part, sc + 3, s)) != EFEM_OK) return st;
+        EFEM_CUDA_TRY(cudaMemcpyAsync(p, z, n * 8, cudaMemcpyDeviceToDevice, s));
+        EFEM_CUDA_TRY(cudaMemcpyAsync(h, sc + 3, 16, cudaMemcpyDeviceToHost, s));
+        EFEM_CUDA_TRY(cudaStreamSynchronize(s));
+        const double bn = std::sqrt(h[1]);
+        *relres = bn > 0 ? std::sqrt(h[0]) / bn : 0.0;
+        if (bn == 0.0 || *relres <= rtol) return EFEM_OK;
+    }
+    const int check = 20;
+    for (int it = 1; it <= maxit; ++it) {
+        if ((st = launch_spmv(A, alpha, beta, p, q, s)) != EFEM_OK) return st;
+        k_mul<<<g, 256, 0, s>>>(p, q, n, t1);
+        EFEM_LAUNCH_CHECK();
+        if ((st = reduce_fixed(t1, n, part, sc + 1, s)) != EFEM_OK) return st;
+        k_cg_update<<<g, 256, 0, s>>>(sc, p, q, dinv, n, x, r, z, t1, t2);
+        EFEM_LAUNCH_CHECK();
+        if ((st = reduce_fixed(t1, n, part, sc + 2, s)) != EFEM_OK) return st;
+        if ((st = reduce_fixed(t2, n, part, sc + 3, s)) != EFEM_OK) return st;
+        k_cg_dir<<<g, 256, 0, s>>>(sc, z, n, p);
+        EFEM_LAUNCH_CHECK();
+        k_copy_scalar<<<1, 1, 0, s>>>(sc + 2, sc + 0);
+        EFEM_LAUNCH_CHECK();
+        *iters = it;
+        if (it % check == 0 || it == maxit) {
+            double h[2];
+            EFEM_CUDA_TRY(cudaMemcpyAsync(h, sc + 3, 16, cudaMemcpyDeviceToHost, s));
+            EFEM_CUDA_TRY(cudaStreamSynchronize(s));
+            *relres = std::sqrt(h[0] / h[1]);
+            if (*relres <= rtol) break;
+        }
+    }
+    return EFEM_OK;
+}
+
+}  // namespace efem
