@@ -817,4 +817,117 @@ int ora_field_error(int dim, int element, int64_t n_elems, const double* coords,
     return ORA_OK;
 }
 
+/* ===========================================================================
+ * SURVEY.md §8(f) row f3 support: linear nodal (P1) elements, used by the
+ * majorant example for the approximation v ("The approximation
+ * v was calculated with linear nodal finite elements"; the P1 code is the
+ * authors' earlier paper [RaVa]).  Textbook closed forms:
+ *   K^K_ab = |K| grad l_a . grad l_b,   M^K_ab = |K| (1 + d_ab) / ((d+1)(d+2)),
+ * grad l_i (i >= 1) = row i-1 of B_K^{-1}, grad l_0 = -sum of the others.
+ * ======================================================================== */
+static void p1_grads(int dim, const double* verts, double gl[4][3], double* vol) {
+    double B[3][3];
+    const double det = affine(dim, verts, B);
+    double BiT[3][3];
+    inverse_transpose(dim, B, det, BiT);
+    /* B^{-1} row i = column i of B^{-T} */
+    for (int i = 0; i < dim; ++i)
+        for (int r = 0; r < dim; ++r) gl[i + 1][r] = BiT[r][i];
+    for (int r = 0; r < dim; ++r) {
+        double s = 0.0;
+        for (int i = 1; i <= dim; ++i) s += gl[i][r];
+        gl[0][r] = -s;
+    }
+    *vol = std::fabs(det) / (dim == 2 ? 2.0 : 6.0);
+}
+
+void* ora_p1_assemble(int dim, int64_t n_nodes, int64_t n_elems, const double* coords, const int32_t* elems,
+                      int* status) {
+    *status = validate(dim, ORA_RT0, n_nodes, n_elems, elems);
+    if (*status != ORA_OK) return nullptr;
+    Result* R = new Result;
+    R->dim = dim;
+    const int nv = dim + 1;
+    std::map<std::pair<int32_t, int32_t>, std::pair<double, double>> acc;
+    std::vector<double> verts(nv * dim);
+    for (int64_t e = 0; e < n_elems; ++e) {
+        const int32_t* g = elems + e * nv;
+        for (int v = 0; v < nv; ++v)
+            for (int c = 0; c < dim; ++c) verts[v * dim + c] = coords[(int64_t)g[v] * dim + c];
+        double gl[4][3], vol;
+        p1_grads(dim, verts.data(), gl, &vol);
+        if (!(vol > 0.0)) {
+            *status = ORA_EDEGENERATE;
+            delete R;
+            return nullptr;
+        }
+        for (int a = 0; a < nv; ++a)
+            for (int b = 0; b < nv; ++b) {
+                double dot = 0.0;
+                for (int r = 0; r < dim; ++r) dot += gl[a][r] * gl[b][r];
+                auto& x = acc[{g[a], g[b]}];
+                x.first += vol * (a == b ? 2.0 : 1.0) / ((dim + 1) * (dim + 2));
+                x.second += vol * dot;
+            }
+    }
+    R->row_ptr.assign((size_t)n_nodes + 1, 0);
+    for (const auto& kv : acc) {
+        R->row_ptr[kv.first.first + 1] += 1;
+        R->col_idx.push_back(kv.first.second);
+        R->vals_M.push_back(kv.second.first);
+        R->vals_K.push_back(kv.second.second);
+    }
+    for (int64_t r = 0; r < n_nodes; ++r) R->row_ptr[r + 1] += R->row_ptr[r];
+    return R;
+}
+
+/* b_a = sum_K sum_q w_q |det B_K| f(x_q) l_a(xh_q), degree-6 points. */
+int ora_p1_load(int dim, int64_t n_elems, const double* coords, const int32_t* elems, int64_t n_nodes,
+                const double* fq, double* b) {
+    if (dim != 2 && dim != 3) return ORA_EINVAL;
+    double xh[72], w[24];
+    const int nq = quad6(dim, xh, w), nv = dim + 1;
+    for (int64_t i = 0; i < n_nodes; ++i) b[i] = 0.0;
+    std::vector<double> verts(nv * dim);
+    for (int64_t e = 0; e < n_elems; ++e) {
+        const int32_t* g = elems + e * nv;
+        for (int v = 0; v < nv; ++v)
+            for (int c = 0; c < dim; ++c) verts[v * dim + c] = coords[(int64_t)g[v] * dim + c];
+        double B[3][3];
+        const double adet = std::fabs(affine(dim, verts.data(), B));
+        for (int q = 0; q < nq; ++q) {
+            double lam[4];
+            lam[0] = 1.0;
+            for (int i = 0; i < dim; ++i) {
+                lam[i + 1] = xh[dim * q + i];
+                lam[0] -= lam[i + 1];
+            }
+            const double f = fq[e * nq + q];
+            for (int a = 0; a < nv; ++a) b[g[a]] += w[q] * adet * f * lam[a];
+        }
+    }
+    return ORA_OK;
+}
+
+/* grad v on every element (piecewise constant): grad[e*dim + r]. */
+int ora_p1_grad(int dim, int64_t n_elems, const double* coords, const int32_t* elems, const double* v,
+                double* grad) {
+    if (dim != 2 && dim != 3) return ORA_EINVAL;
+    const int nv = dim + 1;
+    std::vector<double> verts(nv * dim);
+    for (int64_t e = 0; e < n_elems; ++e) {
+        const int32_t* g = elems + e * nv;
+        for (int k = 0; k < nv; ++k)
+            for (int c = 0; c < dim; ++c) verts[k * dim + c] = coords[(int64_t)g[k] * dim + c];
+        double gl[4][3], vol;
+        p1_grads(dim, verts.data(), gl, &vol);
+        for (int r = 0; r < dim; ++r) {
+            double s = 0.0;
+            for (int a = 0; a < nv; ++a) s += v[g[a]] * gl[a][r];
+            grad[e * dim + r] = s;
+        }
+    }
+    return ORA_OK;
+}
+
 }  // extern "C"

@@ -60,6 +60,10 @@ def lib():
                                ctypes.c_int64, vp, vp]
         L.ora_norm_l2.argtypes = [ctypes.c_int, ctypes.c_int64, vp, vp, vp, ctypes.c_int, vp, vp]
         L.ora_field_error.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.ora_p1_assemble.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, vp, vp, ctypes.POINTER(ctypes.c_int)]
+        L.ora_p1_assemble.restype = ctypes.c_void_p
+        L.ora_p1_load.argtypes = [ctypes.c_int, ctypes.c_int64, vp, vp, ctypes.c_int64, vp, vp]
+        L.ora_p1_grad.argtypes = [ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp]
         L.ora_rows_by_entity.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, vp, vp,
                                          ctypes.c_int64, vp, ctypes.c_int, vp, vp, vp, vp]
         _lib = L
@@ -259,3 +263,43 @@ def field_error(dim: int, element: int, coords, elems, asm: Assembly, coeffs, Eq
     if st != 0:
         raise ValueError(f"ora_field_error failed ({st})")
     return err[0], err[1]
+
+
+# --------------------------------------------------------------------------- f3: P1 (for the majorant example)
+def p1_assemble(dim: int, coords, elems):
+    """P1 (nodal) CSR over the nodes: (row_ptr, col_idx, vals_M, vals_K)."""
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    elems = np.ascontiguousarray(elems, dtype=np.int32)
+    st = ctypes.c_int()
+    h = lib().ora_p1_assemble(dim, coords.shape[0], elems.shape[0], _p(coords), _p(elems), ctypes.byref(st))
+    if not h:
+        raise ValueError(f"ora_p1_assemble failed ({st.value})")
+    try:
+        R, nnz = ctypes.c_int64(), ctypes.c_int64()
+        lib().ora_result_sizes(h, ctypes.byref(R), ctypes.byref(nnz))
+        rp = np.zeros(R.value + 1, np.int32)
+        ci = np.zeros(nnz.value, np.int32)
+        vm = np.zeros(nnz.value)
+        vk = np.zeros(nnz.value)
+        lib().ora_result_copy(h, None, None, None, _p(rp), _p(ci), _p(vm), _p(vk))
+        return rp, ci, vm, vk
+    finally:
+        lib().ora_free(h)
+
+
+def p1_load(dim: int, coords, elems, fq):
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    elems = np.ascontiguousarray(elems, dtype=np.int32)
+    b = np.zeros(coords.shape[0])
+    lib().ora_p1_load(dim, elems.shape[0], _p(coords), _p(elems), coords.shape[0],
+                      _p(np.ascontiguousarray(fq, dtype=np.float64)), _p(b))
+    return b
+
+
+def p1_grad(dim: int, coords, elems, v):
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    elems = np.ascontiguousarray(elems, dtype=np.int32)
+    g = np.zeros((elems.shape[0], dim))
+    lib().ora_p1_grad(dim, elems.shape[0], _p(coords), _p(elems), _p(np.ascontiguousarray(v, dtype=np.float64)),
+                      _p(g))
+    return g

@@ -73,3 +73,43 @@ def eddy_F(x1, x2, xp=np):
     in1 = x1 > x2
     z = xp.zeros_like(x1)
     return xp.where(in1, c2 + e1, z), xp.where(in1, -c1 + e2, z)
+
+
+# --------------------------------------------------------------------------- majorant example
+# Poisson -lap u = f, u = 0 on the boundary of (0,1)^d, exact solution the
+# bubble u(x) = prod_i x_i (x_i - 1); the Friedrichs constant of the unit
+# square / cube (reading F1 in DESIGN.md): C_F = 1 / (pi sqrt(d)).
+
+def bubble_u(x, xp=np):
+    """x: (..., d)."""
+    return xp.prod(x * (x - 1.0), -1) if xp is np else (x * (x - 1.0)).prod(-1)
+
+
+def _others(x, i):
+    d = x.shape[-1]
+    out = None
+    for j in range(d):
+        if j != i:
+            t = x[..., j] * (x[..., j] - 1.0)
+            out = t if out is None else out * t
+    return out
+
+
+def bubble_grad(x, xp=np):
+    d = x.shape[-1]
+    comps = [_others(x, i) * (2.0 * x[..., i] - 1.0) for i in range(d)]
+    return xp.stack(comps, -1) if xp is np else xp.stack(comps, dim=-1)
+
+
+def bubble_f(x, xp=np):
+    """f = -lap u = -sum_i 2 prod_{j != i} x_j (x_j - 1)."""
+    d = x.shape[-1]
+    out = None
+    for i in range(d):
+        t = -2.0 * _others(x, i)
+        out = t if out is None else out + t
+    return out
+
+
+def friedrichs_unit(dim):
+    return 1.0 / (math.pi * math.sqrt(dim))

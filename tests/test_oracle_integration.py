@@ -161,3 +161,103 @@ def test_eddy_current_table5(row):
     r = table5()[row]
     err = eddy_error_oracle(r["n"])
     assert abs(err - r["error"]) <= 0.6e-6 * r["error"], (err, r["error"])
+
+
+# --------------------------------------------------------------------------- f3: majorant
+def _trunc(x, digits):
+    f = 10.0 ** digits
+    return math.floor(x * f + 1e-9) / f
+
+
+def majorant_oracle(dim, n, max_iter=6, stop=1e-4):
+    """Algorithm 1 on the oracle, step by step:
+    v = P1 solution of -lap u = f, u = 0 on the boundary; then alternately
+    (a) solve Eq. (majorantproblem) for y in RT0 with beta fixed,
+    (b) beta = ||grad v - y|| / (C_F ||div y + f||)   (Eq. betaoptimal),
+    stopping when the relative change of the majorant is below 1e-4.
+    Returns [(beta, sqrt(Mcal), I_eff)] per iteration and ||grad(u - v)||^2."""
+    c, e = ora.build_mesh(dim, n, 0.0, 0)
+    N = c.shape[0]
+    X = ora.quad_points(dim, c, e)
+    F = P.bubble_f(X)
+    rp, ci, _, vk = ora.p1_assemble(dim, c, e)
+    K1 = sp.csr_matrix((vk, ci, rp), shape=(N, N))
+    b1 = ora.p1_load(dim, c, e, F)
+    inner = ~np.any((np.abs(c) < 1e-14) | (np.abs(c - 1.0) < 1e-14), axis=1)
+    v = np.zeros(N)
+    v[inner] = spl.spsolve(K1[inner][:, inner].tocsc(), b1[inner])
+    gv = ora.p1_grad(dim, c, e, v)
+    GV = np.repeat(gv[:, None, :], X.shape[1], axis=1)
+    err2, _ = ora.norm_l2(dim, c, e, P.bubble_grad(X) - GV)
+    A = ora.assemble(dim, RT0, c, e)
+    R = A.n_dofs
+    K = sp.csr_matrix((A.vals_K, A.col_idx, A.row_ptr), shape=(R, R))
+    M = sp.csr_matrix((A.vals_M, A.col_idx, A.row_ptr), shape=(R, R))
+    b_div = ora.load(dim, RT0, ora.DERIVATIVE, c, e, A, F[..., None])   # int f div phi
+    b_val = ora.load(dim, RT0, ora.VALUE, c, e, A, GV)                  # int grad v . phi
+    CF = P.friedrichs_unit(dim)
+    beta, prev, hist = 1.0, None, []
+    for _ in range(max_iter):
+        a1, a2 = (1.0 + beta) * CF ** 2, 1.0 + 1.0 / beta
+        y = spl.spsolve((a1 * K + a2 * M).tocsc(), -a1 * b_div + a2 * b_val)
+        d1, d2 = ora.field_error(dim, RT0, c, e, A, y, GV, -F[..., None])  # ||grad v - y||^2, ||div y + f||^2
+        Mcal = a2 * d1 + a1 * d2
+        hist.append((beta, math.sqrt(Mcal), math.sqrt(Mcal / err2)))
+        if prev is not None and abs(prev - Mcal) / prev < stop:
+            break
+        prev = Mcal
+        beta = math.sqrt(d1) / (CF * math.sqrt(d2))
+    return hist, err2
+
+
+def table34():
+    return json.load(open(os.path.join(GOLDEN, "paper_table3_4_majorant.json")))
+
+
+@pytest.mark.parametrize("col", [0, 1], ids=["T512", "T131072"])
+def test_majorant_table3_2d(col):
+    """Table 3: beta and I_eff as printed (truncated),
+    sqrt of the majorant to the printed 6 decimals, same iteration count."""
+    t = table34()["table3_2d"]
+    hist, _ = majorant_oracle(2, t["n"][col])
+    rows = t["rows"][col]
+    assert len(hist) == len(rows)
+    for (beta, sm, ieff), (_, pb, pm, pi) in zip(hist, rows):
+        assert _trunc(beta, 3) == pytest.approx(pb, abs=1e-9)
+        assert abs(sm - pm) <= 0.51e-6
+        assert _trunc(ieff, 2) == pytest.approx(pi, abs=1e-9)
+
+
+def test_majorant_3d_guaranteed_and_monotone():
+    """3D (Table 4's #T = 10 368 mesh size; the paper's tetrahedral mesh
+    structure is not stated, so its numbers are not reproduced -- DESIGN.md
+    F2): the majorant bounds the true error from above at every iterate
+    (Eq. majorantestimate) and never increases."""
+    hist, err2 = majorant_oracle(3, 12)
+    ms = [h[1] ** 2 for h in hist]
+    assert all(m >= err2 for m in ms)
+    assert all(b <= a * (1 + 1e-12) for a, b in zip(ms, ms[1:]))
+    assert all(h[2] >= 1.0 for h in hist)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_p1_closed_forms(dim):
+    """P1 (nodal) oracle: K 1 = 0 (constants in the kernel), sum M = |Omega|,
+    x_r^T K x_r = int |grad x_r|^2 = |Omega|, x_r^T M 1 = int x_r = 1/2,
+    and the load of f = 1 sums to |Omega|; grad of a linear field exact."""
+    c, e = ora.build_mesh(dim, 3, 0.15, 5)
+    rp, ci, vm, vk = ora.p1_assemble(dim, c, e)
+    N = c.shape[0]
+    K = sp.csr_matrix((vk, ci, rp), shape=(N, N))
+    M = sp.csr_matrix((vm, ci, rp), shape=(N, N))
+    one = np.ones(N)
+    assert np.abs(K @ one).max() < 1e-13
+    assert abs(M.sum() - 1.0) < 1e-13
+    for r in range(dim):
+        x = c[:, r]
+        assert abs(x @ (K @ x) - 1.0) < 1e-13
+        assert abs(x @ (M @ one) - 0.5) < 1e-13
+    X = ora.quad_points(dim, c, e)
+    assert abs(ora.p1_load(dim, c, e, np.ones(X.shape[:2])).sum() - 1.0) < 1e-13
+    g = ora.p1_grad(dim, c, e, c @ np.arange(1.0, dim + 1.0))
+    np.testing.assert_allclose(g, np.broadcast_to(np.arange(1.0, dim + 1.0), g.shape), rtol=0, atol=1e-12)
