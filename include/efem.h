@@ -273,6 +273,30 @@ efem_status efem_spmv(const efem_csr* A, double alpha, double beta, const double
 efem_status efem_cg(const efem_csr* A, double alpha, double beta, const double* b, double* x, double rtol, int maxit,
                     int* iters, double* relres, void* ws, size_t* ws_bytes, efem_stream_t stream);
 
+/* ---- SURVEY.md §8(f) f3 support: linear nodal (P1) elements ------------------
+ * The majorant example's approximation v.  Rows = nodes; the
+ * pattern of row a is a and every node sharing an element with it (sorted);
+ * vals_stiff = int grad l_a . grad l_b, vals_mass = int l_a l_b, summed per row
+ * in ascending element order.  Same two-phase protocol as efem_plan. */
+typedef struct efem_p1_plan_s* efem_p1_plan;
+
+efem_status efem_p1_plan_create(efem_p1_plan* plan, const efem_mesh* mesh, size_t* ws_bytes);
+efem_status efem_p1_plan_set_workspace(efem_p1_plan plan, void* ws, size_t ws_bytes);
+efem_status efem_p1_plan_destroy(efem_p1_plan plan);
+/* node -> element incidence, row lengths; synchronising (returns n_rows = n_nodes, nnz);
+ * EFEM_ECAPACITY if a node touches more than 64 elements or 63 neighbours */
+efem_status efem_p1_symbolic(efem_p1_plan plan, int64_t* n_rows, int64_t* nnz, efem_stream_t stream);
+/* row_ptr, col_idx, vals_mass (may be NULL), vals_stiff (may be NULL); synchronising (degenerate check) */
+efem_status efem_p1_numeric(efem_p1_plan plan, efem_csr* out, efem_stream_t stream);
+/* b_a = sum_K sum_q w_q |det B_K| f(x_q) l_a(x_q); fq: T x nq (degree-6 points, efem_quad_points order) */
+efem_status efem_p1_load(efem_p1_plan plan, const double* fq, double* b, efem_stream_t stream);
+/* grad v (piecewise constant) written at every quadrature point: grad_q T x nq x dim */
+efem_status efem_p1_gradient(const efem_mesh* mesh, const double* v, double* grad_q, efem_stream_t stream);
+/* Symmetric Dirichlet elimination on a CSR in place: entries in masked rows or
+ * columns set to 0 (vals_stiff diagonal of masked rows to 1, vals_mass 0);
+ * b[masked] = 0 (b may be NULL).  For homogeneous boundary values. */
+efem_status efem_dirichlet(efem_csr* A, const uint8_t* mask, double* b, efem_stream_t stream);
+
 /* ---- diagnostics ------------------------------------------------------------- */
 const char* efem_status_string(efem_status status);
 const char* efem_last_error(void);

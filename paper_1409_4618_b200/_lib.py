@@ -90,6 +90,14 @@ def load():
         "efem_cg": (st, [ctypes.POINTER(efem_csr), ctypes.c_double, ctypes.c_double, vp, vp, ctypes.c_double,
                          ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), vp,
                          ctypes.POINTER(ctypes.c_size_t), vp]),
+        "efem_p1_plan_create": (st, [ctypes.POINTER(vp), ctypes.POINTER(efem_mesh), ctypes.POINTER(ctypes.c_size_t)]),
+        "efem_p1_plan_set_workspace": (st, [vp, vp, ctypes.c_size_t]),
+        "efem_p1_plan_destroy": (st, [vp]),
+        "efem_p1_symbolic": (st, [vp, i64p, i64p, vp]),
+        "efem_p1_numeric": (st, [vp, ctypes.POINTER(efem_csr), vp]),
+        "efem_p1_load": (st, [vp, vp, vp, vp]),
+        "efem_p1_gradient": (st, [ctypes.POINTER(efem_mesh), vp, vp, vp]),
+        "efem_dirichlet": (st, [ctypes.POINTER(efem_csr), vp, vp, vp]),
         "efem_status_string": (ctypes.c_char_p, [st]),
         "efem_last_error": (ctypes.c_char_p, []),
         "efem_last_bad_element": (i64, []),

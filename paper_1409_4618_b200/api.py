@@ -294,3 +294,76 @@ def cg(A: CSR, b: torch.Tensor, alpha: float = 1.0, beta: float = 1.0, x0: torch
                                         ctypes.byref(it), ctypes.byref(rr), _ptr(ws), ctypes.byref(ws_bytes),
                                         _stream(stream)))
     return x, it.value, rr.value
+
+
+# --------------------------------------------------------------------------- f3: P1 nodal elements
+class P1Assembler:
+    """P1 (nodal) Laplacian stiffness / mass / load on a device mesh (efem_p1_plan)."""
+
+    def __init__(self, coords: torch.Tensor, elems: torch.Tensor):
+        self.coords, self.elems = coords.contiguous(), elems.contiguous()
+        self.device = coords.device
+        L = _lib.load()
+        self._mesh = _mesh_struct(self.coords, self.elems)
+        plan = ctypes.c_void_p()
+        ws = ctypes.c_size_t()
+        _lib.check("efem_p1_plan_create", L.efem_p1_plan_create(ctypes.byref(plan), ctypes.byref(self._mesh),
+                                                                ctypes.byref(ws)))
+        self._plan = plan
+        self.ws = torch.empty(max(int(ws.value), 256), dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check("efem_p1_plan_set_workspace", L.efem_p1_plan_set_workspace(plan, _ptr(self.ws),
+                                                                                  self.ws.numel()))
+        self.n_rows = self.nnz = None
+
+    def __del__(self):
+        try:
+            if self._plan:
+                _lib.load().efem_p1_plan_destroy(self._plan)
+                self._plan = None
+        except Exception:
+            pass
+
+    def assemble(self, stream=None) -> CSR:
+        L = _lib.load()
+        R, nnz = ctypes.c_int64(), ctypes.c_int64()
+        with torch.cuda.device(self.device):
+            _lib.check("efem_p1_symbolic", L.efem_p1_symbolic(self._plan, ctypes.byref(R), ctypes.byref(nnz),
+                                                              _stream(stream)))
+            self.n_rows, self.nnz = R.value, nnz.value
+            dev = self.device
+            out = CSR(torch.empty(self.n_rows + 1, dtype=torch.int32, device=dev),
+                      torch.empty(self.nnz, dtype=torch.int32, device=dev),
+                      torch.empty(self.nnz, dtype=torch.float64, device=dev),
+                      torch.empty(self.nnz, dtype=torch.float64, device=dev))
+            c = _csr_ptrs(out)
+            _lib.check("efem_p1_numeric", L.efem_p1_numeric(self._plan, ctypes.byref(c), _stream(stream)))
+        return out
+
+    def load(self, fq: torch.Tensor, stream=None) -> torch.Tensor:
+        b = torch.empty(self.coords.shape[0], dtype=torch.float64, device=self.device)
+        fq = fq.contiguous()
+        with torch.cuda.device(self.device):
+            _lib.check("efem_p1_load", _lib.load().efem_p1_load(self._plan, _ptr(fq), _ptr(b), _stream(stream)))
+        return b
+
+
+def p1_gradient(coords: torch.Tensor, elems: torch.Tensor, v: torch.Tensor, stream=None) -> torch.Tensor:
+    """grad v of a P1 field at every quadrature point: (T, nq, dim)."""
+    dim = int(coords.shape[1])
+    out = torch.empty((elems.shape[0], quad_size(dim), dim), dtype=torch.float64, device=coords.device)
+    m = _mesh_struct(coords, elems)
+    with torch.cuda.device(coords.device):
+        _lib.check("efem_p1_gradient", _lib.load().efem_p1_gradient(ctypes.byref(m), _ptr(v.contiguous()),
+                                                                    _ptr(out), _stream(stream)))
+    return out
+
+
+def dirichlet(A: CSR, mask: torch.Tensor, b: torch.Tensor | None = None, stream=None):
+    """Symmetric elimination of the masked DOFs (homogeneous values), in place."""
+    c = _csr_ptrs(A)
+    m = mask.to(torch.uint8).contiguous()
+    with torch.cuda.device(A.row_ptr.device):
+        _lib.check("efem_dirichlet", _lib.load().efem_dirichlet(ctypes.byref(c), _ptr(m), _ptr(b),
+                                                                _stream(stream)))
+    return A

@@ -26,7 +26,6 @@ constexpr int NUM_TPB = 128;
 // stages its 32 rows' CSR segment in shared memory (no block barrier) and
 // flushes it with coalesced stores, so every CSR byte is written once.
 // ---------------------------------------------------------------------------------
-constexpr int PAIR_TPB = 256;
 
 // 2D: local row k of one triangle in the frame rotated so that vertex k (the
 // vertex opposite edge k) comes first.  Edge l runs from vertex l+1 to l+2

@@ -499,6 +499,15 @@ __global__ void k_copy_scalar(const double* __restrict__ src, double* __restrict
 // ---- launchers ------------------------------------------------------------------------
 int quad6_size(int dim) { return dim == 2 ? 12 : 24; }
 
+efem_status quad6_host(int dim, double* l, double* w) {
+    const Quad6 q = make_quad6(dim);
+    for (int i = 0; i < 24; ++i) {
+        for (int c = 0; c < 3; ++c) l[3 * i + c] = q.l[i][c];
+        w[i] = q.w[i];
+    }
+    return EFEM_OK;
+}
+
 efem_status launch_quad_points(int dim, const double* coords, const int32_t* elems, int64_t n_elems, double* pts,
                                cudaStream_t s) {
     efem_status st;
