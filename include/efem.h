@@ -128,6 +128,16 @@ efem_status efem_build_mesh(int dim, int n, double jitter_frac, uint64_t seed, d
  * *ws_bytes the device workspace the plan needs (an upper bound derived from
  * n_nodes, n_elems).  No device work.  Errors: EFEM_EINVAL, EFEM_EOVERFLOW,
  * EFEM_ENOMEM. */
+/* the paper's 2D timing domain, the L-shape
+ * (0,1)^2 \ (1/2,1)^2 (Table 1), as the m x m unit-square grid
+ * (m even) with the cells of the removed quadrant dropped; level L of
+ * Table 1 is m = 2^(L+1) (#E = 9/4 m^2 + 2 m).  Nodes / cells row-major over
+ * what remains, 2 triangles per cell as efem_build_mesh; jitter on interior
+ * nodes only (the re-entrant edges are boundary).  Untimed input generator. */
+efem_status efem_lshape_sizes(int m, int64_t* n_nodes, int64_t* n_elems);
+efem_status efem_build_mesh_lshape(int m, double jitter_frac, uint64_t seed, double* coords, int32_t* elems,
+                                   efem_stream_t stream);
+
 efem_status efem_plan_create(efem_plan* plan, const efem_mesh* mesh, efem_element element, size_t* ws_bytes);
 
 /* Attach the caller-allocated device workspace (>= *ws_bytes, 256-byte

@@ -367,6 +367,53 @@ int ora_build_mesh(int dim, int n, double alpha, uint64_t seed, double* coords, 
     return ORA_OK;
 }
 
+/* L-shape (0,1)^2 \ (1/2,1)^2 (Table 1 domain) on the m x m
+ * grid, m even, h = m/2 (reading L1): cells (i, j) with i >= h and j >= h are
+ * dropped, nodes (i, j) with i > h and j > h too; both numbered row-major over
+ * what remains; 2 counter-clockwise triangles per cell as ora_build_mesh;
+ * jitter on nodes off the L's boundary (including the re-entrant edges). */
+int ora_lshape_sizes(int m, int64_t* n_nodes, int64_t* n_elems) {
+    if (m < 2 || (m & 1)) return ORA_EINVAL;
+    int64_t nn = 0, ne = 0;
+    for (int j = 0; j <= m; ++j)
+        for (int i = 0; i <= m; ++i)
+            if (!(i > m / 2 && j > m / 2)) ++nn;
+    for (int j = 0; j < m; ++j)
+        for (int i = 0; i < m; ++i)
+            if (!(i >= m / 2 && j >= m / 2)) ne += 2;
+    *n_nodes = nn;
+    *n_elems = ne;
+    return ORA_OK;
+}
+
+int ora_build_lshape(int m, double alpha, uint64_t seed, double* coords, int32_t* elems) {
+    if (m < 2 || (m & 1)) return ORA_EINVAL;
+    const int h = m / 2;
+    std::vector<int32_t> id((size_t)(m + 1) * (m + 1), -1);
+    int32_t next = 0;
+    for (int j = 0; j <= m; ++j)
+        for (int i = 0; i <= m; ++i) {
+            if (i > h && j > h) continue;
+            const int32_t node = next++;
+            id[(size_t)j * (m + 1) + i] = node;
+            const bool in = i > 0 && i < m && j > 0 && j < m && !(i >= h && j >= h);
+            coords[2 * node + 0] = grid_coord(i, m, in, alpha, seed, (uint64_t)node * 2 + 0);
+            coords[2 * node + 1] = grid_coord(j, m, in, alpha, seed, (uint64_t)node * 2 + 1);
+        }
+    int64_t c = 0;
+    for (int j = 0; j < m; ++j)
+        for (int i = 0; i < m; ++i) {
+            if (i >= h && j >= h) continue;
+            const int32_t v00 = id[(size_t)j * (m + 1) + i], v10 = id[(size_t)j * (m + 1) + i + 1];
+            const int32_t v01 = id[(size_t)(j + 1) * (m + 1) + i], v11 = id[(size_t)(j + 1) * (m + 1) + i + 1];
+            int32_t* e = elems + 6 * c;
+            e[0] = v00; e[1] = v10; e[2] = v11;
+            e[3] = v00; e[4] = v11; e[5] = v01;
+            ++c;
+        }
+    return ORA_OK;
+}
+
 int ora_n_local_dofs(int dim, int element) { return n_local_dofs(dim, element); }
 
 int ora_ref_basis(int dim, int element, const double* xh, double* val, double* dc) {

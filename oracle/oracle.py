@@ -54,6 +54,8 @@ def lib():
         L.ora_result_copy.argtypes = [vp] + [vp] * 7
         L.ora_free.argtypes = [vp]
         L.ora_free.restype = None
+        L.ora_lshape_sizes.argtypes = [ctypes.c_int, i64p, i64p]
+        L.ora_build_lshape.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_uint64, vp, vp]
         L.ora_quad6.argtypes = [ctypes.c_int, vp, vp]
         L.ora_quad_points.argtypes = [ctypes.c_int, ctypes.c_int64, vp, vp, vp]
         L.ora_load.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp,
@@ -91,6 +93,16 @@ def build_mesh(dim: int, n: int, alpha: float, seed: int):
     elems = np.zeros((T, dim + 1), dtype=np.int32)
     if lib().ora_build_mesh(dim, n, alpha, seed, _p(coords), _p(elems)) != 0:
         raise ValueError("ora_build_mesh failed")
+    return coords, elems
+
+
+def build_lshape(m: int, alpha: float = 0.0, seed: int = 0):
+    N, T = ctypes.c_int64(), ctypes.c_int64()
+    if lib().ora_lshape_sizes(m, ctypes.byref(N), ctypes.byref(T)) != 0:
+        raise ValueError("bad L-shape size")
+    coords = np.zeros((N.value, 2))
+    elems = np.zeros((T.value, 3), dtype=np.int32)
+    lib().ora_build_lshape(m, alpha, seed, _p(coords), _p(elems))
     return coords, elems
 
 

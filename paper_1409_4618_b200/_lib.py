@@ -80,6 +80,8 @@ def load():
         "efem_part_scan": (st, [vp, i64, vp, vp, ctypes.POINTER(ctypes.c_size_t), vp]),
         "efem_part_globalize": (st, [vp, vp, vp, vp, vp]),
         "efem_part_numeric": (st, [vp, ctypes.c_uint, i64p, i64, vp, ctypes.POINTER(efem_csr), vp]),
+        "efem_lshape_sizes": (st, [ctypes.c_int, i64p, i64p]),
+        "efem_build_mesh_lshape": (st, [ctypes.c_int, ctypes.c_double, ctypes.c_uint64, vp, vp, vp]),
         "efem_quad_size": (ctypes.c_int, [ctypes.c_int]),
         "efem_quad_points": (st, [ctypes.POINTER(efem_mesh), vp, vp]),
         "efem_assemble_load": (st, [vp, ctypes.c_int, vp, vp, vp]),

@@ -40,6 +40,19 @@ def mesh_sizes(dim: int, n: int):
     return N.value, T.value
 
 
+def build_lshape(m: int, jitter: float = 0.0, seed: int = 0, device="cuda", stream=None):
+    """The paper's 2D timing domain (0,1)^2 minus (1/2,1)^2 on the m x m grid (m even)."""
+    L = _lib.load()
+    N, T = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check("efem_lshape_sizes", L.efem_lshape_sizes(m, ctypes.byref(N), ctypes.byref(T)))
+    coords = torch.empty((N.value, 2), dtype=torch.float64, device=device)
+    elems = torch.empty((T.value, 3), dtype=torch.int32, device=device)
+    with torch.cuda.device(coords.device):
+        _lib.check("efem_build_mesh_lshape", L.efem_build_mesh_lshape(m, jitter, seed, _ptr(coords), _ptr(elems),
+                                                                      _stream(stream)))
+    return coords, elems
+
+
 def build_mesh(dim: int, n: int, jitter: float, seed: int, device="cuda", stream=None):
     """Seeded structured mesh generated on the device (efem_build_mesh)."""
     N, T = mesh_sizes(dim, n)

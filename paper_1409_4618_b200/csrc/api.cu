@@ -16,6 +16,7 @@ namespace efem {
 efem_status launch_enumerate(Plan& p, cudaStream_t s);
 efem_status launch_signs(Plan& p, int8_t* out, cudaStream_t s);
 efem_status launch_rows_any(Plan& p, unsigned forms, efem_csr* out, const RowWindow& w, cudaStream_t s);
+efem_status launch_build_lshape(int m, double alpha, uint64_t seed, double* coords, int32_t* elems, cudaStream_t s);
 // integrate.cu (f1 / f2)
 int quad6_size(int dim);
 efem_status launch_quad_points(int dim, const double* coords, const int32_t* elems, int64_t n_elems, double* pts,
@@ -297,6 +298,34 @@ efem_status efem_build_mesh(int dim, int n, double jitter_frac, uint64_t seed, d
         return EFEM_EINVAL;
     }
     return launch_build_mesh(dim, n, jitter_frac, seed, coords, elems, (cudaStream_t)stream);
+}
+
+efem_status efem_lshape_sizes(int m, int64_t* n_nodes, int64_t* n_elems) {
+    if (m < 2 || (m & 1) || !n_nodes || !n_elems) {
+        set_error("efem_lshape_sizes: m must be even and >= 2, outputs non-NULL");
+        return EFEM_EINVAL;
+    }
+    const int64_t h = m / 2;
+    *n_nodes = (h + 1) * (m + 1) + (m - h) * (h + 1);
+    *n_elems = 2 * (h * m + (m - h) * h);
+    if (*n_elems * 3 >= (1ll << 31)) {
+        set_error("efem_lshape_sizes: mesh does not fit int32 indices");
+        return EFEM_EOVERFLOW;
+    }
+    return EFEM_OK;
+}
+
+efem_status efem_build_mesh_lshape(int m, double jitter_frac, uint64_t seed, double* coords, int32_t* elems,
+                                   efem_stream_t stream) {
+    int64_t N, T;
+    efem_status st = efem_lshape_sizes(m, &N, &T);
+    if (st != EFEM_OK) return st;
+    const double lim = 1.0 / (2.0 * std::sqrt(2.0 * 2));
+    if (!coords || !elems || !(jitter_frac >= 0.0) || !(jitter_frac < lim)) {
+        set_error("efem_build_mesh_lshape: NULL array or jitter_frac outside [0, 1/(4 sqrt(2)))");
+        return EFEM_EINVAL;
+    }
+    return launch_build_lshape(m, jitter_frac, seed, coords, elems, (cudaStream_t)stream);
 }
 
 efem_status efem_plan_create(efem_plan* plan, const efem_mesh* mesh, efem_element element, size_t* ws_bytes) {

@@ -73,7 +73,64 @@ __global__ void k_elems3d(int n, int32_t* __restrict__ elems) {
     }
 }
 
+// L-shape (0,1)^2 minus (1/2,1)^2 on the m x m grid (m even, h = m/2): cells
+// (i, j) with i >= h and j >= h removed, nodes (i, j) with i > h and j > h
+// removed, both numbered row-major over what remains (reading L1).
+__device__ __forceinline__ int64_t lnode(int i, int j, int m) {
+    const int h = m / 2;
+    return j <= h ? (int64_t)j * (m + 1) + i : (int64_t)(h + 1) * (m + 1) + (int64_t)(j - h - 1) * (h + 1) + i;
+}
+
+__global__ void k_lshape_coords(int m, double alpha, uint64_t seed, int64_t n_nodes, double* __restrict__ coords) {
+    const int64_t node = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (node >= n_nodes) return;
+    const int h = m / 2;
+    const int64_t lower = (int64_t)(h + 1) * (m + 1);
+    int i, j;
+    if (node < lower) {
+        j = (int)(node / (m + 1));
+        i = (int)(node % (m + 1));
+    } else {
+        j = h + 1 + (int)((node - lower) / (h + 1));
+        i = (int)((node - lower) % (h + 1));
+    }
+    const bool in = i > 0 && i < m && j > 0 && j < m && !(i >= h && j >= h);
+    coords[2 * node + 0] = grid_coord(i, m, in, alpha, seed, (uint64_t)node * 2 + 0);
+    coords[2 * node + 1] = grid_coord(j, m, in, alpha, seed, (uint64_t)node * 2 + 1);
+}
+
+__global__ void k_lshape_elems(int m, int64_t n_cells, int32_t* __restrict__ elems) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n_cells) return;
+    const int h = m / 2;
+    const int64_t lower = (int64_t)h * m;
+    int i, j;
+    if (c < lower) {
+        j = (int)(c / m);
+        i = (int)(c % m);
+    } else {
+        j = h + (int)((c - lower) / h);
+        i = (int)((c - lower) % h);
+    }
+    const int32_t v00 = (int32_t)lnode(i, j, m), v10 = (int32_t)lnode(i + 1, j, m);
+    const int32_t v01 = (int32_t)lnode(i, j + 1, m), v11 = (int32_t)lnode(i + 1, j + 1, m);
+    int32_t* e = elems + 6 * c;
+    e[0] = v00; e[1] = v10; e[2] = v11;
+    e[3] = v00; e[4] = v11; e[5] = v01;
+}
+
 }  // namespace
+
+efem_status launch_build_lshape(int m, double alpha, uint64_t seed, double* coords, int32_t* elems, cudaStream_t s) {
+    const int h = m / 2;
+    const int64_t N = (int64_t)(h + 1) * (m + 1) + (int64_t)(m - h) * (h + 1);
+    const int64_t C = (int64_t)h * m + (int64_t)(m - h) * h;
+    k_lshape_coords<<<grid_for(N, 256), 256, 0, s>>>(m, alpha, seed, N, coords);
+    EFEM_LAUNCH_CHECK();
+    k_lshape_elems<<<grid_for(C, 256), 256, 0, s>>>(m, C, elems);
+    EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
 
 efem_status launch_build_mesh(int dim, int n, double alpha, uint64_t seed, double* coords, int32_t* elems,
                               cudaStream_t s) {

@@ -261,3 +261,39 @@ def test_p1_closed_forms(dim):
     assert abs(ora.p1_load(dim, c, e, np.ones(X.shape[:2])).sum() - 1.0) < 1e-13
     g = ora.p1_grad(dim, c, e, c @ np.arange(1.0, dim + 1.0))
     np.testing.assert_allclose(g, np.broadcast_to(np.arange(1.0, dim + 1.0), g.shape), rtol=0, atol=1e-12)
+
+
+# --------------------------------------------------------------------------- f4: paper-shape meshes
+def _counts():
+    return json.load(open(os.path.join(GOLDEN, "paper_counts.json")))
+
+
+def test_lshape_sizes_match_table1():
+    """Level L of Table 1 is the m = 2^(L+1) grid (reading L1): the oracle's
+    enumeration at levels 5-6 and the closed form #E = 9/4 m^2 + 2 m at all
+    ten levels give the printed sizes."""
+    rows = dict(_counts()["table1_lshape_size"]["rows"])
+    for L, size in rows.items():
+        m = 2 ** (L + 1)
+        assert 9 * m * m // 4 + 2 * m == size
+    for L in (5, 6):
+        c, e = ora.build_lshape(2 ** (L + 1))
+        assert ora.assemble(2, NED0, c, e).n_dofs == rows[L]
+        assert ora.assemble(2, RT0, c, e).n_dofs == rows[L]
+
+
+def test_lshape_geometry():
+    c, e = ora.build_lshape(8, 0.2, 3)
+    v = c[e]
+    area = 0.5 * ((v[:, 1, 0] - v[:, 0, 0]) * (v[:, 2, 1] - v[:, 0, 1]) - (v[:, 2, 0] - v[:, 0, 0]) * (v[:, 1, 1] - v[:, 0, 1]))
+    assert np.all(area > 0) and abs(area.sum() - 0.75) < 1e-14
+    assert not np.any((c[:, 0] > 0.5 + 1e-12) & (c[:, 1] > 0.5 + 1e-12))
+    X = ora.quad_points(2, c, e)
+    assert abs(ora.norm_l2(2, c, e, np.ones(X.shape[:2]))[0] - 0.75) < 1e-14   # SPEC.md:285: |L| = 3/4
+
+
+def test_cube_levels_match_table2():
+    """Table 2: level L = the n = 6 2^(L-1) Kuhn grid."""
+    for L, F, E in _counts()["table2_unit_cube_F_E"]["rows"]:
+        n = 6 * 2 ** (L - 1)
+        assert 12 * n ** 3 + 6 * n ** 2 == F and 7 * n ** 3 + 9 * n ** 2 + 3 * n == E

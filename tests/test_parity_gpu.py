@@ -325,3 +325,19 @@ def test_full_config(api, cfg):
             assert torch.equal(A.indices(), At.indices())
             diff = (A.values() - At.values()).abs().max()
             assert float(diff) <= REL_TOL * float(vals.abs().max())
+
+
+# ---------------------------------------------------------------------------- f4: the paper's L-shape domain
+@pytest.mark.parametrize("m,alpha", [(2, 0.0), (8, 0.2), (34, 0.1)])
+def test_lshape_bit_exact(api, m, alpha):
+    c, e = api.build_lshape(m, alpha, 5, device="cuda:0")
+    rc, re = ora.build_lshape(m, alpha, 5)
+    assert np.array_equal(e.cpu().numpy(), re)
+    assert c.cpu().numpy().tobytes() == rc.tobytes()
+
+
+@pytest.mark.parametrize("element", [RT0, NED0], ids=["rt0", "ne0"])
+def test_lshape_csr_parity(api, element):
+    c, e = api.build_lshape(16, 0.15, 9, device="cuda:0")
+    ref = ora.assemble(2, element, c.cpu().numpy(), e.cpu().numpy())
+    assert_csr_parity(api.Assembler(c, e, element).assemble(), ref, what="lshape")
