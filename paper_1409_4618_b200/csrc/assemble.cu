@@ -265,37 +265,63 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
     constexpr int M = P::M, NO = M - 1;
     constexpr int NS = 1 + 2 * NO, WSEG = 32 * NS, NW = TRI_TPB / 32;
     __shared__ int s_col[NW][WSEG];
-    __shared__ double s_vm[NW][WSEG];
-    __shared__ double s_vk[NW][WSEG];
+    __shared__ double2 s_v[NW][WSEG];  // (M, K) of one entry: one 16-byte store / load
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int* sc = s_col[wid];
-    double* sm = s_vm[wid];
-    double* sk = s_vk[wid];
+    double2* sv = s_v[wid];
     const int nbatch = (n_rows + 31) >> 5;
     const int stride = gridDim.x * NW;
     int batch = blockIdx.x * NW + wid;
     if (batch >= nbatch) return;
 
-    // prologue: L1 of batches b and b+1, L2 of batch b
+    // Pipeline.  Triangles (coordinates held in Ids): four stages -- while
+    // batch b is computed, the coordinates of b+1, the element data of b+2 and
+    // the records of b+3 are in flight.  Faces (24 doubles of coordinates per
+    // pair): three stages -- coordinates of b, element data of b+1, records
+    // of b+2.
+    constexpr bool DEEP = P::M == 3;
     TriL1 c1 = tri_l1(inc_ptr, rec, batch, nbatch, n_rows, lane);
     TriL1 n1 = tri_l1(inc_ptr, rec, batch + stride, nbatch, n_rows, lane);
-    typename P::Ids T0, T1;
+    TriL1 n2 = DEEP ? tri_l1(inc_ptr, rec, batch + 2 * stride, nbatch, n_rows, lane) : TriL1{};
+    typename P::Ids T0, T1, U0, U1;
     P::load_ids(elems, e2d, c1.rr.x, T0);
     P::load_ids(elems, e2d, c1.rr.y, T1);
-
-    for (; batch < nbatch; batch += stride) {
-        // L3 of batch b
-        typename P::Geo G0, G1;
-        P::load_x(coords, T0, G0);
-        P::load_x(coords, T1, G1);
-        // L2 of batch b+1, L1 of batch b+2
-        typename P::Ids U0, U1;
-        const bool has_next = batch + stride < nbatch;
-        if (has_next) {
+    if constexpr (DEEP) {
+        typename P::Geo g;
+        P::load_x(coords, T0, g);
+        P::load_x(coords, T1, g);
+        if (batch + stride < nbatch) {
             P::load_ids(elems, e2d, n1.rr.x, U0);
             P::load_ids(elems, e2d, n1.rr.y, U1);
         }
-        const TriL1 n2 = tri_l1(inc_ptr, rec, batch + 2 * stride, nbatch, n_rows, lane);
+    }
+
+    for (; batch < nbatch; batch += stride) {
+        typename P::Geo G0, G1;
+        typename P::Ids V0, V1;
+        TriL1 n3{};
+        const bool has_next = batch + stride < nbatch;
+        if constexpr (DEEP) {
+            // L3 of b+1, L2 of b+2, L1 of b+3
+            if (has_next) {
+                P::load_x(coords, U0, G0);
+                P::load_x(coords, U1, G1);
+            }
+            if (batch + 2 * stride < nbatch) {
+                P::load_ids(elems, e2d, n2.rr.x, V0);
+                P::load_ids(elems, e2d, n2.rr.y, V1);
+            }
+            n3 = tri_l1(inc_ptr, rec, batch + 3 * stride, nbatch, n_rows, lane);
+        } else {
+            // L3 of b, L2 of b+1, L1 of b+2
+            P::load_x(coords, T0, G0);
+            P::load_x(coords, T1, G1);
+            if (has_next) {
+                P::load_ids(elems, e2d, n1.rr.x, U0);
+                P::load_ids(elems, e2d, n1.rr.y, U1);
+            }
+            n3 = tri_l1(inc_ptr, rec, batch + 2 * stride, nbatch, n_rows, lane);
+        }
 
         // ---- batch b
         const int w0 = batch * 32;
@@ -362,8 +388,7 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
                 for (int x = 0; x < NS; ++x) {
                     if (x <= NO || two) {
                         sc[o + rk[x]] = cl[x];
-                        sm[o + rk[x]] = am[x];
-                        sk[o + rk[x]] = ak[x];
+                        sv[o + rk[x]] = make_double2(am[x], ak[x]);
                     }
                 }
             }
@@ -373,18 +398,29 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
                 const int x = u * 32 + lane;
                 if (x < segn) {
                     const int gx = gbase + x;
+                    const double2 v = sv[x];
                     if (forms & EFEM_PATTERN) col_idx[gx] = sc[x];
-                    if (forms & EFEM_MASS) vals_m[gx] = sm[x];
-                    if (forms & EFEM_STIFF) vals_k[gx] = sk[x];
+                    if (forms & EFEM_MASS) vals_m[gx] = v.x;
+                    if (forms & EFEM_STIFF) vals_k[gx] = v.y;
                 }
             }
             __syncwarp();
         }
         // rotate the pipeline
-        c1 = n1;
-        n1 = n2;
-        T0 = U0;
-        T1 = U1;
+        if constexpr (DEEP) {
+            c1 = n1;
+            n1 = n2;
+            n2 = n3;
+            T0 = U0;
+            T1 = U1;
+            U0 = V0;
+            U1 = V1;
+        } else {
+            c1 = n1;
+            n1 = n3;
+            T0 = U0;
+            T1 = U1;
+        }
     }
 }
 
@@ -702,7 +738,7 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
     const int32_t* row_ptr = p.row_ptr + w.row0;
     if constexpr (KT::D == 2 || KT::FACES) {
         using P = std::conditional_t<KT::D == 2, TriPolicy, FacePolicy>;
-        constexpr int MINB = KT::D == 2 ? 3 : 2;
+        constexpr int MINB = 2;
         static int grid = 0;
         if (!grid) {
             int dev = 0, sms = 0, per_sm = 0;
