@@ -186,7 +186,7 @@ struct NodeCaps {
     // global-memory slow path
     static constexpr int CAP = KT::D == 2 ? 16 : (KT::FACES ? 32 : 48);
     static constexpr int TPB = KT::D == 2 ? 128 : 64;
-    static constexpr int DCAP = 16;  // 3D edges: distinct larger neighbours held in shared memory
+    static constexpr int DCAP = 12;  // 3D edges: distinct larger neighbours held in registers
 };
 
 struct NodeOut {
@@ -299,14 +299,22 @@ __device__ __forceinline__ void node_sort_generic(const BucketArrays& B, int32_t
 template <class KT>
 __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* __restrict__ gb, int64_t beg, int n,
                                                int a, int* s_grp, int& n_ent, int& n_nnz) {
+    // The distinct list D (ascending) and the per-group counts live in
+    // registers (fully unrolled, compile-time indices): searches and
+    // insertions are compare / select chains with no dependent shared-memory
+    // round trips.  The scatter cursors and link xors use shared memory.
     constexpr int TPB = NodeCaps<KT>::TPB;
-    constexpr int DCAP = NodeCaps<KT>::DCAP;
-    int* D = s_grp + threadIdx.x;  // [p * TPB]: distinct b, ascending
-    int* C = D + DCAP * TPB;       // counts, then running cursors
-    int* S = C + DCAP * TPB;       // group starts
-    int* X = S + DCAP * TPB;       // xor of link edges
+    constexpr int DC = NodeCaps<KT>::DCAP;
+    int* Cur = s_grp + threadIdx.x;  // [p * TPB]: running cursor of group p
+    int* X = Cur + DC * TPB;         // xor of link edges of group p
     const uint64_t* __restrict__ key = B.key + beg;
     const int32_t* __restrict__ xr = B.x + beg;
+    int D[DC], C[DC];
+#pragma unroll
+    for (int q = 0; q < DC; ++q) {
+        D[q] = INT_MAX;
+        C[q] = 0;
+    }
     int nd = 0;
     bool over = false;
     constexpr int U = 4;  // keys loaded ahead of use
@@ -318,31 +326,41 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
         for (int u = 0; u < U; ++u) {
             const int b = bb[u];
             if (b < 0) continue;
-            int p = 0;
-            while (p < nd && D[p * TPB] < b) ++p;
-            if (p < nd && D[p * TPB] == b) {
-                C[p * TPB] += 1;
-            } else if (nd == DCAP) {
+            int lt = 0;
+            bool found = false;
+#pragma unroll
+            for (int q = 0; q < DC; ++q) {  // D[q] = INT_MAX beyond nd
+                lt += D[q] < b;
+                found |= D[q] == b;
+            }
+            if (found) {
+#pragma unroll
+                for (int q = 0; q < DC; ++q) C[q] += q == lt;
+            } else if (nd == DC) {
                 over = true;
             } else {
-                for (int q = nd; q > p; --q) {
-                    D[q * TPB] = D[(q - 1) * TPB];
-                    C[q * TPB] = C[(q - 1) * TPB];
+#pragma unroll
+                for (int q = DC - 1; q > 0; --q) {
+                    D[q] = q > lt ? D[q - 1] : (q == lt ? b : D[q]);
+                    C[q] = q > lt ? C[q - 1] : (q == lt ? 1 : C[q]);
                 }
-                D[p * TPB] = b;
-                C[p * TPB] = 1;
+                D[0] = lt == 0 ? b : D[0];
+                C[0] = lt == 0 ? 1 : C[0];
                 ++nd;
             }
         }
     }
     if (over) return false;
+    int S[DC];
     int off = 0;
-    for (int p = 0; p < nd; ++p) {
-        const int c = C[p * TPB];
-        C[p * TPB] = off;
-        S[p * TPB] = off;
-        X[p * TPB] = 0;
-        off += c;
+#pragma unroll
+    for (int q = 0; q < DC; ++q) {
+        S[q] = off;
+        if (q < nd) {
+            Cur[q * TPB] = off;
+            X[q * TPB] = 0;
+        }
+        off += C[q];
     }
     for (int j0 = 0; j0 < n; j0 += U) {
         uint64_t kk[U];
@@ -356,25 +374,27 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
         for (int u = 0; u < U; ++u) {
             if (j0 + u >= n) continue;
             const int b = (int)(kk[u] >> 32);
-            int lo = 0, hi = nd - 1;  // D sorted, b present
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (D[mid * TPB] < b) lo = mid + 1; else hi = mid;
-            }
-            const int pos = C[lo * TPB];
-            C[lo * TPB] = pos + 1;
-            X[lo * TPB] ^= xx[u] ^ a ^ b;  // c ^ d of this tet
-            gb[pos] = (int)((uint32_t)kk[u] | (pos == S[lo * TPB] ? RUN_FLAG : 0u));
+            int g = 0, st = 0;
+#pragma unroll
+            for (int q = 0; q < DC; ++q) g += D[q] < b;  // b present: its group index
+#pragma unroll
+            for (int q = 0; q < DC; ++q) st = q == g ? S[q] : st;
+            const int pos = Cur[g * TPB];
+            Cur[g * TPB] = pos + 1;
+            X[g * TPB] ^= xx[u] ^ a ^ b;  // c ^ d of this tet
+            gb[pos] = (int)((uint32_t)kk[u] | (pos == st ? RUN_FLAG : 0u));
         }
     }
     int nnz = 0;
-    for (int p = 0; p < nd; ++p) {
-        const int st = S[p * TPB];
-        const int t = C[p * TPB] - st;
-        const bool bnd = X[p * TPB] != 0;  // open link path: L = t + 1
-        if (bnd) atomicOr(gb + st, (int)BND_FLAG);
-        B.key[beg + st] = (uint64_t)(uint32_t)D[p * TPB] << 32;
-        nnz += 1 + 3 * t + 2 * (int)bnd;
+#pragma unroll
+    for (int q = 0; q < DC; ++q) {
+        if (q < nd) {
+            const int st = S[q];
+            const bool bnd = X[q * TPB] != 0;  // open link path: L = t + 1
+            if (bnd) atomicOr(gb + st, (int)BND_FLAG);
+            B.key[beg + st] = (uint64_t)(uint32_t)D[q] << 32;
+            nnz += 1 + 3 * C[q] + 2 * (int)bnd;
+        }
     }
     n_ent = nd;
     n_nnz = nnz;
@@ -434,7 +454,7 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
     constexpr int DCAP = NodeCaps<KT>::DCAP;
     __shared__ uint64_t s_key[NE3 ? 1 : CAP * TPB];
     __shared__ int s_inst[KT::FACES ? CAP * TPB : 1];
-    __shared__ int s_grp[NE3 ? 4 * DCAP * TPB : 1];
+    __shared__ int s_grp[NE3 ? 2 * DCAP * TPB : 1];
     const int64_t a64 = (int64_t)blockIdx.x * TPB + threadIdx.x;
     if (a64 >= n_nodes) return;
     const int a = (int)a64;
