@@ -4,8 +4,9 @@
 
 One JSON line on rank 0.  A "step" is one pass of the whole hot path over the
 device-resident mesh of the chosen BASELINE config: DOF enumeration + signs,
-sparsity pattern, local matrices and CSR values (efem_assemble_symbolic +
-efem_assemble_numeric + efem_plan_check).  L2 is flushed between timed steps
+sparsity pattern, local matrices and CSR values (efem_assemble_async, i.e.
+enumeration + pattern + numeric with the counts kept on the device, then
+efem_plan_check).  L2 is flushed between timed steps
 (a 512 MiB write, untimed).  value = elements / second over all ranks.
 See DESIGN.md "Measurement" for the roofline bytes and the oracle baseline.
 """
@@ -187,8 +188,9 @@ def run_efem(args, cfg):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
     def step():
-        asm.symbolic()
-        asm.numeric(out, api.ALL)
+        # the whole hot path (enumeration, pattern, values) in one asynchronous
+        # call into the CSR sized by the first symbolic call, then the flag check
+        asm.assemble_async(out, api.ALL)
         asm.check()
 
     for _ in range(max(args.warmup, 3)):

@@ -177,6 +177,16 @@ efem_status efem_assemble_symbolic(efem_plan plan, int64_t* n_rows, int64_t* nnz
  * reported by efem_plan_check. */
 efem_status efem_assemble_numeric(efem_plan plan, unsigned forms, efem_csr* out, efem_stream_t stream);
 
+/* The whole hot path in one asynchronous call, for repeated assembly into an
+ * output allocated from an earlier efem_assemble_symbolic of the same (or a
+ * topologically identical) mesh: enumeration, pattern and values are all
+ * recomputed on the device, the row and entry counts stay on the device
+ * (no host round trip); out->n_rows / out->nnz are the CAPACITIES.  A
+ * pattern that does not fit is flagged (EFEM_ECAPACITY) and nothing is
+ * written.  Follow with efem_plan_check, which also makes the new sizes the
+ * plan's (efem_assemble_numeric may then be called).  Never synchronises. */
+efem_status efem_assemble_async(efem_plan plan, unsigned forms, efem_csr* out, efem_stream_t stream);
+
 /* Synchronising: returns EFEM_EDEGENERATE / EFEM_ECAPACITY if a kernel since
  * the last check flagged one, else EFEM_OK (or EFEM_ECUDA). */
 efem_status efem_plan_check(efem_plan plan, efem_stream_t stream);

@@ -175,6 +175,16 @@ class Assembler:
                                                                         _stream(stream)))
         return out
 
+    def assemble_async(self, out: CSR, forms: int = ALL, stream=None) -> CSR:
+        """The whole hot path without a host round trip into an `out` sized by
+        an earlier symbolic call (capacities); follow with check()."""
+        c = _lib.efem_csr(out.n_rows, out.nnz, out.row_ptr.data_ptr(), out.col_idx.data_ptr(),
+                          out.vals_M.data_ptr(), out.vals_K.data_ptr())
+        with torch.cuda.device(self.device):
+            _lib.check("efem_assemble_async", _lib.load().efem_assemble_async(self._plan, forms, ctypes.byref(c),
+                                                                              _stream(stream)))
+        return out
+
     def check(self, stream=None):
         with torch.cuda.device(self.device):
             _lib.check("efem_plan_check", _lib.load().efem_plan_check(self._plan, _stream(stream)))

@@ -111,7 +111,7 @@ efem_status read_flags(Plan& p, cudaStream_t s) {
 // Enumeration = ~10 dependent launches + one D2H of the header; replayed as a
 // CUDA graph (captured once on the plan's internal stream, handshaking with
 // the caller's stream through events) to cut the launch gaps.
-efem_status enumerate_graph(Plan& p, cudaStream_t s, bool* used) {
+efem_status enumerate_graph(Plan& p, cudaStream_t s, bool* used, bool sync = true) {
     *used = false;
     if (p.graph_failed || p.want_d2n || debug_sync()) return EFEM_OK;
     if (!p.g_enum) {
@@ -152,7 +152,7 @@ efem_status enumerate_graph(Plan& p, cudaStream_t s, bool* used) {
     count_launch((int)p.graph_launches);
     EFEM_CUDA_TRY(cudaEventRecord(p.ev_out, p.gstream));
     EFEM_CUDA_TRY(cudaStreamWaitEvent(s, p.ev_out, 0));
-    EFEM_CUDA_TRY(cudaStreamSynchronize(p.gstream));
+    if (sync) EFEM_CUDA_TRY(cudaStreamSynchronize(p.gstream));
     *used = true;
     return EFEM_OK;
 }
@@ -507,7 +507,45 @@ efem_status efem_plan_check(efem_plan plan, efem_stream_t stream) {
     Plan* p = reinterpret_cast<Plan*>(plan);
     efem_status st = need_ws(p);
     if (st != EFEM_OK) return st;
-    return read_flags(*p, (cudaStream_t)stream);
+    st = read_flags(*p, (cudaStream_t)stream);
+    if (p->async_pending) {  // sizes of the last efem_assemble_async
+        p->async_pending = false;
+        p->n_dofs = p->h_hdr->totals[0];
+        p->nnz = p->h_hdr->totals[1];
+        p->enumerated = p->symbolic = st == EFEM_OK;
+    }
+    return st;
+}
+
+efem_status efem_assemble_async(efem_plan plan, unsigned forms, efem_csr* out, efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    efem_status st = need_ws(p);
+    if (st != EFEM_OK) return st;
+    if (!out || out->n_rows < 0 || out->nnz < 0 || (forms & ~7u) || !out->row_ptr ||
+        (out->nnz > 0 && (!out->col_idx || ((forms & EFEM_MASS) && !out->vals_mass) ||
+                          ((forms & EFEM_STIFF) && !out->vals_stiff)))) {
+        set_error("efem_assemble_async: out capacities / arrays (row_ptr always, col_idx, a vals array per form bit)");
+        return EFEM_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    p->enumerated = p->symbolic = false;
+    p->async_pending = true;
+    bool used = false;
+    if ((st = enumerate_graph(*p, s, &used, false)) != EFEM_OK) return st;
+    if (!used && (st = launch_enumerate(*p, s)) != EFEM_OK) return st;
+    RowWindow w;
+    w.row0 = 0;
+    w.n_rows = out->n_rows;  // capacity; the kernels read the real count on the device
+    w.own_base = 0;
+    w.out_base = 0;
+    w.e2d = p->e2d;
+    w.dyn = true;
+    w.cap_nnz = out->nnz;
+    if (out->n_rows == 0) {
+        if (forms & EFEM_PATTERN) EFEM_CUDA_TRY(cudaMemsetAsync(out->row_ptr, 0, 4, s));
+        return EFEM_OK;
+    }
+    return launch_rows_any(*p, forms, out, w, s);
 }
 
 efem_status efem_assemble_host(efem_plan plan, const double* h_coords, const int32_t* h_elems, efem_csr* d_out,

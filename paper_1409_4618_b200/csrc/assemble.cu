@@ -230,6 +230,18 @@ struct FacePolicy {
 // of batch b+1 and the L1 loads of batch b+2 are in flight.
 constexpr int TRI_TPB = 256;
 
+// Asynchronous assembly (efem_assemble_async): the row count comes from the
+// enumeration's header totals on the device; a pattern larger than the output
+// capacities is flagged (F_CAPACITY) and nothing is written.  Returns -1 then.
+__device__ __forceinline__ int dyn_rows(WsHeader* hdr, int cap_rows, long long cap_nnz) {
+    const long long r = *(volatile long long*)&hdr->totals[0], z = *(volatile long long*)&hdr->totals[1];
+    if (r > cap_rows || z > cap_nnz) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&hdr->flags[F_CAPACITY], 1);
+        return -1;
+    }
+    return (int)r;
+}
+
 // L1 of a batch: the lane's row record; lane 0 also the batch's first
 // incidence offset (row offsets follow from t = 1 + (first != last) by a
 // warp scan, so inc_ptr is read once per batch, not per row)
@@ -256,13 +268,18 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
                                                            const int32_t* __restrict__ elems,
                                                            const int32_t* __restrict__ inc_ptr,
                                                            const int2* __restrict__ rec,
-                                                           const int32_t* __restrict__ e2d, int row0, int n_rows,
+                                                           const int32_t* __restrict__ e2d, int row0, int n_rows_arg,
                                                            int own_base, int out_base, unsigned forms,
                                                            int32_t* __restrict__ row_ptr_out,
                                                            int32_t* __restrict__ col_idx,
                                                            double* __restrict__ vals_m, double* __restrict__ vals_k,
-                                                           WsHeader* hdr) {
+                                                           WsHeader* hdr, int dyn, long long cap_nnz) {
     constexpr int M = P::M, NO = M - 1;
+    const int n_rows = dyn ? dyn_rows(hdr, n_rows_arg, cap_nnz) : n_rows_arg;
+    if (n_rows <= 0) {
+        if (dyn && n_rows == 0 && blockIdx.x == 0 && threadIdx.x == 0 && (forms & EFEM_PATTERN)) row_ptr_out[0] = 0;
+        return;
+    }
     constexpr int NS = 1 + 2 * NO, WSEG = 32 * NS, NW = TRI_TPB / 32;
     __shared__ int s_col[NW][WSEG];
     __shared__ double2 s_v[NW][WSEG];  // (M, K) of one entry: one 16-byte store / load
@@ -453,13 +470,18 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
                                                       const int32_t* __restrict__ inc_ptr,
                                                       const int32_t* __restrict__ inc,
                                                       const int32_t* __restrict__ e2d,
-                                                      const int32_t* __restrict__ row_ptr, int n_rows,
+                                                      const int32_t* __restrict__ row_ptr, int n_rows_arg,
                                                       int own_base, int out_base,
                                                       unsigned forms, int fast_ids, int32_t* __restrict__ row_ptr_out,
                                                       int32_t* __restrict__ col_idx,
                                                       double* __restrict__ vals_m, double* __restrict__ vals_k,
-                                                      WsHeader* hdr) {
+                                                      WsHeader* hdr, int dyn, long long cap_nnz) {
     static_assert(KT::D == 3 && !KT::FACES, "NE0 3D only");
+    const int n_rows = dyn ? dyn_rows(hdr, n_rows_arg, cap_nnz) : n_rows_arg;
+    if (n_rows <= 0 || (int)(blockIdx.x * NUM_TPB) >= n_rows) {
+        if (dyn && n_rows == 0 && blockIdx.x == 0 && threadIdx.x == 0 && (forms & EFEM_PATTERN)) row_ptr_out[0] = 0;
+        return;
+    }
     extern __shared__ __align__(16) unsigned char ne3_smem[];
     double* s_vm = reinterpret_cast<double*>(ne3_smem);
     double* s_vk = s_vm + NE3_SLOTS * NE3_LD;
@@ -751,7 +773,7 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
         const int64_t need = (w.n_rows + TRI_TPB - 1) / TRI_TPB;
         k_rows_tri<KT, P, MINB><<<(unsigned)(need < grid ? need : grid), TRI_TPB, 0, s>>>(
             p.coords, p.elems, inc_ptr, p.rec + w.row0, w.e2d, (int)w.row0, (int)w.n_rows, w.own_base, w.out_base,
-            forms, out->row_ptr, out->col_idx, vm, vk, p.hdr);
+            forms, out->row_ptr, out->col_idx, vm, vk, p.hdr, (int)w.dyn, (long long)w.cap_nnz);
     } else {
         const int fast_ids = p.n_nodes < (1ll << 27);
         static bool attr = false;
@@ -762,7 +784,8 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
         }
         k_rows_ne3<KT><<<grid_for(w.n_rows, NUM_TPB), NUM_TPB, NE3_SMEM, s>>>(p.coords, p.elems, inc_ptr, p.bucket, w.e2d, row_ptr,
                                                        (int)w.n_rows, w.own_base, w.out_base, forms, fast_ids,
-                                                       out->row_ptr, out->col_idx, vm, vk, p.hdr);
+                                                       out->row_ptr, out->col_idx, vm, vk, p.hdr, (int)w.dyn,
+                                                       (long long)w.cap_nnz);
     }
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;

@@ -106,6 +106,7 @@ struct Plan {
 
     // state
     bool enumerated = false, symbolic = false;
+    bool async_pending = false;  // efem_assemble_async ran; sizes arrive with efem_plan_check
     int64_t n_dofs = 0, nnz = 0;
 };
 
@@ -116,6 +117,10 @@ struct RowWindow {
     int64_t row0 = 0, n_rows = 0;
     int own_base = 0, out_base = 0;
     const int32_t* e2d = nullptr;
+    // asynchronous assembly: n_rows / nnz are read on the device from the
+    // header totals; n_rows, cap_nnz above are then the output capacities
+    bool dyn = false;
+    int64_t cap_nnz = 0;
 };
 
 // ---- error plumbing --------------------------------------------------------------

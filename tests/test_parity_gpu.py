@@ -341,3 +341,38 @@ def test_lshape_csr_parity(api, element):
     c, e = api.build_lshape(16, 0.15, 9, device="cuda:0")
     ref = ora.assemble(2, element, c.cpu().numpy(), e.cpu().numpy())
     assert_csr_parity(api.Assembler(c, e, element).assemble(), ref, what="lshape")
+
+
+# ---------------------------------------------------------------------------- asynchronous one-call assembly
+@pytest.mark.parametrize("dim,element", KINDS, ids=KIND_IDS)
+def test_assemble_async_equals_two_phase(api, dim, element):
+    """efem_assemble_async (counts stay on the device) gives the same CSR,
+    byte for byte, as symbolic + numeric; repeated calls are identical."""
+    n = 20 if dim == 2 else 5
+    c, e = _gpu_mesh(api, dim, n, 0.2 if dim == 2 else 0.15, 31)
+    asm = api.Assembler(c, e, element)
+    ref = asm.assemble()
+    out = asm.alloc_csr()
+    for t in (out.row_ptr, out.col_idx, out.vals_M, out.vals_K):
+        t.fill_(-7) if t.dtype == torch.int32 else t.fill_(float("nan"))
+    for _ in range(2):
+        asm.assemble_async(out)
+        asm.check()
+        for a, b in zip((ref.row_ptr, ref.col_idx, ref.vals_M, ref.vals_K),
+                        (out.row_ptr, out.col_idx, out.vals_M, out.vals_K)):
+            assert torch.equal(a, b)
+
+
+def test_assemble_async_capacity_flagged(api):
+    c, e = _gpu_mesh(api, 2, 8, 0.1, 2)
+    asm = api.Assembler(c, e, NED0)
+    full = asm.assemble()
+    small = api.CSR(torch.zeros(full.n_rows + 1, dtype=torch.int32, device="cuda"),
+                    torch.zeros(full.nnz - 1, dtype=torch.int32, device="cuda"),
+                    torch.zeros(full.nnz - 1, dtype=torch.float64, device="cuda"),
+                    torch.zeros(full.nnz - 1, dtype=torch.float64, device="cuda"))
+    asm.assemble_async(small)
+    with pytest.raises(api._lib.EfemError) as ei:
+        asm.check()
+    assert ei.value.status == -8  # EFEM_ECAPACITY
+    assert int(small.col_idx.abs().sum()) == 0  # nothing written
