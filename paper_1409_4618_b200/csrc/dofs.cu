@@ -544,8 +544,7 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
             if (t > 2) atomicOr(&out.flags[F_ROW_MISMATCH], 1);
         }
     };
-    for (int j = 0; j < n; ++j) {
-        const int w = __ldg(gb + j);
+    auto visit = [&](int j, int w) {
         const int inst = w & INST_MASK;
         if (w < 0) {  // RUN_FLAG: first instance of a new entity
             if (j > 0) close_run(j);
@@ -578,6 +577,16 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
         }
         if constexpr (!NE3) out.e2d[(int64_t)(inst >> 3) * KT::M + (inst & 7)] = id;  // 3D edges: k_elem_dofs
         prev = inst;
+    };
+    // the words in chunks of 8, loaded ahead of their (dependent) processing
+    constexpr int U = 8;
+    for (int j0 = 0; j0 < n; j0 += U) {
+        int wv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) wv[u] = j0 + u < n ? __ldg(gb + j0 + u) : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (j0 + u < n) visit(j0 + u, wv[u]);
     }
     if (n > 0) close_run(n);
     if (a == n_nodes - 1) {
