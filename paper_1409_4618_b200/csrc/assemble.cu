@@ -110,6 +110,30 @@ struct TriPolicy {
         c[1] = I.d2;
         return tri_row(I, m0, k0, m[0], k[0], m[1], k[1]);
     }
+    // The row's second triangle shares the row's edge with the first: only
+    // its opposite vertex (id + coordinates), its local start vertex (for the
+    // orientation) and its two other DOFs are loaded; the rest is taken from
+    // the first triangle (13 gathers per interior row instead of 16).
+    __device__ __forceinline__ static void load_ids2(const int32_t* __restrict__ elems,
+                                                     const int32_t* __restrict__ e2d, int inst, Ids& I) {
+        const int e = inst >> 3, k = inst & 7;
+        const int k1 = mod3_next(k), k2 = mod3_prev(k);
+        const int32_t* ge = elems + (int64_t)e * 3;
+        const int32_t* de = e2d + (int64_t)e * 3;
+        I.q0 = __ldg(ge + k);
+        I.q1 = __ldg(ge + k1);
+        I.d1 = __ldg(de + k1);
+        I.d2 = __ldg(de + k2);
+    }
+    __device__ __forceinline__ static void load_x2(const double* __restrict__ coords, Ids& I) {
+        I.x0 = __ldg(reinterpret_cast<const double2*>(coords) + I.q0);
+    }
+    __device__ __forceinline__ static void complete2(const Ids& A, Ids& I) {
+        const bool same = I.q1 == A.q1;
+        I.q2 = same ? A.q2 : A.q1;
+        I.x1 = same ? A.x1 : A.x2;
+        I.x2 = same ? A.x2 : A.x1;
+    }
 };
 
 // 3D faces (RT0).  Face k is the face opposite vertex o = 3 - k; with y_v the
@@ -301,16 +325,19 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
     TriL1 n1 = tri_l1(inc_ptr, rec, batch + stride, nbatch, n_rows, lane);
     TriL1 n2 = DEEP ? tri_l1(inc_ptr, rec, batch + 2 * stride, nbatch, n_rows, lane) : TriL1{};
     typename P::Ids T0, T1, U0, U1;
-    P::load_ids(elems, e2d, c1.rr.x, T0);
-    P::load_ids(elems, e2d, c1.rr.y, T1);
     if constexpr (DEEP) {
+        P::load_ids(elems, e2d, c1.rr.x, T0);
+        P::load_ids2(elems, e2d, c1.rr.y, T1);
         typename P::Geo g;
         P::load_x(coords, T0, g);
-        P::load_x(coords, T1, g);
+        P::load_x2(coords, T1);
         if (batch + stride < nbatch) {
             P::load_ids(elems, e2d, n1.rr.x, U0);
-            P::load_ids(elems, e2d, n1.rr.y, U1);
+            P::load_ids2(elems, e2d, n1.rr.y, U1);
         }
+    } else {
+        P::load_ids(elems, e2d, c1.rr.x, T0);
+        P::load_ids(elems, e2d, c1.rr.y, T1);
     }
 
     for (; batch < nbatch; batch += stride) {
@@ -322,11 +349,11 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
             // L3 of b+1, L2 of b+2, L1 of b+3
             if (has_next) {
                 P::load_x(coords, U0, G0);
-                P::load_x(coords, U1, G1);
+                P::load_x2(coords, U1);
             }
             if (batch + 2 * stride < nbatch) {
                 P::load_ids(elems, e2d, n2.rr.x, V0);
-                P::load_ids(elems, e2d, n2.rr.y, V1);
+                P::load_ids2(elems, e2d, n2.rr.y, V1);
             }
             n3 = tri_l1(inc_ptr, rec, batch + 3 * stride, nbatch, n_rows, lane);
         } else {
@@ -368,6 +395,7 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
             if (live) {
                 double m0a, k0a, m0b, k0b, ma[NO], ka[NO], mb[NO], kb[NO];
                 int ca[NO], cb[NO];
+                if constexpr (DEEP) P::complete2(T0, T1);
                 const double da = P::row(T0, G0, m0a, k0a, ca, ma, ka);
                 const double db = P::row(T1, G1, m0b, k0b, cb, mb, kb);
                 const bool bad_a = !(fabs(da) > 0.0 && fabs(da) < INFINITY);
