@@ -147,6 +147,12 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes);
 
 efem_status efem_plan_destroy(efem_plan plan);
 
+/* NE0 3D only (no-op otherwise): size every edge row from the exact number of
+ * distinct link vertices (slower symbolic pass) instead of the manifold
+ * closed form 1 + 3t + 2[boundary] (reading M1), for meshes with
+ * non-manifold edges.  Takes effect at the next symbolic call. */
+efem_status efem_plan_set_exact(efem_plan plan, int exact);
+
 /* ---- the hot path ------------------------------------------------------------ */
 
 /* DOF enumeration + orientation (Sec. 3 get_edges /

@@ -70,6 +70,7 @@ def load():
                                   ctypes.POINTER(ctypes.c_size_t)]),
         "efem_plan_set_workspace": (st, [vp, vp, ctypes.c_size_t]),
         "efem_plan_destroy": (st, [vp]),
+        "efem_plan_set_exact": (st, [vp, ctypes.c_int]),
         "efem_enumerate_dofs": (st, [vp, ctypes.POINTER(efem_dofs), vp]),
         "efem_assemble_symbolic": (st, [vp, i64p, i64p, vp, vp]),
         "efem_assemble_numeric": (st, [vp, ctypes.c_uint, ctypes.POINTER(efem_csr), vp]),

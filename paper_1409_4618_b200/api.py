@@ -129,6 +129,11 @@ class Assembler:
         except Exception:
             pass
 
+    def set_exact(self, exact: bool = True):
+        """NE0 3D: exact edge-row sizes for non-manifold meshes (slower symbolic)."""
+        _lib.check("efem_plan_set_exact", _lib.load().efem_plan_set_exact(self._plan, int(bool(exact))))
+        self.n_rows = self.nnz = None
+
     def enumerate_dofs(self, stream=None):
         """dofs2nodes (R x 2|3), elems2dofs (T x m), signs (T x m int8)."""
         L = _lib.load()

@@ -96,7 +96,9 @@ efem_status flags_status(const Plan& p) {
     }
     if (h.flags[F_ROW_MISMATCH]) {
         set_error("row structure differs from the closed-form row length: the mesh is not conforming "
-                  "(duplicate elements, or an entity shared by more elements than a conforming mesh allows)");
+                  "(duplicate elements, or an entity shared by more elements than a conforming mesh allows), "
+                  "or (NE0 3D) an edge whose tets do not form one fan -- efem_plan_set_exact(plan, 1) "
+                  "sizes such rows exactly");
         return EFEM_EINVAL;
     }
     return EFEM_OK;
@@ -416,6 +418,23 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     if (p->g_enum) {
         cudaGraphExecDestroy(p->g_enum);
         p->g_enum = nullptr;
+    }
+    return EFEM_OK;
+}
+
+efem_status efem_plan_set_exact(efem_plan plan, int exact) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p) {
+        set_error("efem_plan_set_exact: NULL plan");
+        return EFEM_EINVAL;
+    }
+    if (p->exact_ne3 != (exact != 0)) {
+        p->exact_ne3 = exact != 0;
+        p->enumerated = p->symbolic = false;
+        if (p->g_enum) {  // the captured enumeration bakes the mode in
+            cudaGraphExecDestroy(p->g_enum);
+            p->g_enum = nullptr;
+        }
     }
     return EFEM_OK;
 }

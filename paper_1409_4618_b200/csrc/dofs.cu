@@ -405,7 +405,7 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
 // link vertices exactly and set BND_FLAG = (L > t)
 template <class KT>
 __device__ __forceinline__ void ne3_runs_exact(const int32_t* __restrict__ elems, int32_t* __restrict__ gb, int n,
-                                               int a, int& n_nnz) {
+                                               int a, int32_t* __restrict__ xs, int& n_nnz) {
     int j = 0;
     while (j < n) {
         int q = j + 1;
@@ -432,12 +432,13 @@ __device__ __forceinline__ void ne3_runs_exact(const int32_t* __restrict__ elems
                 L += !seen;
             }
         }
-        // rows are sized 1 + 3t + 2 [L > t]; any other L (non-manifold fan)
-        // makes the numeric kernel's exact column count disagree -> flagged
+        // the exact excess L - t (0 interior, 1 boundary, more at a
+        // non-manifold edge) goes to the run start's x slot for pass B
         const int t = q - j;
-        const bool bnd = L > t;
-        if (bnd) gb[j] = (int)((uint32_t)gb[j] | BND_FLAG);
-        n_nnz += 1 + 3 * t + 2 * (int)bnd;
+        const int ex = L - t;
+        if (ex > 0) gb[j] = (int)((uint32_t)gb[j] | BND_FLAG);
+        xs[j] = ex;
+        n_nnz += 1 + 2 * L + t;
         j = q;
     }
 }
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
                                                                   const int32_t* __restrict__ bucket_ptr,
                                                                   BucketArrays B, int32_t* __restrict__ bucket,
                                                                   int64_t n_nodes, int32_t* __restrict__ ent_cnt,
-                                                                  int32_t* __restrict__ nnz_cnt) {
+                                                                  int32_t* __restrict__ nnz_cnt, int exact) {
     constexpr bool NE3 = KT::D == 3 && !KT::FACES;
     constexpr int CAP = NodeCaps<KT>::CAP;
     constexpr int TPB = NodeCaps<KT>::TPB;
@@ -497,12 +498,12 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
     } else if constexpr (KT::FACES) {
         node_sort_generic<KT, true>(B, gb, beg, n, s_key, s_inst, n_ent);
     } else {
-        if (!node_group_ne3<KT>(B, gb, beg, n, a, s_grp, n_ent, n_nnz)) {
+        if (exact || !node_group_ne3<KT>(B, gb, beg, n, a, s_grp, n_ent, n_nnz)) {
             n_ent = 0;
             n_nnz = 0;
             // (the NE3 instantiation has no key smem: sort in global memory)
             node_sort_generic<KT, false>(B, gb, beg, n, s_key, s_inst, n_ent);
-            ne3_runs_exact<KT>(elems, gb, n, a, n_nnz);
+            ne3_runs_exact<KT>(elems, gb, n, a, B.x + beg, n_nnz);
         }
     }
     ent_cnt[a] = n_ent;
@@ -520,6 +521,7 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
                                                     const int32_t* __restrict__ bucket_ptr,
                                                     const int32_t* __restrict__ bucket,
                                                     const uint64_t* __restrict__ bkey,
+                                                    const int32_t* __restrict__ bx,
                                                     const int32_t* __restrict__ ent_ptr,
                                                     const int32_t* __restrict__ nnz_ptr, int64_t n_nodes,
                                                     NodeOut out) {
@@ -532,12 +534,11 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
     const int32_t* gb = bucket + beg;
     int id = __ldg(ent_ptr + a) - 1;
     int nnz_run = NE3 ? __ldg(nnz_ptr + a) : 0;
-    int run0 = 0, first = 0, prev = 0;
-    bool bnd = false;
+    int run0 = 0, first = 0, prev = 0, excess = 0;
     auto close_run = [&](int j_end) {
         const int t = j_end - run0;
         if constexpr (NE3) {
-            nnz_run += 1 + 3 * t + 2 * (int)bnd;
+            nnz_run += 1 + 3 * t + 2 * excess;  // 1 + 2L + t, L = t + excess
         } else {
             out.rec[id] = make_int2(first, prev);
             // a conforming mesh has <= 2 elements per edge (2D) / face (3D)
@@ -551,10 +552,12 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
             ++id;
             run0 = j;
             first = inst;
-            bnd = (w & BND_FLAG) != 0;
             out.inc_ptr[id] = beg + j;
             if constexpr (NE3) {
                 out.row_ptr[id] = nnz_run;
+                // link excess L - t: the BND flag (0 / 1) on the manifold
+                // closed form, the exact count in exact mode
+                excess = bx ? __ldg(bx + beg + j) : (w & BND_FLAG ? 1 : 0);
                 const int b = (int)(__ldg(bkey + beg + j) >> 32);
                 out.nbr[id] = b;
                 if (out.d2n) {
@@ -679,7 +682,7 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     // entity counts in ent_cnt; ent_cnt[N] = nnz_cnt[N] = 0 since the workspace was set)
     constexpr int TPB = NodeCaps<KT>::TPB;
     k_node_count<KT><<<grid_for(N, TPB), TPB, 0, s>>>(p.elems, p.bucket_ptr, barr, p.bucket, N, p.ent_cnt,
-                                                      p.nnz_cnt);
+                                                      p.nnz_cnt, (int)p.exact_ne3);
     EFEM_LAUNCH_CHECK();
     EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.ent_cnt, p.ent_ptr, (int)(N + 1), s));
     count_launch(2);
@@ -691,8 +694,8 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     int* d_flags = reinterpret_cast<int*>(reinterpret_cast<char*>(p.hdr) + offsetof(WsHeader, flags));
     NodeOut o{p.e2d, p.inc_ptr, p.row_ptr, p.want_d2n ? p.d2n : nullptr, p.nbr, p.rec, d_flags, p.bucket,
               p.d_totals};
-    k_node_write<KT><<<grid_for(N, 256), 256, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.bkey, p.ent_ptr, p.nnz_ptr,
-                                                       N, o);
+    k_node_write<KT><<<grid_for(N, 256), 256, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.bkey,
+                                                       p.exact_ne3 ? p.bx : nullptr, p.ent_ptr, p.nnz_ptr, N, o);
     EFEM_LAUNCH_CHECK();
     if constexpr (KT::D == 3 && !KT::FACES) {
         if (T > 0) {

@@ -89,6 +89,7 @@ struct Plan {
     unsigned long long* lb_status = nullptr;  // look-back tile status + ticket
     int64_t* d_totals = nullptr;    // == hdr->totals
     bool want_d2n = false;
+    bool exact_ne3 = false;  // NE0 3D: exact link counts (non-manifold meshes), efem_plan_set_exact
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
 

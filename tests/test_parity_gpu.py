@@ -191,6 +191,26 @@ def test_nonmanifold_edge_ne0_3d_reported(api):
     assert ei.value.status == -1
 
 
+@pytest.mark.parametrize("dim,element", [(3, NED0), (3, RT0), (2, NED0)])
+def test_exact_mode_bowtie_and_regular(api, dim, element):
+    """efem_plan_set_exact: the non-manifold bow-tie assembles exactly (NE0
+    3D), and exact mode changes nothing on a regular mesh (or other kinds)."""
+    if dim == 3:
+        c, e = _bowtie_tets()
+        asm = api.Assembler(torch.from_numpy(c).cuda(), torch.from_numpy(e).cuda(), element)
+        asm.set_exact(True)
+        assert_csr_parity(asm.assemble(), ora.assemble(3, element, c, e), what="bowtie exact")
+    n = 4 if dim == 3 else 9
+    cg, eg = _gpu_mesh(api, dim, n, 0.15, 12)
+    asm = api.Assembler(cg, eg, element)
+    fast = asm.assemble()
+    asm.set_exact(True)
+    exact = asm.assemble()
+    for x, y in zip((fast.row_ptr, fast.col_idx, fast.vals_M, fast.vals_K),
+                    (exact.row_ptr, exact.col_idx, exact.vals_M, exact.vals_K)):
+        assert torch.equal(x, y)
+
+
 @pytest.mark.parametrize("dim,element", KINDS, ids=KIND_IDS)
 def test_single_element_and_unused_nodes(api, dim, element):
     rc, re = ora.build_mesh(dim, 2, 0.1, 3)
