@@ -401,6 +401,107 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
     return true;
 }
 
+// 3D faces: group the node's instances by face key (mid << 32 | hi) with the
+// sorted distinct list and counts in registers (as node_group_ne3), counting
+// scatter, then each face's two tets in element order.  Returns false when
+// the node has more than FDC distinct faces (caller sorts generically).
+template <class KT>
+__device__ __forceinline__ bool node_group_faces(const BucketArrays& B, int32_t* __restrict__ gb, int64_t beg,
+                                                 int n, int* s_cur, int& n_ent) {
+    constexpr int TPB = NodeCaps<KT>::TPB;
+    constexpr int FDC = 16;
+    int* Cur = s_cur + threadIdx.x;  // [p * TPB]
+    const uint64_t* __restrict__ key = B.key + beg;
+    const int32_t* __restrict__ ins = B.inst + beg;
+    uint64_t D[FDC];
+    int C[FDC];
+#pragma unroll
+    for (int q = 0; q < FDC; ++q) {
+        D[q] = ~0ull;
+        C[q] = 0;
+    }
+    int nd = 0;
+    bool over = false;
+    constexpr int U = 4;
+    for (int j0 = 0; j0 < n; j0 += U) {
+        uint64_t kk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) kk[u] = j0 + u < n ? __ldg(key + j0 + u) : ~0ull;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (j0 + u >= n) continue;
+            const uint64_t b = kk[u];
+            int lt = 0;
+            bool found = false;
+#pragma unroll
+            for (int q = 0; q < FDC; ++q) {
+                lt += D[q] < b;
+                found |= D[q] == b;
+            }
+            if (found) {
+#pragma unroll
+                for (int q = 0; q < FDC; ++q) C[q] += q == lt;
+            } else if (nd == FDC) {
+                over = true;
+            } else {
+#pragma unroll
+                for (int q = FDC - 1; q > 0; --q) {
+                    D[q] = q > lt ? D[q - 1] : (q == lt ? b : D[q]);
+                    C[q] = q > lt ? C[q - 1] : (q == lt ? 1 : C[q]);
+                }
+                D[0] = lt == 0 ? b : D[0];
+                C[0] = lt == 0 ? 1 : C[0];
+                ++nd;
+            }
+        }
+    }
+    if (over) return false;
+    int S[FDC];
+    int off = 0;
+#pragma unroll
+    for (int q = 0; q < FDC; ++q) {
+        S[q] = off;
+        if (q < nd) Cur[q * TPB] = off;
+        off += C[q];
+    }
+    for (int j0 = 0; j0 < n; j0 += U) {
+        uint64_t kk[U];
+        int ii[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            kk[u] = j0 + u < n ? __ldg(key + j0 + u) : 0ull;
+            ii[u] = j0 + u < n ? __ldg(ins + j0 + u) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (j0 + u >= n) continue;
+            int g = 0;
+#pragma unroll
+            for (int q = 0; q < FDC; ++q) g += D[q] < kk[u];
+            const int pos = Cur[g * TPB];
+            Cur[g * TPB] = pos + 1;
+            gb[pos] = ii[u];
+        }
+    }
+    // order each face's elements (<= 2 in a conforming mesh; a longer run is
+    // flagged by the write pass) and flag the run starts
+#pragma unroll
+    for (int q = 0; q < FDC; ++q) {
+        if (q < nd) {
+            const int st = S[q];
+            if (C[q] == 2) {
+                const int x = gb[st], y = gb[st + 1];
+                gb[st] = (int)((uint32_t)min(x, y) | RUN_FLAG);
+                gb[st + 1] = max(x, y);
+            } else {  // t == 1, or t > 2 (non-conforming: flagged by the write pass)
+                gb[st] = (int)((uint32_t)gb[st] | RUN_FLAG);
+            }
+        }
+    }
+    n_ent = nd;
+    return true;
+}
+
 // 3D edges, fallback: after node_sort_generic, per run count the distinct
 // link vertices exactly and set BND_FLAG = (L > t)
 template <class KT>
@@ -450,12 +551,12 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
                                                                   int64_t n_nodes, int32_t* __restrict__ ent_cnt,
                                                                   int32_t* __restrict__ nnz_cnt, int exact) {
     constexpr bool NE3 = KT::D == 3 && !KT::FACES;
-    constexpr int CAP = NodeCaps<KT>::CAP;
-    constexpr int TPB = NodeCaps<KT>::TPB;
+        constexpr int TPB = NodeCaps<KT>::TPB;
     constexpr int DCAP = NodeCaps<KT>::DCAP;
-    __shared__ uint64_t s_key[NE3 ? 1 : CAP * TPB];
-    __shared__ int s_inst[KT::FACES ? CAP * TPB : 1];
+    __shared__ uint64_t s_key[1];  // (the generic fallback sorts in global memory)
+    __shared__ int s_inst[1];
     __shared__ int s_grp[NE3 ? 2 * DCAP * TPB : 1];
+    __shared__ int s_cur[KT::FACES ? 16 * TPB : 1];
     const int64_t a64 = (int64_t)blockIdx.x * TPB + threadIdx.x;
     if (a64 >= n_nodes) return;
     const int a = (int)a64;
@@ -492,11 +593,13 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
                     n_ent += st;
                     gb[x] = (int)((uint32_t)rk[x] | (st ? RUN_FLAG : 0u));
                 }
-        } else {
-            node_sort_generic<KT, true>(B, gb, beg, n, s_key, s_inst, n_ent);
+        } else {  // (rare: > 8 instances at a node) sort in global memory
+            node_sort_generic<KT, false>(B, gb, beg, n, s_key, s_inst, n_ent);
         }
     } else if constexpr (KT::FACES) {
-        node_sort_generic<KT, true>(B, gb, beg, n, s_key, s_inst, n_ent);
+        // (fallback sorts in global memory: the fast path needs no key staging,
+        // so the CTA keeps its shared memory small)
+        if (!node_group_faces<KT>(B, gb, beg, n, s_cur, n_ent)) node_sort_generic<KT, false>(B, gb, beg, n, s_key, s_inst, n_ent);
     } else {
         if (exact || !node_group_ne3<KT>(B, gb, beg, n, a, s_grp, n_ent, n_nnz)) {
             n_ent = 0;
