@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
                                                                   int64_t n_nodes, int32_t* __restrict__ ent_cnt,
                                                                   int32_t* __restrict__ nnz_cnt, int exact) {
     constexpr bool NE3 = KT::D == 3 && !KT::FACES;
-        constexpr int TPB = NodeCaps<KT>::TPB;
+    constexpr int TPB = NodeCaps<KT>::TPB;
     constexpr int DCAP = NodeCaps<KT>::DCAP;
     __shared__ uint64_t s_key[1];  // (the generic fallback sorts in global memory)
     __shared__ int s_inst[1];
