@@ -215,7 +215,7 @@ def run_efem(args, cfg):
     T = elems.shape[0]
     value = T * args.steps / (total_ms * 1e-3)
 
-    # dominant kernel (numeric: k_row_fill + row_ptr copy), timed alone the same way
+    # dominant kernel (the numeric call: one row-kernel launch), timed alone the same way
     nk = max(args.steps, 5)
     ks = [torch.cuda.Event(enable_timing=True) for _ in range(nk)]
     ke = [torch.cuda.Event(enable_timing=True) for _ in range(nk)]

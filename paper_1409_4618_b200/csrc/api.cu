@@ -40,7 +40,7 @@ std::atomic<int64_t> g_launches{0};
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-    size_t hdr, cnt, ent_cnt, bucket_ptr, bucket, bkey, binst, bx, nbr, e2d, inc_ptr, row_ptr, rec, d2n, ent_ptr, nnz_cnt, nnz_ptr, lb, totals, cub, total;
+    size_t hdr, cnt, ent_cnt, bucket_ptr, bucket, bkey, binst, bx, nbr, e2d, inc_ptr, row_ptr, rec, d2n, ent_ptr, nnz_cnt, nnz_ptr, totals, cub, total;
 };
 
 Layout layout(const Plan& p, size_t cub_bytes) {
@@ -72,7 +72,6 @@ Layout layout(const Plan& p, size_t cub_bytes) {
     L.ent_ptr = take(N1 * 4);
     L.nnz_cnt = take(N1 * 4);
     L.nnz_ptr = take(N1 * 4);
-    L.lb = take(((size_t)p.n_nodes / 32 + 2) * 8 + 64);
     L.totals = take(16);
     L.cub = take(cub_bytes);
     L.total = off;
@@ -406,7 +405,6 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     p->ent_ptr = reinterpret_cast<int32_t*>(b + L.ent_ptr);
     p->nnz_cnt = reinterpret_cast<int32_t*>(b + L.nnz_cnt);
     p->nnz_ptr = reinterpret_cast<int32_t*>(b + L.nnz_ptr);
-    p->lb_status = reinterpret_cast<unsigned long long*>(b + L.lb);
     p->d_totals = reinterpret_cast<int64_t*>(&p->hdr->totals[0]);
     p->cub_tmp = b + L.cub;
     p->enumerated = p->symbolic = false;

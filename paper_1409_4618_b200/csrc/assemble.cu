@@ -3,12 +3,12 @@
 // 671-696).
 //
 // Row-owner design: one thread per global DOF row i.  The
-// elements containing entity i are the run of the sorted bucket
-// [inc_ptr[i], inc_ptr[i+1]) (ascending element id); row i's values are row k
-// (local index of entity i) of their local matrices, summed in that order.
-// A CTA stages its rows' CSR segment in shared memory and writes it out with
-// coalesced stores, so every CSR byte is written exactly once and no local
-// matrix ever reaches HBM.
+// elements containing entity i are the run of the incidence (sorted bucket)
+// [inc_ptr[i], inc_ptr[i+1]); row i's values are row k (local index of
+// entity i) of their local matrices, summed in ascending element order.
+// Rows are staged in shared memory (per warp: k_rows_tri; per CTA:
+// k_rows_ne3) and written out with coalesced stores, so every CSR byte is
+// written exactly once and no local matrix ever reaches HBM.
 #include <type_traits>
 
 #include "element.cuh"
