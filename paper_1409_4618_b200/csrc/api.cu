@@ -417,6 +417,10 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
         cudaGraphExecDestroy(p->g_enum);
         p->g_enum = nullptr;
     }
+    if (p->g_async) {
+        cudaGraphExecDestroy(p->g_async);
+        p->g_async = nullptr;
+    }
     return EFEM_OK;
 }
 
@@ -433,6 +437,10 @@ efem_status efem_plan_set_exact(efem_plan plan, int exact) {
             cudaGraphExecDestroy(p->g_enum);
             p->g_enum = nullptr;
         }
+        if (p->g_async) {
+            cudaGraphExecDestroy(p->g_async);
+            p->g_async = nullptr;
+        }
     }
     return EFEM_OK;
 }
@@ -443,6 +451,7 @@ efem_status efem_plan_destroy(efem_plan plan) {
     if (p->h_scalars) cudaFreeHost(p->h_scalars);
     if (p->h_hdr) cudaFreeHost(p->h_hdr);
     if (p->g_enum) cudaGraphExecDestroy(p->g_enum);
+    if (p->g_async) cudaGraphExecDestroy(p->g_async);
     if (p->ev_in) cudaEventDestroy(p->ev_in);
     if (p->ev_out) cudaEventDestroy(p->ev_out);
     if (p->gstream) cudaStreamDestroy(p->gstream);
@@ -547,22 +556,64 @@ efem_status efem_assemble_async(efem_plan plan, unsigned forms, efem_csr* out, e
     cudaStream_t s = (cudaStream_t)stream;
     p->enumerated = p->symbolic = false;
     p->async_pending = true;
-    bool used = false;
-    if ((st = enumerate_graph(*p, s, &used, false)) != EFEM_OK) return st;
-    if (!used && (st = launch_enumerate(*p, s)) != EFEM_OK) return st;
-    RowWindow w;
-    w.row0 = 0;
-    w.n_rows = out->n_rows;  // capacity; the kernels read the real count on the device
-    w.own_base = 0;
-    w.out_base = 0;
-    w.e2d = p->e2d;
-    w.dyn = true;
-    w.cap_nnz = out->nnz;
-    if (out->n_rows == 0) {
-        if (forms & EFEM_PATTERN) EFEM_CUDA_TRY(cudaMemsetAsync(out->row_ptr, 0, 4, s));
+    auto enqueue = [&](cudaStream_t q) -> efem_status {
+        efem_status e = launch_enumerate(*p, q);
+        if (e != EFEM_OK) return e;
+        RowWindow w;
+        w.row0 = 0;
+        w.n_rows = out->n_rows;  // capacity; the kernels read the real count on the device
+        w.own_base = 0;
+        w.out_base = 0;
+        w.e2d = p->e2d;
+        w.dyn = true;
+        w.cap_nnz = out->nnz;
+        if (out->n_rows == 0) {
+            if (forms & EFEM_PATTERN) EFEM_CUDA_TRY(cudaMemsetAsync(out->row_ptr, 0, 4, q));
+            return EFEM_OK;
+        }
+        return launch_rows_any(*p, forms, out, w, q);
+    };
+    // one CUDA graph for the whole call (captured on the plan's stream,
+    // replayed with event handshakes); re-captured when the outputs change
+    const bool same = p->g_async && p->async_forms == forms && !std::memcmp(&p->async_key, out, sizeof(efem_csr));
+    if (!same && p->g_async) {
+        cudaGraphExecDestroy(p->g_async);
+        p->g_async = nullptr;
+    }
+    if (!p->g_async && !p->graph_failed && !p->want_d2n && !debug_sync()) {
+        bool ok = p->gstream != nullptr;
+        if (!ok) {
+            ok = cudaStreamCreateWithFlags(&p->gstream, cudaStreamNonBlocking) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming) == cudaSuccess;
+        }
+        cudaGraph_t graph = nullptr;
+        if (ok && cudaStreamBeginCapture(p->gstream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            const int64_t l0 = g_launches.load();
+            const efem_status e = enqueue(p->gstream);
+            const cudaError_t ee = cudaStreamEndCapture(p->gstream, &graph);
+            p->async_launches = g_launches.load() - l0;
+            g_launches.fetch_sub(p->async_launches);  // counted at replay
+            if (e == EFEM_OK && ee == cudaSuccess && cudaGraphInstantiate(&p->g_async, graph, 0) == cudaSuccess) {
+                p->async_key = *out;
+                p->async_forms = forms;
+            } else {
+                p->g_async = nullptr;
+            }
+            if (graph) cudaGraphDestroy(graph);
+        }
+        cudaGetLastError();
+    }
+    if (p->g_async) {
+        EFEM_CUDA_TRY(cudaEventRecord(p->ev_in, s));
+        EFEM_CUDA_TRY(cudaStreamWaitEvent(p->gstream, p->ev_in, 0));
+        EFEM_CUDA_TRY(cudaGraphLaunch(p->g_async, p->gstream));
+        count_launch((int)p->async_launches);
+        EFEM_CUDA_TRY(cudaEventRecord(p->ev_out, p->gstream));
+        EFEM_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_out, 0));
         return EFEM_OK;
     }
-    return launch_rows_any(*p, forms, out, w, s);
+    return enqueue(s);
 }
 
 efem_status efem_assemble_host(efem_plan plan, const double* h_coords, const int32_t* h_elems, efem_csr* d_out,

@@ -103,6 +103,12 @@ struct Plan {
     cudaGraphExec_t g_enum = nullptr;
     bool graph_failed = false;
     int64_t graph_launches = 0;
+    // efem_assemble_async as one graph (enumeration + row kernel), keyed by
+    // the output arrays / capacities / forms it was captured for
+    cudaGraphExec_t g_async = nullptr;
+    int64_t async_launches = 0;
+    efem_csr async_key{};
+    unsigned async_forms = 0;
 
     // state
     bool enumerated = false, symbolic = false;
