@@ -40,7 +40,7 @@ std::atomic<int64_t> g_launches{0};
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-    size_t hdr, cnt, ent_cnt, bucket_ptr, bucket, bkey, binst, bx, nbr, e2d, inc_ptr, row_ptr, rec, d2n, ent_ptr, nnz_cnt, nnz_ptr, totals, cub, total;
+    size_t hdr, cnt, ent_cnt, bucket_ptr, bucket, bkey, binst, bx, nbr, e2d, inc_ptr, row_ptr, rec, d2n, ent_ptr, nnz_cnt, tiles, totals, cub, total;
 };
 
 Layout layout(const Plan& p, size_t cub_bytes) {
@@ -71,7 +71,7 @@ Layout layout(const Plan& p, size_t cub_bytes) {
     L.d2n = take((size_t)p.r_max * p.ek * 4);
     L.ent_ptr = take(N1 * 4);
     L.nnz_cnt = take(N1 * 4);
-    L.nnz_ptr = take(N1 * 4);
+    L.tiles = take(4 * ((size_t)p.n_nodes / 64 + 4) * 4);  // ent / nnz tile sums and prefixes
     L.totals = take(16);
     L.cub = take(cub_bytes);
     L.total = off;
@@ -404,7 +404,14 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     p->d2n = reinterpret_cast<int32_t*>(b + L.d2n);
     p->ent_ptr = reinterpret_cast<int32_t*>(b + L.ent_ptr);
     p->nnz_cnt = reinterpret_cast<int32_t*>(b + L.nnz_cnt);
-    p->nnz_ptr = reinterpret_cast<int32_t*>(b + L.nnz_ptr);
+    {
+        const size_t nt = (size_t)p->n_nodes / 64 + 4;
+        int32_t* tl = reinterpret_cast<int32_t*>(b + L.tiles);
+        p->ent_bsum = tl;
+        p->ent_bpre = tl + nt;
+        p->nnz_bsum = tl + 2 * nt;
+        p->nnz_bpre = tl + 3 * nt;
+    }
     p->d_totals = reinterpret_cast<int64_t*>(&p->hdr->totals[0]);
     p->cub_tmp = b + L.cub;
     p->enumerated = p->symbolic = false;

@@ -29,7 +29,8 @@
 //                        cycle, so L = t + [xor != 0] (BND_FLAG).  The numeric
 //                        kernel re-derives every row's column set and flags
 //                        a mismatch (non-manifold fans) as non-conforming.
-//   CUB scan(s)      -> ent_ptr (+ nnz_ptr for 3D edges)
+//   CUB scan(s) of the node tiles' totals (+ nnz totals for 3D edges);
+//                       k_node_write finishes ent_ptr with a CTA scan
 //   k_node_write     DOF ids, elems2dofs, inc_ptr, row records / row_ptr
 #include <cub/cub.cuh>
 
@@ -549,21 +550,25 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
                                                                   const int32_t* __restrict__ bucket_ptr,
                                                                   BucketArrays B, int32_t* __restrict__ bucket,
                                                                   int64_t n_nodes, int32_t* __restrict__ ent_cnt,
-                                                                  int32_t* __restrict__ nnz_cnt, int exact) {
+                                                                  int32_t* __restrict__ nnz_cnt, int exact,
+                                                                  int32_t* __restrict__ ent_bsum,
+                                                                  int32_t* __restrict__ nnz_bsum) {
     constexpr bool NE3 = KT::D == 3 && !KT::FACES;
     constexpr int TPB = NodeCaps<KT>::TPB;
     constexpr int DCAP = NodeCaps<KT>::DCAP;
+    using BlockReduce = cub::BlockReduce<int, TPB>;
+    __shared__ typename BlockReduce::TempStorage red_tmp;
     __shared__ uint64_t s_key[1];  // (the generic fallback sorts in global memory)
     __shared__ int s_inst[1];
     __shared__ int s_grp[NE3 ? 2 * DCAP * TPB : 1];
     __shared__ int s_cur[KT::FACES ? 16 * TPB : 1];
     const int64_t a64 = (int64_t)blockIdx.x * TPB + threadIdx.x;
-    if (a64 >= n_nodes) return;
+    int n_ent = 0, n_nnz = 0;
+    if (a64 < n_nodes) {
     const int a = (int)a64;
     const int64_t beg = __ldg(bucket_ptr + a);
     const int n = __ldg(bucket_ptr + a + 1) - (int)beg;
     int32_t* gb = bucket + beg;
-    int n_ent = 0, n_nnz = 0;
     constexpr int NREG = 8;
     if constexpr (KT::D == 2) {
         if (n <= NREG) {
@@ -611,6 +616,22 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
     }
     ent_cnt[a] = n_ent;
     if constexpr (NE3) nnz_cnt[a] = n_nnz;
+    }
+    // per-tile totals: the offsets come from a scan of these (one value per
+    // CTA, not per node), finished inside the write pass
+    const int et = BlockReduce(red_tmp).Sum(n_ent);
+    if constexpr (NE3) {
+        __syncthreads();
+        const int nt = BlockReduce(red_tmp).Sum(n_nnz);
+        if (threadIdx.x == 0) nnz_bsum[blockIdx.x] = nt;
+    }
+    if (threadIdx.x == 0) {
+        ent_bsum[blockIdx.x] = et;
+        if (blockIdx.x == 0) {  // the scans' trailing zero
+            ent_bsum[gridDim.x] = 0;
+            if (NE3) nnz_bsum[gridDim.x] = 0;
+        }
+    }
 }
 
 // Pass B: per node, walk its sorted bucket: DOF ids (ent_ptr[a] + run),
@@ -620,23 +641,40 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
 // instance (row i starts at i + (m-1) inc_ptr[i], closed form); 3D edges
 // write row_ptr.
 template <class KT>
-__global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ elems,
-                                                    const int32_t* __restrict__ bucket_ptr,
-                                                    const int32_t* __restrict__ bucket,
-                                                    const uint64_t* __restrict__ bkey,
-                                                    const int32_t* __restrict__ bx,
-                                                    const int32_t* __restrict__ ent_ptr,
-                                                    const int32_t* __restrict__ nnz_ptr, int64_t n_nodes,
-                                                    NodeOut out) {
+__global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t* __restrict__ elems,
+                                                                  const int32_t* __restrict__ bucket_ptr,
+                                                                  const int32_t* __restrict__ bucket,
+                                                                  const uint64_t* __restrict__ bkey,
+                                                                  const int32_t* __restrict__ bx,
+                                                                  const int32_t* __restrict__ ent_cnt,
+                                                                  const int32_t* __restrict__ nnz_cnt,
+                                                                  const int32_t* __restrict__ ent_bpre,
+                                                                  const int32_t* __restrict__ nnz_bpre,
+                                                                  int32_t* __restrict__ ent_ptr, int64_t n_nodes,
+                                                                  NodeOut out) {
     constexpr bool NE3 = KT::D == 3 && !KT::FACES;
-    const int64_t a64 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (a64 >= n_nodes) return;
+    constexpr int TPB = NodeCaps<KT>::TPB;  // the same node tiles as k_node_count
+    using BlockScan = cub::BlockScan<int, TPB>;
+    __shared__ typename BlockScan::TempStorage scan_tmp;
+    const int64_t a64 = (int64_t)blockIdx.x * TPB + threadIdx.x;
+    const bool live = a64 < n_nodes;
     const int a = (int)a64;
+    // node offsets: tile prefix (scanned tile totals) + scan within the tile
+    int e_off, z_off = 0;
+    BlockScan(scan_tmp).ExclusiveSum(live ? __ldg(ent_cnt + a) : 0, e_off);
+    e_off += __ldg(ent_bpre + blockIdx.x);
+    if constexpr (NE3) {
+        __syncthreads();
+        BlockScan(scan_tmp).ExclusiveSum(live ? __ldg(nnz_cnt + a) : 0, z_off);
+        z_off += __ldg(nnz_bpre + blockIdx.x);
+    }
+    if (!live) return;
+    ent_ptr[a] = e_off;
     const int beg = __ldg(bucket_ptr + a);
     const int n = __ldg(bucket_ptr + a + 1) - beg;
     const int32_t* gb = bucket + beg;
-    int id = __ldg(ent_ptr + a) - 1;
-    int nnz_run = NE3 ? __ldg(nnz_ptr + a) : 0;
+    int id = e_off - 1;
+    int nnz_run = z_off;
     int run0 = 0, first = 0, prev = 0, excess = 0;
     auto close_run = [&](int j_end) {
         const int t = j_end - run0;
@@ -697,6 +735,7 @@ __global__ void __launch_bounds__(256) k_node_write(const int32_t* __restrict__ 
     if (n > 0) close_run(n);
     if (a == n_nodes - 1) {
         const int R = id + 1;
+        ent_ptr[n_nodes] = R;
         out.inc_ptr[R] = beg + n;
         if (NE3) out.row_ptr[R] = nnz_run;
         out.totals[0] = R;
@@ -784,21 +823,23 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     // pass A: sort buckets, count entities / row entries per node (cnt reused
     // entity counts in ent_cnt; ent_cnt[N] = nnz_cnt[N] = 0 since the workspace was set)
     constexpr int TPB = NodeCaps<KT>::TPB;
-    k_node_count<KT><<<grid_for(N, TPB), TPB, 0, s>>>(p.elems, p.bucket_ptr, barr, p.bucket, N, p.ent_cnt,
-                                                      p.nnz_cnt, (int)p.exact_ne3);
+    const int nb = (int)grid_for(N, TPB);
+    k_node_count<KT><<<nb, TPB, 0, s>>>(p.elems, p.bucket_ptr, barr, p.bucket, N, p.ent_cnt, p.nnz_cnt,
+                                         (int)p.exact_ne3, p.ent_bsum, p.nnz_bsum);
     EFEM_LAUNCH_CHECK();
-    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.ent_cnt, p.ent_ptr, (int)(N + 1), s));
+    // scans over the CTA tiles' totals only (the write pass finishes per node)
+    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.ent_bsum, p.ent_bpre, nb + 1, s));
     count_launch(2);
     if constexpr (KT::D == 3 && !KT::FACES) {  // row lengths need a union only for 3D edges
-        EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.nnz_cnt, p.nnz_ptr, (int)(N + 1), s));
+        EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.nnz_bsum, p.nnz_bpre, nb + 1, s));
         count_launch(2);
     }
     // pass B: DOF ids, elems2dofs, incidence (+ row_ptr for 3D edges)
     int* d_flags = reinterpret_cast<int*>(reinterpret_cast<char*>(p.hdr) + offsetof(WsHeader, flags));
     NodeOut o{p.e2d, p.inc_ptr, p.row_ptr, p.want_d2n ? p.d2n : nullptr, p.nbr, p.rec, d_flags, p.bucket,
               p.d_totals};
-    k_node_write<KT><<<grid_for(N, 256), 256, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.bkey,
-                                                       p.exact_ne3 ? p.bx : nullptr, p.ent_ptr, p.nnz_ptr, N, o);
+    k_node_write<KT><<<nb, TPB, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.bkey, p.exact_ne3 ? p.bx : nullptr,
+                                         p.ent_cnt, p.nnz_cnt, p.ent_bpre, p.nnz_bpre, p.ent_ptr, N, o);
     EFEM_LAUNCH_CHECK();
     if constexpr (KT::D == 3 && !KT::FACES) {
         if (T > 0) {

@@ -85,7 +85,7 @@ struct Plan {
     int32_t* d2n = nullptr;         // r_max*ek (written only when want_d2n)
     int32_t* ent_ptr = nullptr;     // N+1 first DOF id of each node's entities
     int32_t* nnz_cnt = nullptr;     // N+1 CSR entries of each node's rows
-    int32_t* nnz_ptr = nullptr;     // N+1
+    int32_t *ent_bsum = nullptr, *ent_bpre = nullptr, *nnz_bsum = nullptr, *nnz_bpre = nullptr;  // per node tile
     int64_t* d_totals = nullptr;    // == hdr->totals
     bool want_d2n = false;
     bool exact_ne3 = false;  // NE0 3D: exact link counts (non-manifold meshes), efem_plan_set_exact
