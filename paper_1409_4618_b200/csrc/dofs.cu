@@ -294,8 +294,8 @@ __device__ __forceinline__ void node_sort_generic(const BucketArrays& B, int32_t
 // it; the numeric kernel sorts each row's tets by element id, so sums stay
 // in a fixed order.  Also per group: t, and the xor of its link edges
 // (BND_FLAG, see the file comment).  Writes the grouped instance words (RUN
-// flag on group starts) and b << 32 at every group start of the key array
-// (read by k_node_write).  Returns false when the node has more than DCAP
+// flag on group starts) and group q's b << 32 at key[q] (compact, so the
+// write-back is a sector or two per node; read by k_node_write).  Returns false when the node has more than DCAP
 // distinct larger neighbours (caller falls back to the generic sort).
 template <class KT>
 __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* __restrict__ gb, int64_t beg, int n,
@@ -393,7 +393,7 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
             const int st = S[q];
             const bool bnd = X[q * TPB] != 0;  // open link path: L = t + 1
             if (bnd) atomicOr(gb + st, (int)BND_FLAG);
-            B.key[beg + st] = (uint64_t)(uint32_t)D[q] << 32;
+            B.key[beg + q] = (uint64_t)(uint32_t)D[q] << 32;  // compact: group q's b
             nnz += 1 + 3 * C[q] + 2 * (int)bnd;
         }
     }
@@ -612,6 +612,10 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
             // (the NE3 instantiation has no key smem: sort in global memory)
             node_sort_generic<KT, false>(B, gb, beg, n, s_key, s_inst, n_ent);
             ne3_runs_exact<KT>(elems, gb, n, a, B.x + beg, n_nnz);
+            // the groups' b, compacted to the front of the key range (as the
+            // fast path leaves them; r <= j, so in place)
+            for (int j = 0, r = 0; j < n; ++j)
+                if (gb[j] < 0) B.key[beg + r++] = B.key[beg + j];
         }
     }
     ent_cnt[a] = n_ent;
@@ -675,7 +679,7 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
     const int32_t* gb = bucket + beg;
     int id = e_off - 1;
     int nnz_run = z_off;
-    int run0 = 0, first = 0, prev = 0, excess = 0;
+    int run0 = 0, first = 0, prev = 0, excess = 0, grp = 0;
     auto close_run = [&](int j_end) {
         const int t = j_end - run0;
         if constexpr (NE3) {
@@ -699,7 +703,7 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
                 // link excess L - t: the BND flag (0 / 1) on the manifold
                 // closed form, the exact count in exact mode
                 excess = bx ? __ldg(bx + beg + j) : (w & BND_FLAG ? 1 : 0);
-                const int b = (int)(__ldg(bkey + beg + j) >> 32);
+                const int b = (int)(__ldg(bkey + beg + grp++) >> 32);  // compacted by pass A
                 out.nbr[id] = b;
                 if (out.d2n) {
                     out.d2n[(int64_t)id * 2] = a;
