@@ -59,8 +59,8 @@ Layout layout(const Plan& p, size_t cub_bytes) {
     L.bucket_ptr = take(N1 * 4);
     L.bucket = take(Tm * 4);
     const bool faces = p.dim == 3 && p.element == EFEM_RT0;
-    L.bkey = take(Tm * 8);
-    L.binst = take(faces ? Tm * 4 : 4);
+    L.bkey = take(Tm * (p.dim == 3 ? 16 : 8));  // 3D: 16-byte {key, aux} records
+    L.binst = take(4);
     L.bx = take(p.dim == 3 && !faces ? Tm * 4 : 4);
     L.nbr = take(p.dim == 3 && !faces ? (size_t)p.r_max * 4 : 4);
     L.e2d = take(Tm * 4);

@@ -110,9 +110,14 @@ __device__ __forceinline__ int local_sign(const int (&g)[KT::NV], int k) {
 // ---------------------------------------------------------------------------------
 struct BucketArrays {
     uint64_t* key;  // edges: other node << 32 | inst; faces: mid << 32 | hi
-    int32_t* inst;  // faces only: e << 3 | k
-    int32_t* x;     // 3D edges only: xor of the tet's four vertex ids
+    int32_t* inst;  // (unused: 3D records carry it)
+    int32_t* x;     // 3D edges, exact mode: the runs' link excess
 };
+// 2D: one u64 key per instance.  3D: a 16-byte record {key, aux} per
+// instance (aux = e << 3 | k for faces, the xor of the tet's four vertex ids
+// for edges), so the scattered fill issues one store per instance.
+template <class KT>
+constexpr int KS = KT::D == 3 ? 2 : 1;  // key stride in u64 words
 
 template <class KT, bool FILL>
 __global__ void __launch_bounds__(256) k_bucket(const int32_t* __restrict__ elems, int64_t n_elems, int64_t n_nodes,
@@ -168,11 +173,14 @@ __global__ void __launch_bounds__(256) k_bucket(const int32_t* __restrict__ elem
             const int64_t pos = (int64_t)__ldg(bucket_ptr + amin[k]) + base;
             const int inst = (int)((e << 3) | k);
             if constexpr (KT::FACES) {
-                B.key[pos] = entity_key<KT>(g, k);
-                B.inst[pos] = inst;
+                reinterpret_cast<ulonglong2*>(B.key)[pos] =
+                    make_ulonglong2(entity_key<KT>(g, k), (unsigned long long)(uint32_t)inst);
+            } else if constexpr (KT::D == 3) {
+                reinterpret_cast<ulonglong2*>(B.key)[pos] =
+                    make_ulonglong2((entity_key<KT>(g, k) << 32) | (uint32_t)inst,
+                                    (unsigned long long)(uint32_t)(g[0] ^ g[1] ^ g[2] ^ g[3]));
             } else {
                 B.key[pos] = (entity_key<KT>(g, k) << 32) | (uint32_t)inst;
-                if constexpr (KT::D == 3) B.x[pos] = g[0] ^ g[1] ^ g[2] ^ g[3];
             }
         }
     }
@@ -228,8 +236,8 @@ struct Item {
 template <class KT>
 __device__ __forceinline__ Item<KT> load_item(const BucketArrays& B, int64_t pos) {
     Item<KT> it;
-    it.key = B.key[pos];
-    if constexpr (KT::FACES) it.inst = B.inst[pos];
+    it.key = B.key[pos * KS<KT>];
+    if constexpr (KT::FACES) it.inst = (int)(uint32_t)B.key[pos * KS<KT> + 1];
     else it.inst = (int)(uint32_t)it.key;
     return it;
 }
@@ -259,8 +267,8 @@ __device__ __forceinline__ void node_sort_generic(const BucketArrays& B, int32_t
             K[j * TPB] = it.key;
             if constexpr (KT::FACES) V[j * TPB] = it.inst;
         } else {
-            B.key[beg + j] = it.key;
-            if constexpr (KT::FACES) B.inst[beg + j] = it.inst;
+            B.key[(beg + j) * KS<KT>] = it.key;
+            if constexpr (KT::FACES) B.key[(beg + j) * KS<KT> + 1] = (uint32_t)it.inst;
         }
     };
     if (in_smem) {
@@ -308,8 +316,7 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
     constexpr int DC = NodeCaps<KT>::DCAP;
     int* Cur = s_grp + threadIdx.x;  // [p * TPB]: running cursor of group p
     int* X = Cur + DC * TPB;         // xor of link edges of group p
-    const uint64_t* __restrict__ key = B.key + beg;
-    const int32_t* __restrict__ xr = B.x + beg;
+    const ulonglong2* __restrict__ rec = reinterpret_cast<const ulonglong2*>(B.key) + beg;
     int D[DC], C[DC];
 #pragma unroll
     for (int q = 0; q < DC; ++q) {
@@ -322,7 +329,7 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
     for (int j0 = 0; j0 < n; j0 += U) {
         int bb[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) bb[u] = j0 + u < n ? (int)(__ldg(key + j0 + u) >> 32) : -1;
+        for (int u = 0; u < U; ++u) bb[u] = j0 + u < n ? (int)(__ldg(&rec[j0 + u].x) >> 32) : -1;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int b = bb[u];
@@ -368,8 +375,9 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
         int xx[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            kk[u] = j0 + u < n ? __ldg(key + j0 + u) : 0ull;
-            xx[u] = j0 + u < n ? __ldg(xr + j0 + u) : 0;
+            const ulonglong2 r = j0 + u < n ? __ldg(rec + j0 + u) : make_ulonglong2(0ull, 0ull);
+            kk[u] = r.x;
+            xx[u] = (int)(uint32_t)r.y;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -393,7 +401,7 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
             const int st = S[q];
             const bool bnd = X[q * TPB] != 0;  // open link path: L = t + 1
             if (bnd) atomicOr(gb + st, (int)BND_FLAG);
-            B.key[beg + q] = (uint64_t)(uint32_t)D[q] << 32;  // compact: group q's b
+            B.key[(beg + q) * 2] = (uint64_t)(uint32_t)D[q] << 32;  // compact: group q's b
             nnz += 1 + 3 * C[q] + 2 * (int)bnd;
         }
     }
@@ -412,8 +420,7 @@ __device__ __forceinline__ bool node_group_faces(const BucketArrays& B, int32_t*
     constexpr int TPB = NodeCaps<KT>::TPB;
     constexpr int FDC = 16;
     int* Cur = s_cur + threadIdx.x;  // [p * TPB]
-    const uint64_t* __restrict__ key = B.key + beg;
-    const int32_t* __restrict__ ins = B.inst + beg;
+    const ulonglong2* __restrict__ rec = reinterpret_cast<const ulonglong2*>(B.key) + beg;
     uint64_t D[FDC];
     int C[FDC];
 #pragma unroll
@@ -427,7 +434,7 @@ __device__ __forceinline__ bool node_group_faces(const BucketArrays& B, int32_t*
     for (int j0 = 0; j0 < n; j0 += U) {
         uint64_t kk[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) kk[u] = j0 + u < n ? __ldg(key + j0 + u) : ~0ull;
+        for (int u = 0; u < U; ++u) kk[u] = j0 + u < n ? __ldg(&rec[j0 + u].x) : ~0ull;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (j0 + u >= n) continue;
@@ -470,8 +477,9 @@ __device__ __forceinline__ bool node_group_faces(const BucketArrays& B, int32_t*
         int ii[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            kk[u] = j0 + u < n ? __ldg(key + j0 + u) : 0ull;
-            ii[u] = j0 + u < n ? __ldg(ins + j0 + u) : 0;
+            const ulonglong2 r = j0 + u < n ? __ldg(rec + j0 + u) : make_ulonglong2(0ull, 0ull);
+            kk[u] = r.x;
+            ii[u] = (int)(uint32_t)r.y;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -615,7 +623,7 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
             // the groups' b, compacted to the front of the key range (as the
             // fast path leaves them; r <= j, so in place)
             for (int j = 0, r = 0; j < n; ++j)
-                if (gb[j] < 0) B.key[beg + r++] = B.key[beg + j];
+                if (gb[j] < 0) B.key[(beg + r++) * 2] = B.key[(beg + j) * 2];
         }
     }
     ent_cnt[a] = n_ent;
@@ -703,7 +711,7 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
                 // link excess L - t: the BND flag (0 / 1) on the manifold
                 // closed form, the exact count in exact mode
                 excess = bx ? __ldg(bx + beg + j) : (w & BND_FLAG ? 1 : 0);
-                const int b = (int)(__ldg(bkey + beg + grp++) >> 32);  // compacted by pass A
+                const int b = (int)(__ldg(bkey + (beg + grp++) * 2) >> 32);  // compacted by pass A
                 out.nbr[id] = b;
                 if (out.d2n) {
                     out.d2n[(int64_t)id * 2] = a;
