@@ -302,8 +302,8 @@ __device__ __forceinline__ void node_sort_generic(const BucketArrays& B, int32_t
 // it; the numeric kernel sorts each row's tets by element id, so sums stay
 // in a fixed order.  Also per group: t, and the xor of its link edges
 // (BND_FLAG, see the file comment).  Writes the grouped instance words (RUN
-// flag on group starts) and group q's b << 32 at key[q] (compact, so the
-// write-back is a sector or two per node; read by k_node_write).  Returns false when the node has more than DCAP
+// flag on group starts) and group q's b at x[q] (compact, so the write-back
+// is a sector or two per node; read by k_node_write).  Returns false when the node has more than DCAP
 // distinct larger neighbours (caller falls back to the generic sort).
 template <class KT>
 __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* __restrict__ gb, int64_t beg, int n,
@@ -401,7 +401,7 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
             const int st = S[q];
             const bool bnd = X[q * TPB] != 0;  // open link path: L = t + 1
             if (bnd) atomicOr(gb + st, (int)BND_FLAG);
-            B.key[(beg + q) * 2] = (uint64_t)(uint32_t)D[q] << 32;  // compact: group q's b
+            B.x[beg + q] = D[q];  // compact: group q's b (the x words are consumed)
             nnz += 1 + 3 * C[q] + 2 * (int)bnd;
         }
     }
@@ -620,10 +620,15 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
             // (the NE3 instantiation has no key smem: sort in global memory)
             node_sort_generic<KT, false>(B, gb, beg, n, s_key, s_inst, n_ent);
             ne3_runs_exact<KT>(elems, gb, n, a, B.x + beg, n_nnz);
-            // the groups' b, compacted to the front of the key range (as the
-            // fast path leaves them; r <= j, so in place)
+            // the groups' b, compacted to the front of the range (as the fast
+            // path leaves them; r <= j, so in place): in x, unless exact mode
+            // keeps its excess counts there (then in the key records)
             for (int j = 0, r = 0; j < n; ++j)
-                if (gb[j] < 0) B.key[(beg + r++) * 2] = B.key[(beg + j) * 2];
+                if (gb[j] < 0) {
+                    const uint64_t kb = B.key[(beg + j) * 2];
+                    if (exact) B.key[(beg + r++) * 2] = kb;
+                    else B.x[beg + r++] = (int)(kb >> 32);
+                }
         }
     }
     ent_cnt[a] = n_ent;
@@ -658,6 +663,7 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
                                                                   const int32_t* __restrict__ bucket,
                                                                   const uint64_t* __restrict__ bkey,
                                                                   const int32_t* __restrict__ bx,
+                                                                  const int32_t* __restrict__ bnb,
                                                                   const int32_t* __restrict__ ent_cnt,
                                                                   const int32_t* __restrict__ nnz_cnt,
                                                                   const int32_t* __restrict__ ent_bpre,
@@ -711,7 +717,9 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
                 // link excess L - t: the BND flag (0 / 1) on the manifold
                 // closed form, the exact count in exact mode
                 excess = bx ? __ldg(bx + beg + j) : (w & BND_FLAG ? 1 : 0);
-                const int b = (int)(__ldg(bkey + (beg + grp++) * 2) >> 32);  // compacted by pass A
+                // b, compacted by pass A
+                const int b = bx ? (int)(__ldg(bkey + (beg + grp) * 2) >> 32) : __ldg(bnb + beg + grp);
+                ++grp;
                 out.nbr[id] = b;
                 if (out.d2n) {
                     out.d2n[(int64_t)id * 2] = a;
@@ -850,7 +858,7 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     int* d_flags = reinterpret_cast<int*>(reinterpret_cast<char*>(p.hdr) + offsetof(WsHeader, flags));
     NodeOut o{p.e2d, p.inc_ptr, p.row_ptr, p.want_d2n ? p.d2n : nullptr, p.nbr, p.rec, d_flags, p.bucket,
               p.d_totals};
-    k_node_write<KT><<<nb, TPB, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.bkey, p.exact_ne3 ? p.bx : nullptr,
+    k_node_write<KT><<<nb, TPB, 0, s>>>(p.elems, p.bucket_ptr, p.bucket, p.bkey, p.exact_ne3 ? p.bx : nullptr, p.bx,
                                          p.ent_cnt, p.nnz_cnt, p.ent_bpre, p.nnz_bpre, p.ent_ptr, N, o);
     EFEM_LAUNCH_CHECK();
     if constexpr (KT::D == 3 && !KT::FACES) {
