@@ -582,7 +582,11 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
                                 srt[y] = asc ? hi : lo;
                             }
                         }
-                const int last = srt[max(min(t, NE3_TMAX) - 1, 0)];
+                // (a select chain, not srt[t - 1]: a dynamic index would put
+                // srt in local memory)
+                int last = srt[0];
+#pragma unroll
+                for (int j = 1; j < NE3_TMAX; ++j) last = j == t - 1 ? srt[j] : last;
 #pragma unroll
                 for (int j = 0; j < NE3_TMAX; ++j) inst[j] = j < t ? srt[j] : last;
             }
