@@ -492,6 +492,222 @@ __device__ __forceinline__ int pair_index(int p, int q, int nw) {  // p < q
     return p * nw - ((p * (p + 1)) >> 1) + (q - p - 1);
 }
 
+// The fast path of one row (see above).  SM: the accumulators are the
+// CTA's shared staging columns (stride NE3_LD), so every accumulator access
+// is a shared-memory instruction; otherwise they are the row's CSR segment
+// in global memory (stride 1, an oversize row in the tile).
+template <class KT, bool SM>
+__device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, const int32_t* __restrict__ elems,
+                                             const int32_t* __restrict__ inc, const int32_t* __restrict__ e2d,
+                                             int own_base, int i, int ib, int t, int rlen, unsigned char* P,
+                                             int* ccol, double* cvm, double* cvk, WsHeader* hdr, bool& ok,
+                                             bool& done) {
+    constexpr int st = SM ? NE3_LD : 1;
+    uint32_t key[16];
+    int inst[NE3_TMAX], roles[NE3_TMAX];
+    int a = 0, b = 0;
+    // all index loads first, then all element loads: two round trips
+    // (slots j >= t repeat the last incidence and are masked below)
+#pragma unroll
+    for (int j = 0; j < NE3_TMAX; ++j) inst[j] = __ldg(inc + ib + min(j, t - 1)) & INST_MASK;
+    {   // ascending element id (the symbolic pass groups a node's tets
+        // by edge without ordering them): a fixed summation order
+        int srt[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) srt[j] = j < t && j < NE3_TMAX ? inst[j] : INT_MAX;
+#pragma unroll
+        for (int kk = 2; kk <= 8; kk <<= 1)
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    const int y = x ^ jj;
+                    if (y > x) {
+                        const int lo = min(srt[x], srt[y]), hi = max(srt[x], srt[y]);
+                        const bool asc = (x & kk) == 0;
+                        srt[x] = asc ? lo : hi;
+                        srt[y] = asc ? hi : lo;
+                    }
+                }
+        // (a select chain, not srt[t - 1]: a dynamic index would put
+        // srt in local memory)
+        int last = srt[0];
+#pragma unroll
+        for (int j = 1; j < NE3_TMAX; ++j) last = j == t - 1 ? srt[j] : last;
+#pragma unroll
+        for (int j = 0; j < NE3_TMAX; ++j) inst[j] = j < t ? srt[j] : last;
+    }
+    int4 gq[NE3_TMAX];
+#pragma unroll
+    for (int j = 0; j < NE3_TMAX; ++j) gq[j] = __ldg(reinterpret_cast<const int4*>(elems) + (inst[j] >> 3));
+#pragma unroll
+    for (int j = 0; j < NE3_TMAX; ++j) {
+        const int pe = inst[j];
+        const int k = pe & 7;
+        const int g[4] = {gq[j].x, gq[j].y, gq[j].z, gq[j].w};
+        const int s0 = k < 3 ? 0 : (k == 3 ? 1 : (k == 4 ? 2 : 3));
+        const int s1 = k < 3 ? k + 1 : (k == 3 ? 2 : (k == 4 ? 3 : 1));
+        const int lc = k == 0 ? 2 : (k == 1 ? 1 : (k == 2 ? 1 : 0));
+        const int ld = k == 0 ? 3 : (k == 1 ? 3 : (k == 2 ? 2 : (k == 3 ? 3 : (k == 4 ? 1 : 2))));
+        const int g0 = sel4(g, s0), g1 = sel4(g, s1);
+        const int la = g0 < g1 ? s0 : s1, lb = g0 < g1 ? s1 : s0;
+        if (j == 0) {
+            a = min(g0, g1);
+            b = max(g0, g1);
+        }
+        // local vertex of each role (a, b, c, d), 2 bits each
+        roles[j] = la | (lb << 2) | (lc << 4) | (ld << 6);
+        const bool live = j < t;
+        key[2 * j] = live ? (((uint32_t)sel4(g, lc) << 5) | (uint32_t)(2 * j)) : 0xffffffffu;
+        key[2 * j + 1] = live ? (((uint32_t)sel4(g, ld) << 5) | (uint32_t)(2 * j + 1)) : 0xffffffffu;
+    }
+    key[14] = ((uint32_t)a << 5) | 14u;
+    key[15] = ((uint32_t)b << 5) | 15u;
+#pragma unroll
+    for (int kk = 2; kk <= 16; kk <<= 1)
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+            for (int x = 0; x < 16; ++x) {
+                const int y = x ^ jj;
+                if (y > x) {
+                    const uint32_t lo = min(key[x], key[y]), hi = max(key[x], key[y]);
+                    const bool asc = (x & kk) == 0;
+                    key[x] = asc ? lo : hi;
+                    key[y] = asc ? hi : lo;
+                }
+            }
+    int rk = -1;
+    uint32_t prev = 0xffffffffu;
+#pragma unroll
+    for (int x = 0; x < 16; ++x) {
+        if (key[x] != 0xffffffffu) {
+            const uint32_t v = key[x] >> 5;
+            rk += v != prev;
+            prev = v;
+            P[(key[x] & 31u) * NUM_TPB] = (unsigned char)rk;
+        }
+    }
+    const int nw = rk + 1;
+    if (nw <= 11) {
+        const int pa = P[14 * NUM_TPB], pb = P[15 * NUM_TPB];
+        const int iab = pair_index(pa, pb, nw);
+        // column mask over lexicographic pairs of W positions
+        unsigned long long mask = 1ull << iab;
+        int pidx[NE3_TMAX];  // packed pair indices: ac | ad << 6 | bc << 12 | bd << 18 | cd << 24
+#pragma unroll
+        for (int j = 0; j < NE3_TMAX; ++j) {
+            if (j < t) {
+                const int pc = P[(2 * j) * NUM_TPB], pd = P[(2 * j + 1) * NUM_TPB];
+                const int iac = pair_index(min(pa, pc), max(pa, pc), nw);
+                const int iad = pair_index(min(pa, pd), max(pa, pd), nw);
+                const int ibc = pair_index(min(pb, pc), max(pb, pc), nw);
+                const int ibd = pair_index(min(pb, pd), max(pb, pd), nw);
+                const int icd = pair_index(min(pc, pd), max(pc, pd), nw);
+                mask |= (1ull << iac) | (1ull << iad) | (1ull << ibc) | (1ull << ibd) | (1ull << icd);
+                pidx[j] = iac | (iad << 6) | (ibc << 12) | (ibd << 18) | (icd << 24);
+            }
+        }
+        ok = __popcll(mask) == rlen;
+        done = true;
+        if (ok) {
+            for (int q = 0; q < rlen; ++q) {
+                cvm[q * st] = 0.0;
+                cvk[q * st] = 0.0;
+            }
+            const int sab = __popcll(mask & ((1ull << iab) - 1ull));
+            // role frame: vertices ordered (a, b, c, d), a < b the row's
+            // edge.  The globally oriented Whitney basis of edge {x, y}
+            // is sigma_xy (l_x grad l_y - l_y grad l_x), sigma_xy = +1
+            // iff x < y, which is exactly s_k times the paper's mapped
+            // local basis, so no other signs enter.
+            // With n_v the area normals (adjugate rows) and N_uv = n_u.n_v,
+            // G = N / det^2:
+            //   M_(ab)(pq) = |K|/20 [(1+d_ap)G_bq - (1+d_aq)G_bp - (1+d_bp)G_aq + (1+d_bq)G_ap]
+            //   K_(ab)(pq) = 4 |K| (G_ap G_bq - G_aq G_bp)
+            double xa[3], xb[3];
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                xa[cc] = __ldg(coords + a * 3 + cc);
+                xb[cc] = __ldg(coords + b * 3 + cc);
+            }
+#pragma unroll
+            for (int j = 0; j < NE3_TMAX; ++j) {
+                if (j < t) {
+                    const int e = inst[j] >> 3;
+                    const int rl = roles[j];
+                    const int la = rl & 3, lb = (rl >> 2) & 3, lc = (rl >> 4) & 3, ld = (rl >> 6) & 3;
+                    int g[4];
+                    load_g<KT>(elems, e, g);
+                    const int c = sel4(g, lc), d = sel4(g, ld);
+                    double e1[3], e2[3], e3[3];
+#pragma unroll
+                    for (int cc = 0; cc < 3; ++cc) {
+                        e1[cc] = xb[cc] - xa[cc];
+                        e2[cc] = __ldg(coords + c * 3 + cc) - xa[cc];
+                        e3[cc] = __ldg(coords + d * 3 + cc) - xa[cc];
+                    }
+                    const double nb[3] = {e2[1] * e3[2] - e2[2] * e3[1], e2[2] * e3[0] - e2[0] * e3[2],
+                                          e2[0] * e3[1] - e2[1] * e3[0]};
+                    const double nc[3] = {e3[1] * e1[2] - e3[2] * e1[1], e3[2] * e1[0] - e3[0] * e1[2],
+                                          e3[0] * e1[1] - e3[1] * e1[0]};
+                    const double nd[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                                          e1[0] * e2[1] - e1[1] * e2[0]};
+                    const double det = e1[0] * nb[0] + e1[1] * nb[1] + e1[2] * nb[2];
+                    if (!(det != 0.0) || !isfinite(det)) {
+                        atomicOr(&hdr->flags[F_DEGENERATE], 1);
+                        atomicMin(&hdr->bad_element, (unsigned long long)e);
+                    }
+                    const double na[3] = {-(nb[0] + nc[0] + nd[0]), -(nb[1] + nc[1] + nd[1]),
+                                          -(nb[2] + nc[2] + nd[2])};
+                    auto dot = [](const double* u, const double* v) { return u[0] * v[0] + u[1] * v[1] + u[2] * v[2]; };
+                    const double Naa = dot(na, na), Nbb = dot(nb, nb), Nab = dot(na, nb);
+                    const double Nac = dot(na, nc), Nad = dot(na, nd), Nbc = dot(nb, nc), Nbd = dot(nb, nd);
+                    const double rd = 1.0 / fabs(det);
+                    const double cm = rd * (1.0 / 120.0);
+                    const double ck = (2.0 / 3.0) * rd * rd * rd;
+                    // role columns ab ac ad bc bd cd
+                    const int pc = P[(2 * j) * NUM_TPB], pd = P[(2 * j + 1) * NUM_TPB];
+                    const double sac = pa < pc ? 1.0 : -1.0, sad = pa < pd ? 1.0 : -1.0;
+                    const double sbc = pb < pc ? 1.0 : -1.0, sbd = pb < pd ? 1.0 : -1.0;
+                    const double scd = pc < pd ? 1.0 : -1.0;
+                    const double vm[6] = {cm * (2.0 * (Naa + Nbb - Nab)),
+                                          sac * cm * (2.0 * Nbc - Nab - Nac + Naa),
+                                          sad * cm * (2.0 * Nbd - Nab - Nad + Naa),
+                                          sbc * cm * (Nbc - Nbb - 2.0 * Nac + Nab),
+                                          sbd * cm * (Nbd - Nbb - 2.0 * Nad + Nab),
+                                          scd * cm * (Nbd - Nbc - Nad + Nac)};
+                    const double vk[6] = {ck * (Naa * Nbb - Nab * Nab),
+                                          sac * ck * (Naa * Nbc - Nac * Nab),
+                                          sad * ck * (Naa * Nbd - Nad * Nab),
+                                          sbc * ck * (Nab * Nbc - Nac * Nbb),
+                                          sbd * ck * (Nab * Nbd - Nad * Nbb),
+                                          scd * ck * (Nac * Nbd - Nad * Nbc)};
+                    // local edge id of the role pairs -> DOF ids
+                    auto eid = [](int p, int q) {
+                        const int lo = min(p, q), hi = max(p, q);
+                        return lo == 0 ? hi - 1 : (lo == 1 ? (hi == 2 ? 3 : 5) : 4);
+                    };
+                    const int32_t* de = e2d + e * 6;
+                    const int dof[6] = {own_base + i, __ldg(de + eid(la, lc)), __ldg(de + eid(la, ld)),
+                                        __ldg(de + eid(lb, lc)), __ldg(de + eid(lb, ld)),
+                                        __ldg(de + eid(lc, ld))};
+                    const int pi = pidx[j];
+#pragma unroll
+                    for (int u = 0; u < 6; ++u) {
+                        const int slot =
+                            (u == 0 ? sab : __popcll(mask & ((1ull << ((pi >> (6 * (u - 1))) & 63)) - 1ull))) *
+                            st;
+                        ccol[slot] = dof[u];
+                        cvm[slot] += vm[u];
+                        cvk[slot] += vk[u];
+                    }
+                }
+            }
+        }
+    }
+}
+
 template <class KT>
 __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__ coords,
                                                       const int32_t* __restrict__ elems,
@@ -556,209 +772,12 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
         bool ok = false, done = false;
         if (fast_ids && t >= 1 && t <= NE3_TMAX) {
             unsigned char* P = s_pos + threadIdx.x;  // P[src * NUM_TPB]
-            uint32_t key[16];
-            int inst[NE3_TMAX], roles[NE3_TMAX];
-            int a = 0, b = 0;
-            // all index loads first, then all element loads: two round trips
-            // (slots j >= t repeat the last incidence and are masked below)
-#pragma unroll
-            for (int j = 0; j < NE3_TMAX; ++j) inst[j] = __ldg(inc + ib + min(j, t - 1)) & INST_MASK;
-            {   // ascending element id (the symbolic pass groups a node's tets
-                // by edge without ordering them): a fixed summation order
-                int srt[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) srt[j] = j < t && j < NE3_TMAX ? inst[j] : INT_MAX;
-#pragma unroll
-                for (int kk = 2; kk <= 8; kk <<= 1)
-#pragma unroll
-                    for (int jj = kk >> 1; jj > 0; jj >>= 1)
-#pragma unroll
-                        for (int x = 0; x < 8; ++x) {
-                            const int y = x ^ jj;
-                            if (y > x) {
-                                const int lo = min(srt[x], srt[y]), hi = max(srt[x], srt[y]);
-                                const bool asc = (x & kk) == 0;
-                                srt[x] = asc ? lo : hi;
-                                srt[y] = asc ? hi : lo;
-                            }
-                        }
-                // (a select chain, not srt[t - 1]: a dynamic index would put
-                // srt in local memory)
-                int last = srt[0];
-#pragma unroll
-                for (int j = 1; j < NE3_TMAX; ++j) last = j == t - 1 ? srt[j] : last;
-#pragma unroll
-                for (int j = 0; j < NE3_TMAX; ++j) inst[j] = j < t ? srt[j] : last;
-            }
-            int4 gq[NE3_TMAX];
-#pragma unroll
-            for (int j = 0; j < NE3_TMAX; ++j) gq[j] = __ldg(reinterpret_cast<const int4*>(elems) + (inst[j] >> 3));
-#pragma unroll
-            for (int j = 0; j < NE3_TMAX; ++j) {
-                const int pe = inst[j];
-                const int k = pe & 7;
-                const int g[4] = {gq[j].x, gq[j].y, gq[j].z, gq[j].w};
-                const int s0 = k < 3 ? 0 : (k == 3 ? 1 : (k == 4 ? 2 : 3));
-                const int s1 = k < 3 ? k + 1 : (k == 3 ? 2 : (k == 4 ? 3 : 1));
-                const int lc = k == 0 ? 2 : (k == 1 ? 1 : (k == 2 ? 1 : 0));
-                const int ld = k == 0 ? 3 : (k == 1 ? 3 : (k == 2 ? 2 : (k == 3 ? 3 : (k == 4 ? 1 : 2))));
-                const int g0 = sel4(g, s0), g1 = sel4(g, s1);
-                const int la = g0 < g1 ? s0 : s1, lb = g0 < g1 ? s1 : s0;
-                if (j == 0) {
-                    a = min(g0, g1);
-                    b = max(g0, g1);
-                }
-                // local vertex of each role (a, b, c, d), 2 bits each
-                roles[j] = la | (lb << 2) | (lc << 4) | (ld << 6);
-                const bool live = j < t;
-                key[2 * j] = live ? (((uint32_t)sel4(g, lc) << 5) | (uint32_t)(2 * j)) : 0xffffffffu;
-                key[2 * j + 1] = live ? (((uint32_t)sel4(g, ld) << 5) | (uint32_t)(2 * j + 1)) : 0xffffffffu;
-            }
-            key[14] = ((uint32_t)a << 5) | 14u;
-            key[15] = ((uint32_t)b << 5) | 15u;
-#pragma unroll
-            for (int kk = 2; kk <= 16; kk <<= 1)
-#pragma unroll
-                for (int jj = kk >> 1; jj > 0; jj >>= 1)
-#pragma unroll
-                    for (int x = 0; x < 16; ++x) {
-                        const int y = x ^ jj;
-                        if (y > x) {
-                            const uint32_t lo = min(key[x], key[y]), hi = max(key[x], key[y]);
-                            const bool asc = (x & kk) == 0;
-                            key[x] = asc ? lo : hi;
-                            key[y] = asc ? hi : lo;
-                        }
-                    }
-            int rk = -1;
-            uint32_t prev = 0xffffffffu;
-#pragma unroll
-            for (int x = 0; x < 16; ++x) {
-                if (key[x] != 0xffffffffu) {
-                    const uint32_t v = key[x] >> 5;
-                    rk += v != prev;
-                    prev = v;
-                    P[(key[x] & 31u) * NUM_TPB] = (unsigned char)rk;
-                }
-            }
-            const int nw = rk + 1;
-            if (nw <= 11) {
-                const int pa = P[14 * NUM_TPB], pb = P[15 * NUM_TPB];
-                const int iab = pair_index(pa, pb, nw);
-                // column mask over lexicographic pairs of W positions
-                unsigned long long mask = 1ull << iab;
-                int pidx[NE3_TMAX];  // packed pair indices: ac | ad << 6 | bc << 12 | bd << 18 | cd << 24
-#pragma unroll
-                for (int j = 0; j < NE3_TMAX; ++j) {
-                    if (j < t) {
-                        const int pc = P[(2 * j) * NUM_TPB], pd = P[(2 * j + 1) * NUM_TPB];
-                        const int iac = pair_index(min(pa, pc), max(pa, pc), nw);
-                        const int iad = pair_index(min(pa, pd), max(pa, pd), nw);
-                        const int ibc = pair_index(min(pb, pc), max(pb, pc), nw);
-                        const int ibd = pair_index(min(pb, pd), max(pb, pd), nw);
-                        const int icd = pair_index(min(pc, pd), max(pc, pd), nw);
-                        mask |= (1ull << iac) | (1ull << iad) | (1ull << ibc) | (1ull << ibd) | (1ull << icd);
-                        pidx[j] = iac | (iad << 6) | (ibc << 12) | (ibd << 18) | (icd << 24);
-                    }
-                }
-                ok = __popcll(mask) == rlen;
-                done = true;
-                if (ok) {
-                    for (int q = 0; q < rlen; ++q) {
-                        cvm[q * st] = 0.0;
-                        cvk[q * st] = 0.0;
-                    }
-                    const int sab = __popcll(mask & ((1ull << iab) - 1ull));
-                    // role frame: vertices ordered (a, b, c, d), a < b the row's
-                    // edge.  The globally oriented Whitney basis of edge {x, y}
-                    // is sigma_xy (l_x grad l_y - l_y grad l_x), sigma_xy = +1
-                    // iff x < y, which is exactly s_k times the paper's mapped
-                    // local basis, so no other signs enter.
-                    // With n_v the area normals (adjugate rows) and N_uv = n_u.n_v,
-                    // G = N / det^2:
-                    //   M_(ab)(pq) = |K|/20 [(1+d_ap)G_bq - (1+d_aq)G_bp - (1+d_bp)G_aq + (1+d_bq)G_ap]
-                    //   K_(ab)(pq) = 4 |K| (G_ap G_bq - G_aq G_bp)
-                    double xa[3], xb[3];
-#pragma unroll
-                    for (int cc = 0; cc < 3; ++cc) {
-                        xa[cc] = __ldg(coords + a * 3 + cc);
-                        xb[cc] = __ldg(coords + b * 3 + cc);
-                    }
-#pragma unroll
-                    for (int j = 0; j < NE3_TMAX; ++j) {
-                        if (j < t) {
-                            const int e = inst[j] >> 3;
-                            const int rl = roles[j];
-                            const int la = rl & 3, lb = (rl >> 2) & 3, lc = (rl >> 4) & 3, ld = (rl >> 6) & 3;
-                            int g[4];
-                            load_g<KT>(elems, e, g);
-                            const int c = sel4(g, lc), d = sel4(g, ld);
-                            double e1[3], e2[3], e3[3];
-#pragma unroll
-                            for (int cc = 0; cc < 3; ++cc) {
-                                e1[cc] = xb[cc] - xa[cc];
-                                e2[cc] = __ldg(coords + c * 3 + cc) - xa[cc];
-                                e3[cc] = __ldg(coords + d * 3 + cc) - xa[cc];
-                            }
-                            const double nb[3] = {e2[1] * e3[2] - e2[2] * e3[1], e2[2] * e3[0] - e2[0] * e3[2],
-                                                  e2[0] * e3[1] - e2[1] * e3[0]};
-                            const double nc[3] = {e3[1] * e1[2] - e3[2] * e1[1], e3[2] * e1[0] - e3[0] * e1[2],
-                                                  e3[0] * e1[1] - e3[1] * e1[0]};
-                            const double nd[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
-                                                  e1[0] * e2[1] - e1[1] * e2[0]};
-                            const double det = e1[0] * nb[0] + e1[1] * nb[1] + e1[2] * nb[2];
-                            if (!(det != 0.0) || !isfinite(det)) {
-                                atomicOr(&hdr->flags[F_DEGENERATE], 1);
-                                atomicMin(&hdr->bad_element, (unsigned long long)e);
-                            }
-                            const double na[3] = {-(nb[0] + nc[0] + nd[0]), -(nb[1] + nc[1] + nd[1]),
-                                                  -(nb[2] + nc[2] + nd[2])};
-                            auto dot = [](const double* u, const double* v) { return u[0] * v[0] + u[1] * v[1] + u[2] * v[2]; };
-                            const double Naa = dot(na, na), Nbb = dot(nb, nb), Nab = dot(na, nb);
-                            const double Nac = dot(na, nc), Nad = dot(na, nd), Nbc = dot(nb, nc), Nbd = dot(nb, nd);
-                            const double rd = 1.0 / fabs(det);
-                            const double cm = rd * (1.0 / 120.0);
-                            const double ck = (2.0 / 3.0) * rd * rd * rd;
-                            // role columns ab ac ad bc bd cd
-                            const int pc = P[(2 * j) * NUM_TPB], pd = P[(2 * j + 1) * NUM_TPB];
-                            const double sac = pa < pc ? 1.0 : -1.0, sad = pa < pd ? 1.0 : -1.0;
-                            const double sbc = pb < pc ? 1.0 : -1.0, sbd = pb < pd ? 1.0 : -1.0;
-                            const double scd = pc < pd ? 1.0 : -1.0;
-                            const double vm[6] = {cm * (2.0 * (Naa + Nbb - Nab)),
-                                                  sac * cm * (2.0 * Nbc - Nab - Nac + Naa),
-                                                  sad * cm * (2.0 * Nbd - Nab - Nad + Naa),
-                                                  sbc * cm * (Nbc - Nbb - 2.0 * Nac + Nab),
-                                                  sbd * cm * (Nbd - Nbb - 2.0 * Nad + Nab),
-                                                  scd * cm * (Nbd - Nbc - Nad + Nac)};
-                            const double vk[6] = {ck * (Naa * Nbb - Nab * Nab),
-                                                  sac * ck * (Naa * Nbc - Nac * Nab),
-                                                  sad * ck * (Naa * Nbd - Nad * Nab),
-                                                  sbc * ck * (Nab * Nbc - Nac * Nbb),
-                                                  sbd * ck * (Nab * Nbd - Nad * Nbb),
-                                                  scd * ck * (Nac * Nbd - Nad * Nbc)};
-                            // local edge id of the role pairs -> DOF ids
-                            auto eid = [](int p, int q) {
-                                const int lo = min(p, q), hi = max(p, q);
-                                return lo == 0 ? hi - 1 : (lo == 1 ? (hi == 2 ? 3 : 5) : 4);
-                            };
-                            const int32_t* de = e2d + e * 6;
-                            const int dof[6] = {own_base + i, __ldg(de + eid(la, lc)), __ldg(de + eid(la, ld)),
-                                                __ldg(de + eid(lb, lc)), __ldg(de + eid(lb, ld)),
-                                                __ldg(de + eid(lc, ld))};
-                            const int pi = pidx[j];
-#pragma unroll
-                            for (int u = 0; u < 6; ++u) {
-                                const int slot =
-                                    (u == 0 ? sab : __popcll(mask & ((1ull << ((pi >> (6 * (u - 1))) & 63)) - 1ull))) *
-                                    st;
-                                ccol[slot] = dof[u];
-                                cvm[slot] += vm[u];
-                                cvk[slot] += vk[u];
-                            }
-                        }
-                    }
-                }
-            }
+            if (staged)
+                ne3_fast_row<KT, true>(coords, elems, inc, e2d, own_base, i, ib, t, rlen, P, s_col + threadIdx.x,
+                                       s_vm + threadIdx.x, s_vk + threadIdx.x, hdr, ok, done);
+            else
+                ne3_fast_row<KT, false>(coords, elems, inc, e2d, own_base, i, ib, t, rlen, P, ccol, cvm, cvk, hdr,
+                                        ok, done);
         }
         if (!done) ok = row_generic<KT>(coords, elems, inc, e2d, ib, t, rlen, ccol, cvm, cvk, st, hdr);
         if (!ok) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
