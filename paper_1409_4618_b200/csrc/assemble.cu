@@ -611,9 +611,18 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
         ok = __popcll(mask) == rlen;
         done = true;
         if (ok) {
-            for (int q = 0; q < rlen; ++q) {
-                cvm[q * st] = 0.0;
-                cvk[q * st] = 0.0;
+            if constexpr (SM) {  // rlen <= NE3_SLOTS when staged: predicated, no loop
+#pragma unroll
+                for (int q = 0; q < NE3_SLOTS; ++q)
+                    if (q < rlen) {
+                        cvm[q * st] = 0.0;
+                        cvk[q * st] = 0.0;
+                    }
+            } else {
+                for (int q = 0; q < rlen; ++q) {
+                    cvm[q * st] = 0.0;
+                    cvk[q * st] = 0.0;
+                }
             }
             const int sab = __popcll(mask & ((1ull << iab) - 1ull));
             // role frame: vertices ordered (a, b, c, d), a < b the row's
@@ -783,7 +792,9 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
         if (!ok) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
         if (staged) {
             const int off = s_off[threadIdx.x];
-            for (int q = 0; q < rlen; ++q) s_map[off + q] = (unsigned short)(q * NE3_LD + threadIdx.x);
+#pragma unroll
+            for (int q = 0; q < NE3_SLOTS; ++q)
+                if (q < rlen) s_map[off + q] = (unsigned short)(q * NE3_LD + threadIdx.x);
         }
     }
     if (!staged) return;
