@@ -13,6 +13,7 @@ See DESIGN.md "Measurement" for the roofline bytes and the oracle baseline.
 from __future__ import annotations
 
 import argparse
+import math
 import json
 import os
 import subprocess
@@ -160,7 +161,7 @@ def run_reference(args, cfg):
     value = ts * args.steps / sum(ts / v["value"] for v in vals)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": cfg["name"], "element": ELEMENT_NAMES[cfg["element"]],
                                             "dim": cfg["dim"], "n": cfg["n"], "jitter": cfg["alpha"],
                                             "seed": cfg["seed"], "sample_elems": ts},
@@ -256,7 +257,7 @@ def run_efem(args, cfg):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["name"], "element": ELEMENT_NAMES[cfg["element"]], "dim": cfg["dim"],
                    "n": cfg["n"], "jitter": cfg["alpha"], "seed": cfg["seed"], "n_elems": T,
@@ -332,9 +333,11 @@ def run_efem_dist(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": cfg["name"], "element": ELEMENT_NAMES[cfg["element"]], "dim": cfg["dim"],
                        "n": cfg["n"], "jitter": cfg["alpha"], "seed": cfg["seed"], "n_elems": T,
+                       "elems_per_rank": T / ws,
                        "parallelism": f"row-owned node ranges x{ws} ({backend})",
                        "l2": "flushed between timed steps (512 MiB write)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
@@ -356,13 +359,22 @@ def main():
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=None, choices=sorted(CONFIGS),
-                    help="BASELINE config; default: 2 (configs[1]) at N=1, 5 (the scaling sweep) at N>1")
+                    help="BASELINE config (fixed mesh; at N>1 strong scaling).  Default: 2 (configs[1]); at "
+                         "N>1 config 2 weak-scaled, n = round(1024 sqrt(N)), so every rank keeps ~2.10 M elements")
     ap.add_argument("--impl", default="efem", choices=["efem", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    ws = dist_env()[0]
+    default_sweep = args.config is None
+    weak = default_sweep and ws > 1
     if args.config is None:
-        args.config = 2 if dist_env()[0] == 1 else 5
-    cfg = CONFIGS[args.config]
+        args.config = 2
+    cfg = dict(CONFIGS[args.config])
+    if weak:  # the N = 1 workload per rank: one mesh of ~N x its elements, row-owned slabs
+        cfg["n"] = int(round(1024 * math.sqrt(ws)))
+        cfg["name"] = f"cfg2_ne0_2d_weak_{cfg['n']}x{cfg['n']}"
+    cfg["weak"] = weak
+    cfg["scaling"] = "weak" if default_sweep else "strong"  # the default N = 1, 2, 4, 8 sweep is weak
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
