@@ -248,6 +248,48 @@ efem_status efem_part_globalize(efem_plan plan, const int32_t* sub2global, const
 efem_status efem_part_numeric(efem_plan plan, unsigned forms, const int64_t* info, int64_t global_first_row,
                               const int32_t* e2d_global, efem_csr* slice, efem_stream_t stream);
 
+/* ---- partitioned assembly, asynchronous form ---------------------------------------
+ * The same computation as efem_part_counts / _scan / _globalize / _numeric,
+ * with every size kept on the device, so a rank's step needs no host round
+ * trip before efem_plan_check (which reports capacity overflow and the mesh
+ * flags).  Per step, all enqueued on one stream:
+ *   efem_part_enumerate_async(plan, owned_cnt)   enumeration of the sub-mesh,
+ *        owned_cnt as for efem_part_counts, and the row window on the device
+ *   [caller: allgather of owned_cnt -> global_cnt]
+ *   efem_part_scan(global_cnt, ...)  ->  global_ent_ptr
+ *   efem_part_globalize(plan, sub2global, global_ent_ptr, e2d_global)
+ *        (also records the window's global first row global_ent_ptr[node_lo])
+ *   efem_part_numeric_async(plan, forms, e2d_global, slice)
+ *   efem_plan_check(plan)
+ * DESIGN.md §9. */
+
+/* Binds the sub-mesh plan (workspace set) to the rank's node range: finds
+ * the local node range of [node_lo, node_hi) in sub2global (ascending;
+ * device, kept by pointer until the next bind).  Synchronising; once per
+ * partition.  EFEM_EINVAL on NULL / bad range. */
+efem_status efem_part_bind(efem_plan plan, const int32_t* sub2global, int64_t node_lo, int64_t node_hi,
+                           efem_stream_t stream);
+
+/* Enumeration of a bound plan plus the owned counts: owned_cnt (device,
+ * node_hi - node_lo ints) as efem_part_counts writes them; the row window
+ * {first owned local row, owned rows, local CSR offset of that row, owned
+ * entries} stays on the device.  Asynchronous (one CUDA graph per owned_cnt
+ * array).  EFEM_ESTATE if the plan is not bound. */
+efem_status efem_part_enumerate_async(efem_plan plan, int32_t* owned_cnt, efem_stream_t stream);
+
+/* The owned rows into `slice` (device; slice->n_rows / nnz are CAPACITIES,
+ * the window's sizes are read on the device): row_ptr from 0, global column
+ * ids.  A window larger than the capacities writes nothing and makes
+ * efem_plan_check return EFEM_ECAPACITY.  Needs efem_part_enumerate_async
+ * and efem_part_globalize before it on the stream. */
+efem_status efem_part_numeric_async(efem_plan plan, unsigned forms, const int32_t* e2d_global, efem_csr* slice,
+                                    efem_stream_t stream);
+
+/* Copies the device window {first owned local row, owned rows, local CSR
+ * offset, owned entries, global first row} (5 int64) into window_dev
+ * (device), e.g. for an allgather of the owned entry counts. */
+efem_status efem_part_window(efem_plan plan, int64_t* window_dev, efem_stream_t stream);
+
 /* ---- vectorized integration (Sec. 3.1)
  * The paper's recipe: map the quadrature points of the reference element to
  * every element at once, evaluate the user's function there (the caller does

@@ -82,6 +82,10 @@ def load():
         "efem_part_scan": (st, [vp, i64, vp, vp, ctypes.POINTER(ctypes.c_size_t), vp]),
         "efem_part_globalize": (st, [vp, vp, vp, vp, vp]),
         "efem_part_numeric": (st, [vp, ctypes.c_uint, i64p, i64, vp, ctypes.POINTER(efem_csr), vp]),
+        "efem_part_bind": (st, [vp, vp, i64, i64, vp]),
+        "efem_part_enumerate_async": (st, [vp, vp, vp]),
+        "efem_part_numeric_async": (st, [vp, ctypes.c_uint, vp, ctypes.POINTER(efem_csr), vp]),
+        "efem_part_window": (st, [vp, vp, vp]),
         "efem_lshape_sizes": (st, [ctypes.c_int, i64p, i64p]),
         "efem_build_mesh_lshape": (st, [ctypes.c_int, ctypes.c_double, ctypes.c_uint64, vp, vp, vp]),
         "efem_quad_size": (ctypes.c_int, [ctypes.c_int]),

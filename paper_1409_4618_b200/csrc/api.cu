@@ -90,7 +90,8 @@ efem_status flags_status(const Plan& p) {
         return EFEM_EDEGENERATE;
     }
     if (h.flags[F_CAPACITY]) {
-        set_error("per-thread capacity exceeded (mesh too irregular for EFEM_MAX_* limits)");
+        set_error("capacity exceeded: an output smaller than the assembled pattern (efem_assemble_async / "
+                  "efem_part_numeric_async), or a node too irregular for the per-thread limits");
         return EFEM_ECAPACITY;
     }
     if (h.flags[F_ROW_MISMATCH]) {
@@ -428,6 +429,10 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
         cudaGraphExecDestroy(p->g_async);
         p->g_async = nullptr;
     }
+    if (p->g_part) {
+        cudaGraphExecDestroy(p->g_part);
+        p->g_part = nullptr;
+    }
     return EFEM_OK;
 }
 
@@ -459,6 +464,7 @@ efem_status efem_plan_destroy(efem_plan plan) {
     if (p->h_hdr) cudaFreeHost(p->h_hdr);
     if (p->g_enum) cudaGraphExecDestroy(p->g_enum);
     if (p->g_async) cudaGraphExecDestroy(p->g_async);
+    if (p->g_part) cudaGraphExecDestroy(p->g_part);
     if (p->ev_in) cudaEventDestroy(p->ev_in);
     if (p->ev_out) cudaEventDestroy(p->ev_out);
     if (p->gstream) cudaStreamDestroy(p->gstream);

@@ -266,6 +266,17 @@ __device__ __forceinline__ int dyn_rows(WsHeader* hdr, int cap_rows, long long c
     return (int)r;
 }
 
+// Bound partition (efem_part_numeric_async): rows and entries of the window
+// from the device; a window larger than the slice capacities is flagged.
+__device__ __forceinline__ int win_rows(WsHeader* hdr, const long long* win, int cap_rows, long long cap_nnz) {
+    const long long r = *(volatile const long long*)&win[1], z = *(volatile const long long*)&win[3];
+    if (r > cap_rows || z > cap_nnz) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&hdr->flags[F_CAPACITY], 1);
+        return -1;
+    }
+    return (int)r;
+}
+
 // L1 of a batch: the lane's row record; lane 0 also the batch's first
 // incidence offset (row offsets follow from t = 1 + (first != last) by a
 // warp scan, so inc_ptr is read once per batch, not per row)
@@ -297,11 +308,23 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
                                                            int32_t* __restrict__ row_ptr_out,
                                                            int32_t* __restrict__ col_idx,
                                                            double* __restrict__ vals_m, double* __restrict__ vals_k,
-                                                           WsHeader* hdr, int dyn, long long cap_nnz) {
+                                                           WsHeader* hdr, int dyn, long long cap_nnz,
+                                                           const long long* __restrict__ win) {
     constexpr int M = P::M, NO = M - 1;
-    const int n_rows = dyn ? dyn_rows(hdr, n_rows_arg, cap_nnz) : n_rows_arg;
+    int n_rows = dyn ? dyn_rows(hdr, n_rows_arg, cap_nnz) : n_rows_arg;
+    if (win) {
+        n_rows = win_rows(hdr, win, n_rows_arg, cap_nnz);
+        if (n_rows > 0) {
+            row0 = (int)win[0];
+            out_base = (int)win[2];
+            own_base = (int)win[4];
+            rec += row0;
+            inc_ptr += row0;
+        }
+    }
     if (n_rows <= 0) {
-        if (dyn && n_rows == 0 && blockIdx.x == 0 && threadIdx.x == 0 && (forms & EFEM_PATTERN)) row_ptr_out[0] = 0;
+        if ((dyn || win) && n_rows == 0 && blockIdx.x == 0 && threadIdx.x == 0 && (forms & EFEM_PATTERN))
+            row_ptr_out[0] = 0;
         return;
     }
     constexpr int NS = 1 + 2 * NO, WSEG = 32 * NS, NW = TRI_TPB / 32;
@@ -728,11 +751,23 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
                                                       unsigned forms, int fast_ids, int32_t* __restrict__ row_ptr_out,
                                                       int32_t* __restrict__ col_idx,
                                                       double* __restrict__ vals_m, double* __restrict__ vals_k,
-                                                      WsHeader* hdr, int dyn, long long cap_nnz) {
+                                                      WsHeader* hdr, int dyn, long long cap_nnz,
+                                                      const long long* __restrict__ win) {
     static_assert(KT::D == 3 && !KT::FACES, "NE0 3D only");
-    const int n_rows = dyn ? dyn_rows(hdr, n_rows_arg, cap_nnz) : n_rows_arg;
+    int n_rows = dyn ? dyn_rows(hdr, n_rows_arg, cap_nnz) : n_rows_arg;
+    if (win) {
+        n_rows = win_rows(hdr, win, n_rows_arg, cap_nnz);
+        if (n_rows > 0) {
+            const int r0 = (int)win[0];
+            out_base = (int)win[2];
+            own_base = (int)win[4];
+            inc_ptr += r0;
+            row_ptr += r0;
+        }
+    }
     if (n_rows <= 0 || (int)(blockIdx.x * NUM_TPB) >= n_rows) {
-        if (dyn && n_rows == 0 && blockIdx.x == 0 && threadIdx.x == 0 && (forms & EFEM_PATTERN)) row_ptr_out[0] = 0;
+        if ((dyn || win) && n_rows == 0 && blockIdx.x == 0 && threadIdx.x == 0 && (forms & EFEM_PATTERN))
+            row_ptr_out[0] = 0;
         return;
     }
     extern __shared__ __align__(16) unsigned char ne3_smem[];
@@ -818,8 +853,9 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
     if (w.n_rows == 0) return EFEM_OK;
     double* vm = (forms & EFEM_MASS) ? out->vals_mass : nullptr;
     double* vk = (forms & EFEM_STIFF) ? out->vals_stiff : nullptr;
-    const int32_t* inc_ptr = p.inc_ptr + w.row0;
-    const int32_t* row_ptr = p.row_ptr + w.row0;
+    // (a device window offsets the arrays inside the kernel)
+    const int32_t* inc_ptr = p.inc_ptr + (w.win ? 0 : w.row0);
+    const int32_t* row_ptr = p.row_ptr + (w.win ? 0 : w.row0);
     if constexpr (KT::D == 2 || KT::FACES) {
         using P = std::conditional_t<KT::D == 2, TriPolicy, FacePolicy>;
         constexpr int MINB = 2;
@@ -834,8 +870,8 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
         }
         const int64_t need = (w.n_rows + TRI_TPB - 1) / TRI_TPB;
         k_rows_tri<KT, P, MINB><<<(unsigned)(need < grid ? need : grid), TRI_TPB, 0, s>>>(
-            p.coords, p.elems, inc_ptr, p.rec + w.row0, w.e2d, (int)w.row0, (int)w.n_rows, w.own_base, w.out_base,
-            forms, out->row_ptr, out->col_idx, vm, vk, p.hdr, (int)w.dyn, (long long)w.cap_nnz);
+            p.coords, p.elems, inc_ptr, p.rec + (w.win ? 0 : w.row0), w.e2d, (int)w.row0, (int)w.n_rows, w.own_base,
+            w.out_base, forms, out->row_ptr, out->col_idx, vm, vk, p.hdr, (int)w.dyn, (long long)w.cap_nnz, w.win);
     } else {
         const int fast_ids = p.n_nodes < (1ll << 27);
         static bool attr = false;
@@ -847,7 +883,7 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
         k_rows_ne3<KT><<<grid_for(w.n_rows, NUM_TPB), NUM_TPB, NE3_SMEM, s>>>(p.coords, p.elems, inc_ptr, p.bucket, w.e2d, row_ptr,
                                                        (int)w.n_rows, w.own_base, w.out_base, forms, fast_ids,
                                                        out->row_ptr, out->col_idx, vm, vk, p.hdr, (int)w.dyn,
-                                                       (long long)w.cap_nnz);
+                                                       (long long)w.cap_nnz, w.win);
     }
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;

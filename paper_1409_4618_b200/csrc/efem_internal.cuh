@@ -27,6 +27,10 @@ struct WsHeader {
     unsigned long long bad_element;  // atomicMin of the first degenerate element
     long long totals[2];             // n_dofs, nnz (read back with the flags in one copy)
     long long pad;
+    // row window of a bound partition (efem_part_*_async), written on the
+    // device: first local row, rows, local CSR offset of the first row,
+    // entries, global id of the first row
+    long long win[6];
 };
 
 // Instance words e << 3 | k (element e < 2^27, local entity k); the two top
@@ -110,6 +114,15 @@ struct Plan {
     efem_csr async_key{};
     unsigned async_forms = 0;
 
+    // bound partition (efem_part_bind): the rank's node range [part_lo,
+    // part_hi) and its local node range [part_l0, part_l1) in this sub-mesh
+    bool part_bound = false;
+    int64_t part_lo = 0, part_hi = 0, part_l0 = 0, part_l1 = 0;
+    const int32_t* part_sub2global = nullptr;
+    cudaGraphExec_t g_part = nullptr;  // enumeration + owned counts + window
+    int64_t part_launches = 0;
+    int32_t* part_key = nullptr;
+
     // state
     bool enumerated = false, symbolic = false;
     bool async_pending = false;  // efem_assemble_async ran; sizes arrive with efem_plan_check
@@ -127,6 +140,9 @@ struct RowWindow {
     // header totals; n_rows, cap_nnz above are then the output capacities
     bool dyn = false;
     int64_t cap_nnz = 0;
+    // bound partition, asynchronous: row0 / n_rows / out_base / own_base come
+    // from this device window (WsHeader::win); n_rows, cap_nnz are capacities
+    const long long* win = nullptr;
 };
 
 // ---- error plumbing --------------------------------------------------------------

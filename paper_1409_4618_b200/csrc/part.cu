@@ -147,9 +147,31 @@ __global__ void k_globalize(const int32_t* __restrict__ elems, int64_t n_elems, 
 }
 
 
+// Row window of a bound partition (one thread): local rows [ent_ptr[l0],
+// ent_ptr[l1]) and their CSR entries in the sub-mesh's local numbering.
+__global__ void k_part_window(const int32_t* __restrict__ ent_ptr, const int32_t* __restrict__ inc_ptr,
+                              const int32_t* __restrict__ row_ptr, int64_t l0, int64_t l1, int c,
+                              long long* __restrict__ win) {
+    if (threadIdx.x || blockIdx.x) return;
+    const long long r0 = ent_ptr[l0], r1 = ent_ptr[l1];
+    auto start = [&](long long r) -> long long { return row_ptr ? row_ptr[r] : r + (long long)c * inc_ptr[r]; };
+    const long long z0 = start(r0), z1 = start(r1);
+    win[0] = r0;
+    win[1] = r1 - r0;
+    win[2] = z0;
+    win[3] = z1 - z0;
+}
+
+__global__ void k_part_first_row(const int32_t* __restrict__ global_ent_ptr, int64_t lo, long long* __restrict__ win) {
+    if (threadIdx.x || blockIdx.x) return;
+    win[4] = global_ent_ptr[lo];
+}
+
 }  // namespace
 
 efem_status launch_rows_any(Plan& p, unsigned forms, efem_csr* out, const RowWindow& w, cudaStream_t s);
+efem_status launch_enumerate(Plan& p, cudaStream_t s);
+bool row_ptr_stored(const Plan& p);
 
 }  // namespace efem
 
@@ -296,12 +318,19 @@ efem_status efem_part_scan(const int32_t* global_cnt, int64_t n, int32_t* global
 efem_status efem_part_globalize(efem_plan plan, const int32_t* sub2global, const int32_t* global_ent_ptr,
                                 int32_t* e2d_global, efem_stream_t stream) {
     Plan* p = reinterpret_cast<Plan*>(plan);
-    if (!p || !p->symbolic || !sub2global || !global_ent_ptr || !e2d_global) {
-        set_error("efem_part_globalize: needs a plan after efem_assemble_symbolic and non-NULL arrays");
+    if (!p || !(p->symbolic || (p->part_bound && p->async_pending)) || !sub2global || !global_ent_ptr || !e2d_global) {
+        set_error("efem_part_globalize: needs a plan after efem_assemble_symbolic (or efem_part_enumerate_async) "
+                  "and non-NULL arrays");
         return EFEM_ESTATE;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    if (p->n_elems == 0) return EFEM_OK;
+    if (p->n_elems == 0) {
+        if (p->part_bound) {
+            k_part_first_row<<<1, 32, 0, s>>>(global_ent_ptr, p->part_lo, p->hdr->win);
+            EFEM_LAUNCH_CHECK();
+        }
+        return EFEM_OK;
+    }
     const unsigned grid = grid_for(p->n_elems, 256);
     if (p->dim == 2 && p->element == EFEM_RT0)
         k_globalize<Kind<2, EFEM_RT0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, p->ent_ptr, sub2global,
@@ -316,6 +345,10 @@ efem_status efem_part_globalize(efem_plan plan, const int32_t* sub2global, const
         k_globalize<Kind<3, EFEM_NED0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, p->ent_ptr, sub2global,
                                                              global_ent_ptr, e2d_global);
     EFEM_LAUNCH_CHECK();
+    if (p->part_bound) {  // the window's global first row, for efem_part_numeric_async
+        k_part_first_row<<<1, 32, 0, s>>>(global_ent_ptr, p->part_lo, p->hdr->win);
+        EFEM_LAUNCH_CHECK();
+    }
     return EFEM_OK;
 }
 
@@ -339,6 +372,132 @@ efem_status efem_part_numeric(efem_plan plan, unsigned forms, const int64_t* inf
     w.out_base = (int)info[2];
     w.e2d = e2d_global;
     return launch_rows_any(*p, forms, slice, w, s);
+}
+
+// ---- bound partitions: the asynchronous step -----------------------------------
+efem_status efem_part_bind(efem_plan plan, const int32_t* sub2global, int64_t node_lo, int64_t node_hi,
+                           efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !p->ws || !sub2global || node_lo < 0 || node_hi < node_lo) {
+        set_error("efem_part_bind: needs a plan with workspace, sub2global and 0 <= node_lo <= node_hi");
+        return EFEM_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t* d = reinterpret_cast<int64_t*>(&p->hdr->win[0]);
+    k_lower_bound<<<1, 32, 0, s>>>(sub2global, p->n_nodes, node_lo, node_hi, d);
+    EFEM_LAUNCH_CHECK();
+    int64_t lr[2];
+    EFEM_CUDA_TRY(cudaMemcpyAsync(lr, d, 16, cudaMemcpyDeviceToHost, s));
+    EFEM_CUDA_TRY(cudaStreamSynchronize(s));
+    p->part_lo = node_lo;
+    p->part_hi = node_hi;
+    p->part_l0 = lr[0];
+    p->part_l1 = lr[1];
+    p->part_sub2global = sub2global;
+    p->part_bound = true;
+    if (p->g_part) {
+        cudaGraphExecDestroy(p->g_part);
+        p->g_part = nullptr;
+    }
+    return EFEM_OK;
+}
+
+efem_status efem_part_enumerate_async(efem_plan plan, int32_t* owned_cnt, efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !p->ws || !p->part_bound || !owned_cnt) {
+        set_error("efem_part_enumerate_async: needs a bound plan (efem_part_bind) and owned_cnt");
+        return EFEM_ESTATE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    p->enumerated = p->symbolic = false;
+    p->async_pending = true;
+    auto enqueue = [&](cudaStream_t q) -> efem_status {
+        efem_status e = launch_enumerate(*p, q);
+        if (e != EFEM_OK) return e;
+        const int64_t width = p->part_hi - p->part_lo;
+        if (width > 0) EFEM_CUDA_TRY(cudaMemsetAsync(owned_cnt, 0, width * 4, q));
+        if (p->part_l1 > p->part_l0) {
+            k_owned_counts<<<grid_for(p->part_l1 - p->part_l0, 256), 256, 0, q>>>(
+                p->ent_ptr, p->part_sub2global, p->part_l0, p->part_l1, p->part_lo, owned_cnt);
+            EFEM_LAUNCH_CHECK();
+        }
+        k_part_window<<<1, 32, 0, q>>>(p->ent_ptr, p->inc_ptr, row_ptr_stored(*p) ? p->row_ptr : nullptr,
+                                        p->part_l0, p->part_l1, p->m - 1, p->hdr->win);
+        EFEM_LAUNCH_CHECK();
+        return EFEM_OK;
+    };
+    if (p->g_part && p->part_key != owned_cnt) {
+        cudaGraphExecDestroy(p->g_part);
+        p->g_part = nullptr;
+    }
+    if (!p->g_part && !p->graph_failed && !p->want_d2n && !debug_sync()) {
+        bool ok = p->gstream != nullptr;
+        if (!ok) {
+            ok = cudaStreamCreateWithFlags(&p->gstream, cudaStreamNonBlocking) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming) == cudaSuccess;
+        }
+        cudaGraph_t graph = nullptr;
+        if (ok && cudaStreamBeginCapture(p->gstream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            const int64_t l0 = efem_launch_count();
+            const efem_status e = enqueue(p->gstream);
+            const cudaError_t ee = cudaStreamEndCapture(p->gstream, &graph);
+            p->part_launches = efem_launch_count() - l0;
+            count_launch(-(int)p->part_launches);  // counted at replay
+            if (e == EFEM_OK && ee == cudaSuccess && cudaGraphInstantiate(&p->g_part, graph, 0) == cudaSuccess)
+                p->part_key = owned_cnt;
+            else
+                p->g_part = nullptr;
+            if (graph) cudaGraphDestroy(graph);
+        }
+        cudaGetLastError();
+    }
+    if (p->g_part) {
+        EFEM_CUDA_TRY(cudaEventRecord(p->ev_in, s));
+        EFEM_CUDA_TRY(cudaStreamWaitEvent(p->gstream, p->ev_in, 0));
+        EFEM_CUDA_TRY(cudaGraphLaunch(p->g_part, p->gstream));
+        count_launch((int)p->part_launches);
+        EFEM_CUDA_TRY(cudaEventRecord(p->ev_out, p->gstream));
+        EFEM_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_out, 0));
+        return EFEM_OK;
+    }
+    return enqueue(s);
+}
+
+efem_status efem_part_numeric_async(efem_plan plan, unsigned forms, const int32_t* e2d_global, efem_csr* slice,
+                                    efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !p->part_bound || !p->async_pending || !e2d_global || !slice || slice->n_rows < 0 ||
+        slice->nnz < 0 || !slice->row_ptr || (forms & ~7u) ||
+        (slice->nnz > 0 && (!slice->col_idx || ((forms & EFEM_MASS) && !slice->vals_mass) ||
+                            ((forms & EFEM_STIFF) && !slice->vals_stiff)))) {
+        set_error("efem_part_numeric_async: needs efem_part_enumerate_async + efem_part_globalize first, and a "
+                  "slice with capacities and arrays");
+        return EFEM_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (slice->n_rows == 0) {  // capacity 0: only an empty window fits (else flagged by the check below)
+        if (forms & EFEM_PATTERN) EFEM_CUDA_TRY(cudaMemsetAsync(slice->row_ptr, 0, 4, s));
+    }
+    RowWindow w;
+    w.row0 = 0;
+    w.n_rows = slice->n_rows > 0 ? slice->n_rows : 1;
+    w.e2d = e2d_global;
+    w.cap_nnz = slice->nnz;
+    w.win = p->hdr->win;
+    if (slice->n_rows == 0) w.n_rows = 0;
+    if (w.n_rows == 0) return EFEM_OK;
+    return launch_rows_any(*p, forms, slice, w, s);
+}
+
+efem_status efem_part_window(efem_plan plan, int64_t* window_dev, efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !p->part_bound || !window_dev) {
+        set_error("efem_part_window: needs a bound plan and a device array of 5 int64");
+        return EFEM_EINVAL;
+    }
+    EFEM_CUDA_TRY(cudaMemcpyAsync(window_dev, p->hdr->win, 5 * 8, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return EFEM_OK;
 }
 
 }  // extern "C"

@@ -23,8 +23,13 @@ from .api import ALL, CSR, Assembler, _ptr, _stream
 
 
 def node_ranges(n_nodes: int, world: int):
-    """Contiguous, near-equal node ranges [lo, hi) per rank."""
-    cuts = [(n_nodes * r) // world for r in range(world + 1)]
+    """Contiguous node ranges [lo, hi) per rank, all of width W = ceil(N / P)
+    except the last (shorter, possibly empty): the ranks' W-wide count
+    buffers, gathered in rank order, are then the global per-node counts
+    followed by zeros -- no repacking after the all_gather."""
+    w = -(-n_nodes // world) if world > 0 else 0
+    cuts = [min(n_nodes, r * w) for r in range(world + 1)]
+    cuts[-1] = n_nodes
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 
@@ -130,6 +135,51 @@ class PartAssembler:
     def check(self, stream=None):
         self.asm.check(stream=stream)
 
+    # ---- asynchronous step (no host round trip before check) ---------------
+    def bind(self, width: int, world: int, stream=None):
+        """Binds the sub-mesh plan to the node range (efem_part_bind, once) and
+        allocates the W-wide send buffer and the P*W gathered counts."""
+        L = _lib.load()
+        with torch.cuda.device(self.device):
+            _lib.check("efem_part_bind", L.efem_part_bind(self.asm._plan, _ptr(self.sub2global), self.lo, self.hi,
+                                                          _stream(stream)))
+        self.width = int(width)
+        self.owned_pad = torch.zeros(max(self.width, 1), dtype=torch.int32, device=self.device)
+        self.global_buf = torch.zeros(max(self.width, 1) * world, dtype=torch.int32, device=self.device)
+        self.window = torch.zeros(5, dtype=torch.int64, device=self.device)
+        self.bound = True
+
+    def enumerate_async(self, stream=None):
+        L = _lib.load()
+        with torch.cuda.device(self.device):
+            _lib.check("efem_part_enumerate_async",
+                       L.efem_part_enumerate_async(self.asm._plan, _ptr(self.owned_pad), _stream(stream)))
+        return self.owned_pad
+
+    def globalize_async(self, global_cnt: torch.Tensor, stream=None):
+        L = _lib.load()
+        b = ctypes.c_size_t(self.scan_ws.numel())
+        with torch.cuda.device(self.device):
+            _lib.check("efem_part_scan", L.efem_part_scan(_ptr(global_cnt), self.n_global_nodes,
+                                                          _ptr(self.global_ent_ptr), _ptr(self.scan_ws),
+                                                          ctypes.byref(b), _stream(stream)))
+            _lib.check("efem_part_globalize", L.efem_part_globalize(self.asm._plan, _ptr(self.sub2global),
+                                                                    _ptr(self.global_ent_ptr),
+                                                                    _ptr(self.e2d_global), _stream(stream)))
+
+    def numeric_async(self, out: CSR, forms: int = ALL, stream=None):
+        """out: a slice with capacities (e.g. from alloc_slice after one
+        synchronous step); the window's sizes are read on the device."""
+        L = _lib.load()
+        c = _lib.efem_csr(out.row_ptr.numel() - 1, out.col_idx.numel(), out.row_ptr.data_ptr(),
+                          out.col_idx.data_ptr(), out.vals_M.data_ptr(), out.vals_K.data_ptr())
+        with torch.cuda.device(self.device):
+            _lib.check("efem_part_numeric_async", L.efem_part_numeric_async(self.asm._plan, forms,
+                                                                            _ptr(self.e2d_global), ctypes.byref(c),
+                                                                            _stream(stream)))
+            _lib.check("efem_part_window", L.efem_part_window(self.asm._plan, _ptr(self.window), _stream(stream)))
+        return out
+
 
 def _comm_device(t: torch.Tensor, group=None):
     """NCCL gathers device tensors directly; gloo (CPU tests, or several
@@ -179,6 +229,47 @@ def assemble_rank(part: PartAssembler, ranges, out: CSR | None = None, group=Non
     part.numeric(out, stream=stream)
     part.check(stream=stream)
     return out, part.first_row, offs[dist.get_rank(group)]
+
+
+def assemble_rank_async(part: PartAssembler, ranges, out: CSR, group=None, stream=None, check=True):
+    """One rank's step with every size on the device: enumeration + owned
+    counts, the counts all_gather, scan + globalisation, owned-row numeric,
+    the entry-count all_gather; one host round trip (the flags check) at
+    the end.  `out` holds capacities (from a synchronous assemble_rank).
+    Returns (out, window (device int64[5]: first local row, rows, local CSR
+    offset, entries, global first row), every rank's entry count (device))."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if not getattr(part, "bound", False):
+        part.bind(max(hi - lo for lo, hi in ranges), world, stream=stream)
+    owned = part.enumerate_async(stream=stream)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(part.global_buf, owned, group=group)
+        gcnt = part.global_buf
+    else:  # gloo: host copies
+        parts = [torch.empty_like(owned, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, owned.cpu(), group=group)
+        gcnt = torch.cat(parts).to(part.device)
+    part.globalize_async(gcnt, stream=stream)
+    part.numeric_async(out, stream=stream)
+    nnz_all = _allgather_dev(part.window[3:4].contiguous(), group)
+    if check:
+        part.check(stream=stream)
+    return out, part.window, nnz_all
+
+
+def _allgather_dev(t: torch.Tensor, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty(world * t.numel(), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t, group=group)
+        return out
+    parts = [torch.empty_like(t, device="cpu") for _ in range(world)]
+    dist.all_gather(parts, t.cpu(), group=group)
+    return torch.cat(parts)
 
 
 def concat_slices(slices, entry_offsets):

@@ -26,7 +26,8 @@ def _free_port():
 def _worker(rank, world, port, dim, element, q):
     import torch.distributed as dist
 
-    from paper_1409_4618_b200.dist import allgather_counts, allgather_nnz, node_ranges, offsets_from_counts
+    from paper_1409_4618_b200.dist import (_allgather_dev, allgather_counts, allgather_nnz, node_ranges,
+                                           offsets_from_counts)
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -51,7 +52,18 @@ def _worker(rank, world, port, dim, element, q):
         nnzs = allgather_nnz(my_nnz, torch.device("cpu"))
         offs, total = offsets_from_counts(nnzs)
         ok2 = total == A.col_idx.shape[0] and (len(rows) == 0 or offs[rank] == A.row_ptr[rows[0]])
-        q.put((rank, ok1, ok2))
+        # the asynchronous step's exchange (dist.assemble_rank_async): W-wide
+        # buffers gathered in rank order ARE the global counts (+ zero tail)
+        W = max(h - l for l, h in ranges)
+        pad = torch.zeros(W, dtype=torch.int32)
+        pad[: hi - lo] = owned
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad)
+        flat = torch.cat(parts).numpy()
+        ok3 = bool(np.array_equal(flat[:N], global_cnt.numpy())) and not flat[N:].any()
+        nz = _allgather_dev(torch.tensor([my_nnz], dtype=torch.int64))
+        ok3 = ok3 and [int(v) for v in nz] == nnzs
+        q.put((rank, ok1, ok2 and ok3))
     finally:
         dist.destroy_process_group()
 
@@ -79,4 +91,8 @@ def test_node_ranges_tile():
             rs = node_ranges(N, P)
             assert rs[0][0] == 0 and rs[-1][1] == N
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
-            assert max(h - l for l, h in rs) - min(h - l for l, h in rs) <= 1
+            # all ranges W = ceil(N / P) wide but the last (shorter, maybe empty):
+            # the gathered W-wide buffers are the global counts without repacking
+            W = -(-N // P)
+            assert all(h - l == W for l, h in rs[:-1] if h < N) and 0 <= rs[-1][1] - rs[-1][0] <= W
+            assert all(l == min(N, r * W) for r, (l, h) in enumerate(rs))

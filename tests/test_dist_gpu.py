@@ -85,3 +85,67 @@ def test_partitioned_config5_against_oracle_rows():
         scale = np.abs(m).max()
         assert np.abs(vm[lo:hi] - m).max() <= 1e-12 * scale
         assert np.abs(vk[lo:hi] - k).max() <= 1e-12 * np.abs(k).max()
+
+
+def _emulate_async(coords, elems, element, P, caps):
+    """The asynchronous rank step (dist.assemble_rank_async) for P ranks in
+    this process: every rank's enumeration first, then the gathered counts
+    (== all_gather_into_tensor of the W-wide buffers), then each rank's
+    globalisation and numeric into `caps` (slices with capacities)."""
+    from paper_1409_4618_b200 import dist
+
+    ranges = dist.node_ranges(coords.shape[0], P)
+    W = max(hi - lo for lo, hi in ranges)
+    parts = [dist.PartAssembler(coords, elems, element, lo, hi) for lo, hi in ranges]
+    for p in parts:
+        p.bind(W, P)
+    owned = [p.enumerate_async().clone() for p in parts]
+    gathered = torch.cat(owned)
+    for p, s in zip(parts, caps):
+        p.globalize_async(gathered)
+        p.numeric_async(s)
+    return parts
+
+
+@pytest.mark.parametrize("dim,element", KINDS, ids=KIND_IDS)
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_partitioned_async_equals_sync(dim, element, P):
+    from paper_1409_4618_b200 import api, dist
+
+    n = 24 if dim == 2 else 6
+    coords, elems = api.build_mesh(dim, n, 0.2 if dim == 2 else 0.15, 23)
+    one = api.Assembler(coords, elems, element).assemble()
+    sparts, sslices, offs, total = _emulate(coords, elems, element, P)
+    # capacities from the synchronous pass, one spare row / entry (windows are read on the device)
+    caps = [dist.CSR(torch.full((p.owned_rows + 2,), -1, dtype=torch.int32, device="cuda"),
+                     torch.full((p.owned_nnz + 1,), -1, dtype=torch.int32, device="cuda"),
+                     torch.zeros(p.owned_nnz + 1, dtype=torch.float64, device="cuda"),
+                     torch.zeros(p.owned_nnz + 1, dtype=torch.float64, device="cuda")) for p in sparts]
+    aparts = _emulate_async(coords, elems, element, P, caps)
+    for sp, ap, ss, c in zip(sparts, aparts, sslices, caps):
+        ap.check()  # flags: no capacity overflow, conforming
+        w = ap.window.cpu().numpy()
+        assert (w[1], w[3], w[4]) == (sp.owned_rows, sp.owned_nnz, sp.first_row)
+        r, z = sp.owned_rows, sp.owned_nnz
+        assert torch.equal(c.row_ptr[: r + 1], ss.row_ptr)
+        assert torch.equal(c.col_idx[:z], ss.col_idx)
+        assert torch.equal(c.vals_M[:z], ss.vals_M) and torch.equal(c.vals_K[:z], ss.vals_K)
+    rp, ci, vm, vk = dist.concat_slices(sslices, offs)
+    assert np.array_equal(vm, one.vals_M.cpu().numpy()) and np.array_equal(ci, one.col_idx.cpu().numpy())
+
+
+def test_partitioned_async_capacity_flagged():
+    from paper_1409_4618_b200 import api, dist
+
+    coords, elems = api.build_mesh(2, 16, 0.2, 5)
+    sparts, _, _, _ = _emulate(coords, elems, NED0, 2)
+    p = sparts[0]
+    small = dist.CSR(torch.zeros(p.owned_rows + 1, dtype=torch.int32, device="cuda"),
+                     torch.zeros(p.owned_nnz - 1, dtype=torch.int32, device="cuda"),
+                     torch.zeros(p.owned_nnz - 1, dtype=torch.float64, device="cuda"),
+                     torch.zeros(p.owned_nnz - 1, dtype=torch.float64, device="cuda"))
+    big = [small, sparts[1].alloc_slice()]
+    aparts = _emulate_async(coords, elems, NED0, 2, big)
+    with pytest.raises(RuntimeError, match="ECAPACITY|capacity"):
+        aparts[0].check()
+    aparts[1].check()
