@@ -121,10 +121,17 @@ __global__ void k_owned_counts(const int32_t* __restrict__ ent_ptr, const int32_
     owned_cnt[sub2global[u] - lo] = ent_ptr[u + 1] - ent_ptr[u];
 }
 
+// per local node u: global id of its first entity minus the local one
+__global__ void k_node_shift(const int32_t* __restrict__ ent_ptr, const int32_t* __restrict__ sub2global,
+                             const int32_t* __restrict__ global_ent_ptr, int64_t n_nodes, int32_t* __restrict__ shift) {
+    const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (u < n_nodes) shift[u] = global_ent_ptr[sub2global[u]] - ent_ptr[u];
+}
+
+// a local DOF d of minimum node u has global id d + shift[u]
 template <class KT>
 __global__ void k_globalize(const int32_t* __restrict__ elems, int64_t n_elems, const int32_t* __restrict__ e2d,
-                            const int32_t* __restrict__ ent_ptr, const int32_t* __restrict__ sub2global,
-                            const int32_t* __restrict__ global_ent_ptr, int32_t* __restrict__ e2d_global) {
+                            const int32_t* __restrict__ shift, int32_t* __restrict__ e2d_global) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= n_elems) return;
     int g[KT::NV];
@@ -141,8 +148,7 @@ __global__ void k_globalize(const int32_t* __restrict__ elems, int64_t n_elems, 
         } else {
             u = min(g[edge_start(KT::D, k)], g[edge_end(KT::D, k)]);
         }
-        const int d = e2d[e * KT::M + k];
-        e2d_global[e * KT::M + k] = global_ent_ptr[sub2global[u]] + (d - ent_ptr[u]);
+        e2d_global[e * KT::M + k] = e2d[e * KT::M + k] + __ldg(shift + u);
     }
 }
 
@@ -293,8 +299,10 @@ efem_status efem_part_scan(const int32_t* global_cnt, int64_t n, int32_t* global
         set_error("efem_part_scan: bad arguments");
         return EFEM_EINVAL;
     }
-    size_t need = 0;
+    size_t need = 0, need2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, (const int32_t*)nullptr, (int32_t*)nullptr, (int)(n + 1));
+    cub::DeviceScan::InclusiveSum(nullptr, need2, (const int32_t*)nullptr, (int32_t*)nullptr, (int)(n + 1));
+    if (need2 > need) need = need2;
     need += 256 + (size_t)(n + 1) * 4;
     if (!ws) {
         *ws_bytes = need;
@@ -305,13 +313,14 @@ efem_status efem_part_scan(const int32_t* global_cnt, int64_t n, int32_t* global
         return EFEM_EWORKSPACE;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    int32_t* tmp = reinterpret_cast<int32_t*>(ws);  // n+1 counts with a trailing 0
+    // global_ent_ptr[0] = 0, [i + 1] = inclusive sum of the first i + 1 counts
     char* cub_ws = reinterpret_cast<char*>(ws) + a256((size_t)(n + 1) * 4);
     size_t cb = need - 256 - (size_t)(n + 1) * 4;
-    EFEM_CUDA_TRY(cudaMemcpyAsync(tmp, global_cnt, n * 4, cudaMemcpyDeviceToDevice, s));
-    EFEM_CUDA_TRY(cudaMemsetAsync(tmp + n, 0, 4, s));
-    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_ws, cb, tmp, global_ent_ptr, (int)(n + 1), s));
-    count_launch(2);
+    EFEM_CUDA_TRY(cudaMemsetAsync(global_ent_ptr, 0, 4, s));
+    if (n > 0) {
+        EFEM_CUDA_TRY(cub::DeviceScan::InclusiveSum(cub_ws, cb, global_cnt, global_ent_ptr + 1, (int)n, s));
+        count_launch(2);
+    }
     return EFEM_OK;
 }
 
@@ -331,19 +340,19 @@ efem_status efem_part_globalize(efem_plan plan, const int32_t* sub2global, const
         }
         return EFEM_OK;
     }
+    // (ent_cnt is scratch between enumerations: it holds the shifts here)
+    int32_t* shift = p->ent_cnt;
+    k_node_shift<<<grid_for(p->n_nodes, 256), 256, 0, s>>>(p->ent_ptr, sub2global, global_ent_ptr, p->n_nodes, shift);
+    EFEM_LAUNCH_CHECK();
     const unsigned grid = grid_for(p->n_elems, 256);
     if (p->dim == 2 && p->element == EFEM_RT0)
-        k_globalize<Kind<2, EFEM_RT0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, p->ent_ptr, sub2global,
-                                                            global_ent_ptr, e2d_global);
+        k_globalize<Kind<2, EFEM_RT0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, shift, e2d_global);
     else if (p->dim == 2)
-        k_globalize<Kind<2, EFEM_NED0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, p->ent_ptr, sub2global,
-                                                             global_ent_ptr, e2d_global);
+        k_globalize<Kind<2, EFEM_NED0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, shift, e2d_global);
     else if (p->element == EFEM_RT0)
-        k_globalize<Kind<3, EFEM_RT0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, p->ent_ptr, sub2global,
-                                                            global_ent_ptr, e2d_global);
+        k_globalize<Kind<3, EFEM_RT0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, shift, e2d_global);
     else
-        k_globalize<Kind<3, EFEM_NED0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, p->ent_ptr, sub2global,
-                                                             global_ent_ptr, e2d_global);
+        k_globalize<Kind<3, EFEM_NED0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, shift, e2d_global);
     EFEM_LAUNCH_CHECK();
     if (p->part_bound) {  // the window's global first row, for efem_part_numeric_async
         k_part_first_row<<<1, 32, 0, s>>>(global_ent_ptr, p->part_lo, p->hdr->win);
