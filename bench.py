@@ -282,7 +282,7 @@ def run_efem(args, cfg):
 def run_efem_dist(args, cfg):
     """N > 1: one process per GPU, row-owned partition.  Each
     rank builds the full mesh (untimed) and its two-hop sub-mesh (untimed
-    setup); a timed step is dist.assemble_rank_async: the rank's local
+    setup); a timed step is dist.AsyncStep (= assemble_rank_async): the rank's local
     enumeration, the two all_gathers (per-node entity counts, per-rank nnz),
     globalisation, the owned-row numeric kernel and the flags check (one host
     round trip).  Time = max over ranks of the summed per-step device time."""
@@ -305,8 +305,9 @@ def run_efem_dist(args, cfg):
     out = None
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     out, _, _ = pdist.assemble_rank(part, ranges, out)  # sizes the slice (untimed setup)
+    step = pdist.AsyncStep(part, ranges, out, stream=stream)
     for _ in range(max(args.warmup, 3)):
-        pdist.assemble_rank_async(part, ranges, out)
+        step()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     l0 = api.launch_count()
@@ -316,7 +317,7 @@ def run_efem_dist(args, cfg):
         for k in range(args.steps):
             flush.fill_(k & 0xff)
             starts[k].record(stream)
-            pdist.assemble_rank_async(part, ranges, out)
+            step()
             ends[k].record(stream)
         torch.cuda.synchronize()
         dist.barrier()

@@ -231,6 +231,68 @@ def assemble_rank(part: PartAssembler, ranges, out: CSR | None = None, group=Non
     return out, part.first_row, offs[dist.get_rank(group)]
 
 
+class AsyncStep:
+    """dist.assemble_rank_async with its call arguments marshalled once: per
+    step four library calls, two collectives and the check, no per-step
+    allocation (the host enqueue stays well under the device time)."""
+
+    def __init__(self, part: PartAssembler, ranges, out: CSR, group=None, stream=None, forms: int = ALL):
+        import torch.distributed as dist
+
+        self.part, self.out, self.group = part, out, group
+        self.world = dist.get_world_size(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+        if not getattr(part, "bound", False):
+            part.bind(max(hi - lo for lo, hi in ranges), self.world, stream=stream)
+        self.L = _lib.load()
+        self.s = _stream(stream)
+        self.plan = part.asm._plan
+        self.p_owned = _ptr(part.owned_pad)
+        self.p_gbuf = _ptr(part.global_buf)
+        self.p_gptr = _ptr(part.global_ent_ptr)
+        self.p_sws = _ptr(part.scan_ws)
+        self.p_s2g = _ptr(part.sub2global)
+        self.p_e2dg = _ptr(part.e2d_global)
+        self.p_win = _ptr(part.window)
+        self.sws_bytes = ctypes.c_size_t(part.scan_ws.numel())
+        self.n_global = part.n_global_nodes
+        self.forms = forms
+        self.csr = _lib.efem_csr(out.row_ptr.numel() - 1, out.col_idx.numel(), out.row_ptr.data_ptr(),
+                                 out.col_idx.data_ptr(), out.vals_M.data_ptr(), out.vals_K.data_ptr())
+        self.csr_ref = ctypes.byref(self.csr)
+        self.nnz_mine = part.window[3:4]
+        self.nnz_all = torch.empty(self.world, dtype=torch.int64, device=part.device)
+
+    def __call__(self, check=True):
+        import torch.distributed as dist
+
+        L, ck = self.L, _lib.check
+        ck("efem_part_enumerate_async", L.efem_part_enumerate_async(self.plan, self.p_owned, self.s))
+        if self.nccl:
+            dist.all_gather_into_tensor(self.part.global_buf, self.part.owned_pad, group=self.group)
+            gptr = self.p_gbuf
+        else:  # gloo: host copies
+            o = self.part.owned_pad
+            parts = [torch.empty_like(o, device="cpu") for _ in range(self.world)]
+            dist.all_gather(parts, o.cpu(), group=self.group)
+            self._g = torch.cat(parts).to(o.device)
+            gptr = _ptr(self._g)
+        self.sws_bytes.value = self.part.scan_ws.numel()
+        ck("efem_part_scan", L.efem_part_scan(gptr, self.n_global, self.p_gptr, self.p_sws,
+                                              ctypes.byref(self.sws_bytes), self.s))
+        ck("efem_part_globalize", L.efem_part_globalize(self.plan, self.p_s2g, self.p_gptr, self.p_e2dg, self.s))
+        ck("efem_part_numeric_async", L.efem_part_numeric_async(self.plan, self.forms, self.p_e2dg, self.csr_ref,
+                                                                self.s))
+        ck("efem_part_window", L.efem_part_window(self.plan, self.p_win, self.s))
+        if self.nccl:
+            dist.all_gather_into_tensor(self.nnz_all, self.nnz_mine, group=self.group)
+        else:
+            self.nnz_all = _allgather_dev(self.nnz_mine.contiguous(), self.group)
+        if check:
+            ck("efem_plan_check", L.efem_plan_check(self.plan, self.s))
+        return self.out, self.part.window, self.nnz_all
+
+
 def assemble_rank_async(part: PartAssembler, ranges, out: CSR, group=None, stream=None, check=True):
     """One rank's step with every size on the device: enumeration + owned
     counts, the counts all_gather, scan + globalisation, owned-row numeric,

@@ -149,3 +149,42 @@ def test_partitioned_async_capacity_flagged():
     with pytest.raises(RuntimeError, match="ECAPACITY|capacity"):
         aparts[0].check()
     aparts[1].check()
+
+
+@pytest.mark.parametrize("backend", ["nccl", "gloo"])
+def test_async_step_world1_equals_single(backend):
+    """bench.py's timed multi-GPU step (dist.AsyncStep) in a real process group
+    of size 1: the slice equals the 1-GPU CSR, the window its sizes."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1409_4618_b200 import api
+    from paper_1409_4618_b200 import dist as pdist
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    kw = {"device_id": torch.device("cuda", 0)} if backend == "nccl" else {}
+    dist.init_process_group(backend, rank=0, world_size=1, **kw)
+    try:
+        coords, elems = api.build_mesh(2, 20, 0.2, 9, device="cuda:0")
+        one = api.Assembler(coords, elems, NED0).assemble()
+        ranges = pdist.node_ranges(coords.shape[0], 1)
+        part = pdist.PartAssembler(coords, elems, NED0, *ranges[0])
+        out, _, _ = pdist.assemble_rank(part, ranges, None)
+        out.vals_M.zero_()
+        out.col_idx.zero_()
+        step = pdist.AsyncStep(part, ranges, out)
+        for _ in range(2):
+            o, win, nnz_all = step()
+        assert torch.equal(o.row_ptr, one.row_ptr) and torch.equal(o.col_idx, one.col_idx)
+        assert torch.equal(o.vals_M, one.vals_M) and torch.equal(o.vals_K, one.vals_K)
+        w = win.cpu().tolist()
+        assert w[:5] == [0, one.n_rows, 0, one.nnz, 0] and nnz_all.cpu().tolist() == [one.nnz]
+    finally:
+        dist.destroy_process_group()
