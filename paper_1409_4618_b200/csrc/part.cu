@@ -159,6 +159,10 @@ __global__ void k_part_window(const int32_t* __restrict__ ent_ptr, const int32_t
                               const int32_t* __restrict__ row_ptr, int64_t l0, int64_t l1, int c,
                               long long* __restrict__ win) {
     if (threadIdx.x || blockIdx.x) return;
+    if (l1 <= l0) {  // no owned node in the sub-mesh: an empty window
+        win[0] = win[1] = win[2] = win[3] = 0;
+        return;
+    }
     const long long r0 = ent_ptr[l0], r1 = ent_ptr[l1];
     auto start = [&](long long r) -> long long { return row_ptr ? row_ptr[r] : r + (long long)c * inc_ptr[r]; };
     const long long z0 = start(r0), z1 = start(r1);
@@ -166,6 +170,11 @@ __global__ void k_part_window(const int32_t* __restrict__ ent_ptr, const int32_t
     win[1] = r1 - r0;
     win[2] = z0;
     win[3] = z1 - z0;
+}
+
+__global__ void k_empty_window_check(WsHeader* hdr) {  // a zero-capacity slice fits only an empty window
+    if (threadIdx.x || blockIdx.x) return;
+    if (hdr->win[1] > 0 || hdr->win[3] > 0) atomicOr(&hdr->flags[F_CAPACITY], 1);
 }
 
 __global__ void k_part_first_row(const int32_t* __restrict__ global_ent_ptr, int64_t lo, long long* __restrict__ win) {
@@ -485,17 +494,18 @@ efem_status efem_part_numeric_async(efem_plan plan, unsigned forms, const int32_
         return EFEM_EINVAL;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    if (slice->n_rows == 0) {  // capacity 0: only an empty window fits (else flagged by the check below)
+    if (slice->n_rows == 0) {  // capacity 0: only an empty window fits
         if (forms & EFEM_PATTERN) EFEM_CUDA_TRY(cudaMemsetAsync(slice->row_ptr, 0, 4, s));
+        k_empty_window_check<<<1, 32, 0, s>>>(p->hdr);
+        EFEM_LAUNCH_CHECK();
+        return EFEM_OK;
     }
     RowWindow w;
     w.row0 = 0;
-    w.n_rows = slice->n_rows > 0 ? slice->n_rows : 1;
+    w.n_rows = slice->n_rows;
     w.e2d = e2d_global;
     w.cap_nnz = slice->nnz;
     w.win = p->hdr->win;
-    if (slice->n_rows == 0) w.n_rows = 0;
-    if (w.n_rows == 0) return EFEM_OK;
     return launch_rows_any(*p, forms, slice, w, s);
 }
 

@@ -51,6 +51,17 @@ class PartAssembler:
         self.n_global_nodes = int(coords.shape[0])
         dim = int(coords.shape[1])
         self.device = coords.device
+        self.first_row = 0
+        # a rank with an empty node range (more ranks than ceil-width ranges
+        # need) owns nothing: no sub-mesh, no plan, an empty slice
+        self.empty = self.hi <= self.lo
+        self.scan_ws = torch.empty(256, dtype=torch.uint8, device=self.device)
+        self.global_ent_ptr = torch.empty(self.n_global_nodes + 1, dtype=torch.int32, device=self.device)
+        if self.empty:
+            self.owned_cnt = torch.zeros(1, dtype=torch.int32, device=self.device)
+            self.info = (ctypes.c_int64 * 4)()
+            self.sub2global = self.e2d_global = None
+            return
         full = _lib.efem_mesh(dim, coords.shape[0], elems.shape[0], coords.data_ptr(), elems.data_ptr())
         ws_bytes = ctypes.c_size_t()
         nn, ne = ctypes.c_int64(), ctypes.c_int64()
@@ -83,6 +94,10 @@ class PartAssembler:
         self.scan_ws = torch.empty(max(scan_bytes.value, 256), dtype=torch.uint8, device=self.device)
         self.first_row = 0
 
+    def _empty_slice_rows(self, out: CSR):
+        out.row_ptr[:1].zero_()
+        return out
+
     @property
     def owned_rows(self):
         return int(self.info[1])
@@ -93,6 +108,8 @@ class PartAssembler:
 
     def symbolic(self, stream=None):
         """Local enumeration; returns this rank's per-node entity counts."""
+        if self.empty:
+            return self.owned_cnt[:0]
         L = _lib.load()
         self.asm.symbolic(stream=stream)
         with torch.cuda.device(self.device):
@@ -103,6 +120,8 @@ class PartAssembler:
 
     def globalize(self, global_cnt: torch.Tensor, stream=None):
         """global_cnt: per-node entity counts of ALL nodes (device int32)."""
+        if self.empty:
+            return 0
         L = _lib.load()
         b = ctypes.c_size_t(self.scan_ws.numel())
         with torch.cuda.device(self.device):
@@ -123,6 +142,8 @@ class PartAssembler:
                    torch.empty(self.owned_nnz, dtype=torch.float64, device=dev))
 
     def numeric(self, out: CSR, forms: int = ALL, stream=None):
+        if self.empty:
+            return self._empty_slice_rows(out)
         L = _lib.load()
         c = _lib.efem_csr(self.owned_rows, self.owned_nnz, out.row_ptr.data_ptr(), out.col_idx.data_ptr(),
                           out.vals_M.data_ptr(), out.vals_K.data_ptr())
@@ -133,16 +154,18 @@ class PartAssembler:
         return out
 
     def check(self, stream=None):
-        self.asm.check(stream=stream)
+        if not self.empty:
+            self.asm.check(stream=stream)
 
     # ---- asynchronous step (no host round trip before check) ---------------
     def bind(self, width: int, world: int, stream=None):
         """Binds the sub-mesh plan to the node range (efem_part_bind, once) and
         allocates the W-wide send buffer and the P*W gathered counts."""
         L = _lib.load()
-        with torch.cuda.device(self.device):
-            _lib.check("efem_part_bind", L.efem_part_bind(self.asm._plan, _ptr(self.sub2global), self.lo, self.hi,
-                                                          _stream(stream)))
+        if not self.empty:
+            with torch.cuda.device(self.device):
+                _lib.check("efem_part_bind", L.efem_part_bind(self.asm._plan, _ptr(self.sub2global), self.lo,
+                                                              self.hi, _stream(stream)))
         self.width = int(width)
         self.owned_pad = torch.zeros(max(self.width, 1), dtype=torch.int32, device=self.device)
         self.global_buf = torch.zeros(max(self.width, 1) * world, dtype=torch.int32, device=self.device)
@@ -150,6 +173,8 @@ class PartAssembler:
         self.bound = True
 
     def enumerate_async(self, stream=None):
+        if self.empty:
+            return self.owned_pad  # zeros
         L = _lib.load()
         with torch.cuda.device(self.device):
             _lib.check("efem_part_enumerate_async",
@@ -157,6 +182,8 @@ class PartAssembler:
         return self.owned_pad
 
     def globalize_async(self, global_cnt: torch.Tensor, stream=None):
+        if self.empty:
+            return
         L = _lib.load()
         b = ctypes.c_size_t(self.scan_ws.numel())
         with torch.cuda.device(self.device):
@@ -170,6 +197,9 @@ class PartAssembler:
     def numeric_async(self, out: CSR, forms: int = ALL, stream=None):
         """out: a slice with capacities (e.g. from alloc_slice after one
         synchronous step); the window's sizes are read on the device."""
+        if self.empty:
+            self.window.zero_()
+            return self._empty_slice_rows(out)
         L = _lib.load()
         c = _lib.efem_csr(out.row_ptr.numel() - 1, out.col_idx.numel(), out.row_ptr.data_ptr(),
                           out.col_idx.data_ptr(), out.vals_M.data_ptr(), out.vals_K.data_ptr())
@@ -246,7 +276,8 @@ class AsyncStep:
             part.bind(max(hi - lo for lo, hi in ranges), self.world, stream=stream)
         self.L = _lib.load()
         self.s = _stream(stream)
-        self.plan = part.asm._plan
+        self.empty = part.empty
+        self.plan = None if part.empty else part.asm._plan
         self.p_owned = _ptr(part.owned_pad)
         self.p_gbuf = _ptr(part.global_buf)
         self.p_gptr = _ptr(part.global_ent_ptr)
@@ -267,7 +298,8 @@ class AsyncStep:
         import torch.distributed as dist
 
         L, ck = self.L, _lib.check
-        ck("efem_part_enumerate_async", L.efem_part_enumerate_async(self.plan, self.p_owned, self.s))
+        if not self.empty:
+            ck("efem_part_enumerate_async", L.efem_part_enumerate_async(self.plan, self.p_owned, self.s))
         if self.nccl:
             dist.all_gather_into_tensor(self.part.global_buf, self.part.owned_pad, group=self.group)
             gptr = self.p_gbuf
@@ -277,18 +309,20 @@ class AsyncStep:
             dist.all_gather(parts, o.cpu(), group=self.group)
             self._g = torch.cat(parts).to(o.device)
             gptr = _ptr(self._g)
-        self.sws_bytes.value = self.part.scan_ws.numel()
-        ck("efem_part_scan", L.efem_part_scan(gptr, self.n_global, self.p_gptr, self.p_sws,
-                                              ctypes.byref(self.sws_bytes), self.s))
-        ck("efem_part_globalize", L.efem_part_globalize(self.plan, self.p_s2g, self.p_gptr, self.p_e2dg, self.s))
-        ck("efem_part_numeric_async", L.efem_part_numeric_async(self.plan, self.forms, self.p_e2dg, self.csr_ref,
-                                                                self.s))
-        ck("efem_part_window", L.efem_part_window(self.plan, self.p_win, self.s))
+        if not self.empty:
+            self.sws_bytes.value = self.part.scan_ws.numel()
+            ck("efem_part_scan", L.efem_part_scan(gptr, self.n_global, self.p_gptr, self.p_sws,
+                                                  ctypes.byref(self.sws_bytes), self.s))
+            ck("efem_part_globalize", L.efem_part_globalize(self.plan, self.p_s2g, self.p_gptr, self.p_e2dg,
+                                                            self.s))
+            ck("efem_part_numeric_async", L.efem_part_numeric_async(self.plan, self.forms, self.p_e2dg,
+                                                                    self.csr_ref, self.s))
+            ck("efem_part_window", L.efem_part_window(self.plan, self.p_win, self.s))
         if self.nccl:
             dist.all_gather_into_tensor(self.nnz_all, self.nnz_mine, group=self.group)
         else:
             self.nnz_all = _allgather_dev(self.nnz_mine.contiguous(), self.group)
-        if check:
+        if check and not self.empty:
             ck("efem_plan_check", L.efem_plan_check(self.plan, self.s))
         return self.out, self.part.window, self.nnz_all
 

@@ -188,3 +188,30 @@ def test_async_step_world1_equals_single(backend):
         assert w[:5] == [0, one.n_rows, 0, one.nnz, 0] and nnz_all.cpu().tolist() == [one.nnz]
     finally:
         dist.destroy_process_group()
+
+
+def test_partitioned_async_more_ranks_than_needed():
+    """P larger than useful: trailing ranks own empty node ranges (ceil-width
+    ranges); their windows are empty and the slices still tile the matrix."""
+    from paper_1409_4618_b200 import api, dist
+
+    coords, elems = api.build_mesh(2, 3, 0.1, 2)  # 16 nodes
+    one = api.Assembler(coords, elems, NED0).assemble()
+    P = 12  # W = 2: ranks 8..11 own nothing
+    sparts, sslices, offs, total = _emulate(coords, elems, NED0, P)
+    assert total == one.nnz
+    caps = [dist.CSR(torch.zeros(p.owned_rows + 1, dtype=torch.int32, device="cuda"),
+                     torch.zeros(max(p.owned_nnz, 1), dtype=torch.int32, device="cuda"),
+                     torch.zeros(max(p.owned_nnz, 1), dtype=torch.float64, device="cuda"),
+                     torch.zeros(max(p.owned_nnz, 1), dtype=torch.float64, device="cuda")) for p in sparts]
+    aparts = _emulate_async(coords, elems, NED0, P, caps)
+    rows = 0
+    for sp, ap, c in zip(sparts, aparts, caps):
+        ap.check()
+        w = ap.window.cpu().tolist()
+        assert w[1] == sp.owned_rows and w[3] == sp.owned_nnz
+        rows += w[1]
+        if sp.owned_rows:
+            assert torch.equal(c.col_idx[: sp.owned_nnz], torch.from_numpy(
+                dist.concat_slices(sslices, offs)[1][offs[sparts.index(sp)]:][: sp.owned_nnz]).cuda())
+    assert rows == one.n_rows
