@@ -1,0 +1,134 @@
+"""GPU parity on genuinely unstructured meshes (scipy Delaunay of seeded
+random points) and on high-valence fans: irregular valences drive the
+enumeration's fallbacks (2D buckets of > 8 instances, 3D nodes with more
+larger neighbours / faces than the register lists hold) and the NE0-3D
+rows with more than 7 tets (row_generic).  Bit-exact DOF tables and pattern,
+values within 1e-12 of each row's max, as everywhere else."""
+import numpy as np
+import pytest
+import torch
+from scipy.spatial import Delaunay
+
+from oracle import oracle as ora
+from parity import REL_TOL
+from workloads import NED0, RT0
+
+pytestmark = pytest.mark.gpu
+
+KINDS = [(2, RT0), (2, NED0), (3, RT0), (3, NED0)]
+KIND_IDS = ["rt0_2d", "ne0_2d", "rt0_3d", "ne0_3d"]
+
+
+def delaunay_mesh(dim, n_pts, seed):
+    """Delaunay mesh of n_pts seeded random points in the unit square / cube
+    (corners included), non-flat elements only."""
+    rng = np.random.default_rng(seed)
+    corners = np.array(np.meshgrid(*[[0.0, 1.0]] * dim, indexing="ij")).reshape(dim, -1).T
+    pts = np.concatenate([corners, rng.random((n_pts, dim))])
+    el = Delaunay(pts).simplices.astype(np.int32)
+    el = el[quality(pts, el) > 1e-12]
+    used = np.unique(el)  # drop points no element references (qhull may skip coplanar ones)
+    remap = -np.ones(pts.shape[0], np.int64)
+    remap[used] = np.arange(used.size)
+    return np.ascontiguousarray(pts[used]), np.ascontiguousarray(remap[el].astype(np.int32))
+
+
+def quality(pts, el):
+    """|det B_K| / (longest edge)^d: ~0.1-0.4 for well-shaped elements, -> 0
+    for slivers (whose local matrices are ill-conditioned: two different fp64
+    evaluations of the same integral then differ by ~eps / quality^2)."""
+    x = pts[el]
+    d = x.shape[1] - 1
+    vol = np.abs(np.linalg.det(x[:, 1:] - x[:, :1]))
+    L = np.max(np.stack([np.linalg.norm(x[:, i] - x[:, j], axis=1) for i in range(d + 1)
+                         for j in range(i + 1, d + 1)]), axis=0)
+    return vol / L ** d
+
+
+def fan_mesh(k, seed):
+    """Node 0 at the centre of k triangles (0, i, i+1) closing a disc: node 0
+    owns 2k edge instances (2D bucket fallback); ids shuffled except the centre."""
+    rng = np.random.default_rng(seed)
+    ang = np.sort(rng.random(k)) * 2 * np.pi
+    r = 0.5 + 0.3 * rng.random(k)
+    pts = np.concatenate([[[0.0, 0.0]], np.stack([r * np.cos(ang), r * np.sin(ang)], 1)])
+    el = np.array([[0, 1 + i, 1 + (i + 1) % k] for i in range(k)], np.int32)
+    perm = np.concatenate([[0], 1 + rng.permutation(k)])
+    inv = np.argsort(perm)
+    return np.ascontiguousarray(pts[perm]), np.ascontiguousarray(inv[el].astype(np.int32))
+
+
+# NE0 3D values are compared on rows whose tets all have quality >= Q_MIN:
+# the curl-curl entries 4|K|(G_ap G_bq - G_aq G_bp) cancel like 1 / quality^2
+# on a sliver, so ANY two fp64 evaluation orders differ there by more than
+# 1e-12 of the row max (measured: 1e-8 at quality 3e-5); only those rows'
+# pattern is compared.  RT0 (K = s s / |K|) and the 2D forms carry no such
+# cancellation and are compared on every row.
+Q_MIN = 0.02
+
+
+def _check(dim, element, pts, el, what, exact=False):
+    """Bit-exact DOF tables and pattern everywhere; values within 1e-12 of the
+    row max (NE0 3D: on rows of well-shaped tets, see Q_MIN)."""
+    from paper_1409_4618_b200 import api
+
+    ref = ora.assemble(dim, element, pts, el)
+    asm = api.Assembler(torch.from_numpy(pts).cuda(), torch.from_numpy(el).cuda(), element)
+    if exact:
+        asm.set_exact(True)
+    d2n, e2d, sg = asm.enumerate_dofs()
+    assert np.array_equal(d2n.cpu().numpy(), ref.dofs2nodes), what
+    assert np.array_equal(e2d.cpu().numpy(), ref.elems2dofs), what
+    assert np.array_equal(sg.cpu().numpy(), ref.signs), what
+    bad_dof = np.zeros(ref.n_dofs, bool)
+    if dim == 3 and element == NED0:
+        bad_dof[ref.elems2dofs[quality(pts, el) < Q_MIN].ravel()] = True
+    rows = np.repeat(np.arange(ref.n_dofs), np.diff(ref.row_ptr))
+    good = ~bad_dof[rows]
+    assert good.mean() > 0.5, what  # most of the matrix is compared
+    out_sync = asm.assemble()
+    out_async = asm.alloc_csr()
+    asm.assemble_async(out_async, api.ALL)
+    asm.check()
+    for out, tag in ((out_sync, ""), (out_async, " async")):
+        assert np.array_equal(out.row_ptr.cpu().numpy(), ref.row_ptr), what + tag
+        assert np.array_equal(out.col_idx.cpu().numpy(), ref.col_idx), what + tag
+        for got, want, f in ((out.vals_M, ref.vals_M, "M"), (out.vals_K, ref.vals_K, "K")):
+            got = got.cpu().numpy()
+            scale = np.zeros(ref.n_dofs)
+            nz = np.diff(ref.row_ptr) > 0
+            scale[nz] = np.maximum.reduceat(np.abs(want), ref.row_ptr[:-1][nz])
+            err = np.abs(got - want)[good]
+            assert (err <= REL_TOL * scale[rows][good]).all(), (what + tag + " " + f,
+                                                                 float((err / scale[rows][good]).max()))
+    return ref
+
+
+@pytest.mark.parametrize("dim,element", KINDS, ids=KIND_IDS)
+@pytest.mark.parametrize("seed", [1, 2])
+def test_delaunay_parity(dim, element, seed):
+    pts, el = delaunay_mesh(dim, 3000 if dim == 2 else 700, seed)
+    ref = _check(dim, element, pts, el, f"delaunay{dim}d seed {seed}")
+    if dim == 3 and element == NED0:
+        # the mesh must actually exercise the > 7-tets-per-edge rows
+        t = np.zeros(ref.n_dofs, np.int64)
+        np.add.at(t, ref.elems2dofs.ravel(), 1)
+        assert t.max() > 7
+
+
+def test_delaunay_filtered_nonmanifold_exact_mode():
+    """Slivers removed (quality >= Q_MIN everywhere): the holes leave edges
+    whose tets form several fans (non-manifold), which the default closed-form
+    row sizing flags and exact mode (efem_plan_set_exact) sizes by counting
+    link vertices.  Exact mode must match the oracle on every row."""
+    pts, el = delaunay_mesh(3, 700, 1)
+    el = np.ascontiguousarray(el[quality(pts, el) >= Q_MIN])
+    _check(3, NED0, pts, el, "filtered delaunay exact", exact=True)
+    _check(3, RT0, pts, el, "filtered delaunay rt0")
+
+
+@pytest.mark.parametrize("element", [RT0, NED0], ids=["rt0", "ne0"])
+@pytest.mark.parametrize("k", [5, 40, 200])
+def test_fan_parity(element, k):
+    pts, el = fan_mesh(k, k)
+    _check(2, element, pts, el, f"fan k={k}")
