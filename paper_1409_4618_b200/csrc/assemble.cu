@@ -9,6 +9,7 @@
 // Rows are staged in shared memory (per warp: k_rows_tri; per CTA:
 // k_rows_ne3) and written out with coalesced stores, so every CSR byte is
 // written exactly once and no local matrix ever reaches HBM.
+#include <atomic>
 #include <type_traits>
 
 #include "element.cuh"
@@ -16,6 +17,7 @@
 namespace efem {
 
 constexpr int NUM_TPB = 128;
+constexpr int kMaxDevices = 64;
 
 // ---------------------------------------------------------------------------------
 // 2D edges and 3D faces.  In a conforming mesh an entity lies in t <= 2
@@ -859,14 +861,18 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
     if constexpr (KT::D == 2 || KT::FACES) {
         using P = std::conditional_t<KT::D == 2, TriPolicy, FacePolicy>;
         constexpr int MINB = 2;
-        static int grid = 0;
+        // persistent grid = SMs x resident CTAs, per device (cached)
+        static std::atomic<int> grids[kMaxDevices];
+        int dev = 0;
+        EFEM_CUDA_TRY(cudaGetDevice(&dev));
+        int grid = dev < kMaxDevices ? grids[dev].load(std::memory_order_relaxed) : 0;
         if (!grid) {
-            int dev = 0, sms = 0, per_sm = 0;
-            EFEM_CUDA_TRY(cudaGetDevice(&dev));
+            int sms = 0, per_sm = 0;
             EFEM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
             EFEM_CUDA_TRY(
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_tri<KT, P, MINB>, TRI_TPB, 0));
             grid = sms * (per_sm > 0 ? per_sm : 1);
+            if (dev < kMaxDevices) grids[dev].store(grid, std::memory_order_relaxed);
         }
         const int64_t need = (w.n_rows + TRI_TPB - 1) / TRI_TPB;
         k_rows_tri<KT, P, MINB><<<(unsigned)(need < grid ? need : grid), TRI_TPB, 0, s>>>(
@@ -874,11 +880,13 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
             w.out_base, forms, out->row_ptr, out->col_idx, vm, vk, p.hdr, (int)w.dyn, (long long)w.cap_nnz, w.win);
     } else {
         const int fast_ids = p.n_nodes < (1ll << 27);
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<bool> attr[kMaxDevices];  // the smem opt-in is per device
+        int dev = 0;
+        EFEM_CUDA_TRY(cudaGetDevice(&dev));
+        if (dev >= kMaxDevices || !attr[dev].load(std::memory_order_relaxed)) {
             EFEM_CUDA_TRY(cudaFuncSetAttribute(k_rows_ne3<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)NE3_SMEM));
-            attr = true;
+            if (dev < kMaxDevices) attr[dev].store(true, std::memory_order_relaxed);
         }
         k_rows_ne3<KT><<<grid_for(w.n_rows, NUM_TPB), NUM_TPB, NE3_SMEM, s>>>(p.coords, p.elems, inc_ptr, p.bucket, w.e2d, row_ptr,
                                                        (int)w.n_rows, w.own_base, w.out_base, forms, fast_ids,
