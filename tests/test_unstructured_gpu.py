@@ -132,3 +132,50 @@ def test_delaunay_filtered_nonmanifold_exact_mode():
 def test_fan_parity(element, k):
     pts, el = fan_mesh(k, k)
     _check(2, element, pts, el, f"fan k={k}")
+
+
+@pytest.mark.parametrize("dim,element", KINDS, ids=KIND_IDS)
+def test_delaunay_sweep_small(dim, element):
+    """Many tiny unstructured meshes (4 .. 60 random points, 12 seeds): one to
+    a few hundred elements, mostly boundary entities -- DOF tables, pattern
+    and values against the oracle, both assembly paths."""
+    for seed in range(12):
+        n_pts = [1, 2, 5, 9, 17, 30, 45, 60][seed % 8]
+        pts, el = delaunay_mesh(dim, n_pts, 100 + seed)
+        if el.shape[0] == 0:
+            continue
+        _check(dim, element, pts, el, f"sweep {dim}d n={n_pts} seed={seed}")
+
+
+@pytest.mark.parametrize("dim,element", KINDS, ids=KIND_IDS)
+@pytest.mark.parametrize("P", [3, 5])
+def test_delaunay_partitioned_async(dim, element, P):
+    """Row-owned partitions of an unstructured mesh (irregular sub-meshes,
+    uneven ownership), asynchronous form: the slices concatenate to the
+    1-GPU CSR byte for byte."""
+    from paper_1409_4618_b200 import api, dist
+
+    pts, el = delaunay_mesh(dim, 1500 if dim == 2 else 300, 7)
+    coords, elems = torch.from_numpy(pts).cuda(), torch.from_numpy(el).cuda()
+    one = api.Assembler(coords, elems, element).assemble()
+    ranges = dist.node_ranges(coords.shape[0], P)
+    W = max(hi - lo for lo, hi in ranges)
+    parts = [dist.PartAssembler(coords, elems, element, lo, hi) for lo, hi in ranges]
+    for p in parts:
+        p.symbolic()
+    gcnt = torch.cat([p.symbolic() for p in parts])
+    for p in parts:
+        p.globalize(gcnt)
+    caps = [p.alloc_slice() for p in parts]
+    for p in parts:
+        p.bind(W, P)
+    owned = torch.cat([p.enumerate_async().clone() for p in parts])
+    for p, c in zip(parts, caps):
+        p.globalize_async(owned)
+        p.numeric_async(c)
+        p.check()
+    offs, total = dist.offsets_from_counts([int(p.window[3].item()) for p in parts])
+    assert total == one.nnz
+    rp, ci, vm, vk = dist.concat_slices(caps, offs)
+    assert np.array_equal(rp, one.row_ptr.cpu().numpy()) and np.array_equal(ci, one.col_idx.cpu().numpy())
+    assert np.array_equal(vm, one.vals_M.cpu().numpy()) and np.array_equal(vk, one.vals_K.cpu().numpy())
