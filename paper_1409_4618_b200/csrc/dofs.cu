@@ -325,7 +325,7 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
     }
     int nd = 0;
     bool over = false;
-    constexpr int U = 4;  // keys loaded ahead of use
+    constexpr int U = 8;  // keys loaded ahead of use
     for (int j0 = 0; j0 < n; j0 += U) {
         int bb[U];
 #pragma unroll
