@@ -300,7 +300,7 @@ __device__ __forceinline__ TriL1 tri_l1(const int32_t* __restrict__ inc_ptr, con
     return a;
 }
 
-template <class KT, class P, int MINB>
+template <class KT, class P, int MINB, bool WIN>
 __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __restrict__ coords,
                                                            const int32_t* __restrict__ elems,
                                                            const int32_t* __restrict__ inc_ptr,
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
                                                            const long long* __restrict__ win) {
     constexpr int M = P::M, NO = M - 1;
     int n_rows = dyn ? dyn_rows(hdr, n_rows_arg, cap_nnz) : n_rows_arg;
-    if (win) {
+    if constexpr (WIN) {  // (a template flag: the common path carries none of this)
         n_rows = win_rows(hdr, win, n_rows_arg, cap_nnz);
         if (n_rows > 0) {
             row0 = (int)win[0];
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
         }
     }
     if (n_rows <= 0) {
-        if ((dyn || win) && n_rows == 0 && blockIdx.x == 0 && threadIdx.x == 0 && (forms & EFEM_PATTERN))
+        if ((dyn || WIN) && n_rows == 0 && blockIdx.x == 0 && threadIdx.x == 0 && (forms & EFEM_PATTERN))
             row_ptr_out[0] = 0;
         return;
     }
@@ -861,23 +861,28 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
     if constexpr (KT::D == 2 || KT::FACES) {
         using P = std::conditional_t<KT::D == 2, TriPolicy, FacePolicy>;
         constexpr int MINB = 2;
-        // persistent grid = SMs x resident CTAs, per device (cached)
-        static std::atomic<int> grids[kMaxDevices];
-        int dev = 0;
-        EFEM_CUDA_TRY(cudaGetDevice(&dev));
-        int grid = dev < kMaxDevices ? grids[dev].load(std::memory_order_relaxed) : 0;
-        if (!grid) {
-            int sms = 0, per_sm = 0;
-            EFEM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            EFEM_CUDA_TRY(
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_tri<KT, P, MINB>, TRI_TPB, 0));
-            grid = sms * (per_sm > 0 ? per_sm : 1);
-            if (dev < kMaxDevices) grids[dev].store(grid, std::memory_order_relaxed);
-        }
-        const int64_t need = (w.n_rows + TRI_TPB - 1) / TRI_TPB;
-        k_rows_tri<KT, P, MINB><<<(unsigned)(need < grid ? need : grid), TRI_TPB, 0, s>>>(
-            p.coords, p.elems, inc_ptr, p.rec + (w.win ? 0 : w.row0), w.e2d, (int)w.row0, (int)w.n_rows, w.own_base,
-            w.out_base, forms, out->row_ptr, out->col_idx, vm, vk, p.hdr, (int)w.dyn, (long long)w.cap_nnz, w.win);
+        auto launch = [&](auto kern) -> efem_status {
+            // persistent grid = SMs x resident CTAs, per device (cached)
+            static std::atomic<int> grids[kMaxDevices];
+            int dev = 0;
+            EFEM_CUDA_TRY(cudaGetDevice(&dev));
+            int grid = dev < kMaxDevices ? grids[dev].load(std::memory_order_relaxed) : 0;
+            if (!grid) {
+                int sms = 0, per_sm = 0;
+                EFEM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+                EFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TRI_TPB, 0));
+                grid = sms * (per_sm > 0 ? per_sm : 1);
+                if (dev < kMaxDevices) grids[dev].store(grid, std::memory_order_relaxed);
+            }
+            const int64_t need = (w.n_rows + TRI_TPB - 1) / TRI_TPB;
+            kern<<<(unsigned)(need < grid ? need : grid), TRI_TPB, 0, s>>>(
+                p.coords, p.elems, inc_ptr, p.rec + (w.win ? 0 : w.row0), w.e2d, (int)w.row0, (int)w.n_rows,
+                w.own_base, w.out_base, forms, out->row_ptr, out->col_idx, vm, vk, p.hdr, (int)w.dyn,
+                (long long)w.cap_nnz, w.win);
+            return EFEM_OK;
+        };
+        const efem_status st = w.win ? launch(k_rows_tri<KT, P, MINB, true>) : launch(k_rows_tri<KT, P, MINB, false>);
+        if (st != EFEM_OK) return st;
     } else {
         const int fast_ids = p.n_nodes < (1ll << 27);
         static std::atomic<bool> attr[kMaxDevices];  // the smem opt-in is per device
