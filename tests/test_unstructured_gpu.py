@@ -179,3 +179,38 @@ def test_delaunay_partitioned_async(dim, element, P):
     rp, ci, vm, vk = dist.concat_slices(caps, offs)
     assert np.array_equal(rp, one.row_ptr.cpu().numpy()) and np.array_equal(ci, one.col_idx.cpu().numpy())
     assert np.array_equal(vm, one.vals_M.cpu().numpy()) and np.array_equal(vk, one.vals_K.cpu().numpy())
+
+
+@pytest.mark.parametrize("dim,element", [(3, NED0), (2, NED0)], ids=["ne0_3d", "ne0_2d"])
+def test_node_ids_beyond_2e27(dim, element):
+    """Node ids straddling 2^27 (a coordinate array of 2^27 + 64 nodes, most of
+    them unused): the NE0-3D fast path packs node ids into 27 bits and must
+    hand such meshes to the generic path.  The relabelling is monotone, so
+    DOF numbering, signs and values equal the compact mesh's (oracle)."""
+    from paper_1409_4618_b200 import api
+
+    pts, el = delaunay_mesh(dim, 40 if dim == 3 else 60, 3)
+    ref = ora.assemble(dim, element, pts, el)
+    n = pts.shape[0]
+    off = (1 << 27) - n // 2
+    N = off + n
+    coords = torch.zeros((N, dim), dtype=torch.float64, device="cuda")
+    coords[off:] = torch.from_numpy(pts).cuda()
+    elems = torch.from_numpy(el + off).cuda()
+    asm = api.Assembler(coords, elems, element)
+    out = asm.assemble()
+    assert np.array_equal(out.row_ptr.cpu().numpy(), ref.row_ptr)
+    assert np.array_equal(out.col_idx.cpu().numpy(), ref.col_idx)
+    for got, want in ((out.vals_M, ref.vals_M), (out.vals_K, ref.vals_K)):
+        got = got.cpu().numpy()
+        scale = np.maximum.reduceat(np.abs(want), ref.row_ptr[:-1])
+        rows = np.repeat(np.arange(ref.n_dofs), np.diff(ref.row_ptr))
+        if dim == 3:  # (see Q_MIN: rows of slivers are conditioning-limited)
+            bad = np.zeros(ref.n_dofs, bool)
+            bad[ref.elems2dofs[quality(pts, el) < Q_MIN].ravel()] = True
+            keep = ~bad[rows]
+        else:
+            keep = np.ones(rows.size, bool)
+        assert (np.abs(got - want)[keep] <= REL_TOL * scale[rows][keep]).all()
+    del asm, out, coords
+    torch.cuda.empty_cache()
