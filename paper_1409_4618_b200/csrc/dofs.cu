@@ -414,11 +414,10 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
 // sorted distinct list and counts in registers (as node_group_ne3), counting
 // scatter, then each face's two tets in element order.  Returns false when
 // the node has more than FDC distinct faces (caller sorts generically).
-template <class KT>
+template <class KT, int FDC>
 __device__ __forceinline__ bool node_group_faces(const BucketArrays& B, int32_t* __restrict__ gb, int64_t beg,
                                                  int n, int* s_cur, int& n_ent) {
     constexpr int TPB = NodeCaps<KT>::TPB;
-    constexpr int FDC = 16;
     int* Cur = s_cur + threadIdx.x;  // [p * TPB]
     const ulonglong2* __restrict__ rec = reinterpret_cast<const ulonglong2*>(B.key) + beg;
     uint64_t D[FDC];
@@ -612,7 +611,10 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
     } else if constexpr (KT::FACES) {
         // (fallback sorts in global memory: the fast path needs no key staging,
         // so the CTA keeps its shared memory small)
-        if (!node_group_faces<KT>(B, gb, beg, n, s_cur, n_ent)) node_sort_generic<KT, false>(B, gb, beg, n, s_key, s_inst, n_ent);
+        // (12 distinct faces cover structured tet meshes; 16, then a generic sort)
+        if (!node_group_faces<KT, 12>(B, gb, beg, n, s_cur, n_ent) &&
+            !node_group_faces<KT, 16>(B, gb, beg, n, s_cur, n_ent))
+            node_sort_generic<KT, false>(B, gb, beg, n, s_key, s_inst, n_ent);
     } else {
         if (exact || !node_group_ne3<KT>(B, gb, beg, n, a, s_grp, n_ent, n_nnz)) {
             n_ent = 0;
