@@ -305,7 +305,7 @@ __device__ __forceinline__ void node_sort_generic(const BucketArrays& B, int32_t
 // flag on group starts) and group q's b at x[q] (compact, so the write-back
 // is a sector or two per node; read by k_node_write).  Returns false when the node has more than DCAP
 // distinct larger neighbours (caller falls back to the generic sort).
-template <class KT>
+template <class KT, int DC>
 __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* __restrict__ gb, int64_t beg, int n,
                                                int a, int* s_grp, int& n_ent, int& n_nnz) {
     // The distinct list D (ascending) and the per-group counts live in
@@ -313,9 +313,9 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
     // insertions are compare / select chains with no dependent shared-memory
     // round trips.  The scatter cursors and link xors use shared memory.
     constexpr int TPB = NodeCaps<KT>::TPB;
-    constexpr int DC = NodeCaps<KT>::DCAP;
-    int* Cur = s_grp + threadIdx.x;  // [p * TPB]: running cursor of group p
-    int* X = Cur + DC * TPB;         // xor of link edges of group p
+    static_assert(DC <= NodeCaps<KT>::DCAP, "shared scratch sized for DCAP groups");
+    int* Cur = s_grp + threadIdx.x;                   // [p * TPB]: running cursor of group p
+    int* X = Cur + NodeCaps<KT>::DCAP * TPB;          // xor of link edges of group p
     const ulonglong2* __restrict__ rec = reinterpret_cast<const ulonglong2*>(B.key) + beg;
     int D[DC], C[DC];
 #pragma unroll
@@ -616,7 +616,9 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
             !node_group_faces<KT, 16>(B, gb, beg, n, s_cur, n_ent))
             node_sort_generic<KT, false>(B, gb, beg, n, s_key, s_inst, n_ent);
     } else {
-        if (exact || !node_group_ne3<KT>(B, gb, beg, n, a, s_grp, n_ent, n_nnz)) {
+        // (8 distinct larger neighbours cover structured tet meshes; 12, then a generic sort)
+        if (exact || (!node_group_ne3<KT, 8>(B, gb, beg, n, a, s_grp, n_ent, n_nnz) &&
+                      !node_group_ne3<KT, NodeCaps<KT>::DCAP>(B, gb, beg, n, a, s_grp, n_ent, n_nnz))) {
             n_ent = 0;
             n_nnz = 0;
             // (the NE3 instantiation has no key smem: sort in global memory)
