@@ -521,7 +521,7 @@ __device__ __forceinline__ int pair_index(int p, int q, int nw) {  // p < q
 // CTA's shared staging columns (stride NE3_LD), so every accumulator access
 // is a shared-memory instruction; otherwise they are the row's CSR segment
 // in global memory (stride 1, an oversize row in the tile).
-template <class KT, bool SM>
+template <class KT, bool SM, int TM>
 __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, const int32_t* __restrict__ elems,
                                              const int32_t* __restrict__ inc, const int32_t* __restrict__ e2d,
                                              int own_base, int i, int ib, int t, int rlen, unsigned char* P,
@@ -529,17 +529,17 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                                              bool& done) {
     constexpr int st = SM ? NE3_LD : 1;
     uint32_t key[16];
-    int inst[NE3_TMAX], roles[NE3_TMAX];
+    int inst[TM], roles[TM];
     int a = 0, b = 0;
     // all index loads first, then all element loads: two round trips
     // (slots j >= t repeat the last incidence and are masked below)
 #pragma unroll
-    for (int j = 0; j < NE3_TMAX; ++j) inst[j] = __ldg(inc + ib + min(j, t - 1)) & INST_MASK;
+    for (int j = 0; j < TM; ++j) inst[j] = __ldg(inc + ib + min(j, t - 1)) & INST_MASK;
     {   // ascending element id (the symbolic pass groups a node's tets
         // by edge without ordering them): a fixed summation order
         int srt[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) srt[j] = j < t && j < NE3_TMAX ? inst[j] : INT_MAX;
+        for (int j = 0; j < 8; ++j) srt[j] = j < t && j < TM ? inst[j] : INT_MAX;
 #pragma unroll
         for (int kk = 2; kk <= 8; kk <<= 1)
 #pragma unroll
@@ -558,15 +558,15 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
         // srt in local memory)
         int last = srt[0];
 #pragma unroll
-        for (int j = 1; j < NE3_TMAX; ++j) last = j == t - 1 ? srt[j] : last;
+        for (int j = 1; j < TM; ++j) last = j == t - 1 ? srt[j] : last;
 #pragma unroll
-        for (int j = 0; j < NE3_TMAX; ++j) inst[j] = j < t ? srt[j] : last;
+        for (int j = 0; j < TM; ++j) inst[j] = j < t ? srt[j] : last;
     }
-    int4 gq[NE3_TMAX];
+    int4 gq[TM];
 #pragma unroll
-    for (int j = 0; j < NE3_TMAX; ++j) gq[j] = __ldg(reinterpret_cast<const int4*>(elems) + (inst[j] >> 3));
+    for (int j = 0; j < TM; ++j) gq[j] = __ldg(reinterpret_cast<const int4*>(elems) + (inst[j] >> 3));
 #pragma unroll
-    for (int j = 0; j < NE3_TMAX; ++j) {
+    for (int j = 0; j < TM; ++j) {
         const int pe = inst[j];
         const int k = pe & 7;
         const int g[4] = {gq[j].x, gq[j].y, gq[j].z, gq[j].w};
@@ -586,6 +586,8 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
         key[2 * j] = live ? (((uint32_t)sel4(g, lc) << 5) | (uint32_t)(2 * j)) : 0xffffffffu;
         key[2 * j + 1] = live ? (((uint32_t)sel4(g, ld) << 5) | (uint32_t)(2 * j + 1)) : 0xffffffffu;
     }
+#pragma unroll
+    for (int x = 2 * TM; x < 14; ++x) key[x] = 0xffffffffu;  // (unused slots when TM < 7)
     key[14] = ((uint32_t)a << 5) | 14u;
     key[15] = ((uint32_t)b << 5) | 15u;
 #pragma unroll
@@ -619,9 +621,9 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
         const int iab = pair_index(pa, pb, nw);
         // column mask over lexicographic pairs of W positions
         unsigned long long mask = 1ull << iab;
-        int pidx[NE3_TMAX];  // packed pair indices: ac | ad << 6 | bc << 12 | bd << 18 | cd << 24
+        int pidx[TM];  // packed pair indices: ac | ad << 6 | bc << 12 | bd << 18 | cd << 24
 #pragma unroll
-        for (int j = 0; j < NE3_TMAX; ++j) {
+        for (int j = 0; j < TM; ++j) {
             if (j < t) {
                 const int pc = P[(2 * j) * NUM_TPB], pd = P[(2 * j + 1) * NUM_TPB];
                 const int iac = pair_index(min(pa, pc), max(pa, pc), nw);
@@ -666,7 +668,7 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                 xb[cc] = __ldg(coords + b * 3 + cc);
             }
 #pragma unroll
-            for (int j = 0; j < NE3_TMAX; ++j) {
+            for (int j = 0; j < TM; ++j) {
                 if (j < t) {
                     const int e = inst[j] >> 3;
                     const int rl = roles[j];
@@ -818,12 +820,18 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
         bool ok = false, done = false;
         if (fast_ids && t >= 1 && t <= NE3_TMAX) {
             unsigned char* P = s_pos + threadIdx.x;  // P[src * NUM_TPB]
-            if (staged)
-                ne3_fast_row<KT, true>(coords, elems, inc, e2d, own_base, i, ib, t, rlen, P, s_col + threadIdx.x,
-                                       s_vm + threadIdx.x, s_vk + threadIdx.x, hdr, ok, done);
+            // (rows of <= 6 tets -- every row of a structured tet mesh -- take a
+            // 6-slot instantiation: fewer live registers)
+            if (staged && t <= 6)
+                ne3_fast_row<KT, true, 6>(coords, elems, inc, e2d, own_base, i, ib, t, rlen, P, s_col + threadIdx.x,
+                                          s_vm + threadIdx.x, s_vk + threadIdx.x, hdr, ok, done);
+            else if (staged)
+                ne3_fast_row<KT, true, NE3_TMAX>(coords, elems, inc, e2d, own_base, i, ib, t, rlen, P,
+                                                 s_col + threadIdx.x, s_vm + threadIdx.x, s_vk + threadIdx.x, hdr, ok,
+                                                 done);
             else
-                ne3_fast_row<KT, false>(coords, elems, inc, e2d, own_base, i, ib, t, rlen, P, ccol, cvm, cvk, hdr,
-                                        ok, done);
+                ne3_fast_row<KT, false, NE3_TMAX>(coords, elems, inc, e2d, own_base, i, ib, t, rlen, P, ccol, cvm,
+                                                  cvk, hdr, ok, done);
         }
         if (!done) ok = row_generic<KT>(coords, elems, inc, e2d, ib, t, rlen, ccol, cvm, cvk, st, hdr);
         if (!ok) atomicOr(&hdr->flags[F_ROW_MISMATCH], 1);
