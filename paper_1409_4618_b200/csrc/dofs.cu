@@ -682,15 +682,23 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
     const bool live = a64 < n_nodes;
     const int a = (int)a64;
     // node offsets: tile prefix (scanned tile totals) + scan within the tile
-    int e_off, z_off = 0;
-    BlockScan(scan_tmp).ExclusiveSum(live ? __ldg(ent_cnt + a) : 0, e_off);
-    e_off += __ldg(ent_bpre + blockIdx.x);
+    int e_off, z_off = 0, e_tot;
+    const int e_base = __ldg(ent_bpre + blockIdx.x);
+    BlockScan(scan_tmp).ExclusiveSum(live ? __ldg(ent_cnt + a) : 0, e_off, e_tot);
+    e_off += e_base;
     if constexpr (NE3) {
         __syncthreads();
         BlockScan(scan_tmp).ExclusiveSum(live ? __ldg(nnz_cnt + a) : 0, z_off);
         z_off += __ldg(nnz_bpre + blockIdx.x);
     }
-    if (!live) return;
+    // 2D edges / 3D faces: the CTA's entities are the contiguous ids
+    // [e_base, e_base + e_tot); their records and incidence offsets are staged
+    // in shared memory and stored coalesced (when they fit)
+    constexpr int SREC = NE3 ? 1 : 4 * TPB;
+    __shared__ int2 s_rec[SREC];
+    __shared__ int s_inc[SREC];
+    const bool stage = !NE3 && e_tot <= SREC;
+    if (live) {
     ent_ptr[a] = e_off;
     const int beg = __ldg(bucket_ptr + a);
     const int n = __ldg(bucket_ptr + a + 1) - beg;
@@ -703,7 +711,8 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
         if constexpr (NE3) {
             nnz_run += 1 + 3 * t + 2 * excess;  // 1 + 2L + t, L = t + excess
         } else {
-            out.rec[id] = make_int2(first, prev);
+            if (stage) s_rec[id - e_base] = make_int2(first, prev);
+            else out.rec[id] = make_int2(first, prev);
             // a conforming mesh has <= 2 elements per edge (2D) / face (3D)
             if (t > 2) atomicOr(&out.flags[F_ROW_MISMATCH], 1);
         }
@@ -715,7 +724,8 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
             ++id;
             run0 = j;
             first = inst;
-            out.inc_ptr[id] = beg + j;
+            if (stage) s_inc[id - e_base] = beg + j;
+            else out.inc_ptr[id] = beg + j;
             if constexpr (NE3) {
                 out.row_ptr[id] = nnz_run;
                 // link excess L - t: the BND flag (0 / 1) on the manifold
@@ -765,6 +775,16 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
         out.totals[0] = R;
         // 2D edges / 3D faces: nnz = sum_i (1 + (m-1) t_i) = R + (m-1) (T m)
         out.totals[1] = NE3 ? (int64_t)nnz_run : (int64_t)R + (int64_t)(KT::M - 1) * (beg + n);
+    }
+    }
+    if constexpr (!NE3) {
+        if (stage) {
+            __syncthreads();
+            for (int x = threadIdx.x; x < e_tot; x += TPB) {
+                out.rec[e_base + x] = s_rec[x];
+                out.inc_ptr[e_base + x] = s_inc[x];
+            }
+        }
     }
 }
 
