@@ -694,10 +694,11 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
     // 2D edges / 3D faces: the CTA's entities are the contiguous ids
     // [e_base, e_base + e_tot); their records and incidence offsets are staged
     // in shared memory and stored coalesced (when they fit)
-    constexpr int SREC = NE3 ? 1 : 4 * TPB;
-    __shared__ int2 s_rec[SREC];
+    // (3D edges: incidence offsets, row offsets and the larger endpoints)
+    constexpr int SREC = NE3 ? 8 * TPB : 4 * TPB;
+    __shared__ int2 s_rec[SREC];  // 2D / faces: {first, last}; 3D edges: {row offset, larger endpoint}
     __shared__ int s_inc[SREC];
-    const bool stage = !NE3 && e_tot <= SREC;
+    const bool stage = e_tot <= SREC;
     if (live) {
     ent_ptr[a] = e_off;
     const int beg = __ldg(bucket_ptr + a);
@@ -727,14 +728,15 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
             if (stage) s_inc[id - e_base] = beg + j;
             else out.inc_ptr[id] = beg + j;
             if constexpr (NE3) {
-                out.row_ptr[id] = nnz_run;
+                if (!stage) out.row_ptr[id] = nnz_run;
                 // link excess L - t: the BND flag (0 / 1) on the manifold
                 // closed form, the exact count in exact mode
                 excess = bx ? __ldg(bx + beg + j) : (w & BND_FLAG ? 1 : 0);
                 // b, compacted by pass A
                 const int b = bx ? (int)(__ldg(bkey + (beg + grp) * 2) >> 32) : __ldg(bnb + beg + grp);
                 ++grp;
-                out.nbr[id] = b;
+                if (stage) s_rec[id - e_base] = make_int2(nnz_run, b);
+                else out.nbr[id] = b;
                 if (out.d2n) {
                     out.d2n[(int64_t)id * 2] = a;
                     out.d2n[(int64_t)id * 2 + 1] = b;
@@ -777,13 +779,17 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
         out.totals[1] = NE3 ? (int64_t)nnz_run : (int64_t)R + (int64_t)(KT::M - 1) * (beg + n);
     }
     }
-    if constexpr (!NE3) {
-        if (stage) {
-            __syncthreads();
-            for (int x = threadIdx.x; x < e_tot; x += TPB) {
-                out.rec[e_base + x] = s_rec[x];
-                out.inc_ptr[e_base + x] = s_inc[x];
+    if (stage) {
+        __syncthreads();
+        for (int x = threadIdx.x; x < e_tot; x += TPB) {
+            const int2 r = s_rec[x];
+            if constexpr (NE3) {
+                out.row_ptr[e_base + x] = r.x;
+                out.nbr[e_base + x] = r.y;
+            } else {
+                out.rec[e_base + x] = r;
             }
+            out.inc_ptr[e_base + x] = s_inc[x];
         }
     }
 }
