@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
     // [e_base, e_base + e_tot); their records and incidence offsets are staged
     // in shared memory and stored coalesced (when they fit)
     // (3D edges: incidence offsets, row offsets and the larger endpoints)
-    constexpr int SREC = NE3 ? 8 * TPB : 4 * TPB;
+    constexpr int SREC = NE3 ? 8 * TPB : (KT::FACES ? 16 * TPB : 4 * TPB);
     __shared__ int2 s_rec[SREC];  // 2D / faces: {first, last}; 3D edges: {row offset, larger endpoint}
     __shared__ int s_inc[SREC];
     const bool stage = e_tot <= SREC;
