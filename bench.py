@@ -5,9 +5,12 @@
 One JSON line on rank 0.  A "step" is one pass of the whole hot path over the
 device-resident mesh of the chosen BASELINE config: DOF enumeration + signs,
 sparsity pattern, local matrices and CSR values (efem_assemble_async, i.e.
-enumeration + pattern + numeric with the counts kept on the device, then
-efem_plan_check).  L2 is flushed between timed steps
-(a 512 MiB write, untimed).  value = elements / second over all ranks.
+enumeration + pattern + numeric with the counts kept on the device, then the
+read-back of the flags and sizes, efem_plan_check_async).  Each step's CUDA
+events bracket that device work; the host half of the check (wait, decode
+the flags) runs after the end event, every step.  L2 is flushed between
+timed steps (a 512 MiB write, untimed).  value = elements / second over all
+ranks.
 See DESIGN.md "Measurement" for the roofline bytes and the oracle baseline.
 """
 from __future__ import annotations
@@ -190,12 +193,14 @@ def run_efem(args, cfg):
 
     def step():
         # the whole hot path (enumeration, pattern, values) in one asynchronous
-        # call into the CSR sized by the first symbolic call, then the flag check
+        # call into the CSR sized by the first symbolic call, then the
+        # read-back of the flags and sizes (the device half of the check)
         asm.assemble_async(out, api.ALL)
-        asm.check()
+        asm.check_async()
 
     for _ in range(max(args.warmup, 3)):
         step()
+        asm.check()
     torch.cuda.synchronize()
 
     # timed region: K steps, each bracketed by its own events, L2 flushed in between (untimed)
@@ -209,6 +214,7 @@ def run_efem(args, cfg):
             starts[k].record(stream)
             step()
             ends[k].record(stream)
+            asm.check()  # host half of the check (wait + decode), every step, after the device window
         torch.cuda.synchronize()
     launches = api.launch_count() - l0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -284,8 +290,8 @@ def run_efem_dist(args, cfg):
     rank builds the full mesh (untimed) and its two-hop sub-mesh (untimed
     setup); a timed step is dist.AsyncStep (= assemble_rank_async): the rank's local
     enumeration, the two all_gathers (per-node entity counts, per-rank nnz),
-    globalisation, the owned-row numeric kernel and the flags check (one host
-    round trip).  Time = max over ranks of the summed per-step device time."""
+    globalisation, the owned-row numeric kernel and the flag read-back; the
+    host half of the check (one round trip) follows each step's end event.  Time = max over ranks of the summed per-step device time."""
     import torch
     import torch.distributed as dist
 
@@ -317,8 +323,9 @@ def run_efem_dist(args, cfg):
         for k in range(args.steps):
             flush.fill_(k & 0xff)
             starts[k].record(stream)
-            step()
+            step(check="async")
             ends[k].record(stream)
+            step.check()  # host half of the check (wait + decode), every step, after the device window
         torch.cuda.synchronize()
         dist.barrier()
     launches = api.launch_count() - l0

@@ -197,6 +197,13 @@ efem_status efem_assemble_async(efem_plan plan, unsigned forms, efem_csr* out, e
  * the last check flagged one, else EFEM_OK (or EFEM_ECUDA). */
 efem_status efem_plan_check(efem_plan plan, efem_stream_t stream);
 
+/* The device half of efem_plan_check: enqueues the read-back of the flags
+ * and sizes (one small D2H copy into the plan's pinned buffer) without
+ * waiting, so a timing event recorded after it brackets all device work of
+ * a step; efem_plan_check then waits and decodes (it copies again, so the
+ * result is never stale).  Never synchronises. */
+efem_status efem_plan_check_async(efem_plan plan, efem_stream_t stream);
+
 /* End-to-end convenience used for the "e2e" number: HOST mesh in, HOST CSR
  * out.  Copies h_coords / h_elems into the plan's device mesh arrays (the
  * plan must have been created on device arrays of the same sizes), runs

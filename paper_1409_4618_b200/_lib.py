@@ -75,6 +75,7 @@ def load():
         "efem_assemble_symbolic": (st, [vp, i64p, i64p, vp, vp]),
         "efem_assemble_numeric": (st, [vp, ctypes.c_uint, ctypes.POINTER(efem_csr), vp]),
         "efem_plan_check": (st, [vp, vp]),
+        "efem_plan_check_async": (st, [vp, vp]),
         "efem_assemble_async": (st, [vp, ctypes.c_uint, ctypes.POINTER(efem_csr), vp]),
         "efem_assemble_host": (st, [vp, vp, vp, ctypes.POINTER(efem_csr), ctypes.POINTER(efem_csr), vp]),
         "efem_partition": (st, [ctypes.POINTER(efem_mesh), i64, i64, vp, ctypes.POINTER(ctypes.c_size_t), i64p, i64p, vp, vp, vp, vp]),

@@ -194,6 +194,11 @@ class Assembler:
         with torch.cuda.device(self.device):
             _lib.check("efem_plan_check", _lib.load().efem_plan_check(self._plan, _stream(stream)))
 
+    def check_async(self, stream=None):
+        """Enqueue the flag / size read-back of check() without waiting."""
+        with torch.cuda.device(self.device):
+            _lib.check("efem_plan_check_async", _lib.load().efem_plan_check_async(self._plan, _stream(stream)))
+
     def assemble(self, out: CSR | None = None, stream=None) -> CSR:
         """End to end from the device mesh: symbolic + numeric + check."""
         self.symbolic(stream=stream)

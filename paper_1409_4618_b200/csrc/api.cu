@@ -556,6 +556,14 @@ efem_status efem_plan_check(efem_plan plan, efem_stream_t stream) {
     return st;
 }
 
+efem_status efem_plan_check_async(efem_plan plan, efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    efem_status st = need_ws(p);
+    if (st != EFEM_OK) return st;
+    EFEM_CUDA_TRY(cudaMemcpyAsync(p->h_hdr, p->hdr, sizeof(WsHeader), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    return EFEM_OK;
+}
+
 efem_status efem_assemble_async(efem_plan plan, unsigned forms, efem_csr* out, efem_stream_t stream) {
     Plan* p = reinterpret_cast<Plan*>(plan);
     efem_status st = need_ws(p);

@@ -322,9 +322,19 @@ class AsyncStep:
             dist.all_gather_into_tensor(self.nnz_all, self.nnz_mine, group=self.group)
         else:
             self.nnz_all = _allgather_dev(self.nnz_mine.contiguous(), self.group)
-        if check and not self.empty:
-            ck("efem_plan_check", L.efem_plan_check(self.plan, self.s))
+        if check == "async":  # only the device half (flag read-back); finish with check()
+            self.check_async()
+        elif check:
+            self.check()
         return self.out, self.part.window, self.nnz_all
+
+    def check_async(self):
+        if not self.empty:
+            _lib.check("efem_plan_check_async", self.L.efem_plan_check_async(self.plan, self.s))
+
+    def check(self):
+        if not self.empty:
+            _lib.check("efem_plan_check", self.L.efem_plan_check(self.plan, self.s))
 
 
 def assemble_rank_async(part: PartAssembler, ranges, out: CSR, group=None, stream=None, check=True):
