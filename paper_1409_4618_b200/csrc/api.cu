@@ -626,12 +626,9 @@ efem_status efem_assemble_async(efem_plan plan, unsigned forms, efem_csr* out, e
         cudaGetLastError();
     }
     if (p->g_async) {
-        EFEM_CUDA_TRY(cudaEventRecord(p->ev_in, s));
-        EFEM_CUDA_TRY(cudaStreamWaitEvent(p->gstream, p->ev_in, 0));
-        EFEM_CUDA_TRY(cudaGraphLaunch(p->g_async, p->gstream));
+        // (a graph captured on the plan's stream replays on the caller's)
+        EFEM_CUDA_TRY(cudaGraphLaunch(p->g_async, s));
         count_launch((int)p->async_launches);
-        EFEM_CUDA_TRY(cudaEventRecord(p->ev_out, p->gstream));
-        EFEM_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_out, 0));
         return EFEM_OK;
     }
     return enqueue(s);

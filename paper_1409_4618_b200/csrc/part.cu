@@ -471,12 +471,9 @@ efem_status efem_part_enumerate_async(efem_plan plan, int32_t* owned_cnt, efem_s
         cudaGetLastError();
     }
     if (p->g_part) {
-        EFEM_CUDA_TRY(cudaEventRecord(p->ev_in, s));
-        EFEM_CUDA_TRY(cudaStreamWaitEvent(p->gstream, p->ev_in, 0));
-        EFEM_CUDA_TRY(cudaGraphLaunch(p->g_part, p->gstream));
+        // (a graph captured on the plan's stream replays on the caller's)
+        EFEM_CUDA_TRY(cudaGraphLaunch(p->g_part, s));
         count_launch((int)p->part_launches);
-        EFEM_CUDA_TRY(cudaEventRecord(p->ev_out, p->gstream));
-        EFEM_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_out, 0));
         return EFEM_OK;
     }
     return enqueue(s);
