@@ -556,11 +556,29 @@ efem_status efem_plan_check(efem_plan plan, efem_stream_t stream) {
     return st;
 }
 
+// the header read-back as one warp's stores into the pinned (UVA-mapped)
+// host buffer: a posted PCIe write instead of a copy-engine transfer
+__global__ void k_mirror_hdr(const WsHeader* __restrict__ hdr, WsHeader* h_hdr) {
+    constexpr int W = sizeof(WsHeader) / 4;
+    const int* src = reinterpret_cast<const int*>(hdr);
+    volatile int* dst = reinterpret_cast<volatile int*>(h_hdr);
+    for (int i = threadIdx.x; i < W; i += 32) dst[i] = src[i];
+    __threadfence_system();
+}
+
 efem_status efem_plan_check_async(efem_plan plan, efem_stream_t stream) {
     Plan* p = reinterpret_cast<Plan*>(plan);
     efem_status st = need_ws(p);
     if (st != EFEM_OK) return st;
-    EFEM_CUDA_TRY(cudaMemcpyAsync(p->h_hdr, p->hdr, sizeof(WsHeader), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    WsHeader* dptr = nullptr;
+    if (cudaHostGetDevicePointer((void**)&dptr, p->h_hdr, 0) == cudaSuccess && dptr) {
+        k_mirror_hdr<<<1, 32, 0, (cudaStream_t)stream>>>(p->hdr, dptr);
+        EFEM_LAUNCH_CHECK();
+    } else {
+        cudaGetLastError();
+        EFEM_CUDA_TRY(cudaMemcpyAsync(p->h_hdr, p->hdr, sizeof(WsHeader), cudaMemcpyDeviceToHost,
+                                      (cudaStream_t)stream));
+    }
     return EFEM_OK;
 }
 
