@@ -223,30 +223,42 @@ __device__ __forceinline__ void global_deriv(const Geo<KT::D>& G, double s, int 
 __device__ __forceinline__ const Quad6& quad(int D) { return c_quad[D - 2]; }
 
 // ---- kernels ------------------------------------------------------------------------
+// One thread per element (its vertices gathered once), the CTA's points staged
+// in shared memory and stored coalesced.
+constexpr int QP_TPB = 128;
 template <int D>
-__global__ void k_quad_points(const double* __restrict__ coords, const int32_t* __restrict__ elems, int64_t n_elems,
-                              double* __restrict__ pts) {
+__global__ void __launch_bounds__(QP_TPB) k_quad_points(const double* __restrict__ coords,
+                                                        const int32_t* __restrict__ elems, int64_t n_elems,
+                                                        double* __restrict__ pts) {
     const Quad6& Q = quad(D);
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n_elems * Q.nq) return;
-    const int64_t e = i / Q.nq;
-    const int q = (int)(i - e * Q.nq);
-    double x[D];
-    double X0[D];
-    const int g0 = __ldg(elems + e * (D + 1));
+    constexpr int NQ = D == 2 ? 12 : 24;
+    constexpr int PER = NQ * D;  // doubles per element
+    constexpr int LD = PER + 1;  // padded row (odd stride: no shared-memory bank conflicts)
+    extern __shared__ double s_pts[];  // QP_TPB * LD
+    const int64_t e0 = (int64_t)blockIdx.x * QP_TPB;
+    const int64_t e = e0 + threadIdx.x;
+    if (e < n_elems) {
+        double X[D + 1][D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) X0[c] = __ldg(coords + (int64_t)g0 * D + c);
+        for (int v = 0; v <= D; ++v) {
+            const int gv = __ldg(elems + e * (D + 1) + v);
 #pragma unroll
-    for (int c = 0; c < D; ++c) x[c] = X0[c];
+            for (int c = 0; c < D; ++c) X[v][c] = __ldg(coords + (int64_t)gv * D + c);
+        }
 #pragma unroll
-    for (int v = 1; v <= D; ++v) {
-        const int gv = __ldg(elems + e * (D + 1) + v);
-        const double l = Q.l[q][v - 1];
+        for (int q = 0; q < NQ; ++q) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) x[c] += (__ldg(coords + (int64_t)gv * D + c) - X0[c]) * l;
+            for (int c = 0; c < D; ++c) {
+                double x = X[0][c];
+#pragma unroll
+                for (int v = 1; v <= D; ++v) x += (X[v][c] - X[0][c]) * Q.l[q][v - 1];
+                s_pts[threadIdx.x * LD + q * D + c] = x;
+            }
+        }
     }
-#pragma unroll
-    for (int c = 0; c < D; ++c) pts[i * D + c] = x[c];
+    __syncthreads();
+    const int64_t cnt = (n_elems - e0 < QP_TPB ? n_elems - e0 : QP_TPB) * PER;
+    for (int x = threadIdx.x; x < cnt; x += QP_TPB) pts[e0 * PER + x] = s_pts[(x / PER) * LD + x % PER];
 }
 
 // b_i = sum over the elements of DOF i (ascending element id) of
@@ -514,8 +526,17 @@ efem_status launch_quad_points(int dim, const double* coords, const int32_t* ele
     if ((st = ensure_quad()) != EFEM_OK) return st;
     const int64_t n = n_elems * quad6_size(dim);
     if (n == 0) return EFEM_OK;
-    if (dim == 2) k_quad_points<2><<<grid_for(n, 256), 256, 0, s>>>(coords, elems, n_elems, pts);
-    else k_quad_points<3><<<grid_for(n, 256), 256, 0, s>>>(coords, elems, n_elems, pts);
+    if (dim == 2)
+        k_quad_points<2><<<grid_for(n_elems, QP_TPB), QP_TPB, QP_TPB * 25 * 8, s>>>(coords, elems, n_elems, pts);
+    else {
+        static bool attr = false;  // 3D: 72 doubles per element -> 72 KB per CTA (opt-in)
+        if (!attr) {
+            EFEM_CUDA_TRY(cudaFuncSetAttribute(k_quad_points<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               QP_TPB * 73 * 8));
+            attr = true;
+        }
+        k_quad_points<3><<<grid_for(n_elems, QP_TPB), QP_TPB, QP_TPB * 73 * 8, s>>>(coords, elems, n_elems, pts);
+    }
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;
 }
