@@ -319,6 +319,74 @@ __global__ void __launch_bounds__(128) k_load(const double* __restrict__ coords,
     b[i] = acc;
 }
 
+// A CTA's per-element input rows (per doubles each, contiguous in src) into
+// shared memory rows of odd stride ld: coalesced loads, conflict-free
+// per-thread reads afterwards.  (row, col) advance incrementally: no division
+// in the loop.
+__device__ __forceinline__ void stage_rows(const double* __restrict__ src, int64_t cnt, int per, int ld,
+                                           double* __restrict__ dst) {
+    const int step_r = blockDim.x / per, step_c = blockDim.x % per;
+    int r = threadIdx.x / per, c = threadIdx.x % per;
+    constexpr int U = 8;  // loads in flight per thread
+    for (int64_t x0 = threadIdx.x; x0 < cnt; x0 += (int64_t)U * blockDim.x) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t x = x0 + (int64_t)u * blockDim.x;
+            v[u] = x < cnt ? __ldg(src + x) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (x0 + (int64_t)u * blockDim.x < cnt) dst[r * ld + c] = v[u];
+            r += step_r;
+            c += step_c;
+            if (c >= per) {
+                c -= per;
+                ++r;
+            }
+        }
+    }
+}
+
+constexpr int NORM_TPB = 128;
+template <int D>
+__global__ void __launch_bounds__(NORM_TPB) k_norm_elem_staged(const double* __restrict__ coords,
+                                                               const int32_t* __restrict__ elems, int64_t n_elems,
+                                                               const double* __restrict__ fq, int nf,
+                                                               double* __restrict__ per_elem) {
+    const Quad6& Q = quad(D);
+    constexpr int NQ = D == 2 ? 12 : 24;
+    const int per = NQ * nf, ld = per | 1;
+    extern __shared__ double s_f[];  // NORM_TPB * ld
+    const int64_t e0 = (int64_t)blockIdx.x * NORM_TPB;
+    const int64_t ne = n_elems - e0 < NORM_TPB ? n_elems - e0 : NORM_TPB;
+    const int64_t e = e0 + threadIdx.x;
+    // the element's geometry first: its gathers overlap the staging below
+    double adet = 0.0;
+    if (e < n_elems) {
+        int g[D + 1];
+#pragma unroll
+        for (int v = 0; v <= D; ++v) g[v] = __ldg(elems + e * (D + 1) + v);
+        Geo<D> G;
+        load_geo<D>(coords, g, G);
+        adet = fabs(G.det);
+    }
+    stage_rows(fq + e0 * per, ne * per, per, ld, s_f);
+    __syncthreads();
+    if (e >= n_elems) return;
+    const double* f = s_f + threadIdx.x * ld;
+    double acc = 0.0;
+    for (int q = 0; q < NQ; ++q) {
+        double f2 = 0.0;
+        for (int c = 0; c < nf; ++c) {
+            const double v = f[q * nf + c];
+            f2 += v * v;
+        }
+        acc += Q.w[q] * adet * f2;
+    }
+    per_elem[e] = acc;
+}
+
 template <int D>
 __global__ void k_norm_elem(const double* __restrict__ coords, const int32_t* __restrict__ elems, int64_t n_elems,
                             const double* __restrict__ fq, int nf, double* __restrict__ per_elem) {
@@ -569,8 +637,27 @@ efem_status launch_norm_l2(int dim, const double* coords, const int32_t* elems, 
     efem_status st;
     if ((st = ensure_quad()) != EFEM_OK) return st;
     if (n_elems > 0) {
-        if (dim == 2) k_norm_elem<2><<<grid_for(n_elems, 128), 128, 0, s>>>(coords, elems, n_elems, fq, nf, per_elem);
-        else k_norm_elem<3><<<grid_for(n_elems, 128), 128, 0, s>>>(coords, elems, n_elems, fq, nf, per_elem);
+        const int per = quad6_size(dim) * nf;
+        const size_t smem = (size_t)NORM_TPB * (per | 1) * 8;
+        if (smem <= 96 * 1024) {  // staged (coalesced) reads of the point values
+            static bool attr[2] = {false, false};
+            if (!attr[dim - 2]) {
+                EFEM_CUDA_TRY(cudaFuncSetAttribute(dim == 2 ? (const void*)k_norm_elem_staged<2>
+                                                            : (const void*)k_norm_elem_staged<3>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+                attr[dim - 2] = true;
+            }
+            if (dim == 2)
+                k_norm_elem_staged<2><<<grid_for(n_elems, NORM_TPB), NORM_TPB, smem, s>>>(coords, elems, n_elems, fq,
+                                                                                           nf, per_elem);
+            else
+                k_norm_elem_staged<3><<<grid_for(n_elems, NORM_TPB), NORM_TPB, smem, s>>>(coords, elems, n_elems, fq,
+                                                                                           nf, per_elem);
+        } else if (dim == 2) {
+            k_norm_elem<2><<<grid_for(n_elems, 128), 128, 0, s>>>(coords, elems, n_elems, fq, nf, per_elem);
+        } else {
+            k_norm_elem<3><<<grid_for(n_elems, 128), 128, 0, s>>>(coords, elems, n_elems, fq, nf, per_elem);
+        }
         EFEM_LAUNCH_CHECK();
     }
     return reduce_fixed(per_elem, n_elems, part, total, s);
