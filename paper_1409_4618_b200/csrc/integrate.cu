@@ -261,63 +261,6 @@ __global__ void __launch_bounds__(QP_TPB) k_quad_points(const double* __restrict
     for (int x = threadIdx.x; x < cnt; x += QP_TPB) pts[e0 * PER + x] = s_pts[(x / PER) * LD + x % PER];
 }
 
-// b_i = sum over the elements of DOF i (ascending element id) of
-// sum_q w_q |det| f(x_q) . phi_k(x_q)   (pairing 0)  or  . (div/curl phi_k)(x_q)  (pairing 1)
-template <class KT, int PAIR>
-__global__ void __launch_bounds__(128) k_load(const double* __restrict__ coords, const int32_t* __restrict__ elems,
-                                              const int32_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
-                                              int64_t n_dofs, const double* __restrict__ fq, double* __restrict__ b) {
-    constexpr int D = KT::D, NV = KT::NV;
-    constexpr int ND = n_deriv<KT>();
-    constexpr int NF = PAIR == 0 ? D : ND;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n_dofs) return;
-    const Quad6& Q = quad(D);
-    const int ib = __ldg(inc_ptr + i), t = min(__ldg(inc_ptr + i + 1) - ib, EFEM_MAX_ROW_ELEMS);
-    int ord[EFEM_MAX_ROW_ELEMS];  // ascending element order
-    for (int j = 0; j < t; ++j) {
-        const int v = __ldg(inc + ib + j) & INST_MASK;
-        int q = j;
-        while (q > 0 && ord[q - 1] > v) {
-            ord[q] = ord[q - 1];
-            --q;
-        }
-        ord[q] = v;
-    }
-    double acc = 0.0;
-    for (int j = 0; j < t; ++j) {
-        const int e = ord[j] >> 3, k = ord[j] & 7;
-        int g[NV];
-        load_g<KT>(elems, e, g);
-        Geo<D> G;
-        load_geo<D>(coords, g, G);
-        const double s = sign_d<KT>(g, k);
-        const double adet = fabs(G.det);
-        const double* f = fq + (int64_t)e * Q.nq * NF;
-        double loc = 0.0;
-        if constexpr (PAIR == 1) {
-            double dphi[ND];
-            global_deriv<KT>(G, s, k, dphi);
-            for (int q = 0; q < Q.nq; ++q) {
-                double dot = 0.0;
-#pragma unroll
-                for (int c = 0; c < NF; ++c) dot += __ldg(f + q * NF + c) * dphi[c];
-                loc += Q.w[q] * adet * dot;
-            }
-        } else {
-            for (int q = 0; q < Q.nq; ++q) {
-                double phi[D];
-                global_value<KT>(G, s, k, Q.l[q], phi);
-                double dot = 0.0;
-#pragma unroll
-                for (int c = 0; c < NF; ++c) dot += __ldg(f + q * NF + c) * phi[c];
-                loc += Q.w[q] * adet * dot;
-            }
-        }
-        acc += loc;
-    }
-    b[i] = acc;
-}
 
 // A CTA's per-element input rows (per doubles each, contiguous in src) into
 // shared memory rows of odd stride ld: coalesced loads, conflict-free
@@ -346,6 +289,101 @@ __device__ __forceinline__ void stage_rows(const double* __restrict__ src, int64
             }
         }
     }
+}
+
+// Load vector, element-parallel half: every element's m local contributions
+// l_k = sum_q w_q |det| f(x_q) . phi_k(x_q) (the same arithmetic, in the same
+// order, as the row-owner loop it replaces), its point values staged.
+template <class KT, int PAIR, int TPB>
+__global__ void __launch_bounds__(TPB) k_load_elem(const double* __restrict__ coords,
+                                                   const int32_t* __restrict__ elems, int64_t n_elems,
+                                                   const double* __restrict__ fq, double* __restrict__ loc) {
+    constexpr int D = KT::D, NV = KT::NV, M = KT::M;
+    constexpr int ND = n_deriv<KT>();
+    constexpr int NF = PAIR == 0 ? D : ND;
+    constexpr int NQ = D == 2 ? 12 : 24;
+    constexpr int PER = NQ * NF, LD = PER | 1;
+    extern __shared__ double s_f[];  // TPB * LD
+    const Quad6& Q = quad(D);
+    const int64_t e0 = (int64_t)blockIdx.x * TPB;
+    const int64_t ne = n_elems - e0 < TPB ? n_elems - e0 : TPB;
+    const int64_t e = e0 + threadIdx.x;
+    int g[NV];
+    Geo<D> G;
+    if (e < n_elems) {
+        load_g<KT>(elems, (int)e, g);
+        load_geo<D>(coords, g, G);
+    }
+    stage_rows(fq + e0 * PER, ne * PER, PER, LD, s_f);
+    __syncthreads();
+    if (e >= n_elems) return;
+    const double adet = fabs(G.det);
+    const double* f = s_f + threadIdx.x * LD;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        const double sk = sign_d<KT>(g, k);
+        double l = 0.0;
+        if constexpr (PAIR == 1) {
+            double dphi[ND];
+            global_deriv<KT>(G, sk, k, dphi);
+            for (int q = 0; q < NQ; ++q) {
+                double dot = 0.0;
+#pragma unroll
+                for (int c = 0; c < NF; ++c) dot += f[q * NF + c] * dphi[c];
+                l += Q.w[q] * adet * dot;
+            }
+        } else {
+            for (int q = 0; q < NQ; ++q) {
+                double phi[D];
+                global_value<KT>(G, sk, k, Q.l[q], phi);
+                double dot = 0.0;
+#pragma unroll
+                for (int c = 0; c < NF; ++c) dot += f[q * NF + c] * phi[c];
+                l += Q.w[q] * adet * dot;
+            }
+        }
+        loc[e * M + k] = l;
+    }
+}
+
+// Load vector, row-owner half: b_i = sum of the local contributions of the
+// DOF's elements in ascending element order (registers for t <= 4).
+template <class KT>
+__global__ void __launch_bounds__(256) k_load_gather(const int32_t* __restrict__ inc_ptr,
+                                                     const int32_t* __restrict__ inc, int64_t n_dofs,
+                                                     const double* __restrict__ loc, double* __restrict__ b) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_dofs) return;
+    const int ib = __ldg(inc_ptr + i), t = __ldg(inc_ptr + i + 1) - ib;
+    double acc = 0.0;
+    if (t <= 4) {
+        int w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = j < t ? (__ldg(inc + ib + j) & INST_MASK) : INT_MAX;
+#pragma unroll
+        for (int x = 0; x < 4; ++x)  // (a 4-element sorting network: 6 exchanges)
+#pragma unroll
+            for (int y = x + 1; y < 4; ++y) {
+                const int lo = min(w[x], w[y]), hi = max(w[x], w[y]);
+                w[x] = lo;
+                w[y] = hi;
+            }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < t) acc += __ldg(loc + (int64_t)(w[j] >> 3) * KT::M + (w[j] & 7));
+    } else {
+        int prev = -1;  // ascending element order by repeated minimum search (t is small)
+        for (int j = 0; j < t; ++j) {
+            int best = INT_MAX;
+            for (int u = 0; u < t; ++u) {
+                const int v = __ldg(inc + ib + u) & INST_MASK;
+                if (v > prev && v < best) best = v;
+            }
+            acc += __ldg(loc + (int64_t)(best >> 3) * KT::M + (best & 7));
+            prev = best;
+        }
+    }
+    b[i] = acc;
 }
 
 constexpr int NORM_TPB = 128;
@@ -609,15 +647,31 @@ efem_status launch_quad_points(int dim, const double* coords, const int32_t* ele
     return EFEM_OK;
 }
 
-template <class KT>
-efem_status load_kt(Plan& p, int pairing, const double* fq, double* b, cudaStream_t s) {
-    const unsigned grid = grid_for(p.n_dofs, 128);
-    if (pairing == 0)
-        k_load<KT, 0><<<grid, 128, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.n_dofs, fq, b);
-    else
-        k_load<KT, 1><<<grid, 128, 0, s>>>(p.coords, p.elems, p.inc_ptr, p.bucket, p.n_dofs, fq, b);
+// element contributions staged in the plan's bucket-key array (enumeration
+// scratch, >= 8 bytes per instance, free after the symbolic pass)
+template <class KT, int PAIR>
+efem_status load_kt2(Plan& p, const double* fq, double* b, cudaStream_t s) {
+    constexpr int TPB = 128;
+    constexpr int NF = PAIR == 0 ? KT::D : n_deriv<KT>();
+    constexpr int NQ = KT::D == 2 ? 12 : 24;
+    constexpr size_t smem = (size_t)TPB * ((NQ * NF) | 1) * 8;
+    static bool attr = false;
+    if (!attr) {
+        EFEM_CUDA_TRY(cudaFuncSetAttribute(k_load_elem<KT, PAIR, TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+        attr = true;
+    }
+    double* loc = reinterpret_cast<double*>(p.bkey);
+    k_load_elem<KT, PAIR, TPB><<<grid_for(p.n_elems, TPB), TPB, smem, s>>>(p.coords, p.elems, p.n_elems, fq, loc);
+    EFEM_LAUNCH_CHECK();
+    k_load_gather<KT><<<grid_for(p.n_dofs, 256), 256, 0, s>>>(p.inc_ptr, p.bucket, p.n_dofs, loc, b);
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;
+}
+
+template <class KT>
+efem_status load_kt(Plan& p, int pairing, const double* fq, double* b, cudaStream_t s) {
+    return pairing == 0 ? load_kt2<KT, 0>(p, fq, b, s) : load_kt2<KT, 1>(p, fq, b, s);
 }
 
 efem_status launch_load(Plan& p, int pairing, const double* fq, double* b, cudaStream_t s) {
