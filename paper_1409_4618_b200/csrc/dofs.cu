@@ -691,10 +691,12 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
         BlockScan(scan_tmp).ExclusiveSum(live ? __ldg(nnz_cnt + a) : 0, z_off);
         z_off += __ldg(nnz_bpre + blockIdx.x);
     }
-    // 2D edges / 3D faces: the CTA's entities are the contiguous ids
-    // [e_base, e_base + e_tot); their records and incidence offsets are staged
-    // in shared memory and stored coalesced (when they fit)
-    // (3D edges: incidence offsets, row offsets and the larger endpoints)
+    // The CTA's entities are the contiguous ids [e_base, e_base + e_tot); the
+    // per-entity outputs (2D edges / 3D faces: row records and incidence
+    // offsets; 3D edges: incidence offsets, row offsets, larger endpoints),
+    // which consecutive threads would interleave, are staged in shared memory
+    // and stored coalesced when they fit (capacity: the entities per node of
+    // structured meshes times the CTA size)
     constexpr int SREC = NE3 ? 8 * TPB : (KT::FACES ? 16 * TPB : 4 * TPB);
     __shared__ int2 s_rec[SREC];  // 2D / faces: {first, last}; 3D edges: {row offset, larger endpoint}
     __shared__ int s_inc[SREC];
