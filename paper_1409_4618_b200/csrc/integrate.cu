@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(QP_TPB) k_quad_points(const double* __restrict
 #pragma unroll
             for (int c = 0; c < D; ++c) X[v][c] = __ldg(coords + (int64_t)gv * D + c);
         }
-#pragma unroll
+#pragma unroll 4
         for (int q = 0; q < NQ; ++q) {
 #pragma unroll
             for (int c = 0; c < D; ++c) {
@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(TPB) k_load_elem(const double* __restrict__ co
         if constexpr (PAIR == 1) {
             double dphi[ND];
             global_deriv<KT>(G, sk, k, dphi);
+#pragma unroll 4
             for (int q = 0; q < NQ; ++q) {
                 double dot = 0.0;
 #pragma unroll
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(TPB) k_load_elem(const double* __restrict__ co
                 l += Q.w[q] * adet * dot;
             }
         } else {
+#pragma unroll 4
             for (int q = 0; q < NQ; ++q) {
                 double phi[D];
                 global_value<KT>(G, sk, k, Q.l[q], phi);
@@ -482,7 +484,9 @@ __global__ void k_field_error(const double* __restrict__ coords, const int32_t* 
     }
     const double adet = fabs(G.det);
     double a = 0.0, dd = 0.0;
-    for (int q = 0; q < Q.nq; ++q) {
+    constexpr int NQ = D == 2 ? 12 : 24;
+#pragma unroll 4
+    for (int q = 0; q < NQ; ++q) {
         double v[D];
 #pragma unroll
         for (int r = 0; r < D; ++r) v[r] = 0.0;
@@ -496,12 +500,12 @@ __global__ void k_field_error(const double* __restrict__ coords, const int32_t* 
         double ta = 0.0, td = 0.0;
 #pragma unroll
         for (int r = 0; r < D; ++r) {
-            const double x = __ldg(Eq + (e * Q.nq + q) * D + r) - v[r];
+            const double x = __ldg(Eq + (e * NQ + q) * D + r) - v[r];
             ta += x * x;
         }
 #pragma unroll
         for (int r = 0; r < ND; ++r) {
-            const double x = __ldg(Dq + (e * Q.nq + q) * ND + r) - dv[r];
+            const double x = __ldg(Dq + (e * NQ + q) * ND + r) - dv[r];
             td += x * x;
         }
         a += Q.w[q] * adet * ta;
