@@ -608,13 +608,88 @@ __global__ void k_cg_update(const double* __restrict__ sc, const double* __restr
 }
 
 // p = z + (rz_new / rz_old) p ; then rz_old = rz_new
-__global__ void k_cg_dir(double* __restrict__ sc, const double* __restrict__ z, int64_t n, double* __restrict__ p) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    p[i] = z[i] + (sc[2] / sc[0]) * p[i];
+
+
+// ---- fused CG iteration: the dot products are reduced per CTA by the kernel
+// that produces their terms (fixed shared-memory tree), then across CTAs by
+// one fixed-order final pass -- 5 launches per iteration instead of 11.
+__device__ __forceinline__ double cta_sum(double v, double* sm) {  // RED_TPB threads, fixed tree
+    sm[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = RED_TPB / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) sm[threadIdx.x] += sm[threadIdx.x + s];
+        __syncthreads();
+    }
+    return sm[0];
 }
 
-__global__ void k_copy_scalar(const double* __restrict__ src, double* __restrict__ dst) { dst[0] = src[0]; }
+// q = (alpha K + beta M) p and the CTA partial of p.q
+__global__ void __launch_bounds__(RED_TPB) k_cg_spmv(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                     const double* __restrict__ vk, const double* __restrict__ vm,
+                                                     double alpha, double beta, int64_t n,
+                                                     const double* __restrict__ p, double* __restrict__ q,
+                                                     double* __restrict__ part_pq) {
+    __shared__ double sm[RED_TPB];
+    const int64_t i = blockIdx.x * (int64_t)RED_TPB + threadIdx.x;
+    double pq = 0.0;
+    if (i < n) {
+        double acc = 0.0;
+        for (int j = __ldg(rp + i); j < __ldg(rp + i + 1); ++j)
+            acc += (alpha * __ldg(vk + j) + beta * __ldg(vm + j)) * __ldg(p + __ldg(ci + j));
+        q[i] = acc;
+        pq = p[i] * acc;
+    }
+    const double t = cta_sum(pq, sm);
+    if (threadIdx.x == 0) part_pq[blockIdx.x] = t;
+}
+
+// x += a p, r -= a q, z = D^-1 r (a = rz_old / pq) and the CTA partials of r.z, r.r
+__global__ void __launch_bounds__(RED_TPB) k_cg_step(const double* __restrict__ sc, int o,
+                                                     const double* __restrict__ p, const double* __restrict__ q,
+                                                     const double* __restrict__ dinv, int64_t n, double* __restrict__ x,
+                                                     double* __restrict__ r, double* __restrict__ z,
+                                                     double* __restrict__ part_rz, double* __restrict__ part_rr) {
+    __shared__ double sm[RED_TPB];
+    const int64_t i = blockIdx.x * (int64_t)RED_TPB + threadIdx.x;
+    double rz = 0.0, rr = 0.0;
+    if (i < n) {
+        const double a = sc[o] / sc[2];
+        x[i] += a * p[i];
+        const double ri = r[i] - a * q[i];
+        r[i] = ri;
+        const double zi = dinv[i] * ri;
+        z[i] = zi;
+        rz = ri * zi;
+        rr = ri * ri;
+    }
+    const double t1 = cta_sum(rz, sm);
+    __syncthreads();
+    const double t2 = cta_sum(rr, sm);
+    if (threadIdx.x == 0) {
+        part_rz[blockIdx.x] = t1;
+        part_rr[blockIdx.x] = t2;
+    }
+}
+
+// out_a = sum part_a[0..np), out_b = sum part_b[0..np) (fixed trees; block 0 / 1)
+__global__ void __launch_bounds__(RED_TPB) k_reduce_final2(const double* __restrict__ part_a,
+                                                           const double* __restrict__ part_b, int np,
+                                                           double* __restrict__ out_a, double* __restrict__ out_b) {
+    __shared__ double sm[RED_TPB];
+    const double* part = blockIdx.x == 0 ? part_a : part_b;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < np; i += RED_TPB) acc += part[i];
+    const double t = cta_sum(acc, sm);
+    if (threadIdx.x == 0) (blockIdx.x == 0 ? out_a : out_b)[0] = t;
+}
+
+// p = z + (rz_new / rz_old) p
+__global__ void k_cg_dir2(const double* __restrict__ sc, int o, const double* __restrict__ z, int64_t n,
+                          double* __restrict__ p) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    p[i] = z[i] + (sc[1 - o] / sc[o]) * p[i];
+}
 
 }  // namespace
 
@@ -801,19 +876,24 @@ efem_status run_cg(const efem_csr* A, double alpha, double beta, const double* b
         if (bn == 0.0 || *relres <= rtol) return EFEM_OK;
     }
     const int check = 20;
+    // scalars: sc[0] / sc[1] rz (ping-pong: the iteration's old value at sc[o]),
+    // sc[2] p.q, sc[3] r.r, sc[4] b.b; CTA partials in t1 / t2 (n >> #CTAs)
+    const unsigned gr = grid_for(n, RED_TPB);
+    double *part_a = t1, *part_b = t2;
+    int o = 0;
     for (int it = 1; it <= maxit; ++it) {
-        if ((st = launch_spmv(A, alpha, beta, p, q, s)) != EFEM_OK) return st;
-        k_mul<<<g, 256, 0, s>>>(p, q, n, t1);
+        k_cg_spmv<<<gr, RED_TPB, 0, s>>>(A->row_ptr, A->col_idx, A->vals_stiff, A->vals_mass, alpha, beta, n, p, q,
+                                          part_a);
         EFEM_LAUNCH_CHECK();
-        if ((st = reduce_fixed(t1, n, part, sc + 1, s)) != EFEM_OK) return st;
-        k_cg_update<<<g, 256, 0, s>>>(sc, p, q, dinv, n, x, r, z, t1, t2);
+        k_reduce_final<<<1, RED_TPB, 0, s>>>(part_a, (int)gr, sc + 2);
         EFEM_LAUNCH_CHECK();
-        if ((st = reduce_fixed(t1, n, part, sc + 2, s)) != EFEM_OK) return st;
-        if ((st = reduce_fixed(t2, n, part, sc + 3, s)) != EFEM_OK) return st;
-        k_cg_dir<<<g, 256, 0, s>>>(sc, z, n, p);
+        k_cg_step<<<gr, RED_TPB, 0, s>>>(sc, o, p, q, dinv, n, x, r, z, part_a, part_b);
         EFEM_LAUNCH_CHECK();
-        k_copy_scalar<<<1, 1, 0, s>>>(sc + 2, sc + 0);
+        k_reduce_final2<<<2, RED_TPB, 0, s>>>(part_a, part_b, (int)gr, sc + (1 - o), sc + 3);
         EFEM_LAUNCH_CHECK();
+        k_cg_dir2<<<g, 256, 0, s>>>(sc, o, z, n, p);
+        EFEM_LAUNCH_CHECK();
+        o = 1 - o;
         *iters = it;
         if (it % check == 0 || it == maxit) {
             double h[2];
