@@ -714,12 +714,9 @@ efem_status launch_quad_points(int dim, const double* coords, const int32_t* ele
     if (dim == 2)
         k_quad_points<2><<<grid_for(n_elems, QP_TPB), QP_TPB, QP_TPB * 25 * 8, s>>>(coords, elems, n_elems, pts);
     else {
-        static bool attr = false;  // 3D: 72 doubles per element -> 72 KB per CTA (opt-in)
-        if (!attr) {
-            EFEM_CUDA_TRY(cudaFuncSetAttribute(k_quad_points<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               QP_TPB * 73 * 8));
-            attr = true;
-        }
+        // 3D: 73 doubles per element -> 73 KB per CTA (opt-in; per device, so set at every call)
+        EFEM_CUDA_TRY(cudaFuncSetAttribute(k_quad_points<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           QP_TPB * 73 * 8));
         k_quad_points<3><<<grid_for(n_elems, QP_TPB), QP_TPB, QP_TPB * 73 * 8, s>>>(coords, elems, n_elems, pts);
     }
     EFEM_LAUNCH_CHECK();
@@ -734,12 +731,9 @@ efem_status load_kt2(Plan& p, const double* fq, double* b, cudaStream_t s) {
     constexpr int NF = PAIR == 0 ? KT::D : n_deriv<KT>();
     constexpr int NQ = KT::D == 2 ? 12 : 24;
     constexpr size_t smem = (size_t)TPB * ((NQ * NF) | 1) * 8;
-    static bool attr = false;
-    if (!attr) {
-        EFEM_CUDA_TRY(cudaFuncSetAttribute(k_load_elem<KT, PAIR, TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
-        attr = true;
-    }
+    // (the shared-memory opt-in is per device: set at every call)
+    EFEM_CUDA_TRY(cudaFuncSetAttribute(k_load_elem<KT, PAIR, TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
     double* loc = reinterpret_cast<double*>(p.bkey);
     k_load_elem<KT, PAIR, TPB><<<grid_for(p.n_elems, TPB), TPB, smem, s>>>(p.coords, p.elems, p.n_elems, fq, loc);
     EFEM_LAUNCH_CHECK();
@@ -773,13 +767,10 @@ efem_status launch_norm_l2(int dim, const double* coords, const int32_t* elems, 
         const int per = quad6_size(dim) * nf;
         const size_t smem = (size_t)NORM_TPB * (per | 1) * 8;
         if (smem <= 96 * 1024) {  // staged (coalesced) reads of the point values
-            static bool attr[2] = {false, false};
-            if (!attr[dim - 2]) {
-                EFEM_CUDA_TRY(cudaFuncSetAttribute(dim == 2 ? (const void*)k_norm_elem_staged<2>
-                                                            : (const void*)k_norm_elem_staged<3>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-                attr[dim - 2] = true;
-            }
+            // (the shared-memory opt-in is per device: set at every call)
+            EFEM_CUDA_TRY(cudaFuncSetAttribute(dim == 2 ? (const void*)k_norm_elem_staged<2>
+                                                        : (const void*)k_norm_elem_staged<3>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
             if (dim == 2)
                 k_norm_elem_staged<2><<<grid_for(n_elems, NORM_TPB), NORM_TPB, smem, s>>>(coords, elems, n_elems, fq,
                                                                                            nf, per_elem);
