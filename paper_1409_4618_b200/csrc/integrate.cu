@@ -6,6 +6,7 @@
 // (PAPER.md:863-918).  Every reduction runs in a fixed order (per-element
 // values, then a two-level tree), so results are bitwise reproducible.
 // Product path only; shares nothing with oracle/.
+#include <atomic>
 #include <cmath>
 #include <vector>
 
@@ -81,13 +82,16 @@ Quad6 make_quad6(int dim) {
     return Q;
 }
 
-bool g_quad_ready = false;
+std::atomic<bool> g_quad_ready[64];
 
+// __constant__ memory is per device: the tables are uploaded once per device
 efem_status ensure_quad() {
-    if (g_quad_ready) return EFEM_OK;
+    int dev = 0;
+    EFEM_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 64 && g_quad_ready[dev].load(std::memory_order_acquire)) return EFEM_OK;
     Quad6 q[2] = {make_quad6(2), make_quad6(3)};
     EFEM_CUDA_TRY(cudaMemcpyToSymbol(c_quad, q, sizeof(q)));
-    g_quad_ready = true;
+    if (dev < 64) g_quad_ready[dev].store(true, std::memory_order_release);
     return EFEM_OK;
 }
 

@@ -6,6 +6,7 @@
 // M_ab = |K| (1 + d_ab) / ((d+1)(d+2)) summed per row in ascending element
 // order, the load sum_K sum_q w |det| f l_a, grad v at the quadrature points,
 // and symmetric Dirichlet elimination.  Not the hot path; product code only.
+#include <atomic>
 #include <cub/cub.cuh>
 
 #include <new>
@@ -224,10 +225,12 @@ struct P1Quad {
     int nq;
 };
 __constant__ P1Quad c_p1q[2];
-bool g_p1q = false;
+std::atomic<bool> g_p1q[64];  // per device (__constant__ memory is per device)
 
 efem_status ensure_p1q() {
-    if (g_p1q) return EFEM_OK;
+    int dev = 0;
+    EFEM_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 64 && g_p1q[dev].load(std::memory_order_acquire)) return EFEM_OK;
     P1Quad q[2]{};
     for (int d = 2; d <= 3; ++d) {
         efem_status st = quad6_host(d, &q[d - 2].l[0][0], q[d - 2].w);
@@ -235,7 +238,7 @@ efem_status ensure_p1q() {
         q[d - 2].nq = quad6_size(d);
     }
     EFEM_CUDA_TRY(cudaMemcpyToSymbol(c_p1q, q, sizeof(q)));
-    g_p1q = true;
+    if (dev < 64) g_p1q[dev].store(true, std::memory_order_release);
     return EFEM_OK;
 }
 
