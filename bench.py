@@ -127,6 +127,9 @@ def dist_env():
     return ws, rank, local
 
 
+_ORACLE_MESH = {}
+
+
 def cpu_baseline(cfg, budget_elems=None):
     """The oracle as it stands, single thread, on a bounded sample of the same
     workload: the first T_s elements of the config's mesh (all their DOFs and
@@ -135,7 +138,11 @@ def cpu_baseline(cfg, budget_elems=None):
 
     from oracle import oracle as ora
 
-    coords, elems = ora.build_mesh(cfg["dim"], cfg["n"], cfg["alpha"], cfg["seed"])
+    key = (cfg["dim"], cfg["n"], cfg["alpha"], cfg["seed"])
+    if key not in _ORACLE_MESH:  # (built once per run: the reference arm calls this every step)
+        _ORACLE_MESH.clear()
+        _ORACLE_MESH[key] = ora.build_mesh(*key)
+    coords, elems = _ORACLE_MESH[key]
     if budget_elems is None:
         budget_elems = (1 << 21) if cfg["dim"] == 2 else (1 << 20)
     ts = min(elems.shape[0], budget_elems)
@@ -152,7 +159,10 @@ def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    budget = (1 << 19) if cfg["dim"] == 2 else (1 << 18)
+    # the whole run stays within about a minute of oracle work, whatever K is:
+    # ~2^24 (2D) / 2^22 (3D) elements in total, split over the K steps
+    total = (1 << 24) if cfg["dim"] == 2 else (1 << 22)
+    budget = int(min(max(total // max(args.steps, 1), 1 << 12), (1 << 21) if cfg["dim"] == 2 else (1 << 20)))
     for _ in range(args.warmup):
         cpu_baseline(cfg, budget_elems=1 << 12)
     vals = []
