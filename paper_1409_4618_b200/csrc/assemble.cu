@@ -720,9 +720,10 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                                           sbd * ck * (Nab * Nbd - Nad * Nbb),
                                           scd * ck * (Nac * Nbd - Nad * Nbc)};
                     // local edge id of the role pairs -> DOF ids
+                    // local edge id of the vertex pair {p, q}: a 4-bit field of one
+                    // 64-bit constant at index 4p + q (Fig. 1 numbering, reading C4)
                     auto eid = [](int p, int q) {
-                        const int lo = min(p, q), hi = max(p, q);
-                        return lo == 0 ? hi - 1 : (lo == 1 ? (hi == 2 ? 3 : 5) : 4);
+                        return (int)((0x452403153002100ull >> (4 * (4 * p + q))) & 7ull);
                     };
                     const int32_t* de = e2d + e * 6;
                     const int dof[6] = {own_base + i, __ldg(de + eid(la, lc)), __ldg(de + eid(la, ld)),
