@@ -570,10 +570,10 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
         const int pe = inst[j];
         const int k = pe & 7;
         const int g[4] = {gq[j].x, gq[j].y, gq[j].z, gq[j].w};
-        const int s0 = k < 3 ? 0 : (k == 3 ? 1 : (k == 4 ? 2 : 3));
-        const int s1 = k < 3 ? k + 1 : (k == 3 ? 2 : (k == 4 ? 3 : 1));
-        const int lc = k == 0 ? 2 : (k == 1 ? 1 : (k == 2 ? 1 : 0));
-        const int ld = k == 0 ? 3 : (k == 1 ? 3 : (k == 2 ? 2 : (k == 3 ? 3 : (k == 4 ? 1 : 2))));
+        // local edge k = (s0, s1) (Fig. 1, reading C4) and the other two
+        // vertices (lc, ld): 2-bit fields of one byte per k of a 48-bit constant
+        const unsigned rk8 = (unsigned)(0x874ec99cd8e4ull >> (8 * k));
+        const int s0 = rk8 & 3, s1 = (rk8 >> 2) & 3, lc = (rk8 >> 4) & 3, ld = (rk8 >> 6) & 3;
         const int g0 = sel4(g, s0), g1 = sel4(g, s1);
         const int la = g0 < g1 ? s0 : s1, lb = g0 < g1 ? s1 : s0;
         if (j == 0) {
