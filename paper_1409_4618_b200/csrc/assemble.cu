@@ -521,6 +521,12 @@ __device__ __forceinline__ int pair_index(int p, int q, int nw) {  // p < q
 // CTA's shared staging columns (stride NE3_LD), so every accumulator access
 // is a shared-memory instruction; otherwise they are the row's CSR segment
 // in global memory (stride 1, an oversize row in the tile).
+// g[i] of a tet's vertex ids held as two 64-bit pairs: one select + one shift
+__device__ __forceinline__ int sel4p(unsigned long long g01, unsigned long long g23, int i) {
+    const unsigned long long w = (i & 2) ? g23 : g01;
+    return (int)(uint32_t)(w >> ((i & 1) * 32));
+}
+
 template <class KT, bool SM, int TM>
 __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, const int32_t* __restrict__ elems,
                                              const int32_t* __restrict__ inc, const int32_t* __restrict__ e2d,
@@ -574,7 +580,9 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
         // vertices (lc, ld): 2-bit fields of one byte per k of a 48-bit constant
         const unsigned rk8 = (unsigned)(0x874ec99cd8e4ull >> (8 * k));
         const int s0 = rk8 & 3, s1 = (rk8 >> 2) & 3, lc = (rk8 >> 4) & 3, ld = (rk8 >> 6) & 3;
-        const int g0 = sel4(g, s0), g1 = sel4(g, s1);
+        const unsigned long long g01 = ((unsigned long long)(uint32_t)g[1] << 32) | (uint32_t)g[0];
+        const unsigned long long g23 = ((unsigned long long)(uint32_t)g[3] << 32) | (uint32_t)g[2];
+        const int g0 = sel4p(g01, g23, s0), g1 = sel4p(g01, g23, s1);
         const int la = g0 < g1 ? s0 : s1, lb = g0 < g1 ? s1 : s0;
         if (j == 0) {
             a = min(g0, g1);
@@ -583,8 +591,8 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
         // local vertex of each role (a, b, c, d), 2 bits each
         roles[j] = la | (lb << 2) | (lc << 4) | (ld << 6);
         const bool live = j < t;
-        key[2 * j] = live ? (((uint32_t)sel4(g, lc) << 5) | (uint32_t)(2 * j)) : 0xffffffffu;
-        key[2 * j + 1] = live ? (((uint32_t)sel4(g, ld) << 5) | (uint32_t)(2 * j + 1)) : 0xffffffffu;
+        key[2 * j] = live ? (((uint32_t)sel4p(g01, g23, lc) << 5) | (uint32_t)(2 * j)) : 0xffffffffu;
+        key[2 * j + 1] = live ? (((uint32_t)sel4p(g01, g23, ld) << 5) | (uint32_t)(2 * j + 1)) : 0xffffffffu;
     }
 #pragma unroll
     for (int x = 2 * TM; x < 14; ++x) key[x] = 0xffffffffu;  // (unused slots when TM < 7)
@@ -675,7 +683,9 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                     const int la = rl & 3, lb = (rl >> 2) & 3, lc = (rl >> 4) & 3, ld = (rl >> 6) & 3;
                     int g[4];
                     load_g<KT>(elems, e, g);
-                    const int c = sel4(g, lc), d = sel4(g, ld);
+                    const unsigned long long h01 = ((unsigned long long)(uint32_t)g[1] << 32) | (uint32_t)g[0];
+                    const unsigned long long h23 = ((unsigned long long)(uint32_t)g[3] << 32) | (uint32_t)g[2];
+                    const int c = sel4p(h01, h23, lc), d = sel4p(h01, h23, ld);
                     double e1[3], e2[3], e3[3];
 #pragma unroll
                     for (int cc = 0; cc < 3; ++cc) {
