@@ -714,21 +714,23 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                     const double ck = (2.0 / 3.0) * rd * rd * rd;
                     // role columns ab ac ad bc bd cd
                     const int pc = P[(2 * j) * NUM_TPB], pd = P[(2 * j + 1) * NUM_TPB];
-                    const double sac = pa < pc ? 1.0 : -1.0, sad = pa < pd ? 1.0 : -1.0;
-                    const double sbc = pb < pc ? 1.0 : -1.0, sbd = pb < pd ? 1.0 : -1.0;
-                    const double scd = pc < pd ? 1.0 : -1.0;
+                    // orientation signs as sign-bit flips ((+-cm) x == +-(cm x) exactly)
+                    auto sgn = [](bool pos, double v) {
+                        return __longlong_as_double(__double_as_longlong(v) ^ ((unsigned long long)!pos << 63));
+                    };
+                    const bool sac = pa < pc, sad = pa < pd, sbc = pb < pc, sbd = pb < pd, scd = pc < pd;
                     const double vm[6] = {cm * (2.0 * (Naa + Nbb - Nab)),
-                                          sac * cm * (2.0 * Nbc - Nab - Nac + Naa),
-                                          sad * cm * (2.0 * Nbd - Nab - Nad + Naa),
-                                          sbc * cm * (Nbc - Nbb - 2.0 * Nac + Nab),
-                                          sbd * cm * (Nbd - Nbb - 2.0 * Nad + Nab),
-                                          scd * cm * (Nbd - Nbc - Nad + Nac)};
+                                          sgn(sac, cm * (2.0 * Nbc - Nab - Nac + Naa)),
+                                          sgn(sad, cm * (2.0 * Nbd - Nab - Nad + Naa)),
+                                          sgn(sbc, cm * (Nbc - Nbb - 2.0 * Nac + Nab)),
+                                          sgn(sbd, cm * (Nbd - Nbb - 2.0 * Nad + Nab)),
+                                          sgn(scd, cm * (Nbd - Nbc - Nad + Nac))};
                     const double vk[6] = {ck * (Naa * Nbb - Nab * Nab),
-                                          sac * ck * (Naa * Nbc - Nac * Nab),
-                                          sad * ck * (Naa * Nbd - Nad * Nab),
-                                          sbc * ck * (Nab * Nbc - Nac * Nbb),
-                                          sbd * ck * (Nab * Nbd - Nad * Nbb),
-                                          scd * ck * (Nac * Nbd - Nad * Nbc)};
+                                          sgn(sac, ck * (Naa * Nbc - Nac * Nab)),
+                                          sgn(sad, ck * (Naa * Nbd - Nad * Nab)),
+                                          sgn(sbc, ck * (Nab * Nbc - Nac * Nbb)),
+                                          sgn(sbd, ck * (Nab * Nbd - Nad * Nbb)),
+                                          sgn(scd, ck * (Nac * Nbd - Nad * Nbc))};
                     // local edge id of the role pairs -> DOF ids
                     // local edge id of the vertex pair {p, q}: a 4-bit field of one
                     // 64-bit constant at index 4p + q (Fig. 1 numbering, reading C4)
