@@ -583,13 +583,18 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
         const unsigned long long g01 = ((unsigned long long)(uint32_t)g[1] << 32) | (uint32_t)g[0];
         const unsigned long long g23 = ((unsigned long long)(uint32_t)g[3] << 32) | (uint32_t)g[2];
         const int g0 = sel4p(g01, g23, s0), g1 = sel4p(g01, g23, s1);
-        const int la = g0 < g1 ? s0 : s1, lb = g0 < g1 ? s1 : s0;
+        const int sw = g0 > g1;  // local vertex s1 carries the row's a
         if (j == 0) {
             a = min(g0, g1);
             b = max(g0, g1);
         }
-        // local vertex of each role (a, b, c, d), 2 bits each
-        roles[j] = la | (lb << 2) | (lc << 4) | (ld << 6);
+        // lc, ld (2 bits each) and the local edge ids of the role pairs ac, ad,
+        // bc, bd, cd (3 bits each) from a table over (k, swap): Fig. 1 numbering
+        const int ti = 2 * k + sw;
+        const unsigned long long tw =
+            ti < 4 ? 0x542358d0446b4ad1ull : (ti < 8 ? 0x2a21286832253948ull : 0x18981622066a0a99ull);
+        const int e5 = (int)((tw >> (16 * (ti & 3))) & 0x7fffull);
+        roles[j] = lc | (ld << 2) | (e5 << 4);
         const bool live = j < t;
         key[2 * j] = live ? (((uint32_t)sel4p(g01, g23, lc) << 5) | (uint32_t)(2 * j)) : 0xffffffffu;
         key[2 * j + 1] = live ? (((uint32_t)sel4p(g01, g23, ld) << 5) | (uint32_t)(2 * j + 1)) : 0xffffffffu;
@@ -680,7 +685,7 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                 if (j < t) {
                     const int e = inst[j] >> 3;
                     const int rl = roles[j];
-                    const int la = rl & 3, lb = (rl >> 2) & 3, lc = (rl >> 4) & 3, ld = (rl >> 6) & 3;
+                    const int lc = rl & 3, ld = (rl >> 2) & 3, e5 = rl >> 4;
                     int g[4];
                     load_g<KT>(elems, e, g);
                     const unsigned long long h01 = ((unsigned long long)(uint32_t)g[1] << 32) | (uint32_t)g[0];
@@ -731,16 +736,12 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                                           sgn(sbc, ck * (Nab * Nbc - Nac * Nbb)),
                                           sgn(sbd, ck * (Nab * Nbd - Nad * Nbb)),
                                           sgn(scd, ck * (Nac * Nbd - Nad * Nbc))};
-                    // local edge id of the role pairs -> DOF ids
-                    // local edge id of the vertex pair {p, q}: a 4-bit field of one
-                    // 64-bit constant at index 4p + q (Fig. 1 numbering, reading C4)
-                    auto eid = [](int p, int q) {
-                        return (int)((0x452403153002100ull >> (4 * (4 * p + q))) & 7ull);
-                    };
+                    // DOF ids of the role pairs ac ad bc bd cd (local edge ids packed with
+                    // the roles in the first pass)
                     const int32_t* de = e2d + e * 6;
-                    const int dof[6] = {own_base + i, __ldg(de + eid(la, lc)), __ldg(de + eid(la, ld)),
-                                        __ldg(de + eid(lb, lc)), __ldg(de + eid(lb, ld)),
-                                        __ldg(de + eid(lc, ld))};
+                    const int dof[6] = {own_base + i, __ldg(de + (e5 & 7)), __ldg(de + ((e5 >> 3) & 7)),
+                                        __ldg(de + ((e5 >> 6) & 7)), __ldg(de + ((e5 >> 9) & 7)),
+                                        __ldg(de + ((e5 >> 12) & 7))};
                     const int pi = pidx[j];
 #pragma unroll
                     for (int u = 0; u < 6; ++u) {
