@@ -745,9 +745,10 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                     const int pi = pidx[j];
 #pragma unroll
                     for (int u = 0; u < 6; ++u) {
-                        const int slot =
-                            (u == 0 ? sab : __popcll(mask & ((1ull << ((pi >> (6 * (u - 1))) & 63)) - 1ull))) *
-                            st;
+                        // rank of the column's bit among the row's: popcount of the
+                        // bits below it (mask shifted up: no 64-bit subtract / and)
+                        const int pb_ = (pi >> (6 * (u - 1))) & 63;
+                        const int slot = (u == 0 ? sab : (pb_ ? __popcll(mask << (64 - pb_)) : 0)) * st;
                         ccol[slot] = dof[u];
                         cvm[slot] += vm[u];
                         cvk[slot] += vk[u];
