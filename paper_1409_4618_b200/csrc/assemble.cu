@@ -398,14 +398,14 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
         const bool live = li < n_rows;
         const bool two = c1.rr.x != c1.rr.y;
         const int t = live ? 1 + two : 0;
-        int incl = t;  // warp inclusive scan of t
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += v;
-        }
+        // warp prefix of t in {0, 1, 2}: live rows below plus two-element rows
+        // below (two ballots and popcounts instead of a shuffle scan)
+        const unsigned b_live = __ballot_sync(0xffffffffu, live);
+        const unsigned b_two = __ballot_sync(0xffffffffu, live && two);
+        const unsigned below = (1u << lane) - 1u;
+        const int incl = __popc(b_live & below) + __popc(b_two & below) + t;
         const int ib0 = __shfl_sync(0xffffffffu, c1.ib0, 0);
-        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        const int tot = __popc(b_live) + __popc(b_two);
         const int nr = min(32, n_rows - w0);
         const int gbase = row0 + w0 + NO * ib0 - out_base;
         const int segn = nr + NO * tot;
