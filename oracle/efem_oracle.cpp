@@ -28,12 +28,14 @@
  */
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <map>
 #include <set>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -550,6 +552,172 @@ int ora_result_copy(void* h, int32_t* dofs2nodes, int32_t* elems2dofs, int8_t* s
 }
 
 void ora_free(void* h) { delete (Result*)h; }
+
+/* Row-range (block) form of ora_assemble, for full-size parity at every
+ * BASELINE config and for the all-core CPU baseline ("a
+ * row-range-partitioned OpenMP variant on all nproc host cores; each thread
+ * owns a contiguous row range and scans all elements").
+ *
+ * DOF ids are lexicographic ranks of the sorted node tuples (PAPER.md:386,
+ * reading C10), so the entities whose MINIMUM node lies in a node range
+ * [lo, hi) are a contiguous block of global DOF ids (= rows).  The node range
+ * [0, n_nodes) is cut into n_blocks contiguous ranges; blocks are handed to
+ * n_threads threads.  Per block, the same steps as ora_assemble, restricted
+ * to the block's rows:
+ *   A. scan ALL elements in ascending order; keep those with a local entity
+ *      whose minimum node lies in [lo, hi); the block's entity set is the
+ *      std::set of those entities
+ *   B. (serial) the block's first DOF id = sum of the sizes of the earlier
+ *      blocks' sets; dofs2nodes = the sets in block order
+ *   C. for the kept elements in ascending order: signs (sign_of), local
+ *      matrices (local_matrices, the full m x m quadrature of PAPER.md:344-363),
+ *      and for every local DOF k the block owns, row k added into a
+ *      std::map<(row, col)> -- column ids looked up in the owning block's set
+ *   D. (serial) CSR emit, blocks in order.
+ * Every (row, col) entry receives its contributions in ascending element
+ * order, as in ora_assemble, so the result is bitwise identical to it
+ * (pinned: tests/test_oracle_pins.py::test_blocked_equals_serial). */
+void* ora_assemble_blocked(int dim, int element, int64_t n_nodes, int64_t n_elems, const double* coords,
+                           const int32_t* elems, int n_threads, int n_blocks, int* status) {
+    *status = validate(dim, element, n_nodes, n_elems, elems);
+    if (*status != ORA_OK) return nullptr;
+    if (n_threads < 1) n_threads = 1;
+    if (n_blocks < 1) n_blocks = 1;
+    if (n_nodes > 0 && n_blocks > n_nodes) n_blocks = (int)n_nodes;
+    const int m = n_local_dofs(dim, element);
+    const int ek = (dim == 3 && element == ORA_RT0) ? 3 : 2;
+    const int nv = dim + 1;
+    std::vector<int64_t> lo(n_blocks + 1);
+    for (int b = 0; b <= n_blocks; ++b) lo[b] = n_nodes * b / n_blocks;
+    auto block_of = [&](int node) {
+        return (int)(std::upper_bound(lo.begin(), lo.end(), (int64_t)node) - lo.begin()) - 1;
+    };
+    struct Block {
+        std::vector<int64_t> elist;
+        std::vector<std::array<int, 3>> keys;  // sorted entity set
+        int64_t first = 0;
+        std::vector<int32_t> row_len, col;
+        std::vector<double> vm, vk;
+        int64_t bad = -1;
+    };
+    std::vector<Block> B(n_blocks);
+    Result* R = new Result;
+    R->dim = dim;
+    R->element = element;
+    R->m = m;
+    R->ek = ek;
+    R->elems2dofs.assign((size_t)n_elems * m, -1);
+    R->signs.assign((size_t)n_elems * m, 0);
+
+    auto run = [&](auto&& body) {
+        std::atomic<int> next{0};
+        std::vector<std::thread> pool;
+        for (int t = 0; t < n_threads; ++t)
+            pool.emplace_back([&] {
+                for (int b = next++; b < n_blocks; b = next++) body(b);
+            });
+        for (auto& th : pool) th.join();
+    };
+
+    /* A */
+    run([&](int b) {
+        Block& blk = B[b];
+        std::set<std::array<int, 3>> ents;
+        for (int64_t e = 0; e < n_elems; ++e) {
+            const int32_t* g = elems + e * nv;
+            bool keep = false;
+            for (int k = 0; k < m; ++k) {
+                const std::array<int, 3> t = entity_key(dim, element, g, k);
+                if (t[0] >= lo[b] && t[0] < lo[b + 1]) {
+                    ents.insert(t);
+                    keep = true;
+                }
+            }
+            if (keep) blk.elist.push_back(e);
+        }
+        blk.keys.assign(ents.begin(), ents.end());
+    });
+    /* B */
+    int64_t total = 0;
+    for (int b = 0; b < n_blocks; ++b) {
+        B[b].first = total;
+        total += (int64_t)B[b].keys.size();
+        for (const auto& t : B[b].keys)
+            for (int c = 0; c < ek; ++c) R->dofs2nodes.push_back(t[c]);
+    }
+    auto dof_of = [&](const std::array<int, 3>& t) -> int64_t {
+        const Block& o = B[block_of(t[0])];
+        const auto it = std::lower_bound(o.keys.begin(), o.keys.end(), t);
+        return o.first + (int64_t)(it - o.keys.begin());
+    };
+    /* C */
+    run([&](int b) {
+        Block& blk = B[b];
+        std::map<std::pair<int32_t, int32_t>, std::pair<double, double>> acc;
+        std::vector<double> verts(nv * dim);
+        double M[36], K[36];
+        int s[6];
+        for (const int64_t e : blk.elist) {
+            const int32_t* g = elems + e * nv;
+            for (int v = 0; v < nv; ++v)
+                for (int c = 0; c < dim; ++c) verts[v * dim + c] = coords[(int64_t)g[v] * dim + c];
+            int32_t dof[6];
+            bool own[6];
+            for (int k = 0; k < m; ++k) {
+                const std::array<int, 3> t = entity_key(dim, element, g, k);
+                dof[k] = (int32_t)dof_of(t);
+                own[k] = t[0] >= lo[b] && t[0] < lo[b + 1];
+                s[k] = sign_of(dim, element, g, verts.data(), k);
+                if (own[k]) {
+                    R->elems2dofs[(size_t)e * m + k] = dof[k];
+                    R->signs[(size_t)e * m + k] = (int8_t)s[k];
+                }
+            }
+            if (local_matrices(dim, element, verts.data(), s, M, K) != ORA_OK) {
+                blk.bad = e;
+                return;
+            }
+            for (int k = 0; k < m; ++k) {
+                if (!own[k]) continue;
+                for (int l = 0; l < m; ++l) {
+                    auto& a = acc[{dof[k], dof[l]}];
+                    a.first += M[k * m + l];
+                    a.second += K[k * m + l];
+                }
+            }
+        }
+        blk.row_len.assign(blk.keys.size(), 0);
+        for (const auto& kv : acc) {
+            blk.row_len[kv.first.first - blk.first] += 1;
+            blk.col.push_back(kv.first.second);
+            blk.vm.push_back(kv.second.first);
+            blk.vk.push_back(kv.second.second);
+        }
+    });
+    /* D */
+    int64_t bad = -1;
+    for (const Block& blk : B)
+        if (blk.bad >= 0 && (bad < 0 || blk.bad < bad)) bad = blk.bad;
+    if (bad >= 0) {
+        *status = ORA_EDEGENERATE;
+        delete R;
+        return nullptr;
+    }
+    R->row_ptr.assign((size_t)total + 1, 0);
+    size_t nnz = 0;
+    for (const Block& blk : B) nnz += blk.col.size();
+    R->col_idx.reserve(nnz);
+    R->vals_M.reserve(nnz);
+    R->vals_K.reserve(nnz);
+    for (const Block& blk : B) {
+        for (size_t r = 0; r < blk.row_len.size(); ++r)
+            R->row_ptr[blk.first + r + 1] = R->row_ptr[blk.first + r] + blk.row_len[r];
+        R->col_idx.insert(R->col_idx.end(), blk.col.begin(), blk.col.end());
+        R->vals_M.insert(R->vals_M.end(), blk.vm.begin(), blk.vm.end());
+        R->vals_K.insert(R->vals_K.end(), blk.vk.begin(), blk.vk.end());
+    }
+    return R;
+}
 
 /* Sampled rows for meshes too large for the full oracle.  For each query
  * entity (sorted node tuple, ek ints, trailing -1 for edges), scan every

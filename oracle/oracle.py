@@ -28,7 +28,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so (g++ -O2 -ffp-contract=off, host only)."""
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
         subprocess.check_call(
-            ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fPIC", "-shared", "-o", _LIB_PATH, _SRC]
+            ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fPIC", "-shared", "-pthread", "-o", _LIB_PATH, _SRC]
         )
     return _LIB_PATH
 
@@ -50,6 +50,9 @@ def lib():
         L.ora_assemble.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, vp, vp,
                                    ctypes.POINTER(ctypes.c_int)]
         L.ora_assemble.restype = ctypes.c_void_p
+        L.ora_assemble_blocked.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, vp, vp,
+                                           ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.ora_assemble_blocked.restype = ctypes.c_void_p
         L.ora_result_sizes.argtypes = [vp, i64p, i64p]
         L.ora_result_copy.argtypes = [vp] + [vp] * 7
         L.ora_free.argtypes = [vp]
@@ -167,11 +170,20 @@ class Assembly:
         return M, K
 
 
-def assemble(dim: int, element: int, coords, elems) -> Assembly:
+def assemble(dim: int, element: int, coords, elems, threads: int = 0, blocks: int = 0) -> Assembly:
+    """The whole oracle assembly.  threads = 0: the serial ora_assemble;
+    threads >= 1: the row-range form ora_assemble_blocked (bitwise the same
+    result) on that many threads, over `blocks` node ranges (default 4 per
+    thread)."""
     coords = np.ascontiguousarray(coords, dtype=np.float64)
     elems = np.ascontiguousarray(elems, dtype=np.int32)
     st = ctypes.c_int()
-    h = lib().ora_assemble(dim, element, coords.shape[0], elems.shape[0], _p(coords), _p(elems), ctypes.byref(st))
+    if threads:
+        h = lib().ora_assemble_blocked(dim, element, coords.shape[0], elems.shape[0], _p(coords), _p(elems),
+                                       threads, blocks or 4 * threads, ctypes.byref(st))
+    else:
+        h = lib().ora_assemble(dim, element, coords.shape[0], elems.shape[0], _p(coords), _p(elems),
+                               ctypes.byref(st))
     if not h:
         raise ValueError(f"ora_assemble failed ({st.value})")
     try:

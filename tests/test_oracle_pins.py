@@ -419,3 +419,30 @@ def test_oracle_rejects_degenerate_and_bad_input():
         ora.assemble(2, RT0, coords, np.array([[0, 1, 2]], np.int32))
     with pytest.raises(ValueError):
         ora.assemble(2, RT0, coords, np.array([[0, 1, 3]], np.int32))
+
+
+@pytest.mark.parametrize("dim,element", KINDS, ids=KIND_IDS)
+@pytest.mark.parametrize("threads,blocks", [(1, 1), (2, 5), (4, 37)])
+def test_blocked_equals_serial(dim, element, threads, blocks):
+    """The row-range form (ora_assemble_blocked: node ranges -> contiguous
+    DOF blocks, each summing its rows in ascending element order) is bitwise
+    the serial oracle, on a permuted unstructured-order mesh too (random node
+    labels and element order, so block boundaries cut rows anywhere)."""
+    n = 9 if dim == 2 else 3
+    c, e = ora.build_mesh(dim, n, 0.2 if dim == 2 else 0.15, 21)
+    rng = np.random.default_rng(dim * 7 + element)
+    perm = rng.permutation(c.shape[0])
+    c = np.ascontiguousarray(c[perm])
+    e = np.ascontiguousarray(np.argsort(perm)[e][rng.permutation(e.shape[0])].astype(np.int32))
+    a = ora.assemble(dim, element, c, e)
+    b = ora.assemble(dim, element, c, e, threads=threads, blocks=blocks)
+    for f in ("dofs2nodes", "elems2dofs", "signs", "row_ptr", "col_idx", "vals_M", "vals_K"):
+        assert getattr(a, f).tobytes() == getattr(b, f).tobytes(), f
+
+
+def test_blocked_rejects_degenerate():
+    c, e = ora.build_mesh(2, 4, 0.0, 0)
+    c = c.copy()
+    c[e[13][2]] = 0.5 * (c[e[13][0]] + c[e[13][1]])
+    with pytest.raises(ValueError):
+        ora.assemble(2, NED0, c, e, threads=3)

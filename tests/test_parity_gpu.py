@@ -6,6 +6,8 @@ Full BASELINE sizes: sampled rows against the oracle computed row by row,
 plus properties that hold at any size (DOF table validity, de Rham, constant
 field interpolation, symmetry).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -104,12 +106,15 @@ def test_config1_full_parity(api, cfg):
     assert_csr_parity(asm.assemble(), ref, what="cfg1")
 
 
-@pytest.mark.parametrize("dim,element,n", [(2, NED0, 160), (3, RT0, 14), (3, NED0, 12)],
-                         ids=["ne0_2d_160", "rt0_3d_14", "ne0_3d_12"])
+@pytest.mark.parametrize("dim,element,n", [(2, NED0, 160), (2, RT0, 700), (3, RT0, 14), (3, RT0, 30), (3, NED0, 12),
+                                            (3, NED0, 31)],
+                         ids=["ne0_2d_160", "rt0_2d_700", "rt0_3d_14", "rt0_3d_30", "ne0_3d_12", "ne0_3d_31"])
 def test_csr_parity_medium(api, dim, element, n):
-    """Sizes that span many CTA tiles with a ragged tail, full oracle."""
+    """Sizes that span many CTA tiles with a ragged tail, full oracle (the
+    larger ones run every persistent warp through several grid-stride
+    batches)."""
     c, e = _gpu_mesh(api, dim, n, 0.2 if dim == 2 else 0.15, 5)
-    ref = ora.assemble(dim, element, c.cpu().numpy(), e.cpu().numpy())
+    ref = ora.assemble(dim, element, c.cpu().numpy(), e.cpu().numpy(), threads=os.cpu_count() or 1)
     asm = api.Assembler(c, e, element)
     assert_csr_parity(asm.assemble(), ref, what="medium")
 
@@ -248,6 +253,32 @@ def test_assemble_host_matches_device(api):
 
 
 # ---------------------------------------------------------------------------- full BASELINE sizes
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_full_config_oracle_parity(api, cfg):
+    """north_star's target: at every BASELINE config, the whole CSR of both
+    matrices against the oracle (its row-range form on all host cores,
+    bitwise the serial oracle): dofs2nodes, elems2dofs, signs, row_ptr and
+    col_idx byte for byte; every row of M and K within 1e-12 of the row's
+    max |entry| (PAPER.md:335-363)."""
+    C = CONFIGS[cfg]
+    dim, el, n = C["dim"], C["element"], C["n"]
+    c, e = _gpu_mesh(api, dim, n, C["alpha"], C["seed"])
+    asm = api.Assembler(c, e, el)
+    d2n, e2d, sg = asm.enumerate_dofs()
+    d2n, e2d, sg = d2n.cpu().numpy(), e2d.cpu().numpy(), sg.cpu().numpy()
+    csr = asm.assemble()
+    got = api.CSR(*(t.cpu() for t in (csr.row_ptr, csr.col_idx, csr.vals_M, csr.vals_K)))
+    c_h, e_h = c.cpu().numpy(), e.cpu().numpy()
+    del csr, asm, c, e
+    torch.cuda.empty_cache()
+    ref = ora.assemble(dim, el, c_h, e_h, threads=os.cpu_count() or 1)
+    assert np.array_equal(d2n, ref.dofs2nodes)
+    assert np.array_equal(e2d, ref.elems2dofs)
+    assert np.array_equal(sg, ref.signs)
+    del d2n, e2d, sg
+    assert_csr_parity(got, ref, what=f"cfg{cfg} full")
+
+
 def _sample_rows(R, rng, k=160):
     fixed = [0, 1, 2, R // 3, R // 2, R - 3, R - 2, R - 1]
     return np.unique(np.concatenate([fixed, rng.integers(0, R, k)]))
