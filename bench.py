@@ -42,11 +42,14 @@ def algorithmic_bytes(cfg):
     return mesh_in + csr_out, T
 
 
-def traffic_bytes(cfg):
-    """DRAM bytes per launch of the numeric kernel from a committed ncu capture."""
+def traffic_capture(cfg):
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of one whole
+    step, summed over its kernels, and per kernel, from the committed ncu
+    capture of tools/profile_step.py (profiles/traffic.json, written by
+    tools/traffic_json.py).  A static capture, not measured in this run."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        return t[cfg["name"]]["dram_bytes"]
+        return t[cfg["name"]]
     except Exception:
         return None
 
@@ -130,10 +133,19 @@ def dist_env():
 _ORACLE_MESH = {}
 
 
-def cpu_baseline(cfg, budget_elems=None):
-    """The oracle as it stands, single thread, on a bounded sample of the same
-    workload: the first T_s elements of the config's mesh (all their DOFs and
-    rows), mesh already in host RAM."""
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg, budget_elems=None, threads=None):
+    """The oracle as it stands on a bounded sample of the same workload (the
+    first T_s elements of the config's mesh: all their DOFs and rows), mesh
+    already in host RAM.  threads = None: the row-range form
+    (ora_assemble_blocked, bitwise the serial oracle) on every host core;
+    threads = 0: the serial ora_assemble (one core)."""
     import numpy as np
 
     from oracle import oracle as ora
@@ -143,15 +155,18 @@ def cpu_baseline(cfg, budget_elems=None):
         _ORACLE_MESH.clear()
         _ORACLE_MESH[key] = ora.build_mesh(*key)
     coords, elems = _ORACLE_MESH[key]
+    if threads is None:
+        threads = host_cores()
     if budget_elems is None:
-        budget_elems = (1 << 21) if cfg["dim"] == 2 else (1 << 20)
+        budget_elems = (1 << 23) if cfg["dim"] == 2 else (1 << 21)
     ts = min(elems.shape[0], budget_elems)
     sub = np.ascontiguousarray(elems[:ts])
     t0 = time.perf_counter()
-    ora.assemble(cfg["dim"], cfg["element"], coords, sub)
+    ora.assemble(cfg["dim"], cfg["element"], coords, sub, threads=threads)
     dt = time.perf_counter() - t0
-    return {"value": ts / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {ts} of {elems.shape[0]} elements of {cfg['name']} ({dt:.1f} s, 1 thread, "
+    how = (f"{threads} threads, row-range blocks" if threads else "1 thread")
+    return {"value": ts / dt, "unit": UNIT, "cores": max(threads, 1), "kind": "oracle",
+            "sample": f"first {ts} of {elems.shape[0]} elements of {cfg['name']} ({dt:.1f} s, {how}, "
                       f"g++ -O2 -ffp-contract=off, std::map accumulator)"}
 
 
@@ -159,10 +174,11 @@ def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    # the whole run stays within about a minute of oracle work, whatever K is:
-    # ~2^24 (2D) / 2^22 (3D) elements in total, split over the K steps
-    total = (1 << 24) if cfg["dim"] == 2 else (1 << 22)
-    budget = int(min(max(total // max(args.steps, 1), 1 << 12), (1 << 21) if cfg["dim"] == 2 else (1 << 20)))
+    # the whole run stays within about a minute of oracle work on all host
+    # cores, whatever K is: ~2^26 (2D) / 2^23 (3D) elements in total, split
+    # over the K steps
+    total = (1 << 26) if cfg["dim"] == 2 else (1 << 23)
+    budget = int(min(max(total // max(args.steps, 1), 1 << 12), (1 << 23) if cfg["dim"] == 2 else (1 << 21)))
     for _ in range(args.warmup):
         cpu_baseline(cfg, budget_elems=1 << 12)
     vals = []
@@ -178,7 +194,7 @@ def run_reference(args, cfg):
             "data": "synthetic", "config": {"workload": cfg["name"], "element": ELEMENT_NAMES[cfg["element"]],
                                             "dim": cfg["dim"], "n": cfg["n"], "jitter": cfg["alpha"],
                                             "seed": cfg["seed"], "sample_elems": ts},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": vals[-1]["cores"], "kind": "oracle",
                              "sample": vals[-1]["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -249,10 +265,12 @@ def run_efem(args, cfg):
     alg_bytes, _ = algorithmic_bytes(cfg)
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs")
-    peak_src = "measured" if peak else "fallback"
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)" if peak else "fallback (B200_PROFILING.md)"
     peak = peak or 6650.0
-    achieved = alg_bytes / (num_ms * 1e-3) / 1e9
-    e2e_gbs = alg_bytes / (total_ms / args.steps * 1e-3) / 1e9
+    step_s = total_ms / args.steps * 1e-3
+    step_gbs = alg_bytes / step_s / 1e9
+    num_gbs = alg_bytes / (num_ms * 1e-3) / 1e9
+    cap = traffic_capture(cfg)
 
     # end to end through the public API with HOST buffers (copies inside the timed region)
     h_c = coords.cpu().pin_memory()
@@ -279,12 +297,20 @@ def run_efem(args, cfg):
                    "n": cfg["n"], "jitter": cfg["alpha"], "seed": cfg["seed"], "n_elems": T,
                    "n_rows": asm.n_rows, "nnz": asm.nnz, "l2": "flushed between timed steps (512 MiB write)"},
         "phase_ms": {"symbolic": sym_ms, "numeric": num_ms},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic_bytes(cfg),
-                     "kernel": ("k_rows_ne3" if (cfg["dim"] == 3 and cfg["element"] == 1) else "k_rows_tri")
-                               + " (the numeric call: one launch)",
-                     "peak_source": peak_src, "algorithmic_bytes": alg_bytes,
-                     "e2e_achieved": e2e_gbs, "e2e_frac": e2e_gbs / peak},
+        # the whole step (enumeration + pattern + values, every kernel of one
+        # efem_assemble_async) against the HBM roofline of north_star's
+        # algorithmic bytes (mesh in + CSR out), DESIGN.md §8
+        "roofline": {"bound": "hbm", "achieved": step_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": step_gbs / peak,
+                     "traffic": cap["step_dram_bytes"] if cap else None,
+                     "kernel": "whole step (all kernels of efem_assemble_async, one CUDA graph)",
+                     "algorithmic_bytes": alg_bytes, "peak_source": peak_src,
+                     "traffic_read": cap["step_dram_read"] if cap else None,
+                     "traffic_write": cap["step_dram_write"] if cap else None,
+                     "traffic_source": (cap or {}).get("source", "none"),
+                     "numeric_kernel": {"kernel": ("k_rows_ne3" if (cfg["dim"] == 3 and cfg["element"] == 1)
+                                                   else "k_rows_tri") + " (the numeric call alone)",
+                                        "ms": num_ms, "achieved": num_gbs, "frac": num_gbs / peak}},
         "e2e": {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -373,28 +399,45 @@ def run_efem_dist(args, cfg):
     dist.destroy_process_group()
 
 
+def relaunch_distributed(n):
+    """`python bench.py --gpus N` outside torchrun: launch the N ranks here
+    (one process per GPU, torch.distributed.run on 127.0.0.1), or fail when
+    the node has fewer GPUs than asked for."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} but only {have} GPU(s) visible", file=sys.stderr)
+        sys.exit(2)
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=None, choices=sorted(CONFIGS),
-                    help="BASELINE config (fixed mesh; at N>1 strong scaling).  Default: 2 (configs[1]); at "
-                         "N>1 config 2 weak-scaled, n = round(1024 sqrt(N)), so every rank keeps ~2.10 M elements")
+    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS),
+                    help="BASELINE config.  Default 5 (RT0 2D 4096^2, 33.5 M triangles): the largest config, "
+                         "the one BASELINE sweeps over 1/2/4/8 GPUs (strong scaling: the mesh is fixed)")
     ap.add_argument("--impl", default="efem", choices=["efem", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     ws = dist_env()[0]
-    default_sweep = args.config is None
-    weak = default_sweep and ws > 1
-    if args.config is None:
-        args.config = 2
+    if "WORLD_SIZE" in os.environ and ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+        sys.exit(2)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args.gpus)
     cfg = dict(CONFIGS[args.config])
-    if weak:  # the N = 1 workload per rank: one mesh of ~N x its elements, row-owned slabs
-        cfg["n"] = int(round(1024 * math.sqrt(ws)))
-        cfg["name"] = f"cfg2_ne0_2d_weak_{cfg['n']}x{cfg['n']}"
-    cfg["weak"] = weak
-    cfg["scaling"] = "weak" if default_sweep else "strong"  # the default N = 1, 2, 4, 8 sweep is weak
+    cfg["scaling"] = "strong"  # the mesh is fixed; N ranks split it
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
