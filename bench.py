@@ -302,11 +302,11 @@ def run_efem(args, cfg):
         # algorithmic bytes (mesh in + CSR out), DESIGN.md §8
         "roofline": {"bound": "hbm", "achieved": step_gbs, "peak": peak, "unit": "GB/s",
                      "frac": step_gbs / peak,
-                     "traffic": cap["step_dram_bytes"] if cap else None,
+                     "traffic": (cap or {}).get("step_dram_bytes"),
                      "kernel": "whole step (all kernels of efem_assemble_async, one CUDA graph)",
                      "algorithmic_bytes": alg_bytes, "peak_source": peak_src,
-                     "traffic_read": cap["step_dram_read"] if cap else None,
-                     "traffic_write": cap["step_dram_write"] if cap else None,
+                     "traffic_read": (cap or {}).get("step_dram_read"),
+                     "traffic_write": (cap or {}).get("step_dram_write"),
                      "traffic_source": (cap or {}).get("source", "none"),
                      "numeric_kernel": {"kernel": ("k_rows_ne3" if (cfg["dim"] == 3 and cfg["element"] == 1)
                                                    else "k_rows_tri") + " (the numeric call alone)",
