@@ -13,7 +13,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["mesh.cu", "dofs.cu", "assemble.cu", "api.cu", "part.cu", "integrate.cu", "p1.cu"]
+SOURCES = ["mesh.cu", "dofs.cu", "assemble.cu", "api.cu", "fan2d.cu", "part.cu", "integrate.cu", "p1.cu"]
 LIB = os.path.join(HERE, "libefem.so")
 BUILD_DIR = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -41,6 +41,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
     size_t hdr, cnt, ent_cnt, bucket_ptr, bucket, bkey, binst, bx, nbr, e2d, inc_ptr, row_ptr, rec, d2n, ent_ptr, nnz_cnt, tiles, totals, cub, total;
+    size_t fan_ptr, fan, fan_tiles;
 };
 
 Layout layout(const Plan& p, size_t cub_bytes) {
@@ -74,6 +75,10 @@ Layout layout(const Plan& p, size_t cub_bytes) {
     L.tiles = take(4 * ((size_t)p.n_nodes / 64 + 4) * 4);  // ent / nnz tile sums and prefixes
     L.totals = take(16);
     L.cub = take(cub_bytes);
+    const bool fan = uses_fan(p);
+    L.fan_ptr = take(fan ? N1 * 4 : 4);
+    L.fan = take(fan ? (size_t)p.n_elems * 2 * 4 : 4);
+    L.fan_tiles = take(fan ? fan_tiles_bytes(p.n_nodes) : 8);
     L.total = off;
     return L;
 }
@@ -219,11 +224,22 @@ efem_status run_enumerate(Plan& p, cudaStream_t s) {
     return EFEM_OK;
 }
 
-// Enumeration already yields the exact row lengths and row_ptr (closed-form
-// counts, dofs.cu); symbolic = enumeration + the int32 overflow guard.
+efem_status ensure_enumerated(Plan& p, cudaStream_t s) {
+    return p.enumerated ? EFEM_OK : run_enumerate(p, s);
+}
+
+// 2D: the node-fan pipeline's symbolic half (fan2d.cu) and one read-back of
+// the flags and sizes.  3D: the enumeration already yields the exact row
+// lengths (closed-form counts, dofs.cu).
 efem_status run_symbolic(Plan& p, cudaStream_t s) {
     efem_status st;
-    if (!p.enumerated) {
+    if (uses_fan(p)) {
+        if ((st = launch_fan_symbolic(p, s)) != EFEM_OK) return st;
+        if ((st = read_flags(p, s)) != EFEM_OK) return st;
+        p.n_dofs = p.h_hdr->totals[0];
+        p.nnz = p.h_hdr->totals[1];
+        p.fan_valid = true;
+    } else if (!p.enumerated) {
         if ((st = run_enumerate(p, s)) != EFEM_OK) return st;
     }
     p.symbolic = true;
@@ -236,6 +252,10 @@ efem_status run_numeric(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s) 
     if (p.n_dofs == 0) {
         if (forms & EFEM_PATTERN) EFEM_CUDA_TRY(cudaMemsetAsync(out->row_ptr, 0, 4, s));
         return EFEM_OK;
+    }
+    if (uses_fan(p) && !p.fan_valid && !p.enumerated) {  // (either pipeline writes rec / inc_ptr / e2d)
+        if ((st = launch_fan_symbolic(p, s)) != EFEM_OK) return st;
+        p.fan_valid = true;
     }
     RowWindow w;
     w.row0 = 0;
@@ -415,6 +435,10 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     }
     p->d_totals = reinterpret_cast<int64_t*>(&p->hdr->totals[0]);
     p->cub_tmp = b + L.cub;
+    p->fan_ptr = reinterpret_cast<int32_t*>(b + L.fan_ptr);
+    p->fan = reinterpret_cast<int32_t*>(b + L.fan);
+    p->fan_tiles = reinterpret_cast<unsigned long long*>(b + L.fan_tiles);
+    p->fan_valid = false;
     p->enumerated = p->symbolic = false;
     // counters that must start at zero (the fill pass restores cnt to zero;
     // entry N of the count arrays is never written)
@@ -519,7 +543,10 @@ efem_status efem_assemble_symbolic(efem_plan plan, int64_t* n_rows, int64_t* nnz
     if ((st = run_symbolic(*p, s)) != EFEM_OK) return st;
     if (n_rows) *n_rows = p->n_dofs;
     if (nnz) *nnz = p->nnz;
-    if (row_ptr) return write_row_ptr(*p, 0, p->n_dofs, row_ptr, s);
+    if (row_ptr) {
+        if ((st = ensure_enumerated(*p, s)) != EFEM_OK) return st;
+        return write_row_ptr(*p, 0, p->n_dofs, row_ptr, s);
+    }
     return EFEM_OK;
 }
 
@@ -551,7 +578,9 @@ efem_status efem_plan_check(efem_plan plan, efem_stream_t stream) {
         p->async_pending = false;
         p->n_dofs = p->h_hdr->totals[0];
         p->nnz = p->h_hdr->totals[1];
-        p->enumerated = p->symbolic = st == EFEM_OK;
+        p->symbolic = st == EFEM_OK;
+        if (p->async_fan) p->fan_valid = st == EFEM_OK;
+        else p->enumerated = st == EFEM_OK;
     }
     return st;
 }
@@ -594,9 +623,11 @@ efem_status efem_assemble_async(efem_plan plan, unsigned forms, efem_csr* out, e
     }
     cudaStream_t s = (cudaStream_t)stream;
     p->enumerated = p->symbolic = false;
+    p->fan_valid = false;
     p->async_pending = true;
+    p->async_fan = uses_fan(*p);
     auto enqueue = [&](cudaStream_t q) -> efem_status {
-        efem_status e = launch_enumerate(*p, q);
+        efem_status e = uses_fan(*p) ? launch_fan_symbolic(*p, q) : launch_enumerate(*p, q);
         if (e != EFEM_OK) return e;
         RowWindow w;
         w.row0 = 0;
@@ -710,6 +741,7 @@ efem_status efem_assemble_load(efem_plan plan, int pairing, const double* fq, do
         set_error("efem_assemble_load: pairing must be EFEM_PAIR_VALUE or EFEM_PAIR_DERIV, arrays non-NULL");
         return EFEM_EINVAL;
     }
+    if ((st = ensure_enumerated(*p, (cudaStream_t)stream)) != EFEM_OK) return st;
     return launch_load(*p, pairing, fq, b, (cudaStream_t)stream);
 }
 
@@ -754,6 +786,7 @@ efem_status efem_field_error(efem_plan plan, const double* coeffs, const double*
         set_error("efem_field_error: bad arguments or workspace too small");
         return EFEM_EINVAL;
     }
+    if ((st = ensure_enumerated(*p, (cudaStream_t)stream)) != EFEM_OK) return st;
     return launch_field_error(*p, coeffs, Eq, Dq, err2, static_cast<double*>(ws), (cudaStream_t)stream);
 }
 

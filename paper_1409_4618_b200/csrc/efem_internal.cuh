@@ -31,6 +31,8 @@ struct WsHeader {
     // device: first local row, rows, local CSR offset of the first row,
     // entries, global id of the first row
     long long win[6];
+    int tile_ticket;  // dynamic tile ids of the look-back scans (fan2d.cu)
+    int pad2;
 };
 
 // Instance words e << 3 | k (element e < 2^27, local entity k); the two top
@@ -91,6 +93,12 @@ struct Plan {
     int32_t* nnz_cnt = nullptr;     // N+1 CSR entries of each node's rows
     int32_t *ent_bsum = nullptr, *ent_bpre = nullptr, *nnz_bsum = nullptr, *nnz_bpre = nullptr;  // per node tile
     int64_t* d_totals = nullptr;    // == hdr->totals
+    // 2D node-fan pipeline (fan2d.cu): fans of the triangles by smallest /
+    // middle vertex; it writes rec / inc_ptr / e2d above for k_rows_tri
+    int32_t* fan_ptr = nullptr;      // N+1
+    int32_t* fan = nullptr;          // 2T triangle ids
+    unsigned long long* fan_tiles = nullptr;  // look-back tile states
+    bool fan_valid = false;          // rec / inc_ptr / e2d are current from the fan pipeline
     bool want_d2n = false;
     bool exact_ne3 = false;  // NE0 3D: exact link counts (non-manifold meshes), efem_plan_set_exact
     void* cub_tmp = nullptr;
@@ -123,9 +131,11 @@ struct Plan {
     int64_t part_launches = 0;
     int32_t* part_key = nullptr;
 
-    // state
+    // state: enumerated = the bucket-pipeline arrays (dofs.cu: incidence,
+    // elems2dofs, ...) are current; symbolic = n_dofs / nnz are known
     bool enumerated = false, symbolic = false;
     bool async_pending = false;  // efem_assemble_async ran; sizes arrive with efem_plan_check
+    bool async_fan = false;      // ... through the 2D node-fan pipeline (else the bucket pipeline)
     int64_t n_dofs = 0, nnz = 0;
 };
 
@@ -182,6 +192,13 @@ efem_status run_enumerate(Plan& p, cudaStream_t s);
 efem_status run_symbolic(Plan& p, cudaStream_t s);
 efem_status run_numeric(Plan& p, unsigned forms, efem_csr* out, cudaStream_t s);
 efem_status run_signs(Plan& p, cudaStream_t s);
+// the bucket-pipeline arrays for the consumers that need them (DOF tables,
+// loads, field errors, partitions): enumerates if they are not current
+efem_status ensure_enumerated(Plan& p, cudaStream_t s);
+// 2D node-fan pipeline (fan2d.cu)
+inline bool uses_fan(const Plan& p) { return p.dim == 2; }
+efem_status launch_fan_symbolic(Plan& p, cudaStream_t s);
+size_t fan_tiles_bytes(int64_t n_nodes);
 // row_ptr helpers (api.cu): 2D edges / 3D faces keep no row_ptr array, row r
 // starts at r + (m-1) inc_ptr[r]; 3D edges store it (plan row_ptr).
 bool row_ptr_stored(const Plan& p);

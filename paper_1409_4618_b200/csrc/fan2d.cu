@@ -1,0 +1,415 @@
+// fan2d.cu -- the symbolic half of the 2D hot path (RT0 and NE0 on
+// triangles) as a node-fan pipeline: DOF enumeration and the sparsity
+// pattern's row structure in three kernels.
+//
+// The method (Sec. 2.4; 671-696, Sec. 3.2): global edge
+// DOFs numbered by the lexicographic rank of their sorted node pair (reading
+// C10), local matrices of every triangle summed into the global M and K.
+// Every global row is an edge (a, b), a < b; all rows of node a -- its larger
+// neighbours b -- are enumerated together by one thread from the node's FAN:
+// the triangles in which a is the smallest or the middle vertex (exactly the
+// triangles holding an edge whose smaller node is a).
+//
+//   k_fan_bucket<count>  per triangle (p < q < r): one atomic at p and at q
+//   CUB scan             -> fan_ptr
+//   k_fan_bucket<fill>   per triangle: its id into the fans of p and q
+//   k_fan_nodes          per node: the owned edges as sorted (b, element,
+//                        local edge) keys in registers; DOF ids and instance
+//                        offsets by a single-pass decoupled look-back over
+//                        node tiles; row records, incidence offsets and
+//                        elems2dofs in the layout the numeric kernel
+//                        k_rows_tri (assemble.cu) reads
+//
+// Against the bucket pipeline of dofs.cu (instances of all 3 T edges keyed
+// by minimum node, 8-byte keys, a count pass and a write pass over them) the
+// fans hold 2 T 4-byte triangle ids and one pass over them does the rest
+// (DESIGN.md §7).
+#include <cub/cub.cuh>
+
+#include <atomic>
+#include <type_traits>
+
+#include "efem_internal.cuh"
+
+namespace efem {
+namespace {
+
+constexpr int FAN_TPB = 128;
+constexpr int FAN_REG = 8;                   // fast path: fan size and neighbour count per node
+constexpr unsigned long long TS_AGG = 1ull << 62, TS_PRE = 2ull << 62, TS_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ bool invalid_node(int v, int64_t n) { return (unsigned long long)(unsigned)v >= (unsigned long long)n; }
+
+__device__ __forceinline__ void sort3(int& p, int& q, int& r) {
+    const int a = min(p, q), b = max(p, q);
+    p = min(a, r);
+    const int m = max(a, r);
+    q = min(b, m);
+    r = max(b, m);
+}
+
+// ---------------------------------------------------------------------------------
+// K1 / K2: counting sort of the fan instances (triangle e into the fans of
+// its smallest and middle vertex).  The fill takes slots from the top of
+// each count (atomicSub), which returns the counts to zero for the next
+// call; the order inside a fan is fixed later (ascending e).
+// ---------------------------------------------------------------------------------
+template <bool FILL>
+__global__ void __launch_bounds__(256) k_fan_bucket(const int32_t* __restrict__ elems, int64_t n_elems, int64_t n_nodes,
+                                                    int32_t* __restrict__ cnt, const int32_t* __restrict__ fan_ptr,
+                                                    int32_t* __restrict__ fan, WsHeader* hdr) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n_elems) return;
+    int p = __ldg(elems + 3 * e), q = __ldg(elems + 3 * e + 1), r = __ldg(elems + 3 * e + 2);
+    if (invalid_node(p, n_nodes) || invalid_node(q, n_nodes) || invalid_node(r, n_nodes)) {
+        if (!FILL) atomicOr(&hdr->flags[F_INVALID_NODE], 1);
+        return;  // (skipped consistently by count and fill; the call reports EFEM_EINVAL)
+    }
+    sort3(p, q, r);
+    if constexpr (!FILL) {
+        atomicAdd(cnt + p, 1);
+        if (q != p) atomicAdd(cnt + q, 1);
+    } else {
+        fan[__ldg(fan_ptr + p) + atomicSub(cnt + p, 1) - 1] = (int)e;
+        if (q != p) fan[__ldg(fan_ptr + q) + atomicSub(cnt + q, 1) - 1] = (int)e;
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// K3: per node a, the edges it owns (its distinct larger neighbours b, in
+// ascending order: DOF id = first id of the node + rank) and, per edge, the
+// fan instances holding it (e << 3 | k, k the local edge of (a, b) in
+// triangle e; t <= 2 in a conforming mesh).  Global DOF ids and instance
+// offsets come from a single-pass decoupled look-back over node tiles.
+// Outputs, in the layout of the bucket pipeline (dofs.cu) that the numeric
+// kernel k_rows_tri reads:
+//   rec[i]     {first, last} instance of row i (ascending element id)
+//   inc_ptr[i] instances of the rows before i (row i starts at i + 2 inc_ptr[i])
+//   e2d[3e+k]  DOF id of local edge k of triangle e
+// ---------------------------------------------------------------------------------
+struct FanNodesArgs {
+    const int32_t* elems;
+    const int32_t* fan_ptr;
+    int32_t* fan;  // big fans (> FAN_REG) are sorted in place here
+    int64_t n_nodes;
+    int2* rec;
+    int32_t* inc_ptr;
+    int32_t* e2d;
+    unsigned long long* tile_state;
+    WsHeader* hdr;
+};
+
+__device__ __forceinline__ void load_tri(const int32_t* __restrict__ elems, int e, int& g0, int& g1, int& g2) {
+    const int32_t* p = elems + 3 * (int64_t)e;
+    g0 = __ldg(p);
+    g1 = __ldg(p + 1);
+    g2 = __ldg(p + 2);
+}
+
+// the owned-edge keys of fan triangle e at node a: (b << 32 | e << 3 | k) for
+// each vertex b > a of the triangle, k = the local edge {a, b} (its opposite
+// vertex); ~0 when the vertex is not larger than a
+__device__ __forceinline__ void tri_keys(int a, int e, int g0, int g1, int g2, unsigned long long& k1,
+                                         unsigned long long& k2) {
+    const int la = g0 == a ? 0 : (g1 == a ? 1 : 2);
+    const int w1 = la == 0 ? 1 : 0, w2 = la == 2 ? 1 : 2;  // the two other positions
+    const int v1 = w1 == 0 ? g0 : g1, v2 = w2 == 1 ? g1 : g2;
+    const unsigned long long inst1 = (unsigned long long)(((unsigned)e << 3) | (unsigned)(3 - la - w1));
+    const unsigned long long inst2 = (unsigned long long)(((unsigned)e << 3) | (unsigned)(3 - la - w2));
+    k1 = v1 > a ? ((unsigned long long)(unsigned)v1 << 32) | inst1 : ~0ull;
+    k2 = v2 > a ? ((unsigned long long)(unsigned)v2 << 32) | inst2 : ~0ull;
+}
+
+// big fan (> FAN_REG instances, rare): insertion sort of the fan in place by
+// triangle id; the owned edges are then visited in ascending b by repeated
+// minimum scans (quadratic, global memory)
+__device__ void fan_sort_inplace(int32_t* f, int n) {
+    for (int j = 1; j < n; ++j) {
+        const int v = f[j];
+        int k = j;
+        while (k > 0 && f[k - 1] > v) {
+            f[k] = f[k - 1];
+            --k;
+        }
+        f[k] = v;
+    }
+}
+
+// calls visit(b, first_inst, last_inst, t) for every owned edge (a, b) of the
+// big fan f (sorted by element), ascending b
+template <class V>
+__device__ void fan_edges_slow(const int32_t* __restrict__ elems, const int32_t* f, int a, int n, V&& visit) {
+    long long last = a;
+    for (;;) {
+        int best = INT_MAX;
+        for (int j = 0; j < n; ++j) {
+            int g0, g1, g2;
+            load_tri(elems, f[j], g0, g1, g2);
+            unsigned long long k1, k2;
+            tri_keys(a, f[j], g0, g1, g2, k1, k2);
+            const int b1 = (int)(k1 >> 32), b2 = (int)(k2 >> 32);
+            if (k1 != ~0ull && b1 > last && b1 < best) best = b1;
+            if (k2 != ~0ull && b2 > last && b2 < best) best = b2;
+        }
+        if (best == INT_MAX) return;
+        int first = -1, lst = -1, t = 0;
+        for (int j = 0; j < n; ++j) {  // ascending element id
+            int g0, g1, g2;
+            load_tri(elems, f[j], g0, g1, g2);
+            unsigned long long k1, k2;
+            tri_keys(a, f[j], g0, g1, g2, k1, k2);
+            for (const unsigned long long k : {k1, k2})
+                if (k != ~0ull && (int)(k >> 32) == best) {
+                    if (t == 0) first = (int)(unsigned)k;
+                    lst = (int)(unsigned)k;
+                    ++t;
+                }
+        }
+        visit(best, first, lst, t);
+        last = best;
+    }
+}
+
+constexpr int FAN_REC_STAGE = FAN_TPB * 4;  // staged rows per tile
+// register path: one 32-bit key per owned-edge candidate,
+//   (b - a) << 5 | j << 2 | k   (j = position in the fan, k = local edge),
+// so one sort orders the candidates by b; b - a < 2^27 (else the slow path)
+constexpr unsigned KEY_NONE = 0xffffffffu;
+constexpr int KEY_DMAX = 1 << 27;
+
+template <int C>
+__device__ __forceinline__ void sort_keys(unsigned (&key)[2 * FAN_REG]) {
+#pragma unroll
+    for (int kk = 2; kk <= C; kk <<= 1)
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+            for (int x = 0; x < C; ++x) {
+                const int y = x ^ jj;
+                if (y > x) {
+                    const unsigned lo = min(key[x], key[y]), hi = max(key[x], key[y]);
+                    const bool asc = (x & kk) == 0;
+                    key[x] = asc ? lo : hi;
+                    key[y] = asc ? hi : lo;
+                }
+            }
+}
+
+// walk the sorted keys: row(first, last, t) per run of equal b, the run's
+// instances e << 3 | k ordered by element
+template <int C, class R>
+__device__ __forceinline__ void key_runs(const unsigned (&key)[2 * FAN_REG], const int (&ev)[FAN_REG], R&& row) {
+    int first = 0, last = 0, t = 0;
+    unsigned prev = KEY_NONE;
+#pragma unroll
+    for (int x = 0; x < C; ++x) {
+        const unsigned k = key[x];
+        if (k == KEY_NONE) continue;
+        const int j = (k >> 2) & 7;
+        int e = ev[0];
+#pragma unroll
+        for (int q = 1; q < FAN_REG; ++q) e = j == q ? ev[q] : e;
+        const int inst = (e << 3) | (int)(k & 3);
+        if ((k >> 5) != (prev >> 5)) {
+            if (t) row(first, last, t);
+            first = last = inst;
+            t = 1;
+        } else {
+            first = min(first, inst);
+            last = max(last, inst);
+            ++t;
+        }
+        prev = k;
+    }
+    if (t) row(first, last, t);
+}
+
+__global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
+    using BlockScan = cub::BlockScan<unsigned long long, FAN_TPB>;
+    __shared__ typename BlockScan::TempStorage scan_tmp;
+    __shared__ int s_tile;
+    __shared__ unsigned long long s_excl;
+    __shared__ int2 s_rec[FAN_REC_STAGE];
+    __shared__ int s_inc[FAN_REC_STAGE];
+    if (threadIdx.x == 0) s_tile = atomicAdd(&A.hdr->tile_ticket, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t a64 = (int64_t)tile * FAN_TPB + threadIdx.x;
+    const bool live = a64 < A.n_nodes;
+    const int a = (int)a64;
+    int n_ent = 0, n_inst = 0, beg = 0, n = 0;
+    bool bad = false, slow = false;
+    unsigned key[2 * FAN_REG];
+    int ev[FAN_REG];
+#pragma unroll
+    for (int x = 0; x < 2 * FAN_REG; ++x) key[x] = KEY_NONE;
+#pragma unroll
+    for (int j = 0; j < FAN_REG; ++j) ev[j] = 0;
+    if (live) {
+        beg = __ldg(A.fan_ptr + a);
+        n = __ldg(A.fan_ptr + a + 1) - beg;
+        slow = n > FAN_REG;
+        if (!slow) {
+#pragma unroll
+            for (int j = 0; j < FAN_REG; ++j) ev[j] = j < n ? A.fan[beg + j] : 0;
+#pragma unroll
+            for (int j = 0; j < FAN_REG; ++j) {
+                if (j < n) {
+                    int g0, g1, g2;
+                    load_tri(A.elems, ev[j], g0, g1, g2);
+                    const int la = g0 == a ? 0 : (g1 == a ? 1 : 2);
+                    const int w1 = la == 0 ? 1 : 0, w2 = la == 2 ? 1 : 2;  // the two other positions
+                    const int v1 = w1 == 0 ? g0 : g1, v2 = w2 == 1 ? g1 : g2;
+                    // (a vertex id above a by 2^27 or more takes the slow path)
+                    slow |= (v1 > a && v1 - a >= KEY_DMAX) || (v2 > a && v2 - a >= KEY_DMAX);
+                    if (v1 > a) key[2 * j] = ((unsigned)(v1 - a) << 5) | (j << 2) | (unsigned)(3 - la - w1);
+                    if (v2 > a) key[2 * j + 1] = ((unsigned)(v2 - a) << 5) | (j << 2) | (unsigned)(3 - la - w2);
+                }
+            }
+        }
+        if (!slow) {
+            auto count = [&](auto cmax) {
+                constexpr int CM = decltype(cmax)::value;
+                sort_keys<CM>(key);
+#pragma unroll
+                for (int x = 0; x < CM; ++x) {
+                    const bool v = key[x] != KEY_NONE;
+                    n_inst += v;
+                    n_ent += v && (x == 0 || (key[x] >> 5) != (key[x - 1] >> 5));
+                    if (x >= 2) bad |= v && (key[x] >> 5) == (key[x - 2] >> 5);  // an edge in three triangles
+                }
+            };
+            if (n <= FAN_REG / 2) count(std::integral_constant<int, FAN_REG>{});
+            else count(std::integral_constant<int, 2 * FAN_REG>{});
+        } else {
+            fan_sort_inplace(A.fan + beg, n);
+            fan_edges_slow(A.elems, A.fan + beg, a, n, [&](int, int, int, int t) {
+                ++n_ent;
+                n_inst += t;
+                bad |= t > 2;
+            });
+        }
+        if (bad) atomicOr(&A.hdr->flags[F_ROW_MISMATCH], 1);
+    }
+    // tile prefix of (entities << 31 | instances)
+    const unsigned long long mine = ((unsigned long long)n_ent << 31) | (unsigned long long)n_inst;
+    unsigned long long off, agg;
+    BlockScan(scan_tmp).ExclusiveSum(mine, off, agg);
+    if (threadIdx.x < 32) {
+        // decoupled look-back (warp 0): publish the aggregate, sum the
+        // predecessors' aggregates back to the nearest inclusive prefix
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            if (threadIdx.x == 0) atomicExch(A.tile_state, TS_PRE | agg);
+        } else {
+            if (threadIdx.x == 0) atomicExch(A.tile_state + tile, TS_AGG | agg);
+            int j = tile - 1;
+            for (;;) {
+                const int idx = j - (int)threadIdx.x;
+                unsigned long long st = TS_PRE;  // (before tile 0: an empty prefix)
+                if (idx >= 0) {
+                    do {
+                        st = *(volatile unsigned long long*)(A.tile_state + idx);
+                    } while ((st >> 62) == 0);
+                }
+                const unsigned pre = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+                const int stop = pre ? __ffs(pre) - 1 : 32;  // nearest lane with an inclusive prefix
+                unsigned long long v = (int)threadIdx.x <= stop ? (st & TS_VAL) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                excl += v;
+                if (pre) break;
+                j -= 32;
+            }
+            if (threadIdx.x == 0) atomicExch(A.tile_state + tile, TS_PRE | (excl + agg));
+        }
+        if (threadIdx.x == 0) s_excl = excl;
+    }
+    __syncthreads();
+    const unsigned long long base = s_excl;
+    const int e_tile0 = (int)(base >> 31), i_tile0 = (int)(base & 0x7fffffffull);
+    const int e_off = (int)(off >> 31);
+    const int e_tot = (int)(agg >> 31);
+    const bool stage = e_tot <= FAN_REC_STAGE;
+    if (live) {
+        int id = e_tile0 + e_off;  // first DOF of node a
+        int inst = i_tile0 + (int)(off & 0x7fffffffull);
+        auto row = [&](int first, int last, int t) {
+            if (stage) {
+                s_rec[id - e_tile0] = make_int2(first, last);
+                s_inc[id - e_tile0] = inst;
+            } else {
+                A.rec[id] = make_int2(first, last);
+                A.inc_ptr[id] = inst;
+            }
+            A.e2d[(int64_t)(first >> 3) * 3 + (first & 7)] = id;
+            if (t > 1) A.e2d[(int64_t)(last >> 3) * 3 + (last & 7)] = id;
+            ++id;
+            inst += t;
+        };
+        if (!slow) {
+            if (n <= FAN_REG / 2) key_runs<FAN_REG>(key, ev, row);
+            else key_runs<2 * FAN_REG>(key, ev, row);
+        } else {
+            fan_edges_slow(A.elems, A.fan + beg, a, n, [&](int, int first, int last, int t) { row(first, last, min(t, 2)); });
+        }
+        if (a == A.n_nodes - 1) {
+            A.inc_ptr[id] = inst;
+            A.hdr->totals[0] = id;
+            A.hdr->totals[1] = (long long)id + 2ll * inst;  // sum_i (1 + 2 t_i)
+        }
+    }
+    if (stage) {
+        __syncthreads();
+        for (int x = threadIdx.x; x < e_tot; x += FAN_TPB) {
+            A.rec[e_tile0 + x] = s_rec[x];
+            A.inc_ptr[e_tile0 + x] = s_inc[x];
+        }
+    }
+}
+
+}  // namespace
+
+namespace {
+__global__ void k_fan_init(WsHeader* hdr) {
+    const int i = threadIdx.x;
+    if (i < F_NFLAGS) hdr->flags[i] = 0;
+    if (i == 0) {
+        hdr->bad_element = ~0ull;
+        hdr->totals[0] = 0;
+        hdr->totals[1] = 0;
+        hdr->tile_ticket = 0;
+    }
+}
+
+}  // namespace
+
+// The symbolic half (K1-K3): sizes in the header totals, offsets and
+// neighbour lists in the plan's fan arrays.  Enqueue only.
+efem_status launch_fan_symbolic(Plan& p, cudaStream_t s) {
+    const int64_t N = p.n_nodes, T = p.n_elems;
+    k_fan_init<<<1, 32, 0, s>>>(p.hdr);
+    EFEM_LAUNCH_CHECK();
+    const int ntiles = (int)grid_for(N, FAN_TPB);
+    if (ntiles > 0) EFEM_CUDA_TRY(cudaMemsetAsync(p.fan_tiles, 0, (size_t)ntiles * 8, s));
+    if (T > 0) {
+        k_fan_bucket<false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, nullptr, nullptr, p.hdr);
+        EFEM_LAUNCH_CHECK();
+    }
+    size_t bytes = p.cub_bytes;
+    EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.fan_ptr, (int)(N + 1), s));
+    count_launch(2);
+    if (T > 0) {
+        k_fan_bucket<true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, p.fan_ptr, p.fan, p.hdr);
+        EFEM_LAUNCH_CHECK();
+    }
+    if (N == 0) return EFEM_OK;
+    FanNodesArgs A{p.elems, p.fan_ptr, p.fan, N, p.rec, p.inc_ptr, p.e2d, p.fan_tiles, p.hdr};
+    k_fan_nodes<<<ntiles, FAN_TPB, 0, s>>>(A);
+    EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
+
+size_t fan_tiles_bytes(int64_t n_nodes) { return ((size_t)(n_nodes + FAN_TPB - 1) / FAN_TPB + 1) * 8; }
+
+}  // namespace efem

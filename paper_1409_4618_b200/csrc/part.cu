@@ -275,6 +275,10 @@ efem_status efem_part_counts(efem_plan plan, const int32_t* sub2global, int64_t 
         return EFEM_ESTATE;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    {
+        const efem_status e = ensure_enumerated(*p, s);  // (2D symbolic runs the fan pipeline)
+        if (e != EFEM_OK) return e;
+    }
     if (node_hi > node_lo) EFEM_CUDA_TRY(cudaMemsetAsync(owned_cnt, 0, (node_hi - node_lo) * 4, s));
     int64_t* d = reinterpret_cast<int64_t*>(p->d_totals);  // scratch: totals already read back
     k_lower_bound<<<1, 32, 0, s>>>(sub2global, p->n_nodes, node_lo, node_hi, d);
@@ -342,6 +346,10 @@ efem_status efem_part_globalize(efem_plan plan, const int32_t* sub2global, const
         return EFEM_ESTATE;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    if (!p->async_pending) {
+        const efem_status e = ensure_enumerated(*p, s);
+        if (e != EFEM_OK) return e;
+    }
     if (p->n_elems == 0) {
         if (p->part_bound) {
             k_part_first_row<<<1, 32, 0, s>>>(global_ent_ptr, p->part_lo, p->hdr->win);
@@ -379,6 +387,10 @@ efem_status efem_part_numeric(efem_plan plan, unsigned forms, const int64_t* inf
         return EFEM_EINVAL;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    {
+        const efem_status e = ensure_enumerated(*p, s);
+        if (e != EFEM_OK) return e;
+    }
     if (info[1] == 0) {  // the row kernels write row_ptr; an empty slice still needs its 0
         if (forms & EFEM_PATTERN) EFEM_CUDA_TRY(cudaMemsetAsync(slice->row_ptr, 0, 4, s));
         return EFEM_OK;
@@ -429,6 +441,7 @@ efem_status efem_part_enumerate_async(efem_plan plan, int32_t* owned_cnt, efem_s
     cudaStream_t s = (cudaStream_t)stream;
     p->enumerated = p->symbolic = false;
     p->async_pending = true;
+    p->async_fan = false;
     auto enqueue = [&](cudaStream_t q) -> efem_status {
         efem_status e = launch_enumerate(*p, q);
         if (e != EFEM_OK) return e;

@@ -214,3 +214,60 @@ def test_node_ids_beyond_2e27(dim, element):
         assert (np.abs(got - want)[keep] <= REL_TOL * scale[rows][keep]).all()
     del asm, out, coords
     torch.cuda.empty_cache()
+
+
+def test_ne3_sliver_rows_against_exact_rationals():
+    """The NE0-3D rows that _check leaves out of the 1e-12 value comparison
+    (rows touching tets of quality < Q_MIN) are checked against the EXACT
+    matrix entries: the fp64 coordinates are exact rationals, so
+    bruteforce.element_matrices(exact=True) (physical-space DOF duality in
+    fractions.Fraction, no Piola, no quadrature) gives the exact local
+    matrices of PAPER.md:352-363.  Both fp64 evaluations (the GPU's closed
+    form and the oracle's quadrature) must sit within the conditioning bound
+    16 eps / q^2 of the row max (q = the smallest quality among the row's
+    tets: the curl-curl entries cancel like 1 / q^2); the GPU is not allowed
+    to be the worse one by more than that bound either."""
+    import bruteforce
+    from paper_1409_4618_b200 import api
+
+    pts, el = delaunay_mesh(3, 700, 1)
+    q = quality(pts, el)
+    ref = ora.assemble(3, NED0, pts, el)
+    asm = api.Assembler(torch.from_numpy(pts).cuda(), torch.from_numpy(el).cuda(), NED0)
+    out = asm.assemble()
+    gm, gk = out.vals_M.cpu().numpy(), out.vals_K.cpu().numpy()
+    rp, ci = ref.row_ptr, ref.col_idx
+    # rows of the worst slivers
+    qmin_row = np.full(ref.n_dofs, np.inf)
+    np.minimum.at(qmin_row, ref.elems2dofs.ravel(), np.repeat(q, 6))
+    rows = np.argsort(qmin_row)[:24]
+    assert qmin_row[rows].max() < Q_MIN
+    tets_of = {}
+    for t in range(el.shape[0]):
+        for k in range(6):
+            tets_of.setdefault(int(ref.elems2dofs[t, k]), []).append(t)
+    d2n = [tuple(r) for r in ref.dofs2nodes]
+    eps = np.finfo(float).eps
+    worst = 0.0
+    for r in rows:
+        exact_m, exact_k = {}, {}
+        for t in tets_of[int(r)]:
+            g = [int(v) for v in el[t]]
+            keys, M, K = bruteforce.element_matrices(3, NED0, pts[g].tolist(), g, exact=True)
+            kr = keys.index(d2n[r])
+            for l, key in enumerate(keys):
+                exact_m[key] = exact_m.get(key, 0) + M[kr][l]
+                exact_k[key] = exact_k.get(key, 0) + K[kr][l]
+        lo, hi = rp[r], rp[r + 1]
+        cols = [d2n[c] for c in ci[lo:hi]]
+        assert sorted(cols) == sorted(exact_m)  # the pattern is the exact one
+        bound = 16 * eps / qmin_row[r] ** 2
+        for got, ora_v, ex in ((gm, ref.vals_M, exact_m), (gk, ref.vals_K, exact_k)):
+            xv = np.array([float(ex[c]) for c in cols])
+            scale = np.abs(xv).max()
+            e_gpu = np.abs(got[lo:hi] - xv).max() / scale
+            e_ora = np.abs(ora_v[lo:hi] - xv).max() / scale
+            assert e_gpu <= bound, (int(r), e_gpu, e_ora, bound)
+            assert e_ora <= bound, (int(r), e_gpu, e_ora, bound)
+            worst = max(worst, e_gpu * qmin_row[r] ** 2 / eps)
+    print(f"worst GPU error x q^2 / eps over the sliver rows: {worst:.3g}")
