@@ -297,6 +297,78 @@ efem_status efem_part_numeric_async(efem_plan plan, unsigned forms, const int32_
  * (device), e.g. for an allgather of the owned entry counts. */
 efem_status efem_part_window(efem_plan plan, int64_t* window_dev, efem_stream_t stream);
 
+/* ---- distributed 2D assembly over NCCL (BASELINE north_star) -----------
+ * The elements are split into contiguous slabs, one per rank (one process
+ * per GPU).  Rank r owns the nodes [lo_r, lo_{r+1}), lo_r = the smallest
+ * vertex of its slab (made non-decreasing; lo_0 = 0, lo_P = n_nodes), hence
+ * the edges whose smaller node it owns: the contiguous block of global rows
+ * [first_row, first_row + rows) of M and K (DOF ids are lexicographic in the
+ * sorted node pair; the global matrices PAPER.md:335-342).
+ * Per step a rank computes the local matrices of its own
+ * slab only and sends those of the triangles holding another rank's rows to
+ * that rank (grouped ncclSend / ncclRecv), the ranks all-gather their row /
+ * entry totals, and the owners answer the ids of the columns they own; each
+ * rank then writes its CSR slice: row_ptr from 0, global column ids, values
+ * summed in ascending element order.  The slices concatenated in rank order
+ * are the 1-GPU matrices (pattern byte for byte).  NCCL is called by this
+ * library; the caller only moves the 128-byte unique id between processes.
+ * Triangles (dim 2) only; 3D meshes use efem_part_* (owner computes). */
+typedef struct efem_comm_s* efem_comm;
+typedef struct efem_dist_plan_s* efem_dist_plan;
+
+/* A fresh ncclUniqueId (128 bytes) into id (host), on one rank. */
+efem_status efem_comm_unique_id(unsigned char* id);
+/* ncclCommInitRank over the given id; collective over the nranks processes
+ * (blocking).  The CUDA device current at the call is the rank's device. */
+efem_status efem_comm_init(efem_comm* comm, const unsigned char* id, int nranks, int rank);
+efem_status efem_comm_destroy(efem_comm comm);
+
+/* Setup of one rank (collective, synchronising, untimed): mesh = the whole
+ * mesh in this rank's device memory (dim 2; kept by pointer), the rank's
+ * slab [elem_lo, elem_hi) of it, comm from efem_comm_init.  Computes the node
+ * ranges and the communication pattern (which triangles go to which rank,
+ * which column ids each rank answers) and allocates the plan's own device
+ * buffers (freed by efem_dist_plan_destroy).  EFEM_EINVAL: not a 2D mesh,
+ * bad slab, node id out of range; EFEM_ENCCL / EFEM_ECUDA. */
+efem_status efem_dist_plan_create(efem_dist_plan* plan, const efem_mesh* mesh, efem_element element, int64_t elem_lo,
+                                  int64_t elem_hi, efem_comm comm, efem_stream_t stream);
+
+/* The same for all nranks ranks of a LOCAL GROUP inside one process on one
+ * device (elem_bounds: nranks + 1 non-decreasing slab bounds, 0 ..
+ * n_elems): every exchange becomes a device-to-device copy.  For testing
+ * the multi-rank logic where only one GPU exists; plans[r] is rank r. */
+efem_status efem_dist_group_create(efem_dist_plan* plans, int nranks, const efem_mesh* mesh, efem_element element,
+                                   const int64_t* elem_bounds, efem_stream_t stream);
+
+/* Host-only: the partition this library computes at setup, for rank `rank`
+ * of nranks over the HOST copy h_elems of a 2D mesh split at elem_bounds
+ * (nranks + 1): out (host, 3 + nranks) = {owned nodes lo, hi, kept slab
+ * triangles, triangles sent to rank 0 .. nranks-1}.  No device work (used
+ * by the CPU tests of the multi-rank logic). */
+efem_status efem_dist_layout(const int32_t* h_elems, int64_t n_nodes, int64_t n_elems, const int64_t* elem_bounds,
+                             int nranks, int rank, int64_t* out);
+
+/* info (host, 8): owned nodes lo, hi; kept slab triangles; ghost triangles
+ * received; triangles sent; column ids requested; ids answered; bytes this
+ * rank sends per step. */
+efem_status efem_dist_info(efem_dist_plan plan, int64_t* info);
+
+/* One step on this rank (collective; asynchronous on the stream): the slice
+ * (device) has CAPACITIES slice->n_rows / nnz; a window larger than them is
+ * not written and makes efem_dist_check return EFEM_ECAPACITY (a first call
+ * with zero capacities is the size query).  forms as efem_assemble_numeric. */
+efem_status efem_dist_assemble(efem_dist_plan plan, unsigned forms, efem_csr* slice, efem_stream_t stream);
+
+/* One step of every rank of a local group (slices[r] for rank r). */
+efem_status efem_dist_assemble_group(efem_dist_plan* plans, int nranks, unsigned forms, efem_csr* slices,
+                                     efem_stream_t stream);
+
+/* Synchronising: window (host, 4) = {global first row, rows, global offset of
+ * the first entry, entries} of the last step; the step's status
+ * (EFEM_EDEGENERATE / EFEM_ECAPACITY / EFEM_EINVAL for a non-conforming mesh). */
+efem_status efem_dist_check(efem_dist_plan plan, int64_t* window, efem_stream_t stream);
+efem_status efem_dist_plan_destroy(efem_dist_plan plan);
+
 /* ---- vectorized integration (Sec. 3.1)
  * The paper's recipe: map the quadrature points of the reference element to
  * every element at once, evaluate the user's function there (the caller does

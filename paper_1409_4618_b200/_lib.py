@@ -107,6 +107,17 @@ def load():
         "efem_p1_load": (st, [vp, vp, vp, vp]),
         "efem_p1_gradient": (st, [ctypes.POINTER(efem_mesh), vp, vp, vp]),
         "efem_dirichlet": (st, [ctypes.POINTER(efem_csr), vp, vp, vp]),
+        "efem_comm_unique_id": (st, [vp]),
+        "efem_comm_init": (st, [ctypes.POINTER(vp), vp, ctypes.c_int, ctypes.c_int]),
+        "efem_comm_destroy": (st, [vp]),
+        "efem_dist_plan_create": (st, [ctypes.POINTER(vp), ctypes.POINTER(efem_mesh), ctypes.c_int, i64, i64, vp, vp]),
+        "efem_dist_group_create": (st, [vp, ctypes.c_int, ctypes.POINTER(efem_mesh), ctypes.c_int, vp, vp]),
+        "efem_dist_layout": (st, [vp, i64, i64, vp, ctypes.c_int, ctypes.c_int, vp]),
+        "efem_dist_info": (st, [vp, vp]),
+        "efem_dist_assemble": (st, [vp, ctypes.c_uint, ctypes.POINTER(efem_csr), vp]),
+        "efem_dist_assemble_group": (st, [vp, ctypes.c_int, ctypes.c_uint, vp, vp]),
+        "efem_dist_check": (st, [vp, vp, vp]),
+        "efem_dist_plan_destroy": (st, [vp]),
         "efem_status_string": (ctypes.c_char_p, [st]),
         "efem_last_error": (ctypes.c_char_p, []),
         "efem_last_bad_element": (i64, []),

@@ -13,12 +13,29 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["mesh.cu", "dofs.cu", "assemble.cu", "api.cu", "fan2d.cu", "part.cu", "integrate.cu", "p1.cu"]
+SOURCES = ["mesh.cu", "dofs.cu", "assemble.cu", "api.cu", "fan2d.cu", "dist2d.cu", "part.cu", "integrate.cu", "p1.cu"]
 LIB = os.path.join(HERE, "libefem.so")
 BUILD_DIR = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+def _nccl_dir():
+    """The NCCL that torch loads (the venv's nvidia-nccl wheel): libefem.so
+    links the same libnccl.so.2, so one NCCL lives in the process."""
+    try:
+        import nvidia.nccl as m
+
+        d = list(m.__path__)[0]
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    except Exception:
+        pass
+    raise RuntimeError("nccl.h / libnccl.so.2 not found (nvidia-nccl wheel)")
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xcompiler", "-fPIC",
-         "-I" + os.path.join(ROOT, "include")]
+         "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(NCCL, "include")]
+LINK = ["-L" + os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
 
 
 def _stale(target, deps):
@@ -49,7 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         list(ex.map(run, jobs))
     if force or jobs or _stale(LIB, objs):
-        run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs)
+        run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + LINK)
     return LIB
 
 

@@ -68,28 +68,26 @@ __device__ __forceinline__ void tri_load_x(const double* __restrict__ coords, Tr
 // returns det; m0/k0 own entry, m1,k1 / m2,k2 the entries of columns d1, d2
 __device__ __forceinline__ double tri_row(const Tri& T, double& m0, double& k0, double& m1, double& k1,
                                           double& m2, double& k2) {
-    const double ax = T.x1.x - T.x0.x, ay = T.x1.y - T.x0.y;  // q1 - q0
-    const double bx = T.x2.x - T.x0.x, by = T.x2.y - T.x0.y;  // q2 - q0
-    const double det = ax * by - bx * ay;
-    const double cx = (ax + bx) * (1.0 / 3.0), cy = (ay + by) * (1.0 / 3.0);
-    const double y0x = -cx, y0y = -cy;
-    const double y1x = ax - cx, y1y = ay - cy;
-    const double y2x = bx - cx, y2y = by - cy;
-    const double n0 = y0x * y0x + y0y * y0y;
-    const double Q = (n0 + (y1x * y1x + y1y * y1y) + (y2x * y2x + y2y * y2y)) * (1.0 / 12.0);
-    const double rad = 1.0 / fabs(det);
-    const double cm = 0.5 * rad, ck = 2.0 * rad;
+    const TriVals V = tri_vals(T.x0, T.x1, T.x2);
     const bool so = T.q1 < T.q2;  // s_own
     const bool sg1 = so == (T.q2 < T.q0), sg2 = so == (T.q0 < T.q1);  // s_own s_l > 0
-    m0 = cm * (n0 + Q);
-    k0 = ck;
-    const double v1 = cm * ((y0x * y1x + y0y * y1y) + Q), v2 = cm * ((y0x * y2x + y0y * y2y) + Q);
-    m1 = sg1 ? v1 : -v1;
-    m2 = sg2 ? v2 : -v2;
-    k1 = sg1 ? ck : -ck;
-    k2 = sg2 ? ck : -ck;
-    return det;
+    m0 = V.m0;
+    k0 = V.ck;
+    m1 = sg1 ? V.v1 : -V.v1;
+    m2 = sg2 ? V.v2 : -V.v2;
+    k1 = sg1 ? V.ck : -V.ck;
+    k2 = sg2 ? V.ck : -V.ck;
+    return V.det;
 }
+
+// Ghost triangles of a distributed assembly (dist2d.cu): triangles of another
+// rank's slab whose local matrices that rank computed and sent.  A triangle
+// with (local) index e >= base is a ghost; its row k values are
+// vals[(e - base) * 12 + 4 k + {0..3}] = {M_kk, M_k,k+1, M_k,k+2 (unsigned), 2/|det|}
+// in the same rotated frame tri_row uses (bitwise the values tri_row gives).
+// Columns of the distributed path are e2d + col_base (elems2dofs held in
+// rank-local ids; the own DOF comes from own_base).
+// (GhostArgs: efem_internal.cuh)
 
 // Element policies of the pipelined pair kernel (rows of t <= 2 elements).
 // Ids = the gathers that depend only on the instance (L2), Geo = the
@@ -97,17 +95,19 @@ __device__ __forceinline__ double tri_row(const Tri& T, double& m0, double& k0, 
 // other entries of the element's local row.
 struct TriPolicy {
     static constexpr int M = 3;
+    static constexpr bool DEEP = true;   // four-stage pipeline, shared-edge loads (load_ids2 / complete2)
+    static constexpr bool GHOST = false;
     using Ids = Tri;
     struct Geo {};
     __device__ __forceinline__ static void load_ids(const int32_t* __restrict__ elems,
                                                     const int32_t* __restrict__ e2d, int inst, Ids& I) {
         tri_load_ids(elems, e2d, inst, I);
     }
-    __device__ __forceinline__ static void load_x(const double* __restrict__ coords, Ids& I, Geo&) {
+    __device__ __forceinline__ static void load_x(const double* __restrict__ coords, const GhostArgs&, Ids& I, Geo&) {
         tri_load_x(coords, I);
     }
-    __device__ __forceinline__ static double row(const Ids& I, const Geo&, double& m0, double& k0, int (&c)[2],
-                                                 double (&m)[2], double (&k)[2]) {
+    __device__ __forceinline__ static double row(const Ids& I, const Geo&, const GhostArgs&, double& m0, double& k0,
+                                                 int (&c)[2], double (&m)[2], double (&k)[2]) {
         c[0] = I.d1;
         c[1] = I.d2;
         return tri_row(I, m0, k0, m[0], k[0], m[1], k[1]);
@@ -143,6 +143,8 @@ struct TriPolicy {
 // Q = sum |y|^2 / 20, K_kl = 6 s_k s_l / |det| (see local_row).
 struct FacePolicy {
     static constexpr int M = 4;
+    static constexpr bool DEEP = false;
+    static constexpr bool GHOST = false;
     struct Ids {
         int4 g, d;
         int k;
@@ -157,15 +159,16 @@ struct FacePolicy {
         I.g = __ldg(reinterpret_cast<const int4*>(elems) + e);
         I.d = __ldg(reinterpret_cast<const int4*>(e2d) + e);
     }
-    __device__ __forceinline__ static void load_x(const double* __restrict__ coords, Ids& I, Geo& G) {
+    __device__ __forceinline__ static void load_x(const double* __restrict__ coords, const GhostArgs&, Ids& I,
+                                                  Geo& G) {
         const int g[4] = {I.g.x, I.g.y, I.g.z, I.g.w};
 #pragma unroll
         for (int v = 0; v < 4; ++v)
 #pragma unroll
             for (int c = 0; c < 3; ++c) G.x[v][c] = __ldg(coords + (int64_t)g[v] * 3 + c);
     }
-    __device__ __forceinline__ static double row(const Ids& I, const Geo& G, double& m0, double& k0, int (&c)[3],
-                                                 double (&m)[3], double (&kv)[3]) {
+    __device__ __forceinline__ static double row(const Ids& I, const Geo& G, const GhostArgs&, double& m0,
+                                                 double& k0, int (&c)[3], double (&m)[3], double (&kv)[3]) {
         const int g[4] = {I.g.x, I.g.y, I.g.z, I.g.w};
         const int d[4] = {I.d.x, I.d.y, I.d.z, I.d.w};
         double ev[4][3], cen[3];
@@ -248,6 +251,55 @@ struct FacePolicy {
     }
 };
 
+// 2D with ghost triangles (distributed assembly): every triangle loaded in
+// full (no shared-edge shortcut), a ghost's row values read from the
+// received buffer instead of computed, columns shifted by col_base.
+struct GhostTriPolicy {
+    static constexpr int M = 3;
+    static constexpr bool DEEP = false;
+    static constexpr bool GHOST = true;
+    struct Ids {
+        Tri t;
+        int e, k;
+    };
+    struct Geo {
+        double2 gv0, gv1;  // ghost: {M_kk, M_k,k+1}, {M_k,k+2, 2/|det|}
+    };
+    __device__ __forceinline__ static void load_ids(const int32_t* __restrict__ elems,
+                                                    const int32_t* __restrict__ e2d, int inst, Ids& I) {
+        tri_load_ids(elems, e2d, inst, I.t);
+        I.e = inst >> 3;
+        I.k = inst & 7;
+    }
+    __device__ __forceinline__ static void load_x(const double* __restrict__ coords, const GhostArgs& gh, Ids& I,
+                                                  Geo& G) {
+        if (I.e >= gh.base) {
+            const double2* v = reinterpret_cast<const double2*>(gh.vals + (int64_t)(I.e - gh.base) * 12 + 4 * I.k);
+            G.gv0 = __ldg(v);
+            G.gv1 = __ldg(v + 1);
+        } else {
+            tri_load_x(coords, I.t);
+        }
+    }
+    __device__ __forceinline__ static double row(const Ids& I, const Geo& G, const GhostArgs& gh, double& m0,
+                                                 double& k0, int (&c)[2], double (&m)[2], double (&k)[2]) {
+        c[0] = I.t.d1 + gh.col_base;
+        c[1] = I.t.d2 + gh.col_base;
+        if (I.e < gh.base) return tri_row(I.t, m0, k0, m[0], k[0], m[1], k[1]);
+        const Tri& T = I.t;
+        const bool so = T.q1 < T.q2;
+        const bool sg1 = so == (T.q2 < T.q0), sg2 = so == (T.q0 < T.q1);
+        const double ck = G.gv1.y;
+        m0 = G.gv0.x;
+        k0 = ck;
+        m[0] = sg1 ? G.gv0.y : -G.gv0.y;
+        m[1] = sg2 ? G.gv1.x : -G.gv1.x;
+        k[0] = sg1 ? ck : -ck;
+        k[1] = sg2 ? ck : -ck;
+        return 1.0;  // (the sending rank checked the determinant)
+    }
+};
+
 // 2D, persistent and software-pipelined: every warp walks 32-row batches
 // (grid-stride, so concurrently running warps work on neighbouring rows and
 // share element data in L2).  The gather chain per row is
@@ -311,7 +363,7 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
                                                            int32_t* __restrict__ col_idx,
                                                            double* __restrict__ vals_m, double* __restrict__ vals_k,
                                                            WsHeader* hdr, int dyn, long long cap_nnz,
-                                                           const long long* __restrict__ win) {
+                                                           const long long* __restrict__ win, GhostArgs gh) {
     constexpr int M = P::M, NO = M - 1;
     int n_rows = dyn ? dyn_rows(hdr, n_rows_arg, cap_nnz) : n_rows_arg;
     if constexpr (WIN) {  // (a template flag: the common path carries none of this)
@@ -345,7 +397,7 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
     // the records of b+3 are in flight.  Faces (24 doubles of coordinates per
     // pair): three stages -- coordinates of b, element data of b+1, records
     // of b+2.
-    constexpr bool DEEP = P::M == 3;
+    constexpr bool DEEP = P::DEEP;
     TriL1 c1 = tri_l1(inc_ptr, rec, batch, nbatch, n_rows, lane);
     TriL1 n1 = tri_l1(inc_ptr, rec, batch + stride, nbatch, n_rows, lane);
     TriL1 n2 = DEEP ? tri_l1(inc_ptr, rec, batch + 2 * stride, nbatch, n_rows, lane) : TriL1{};
@@ -354,7 +406,7 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
         P::load_ids(elems, e2d, c1.rr.x, T0);
         P::load_ids2(elems, e2d, c1.rr.y, T1);
         typename P::Geo g;
-        P::load_x(coords, T0, g);
+        P::load_x(coords, gh, T0, g);
         P::load_x2(coords, T1);
         if (batch + stride < nbatch) {
             P::load_ids(elems, e2d, n1.rr.x, U0);
@@ -373,7 +425,7 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
         if constexpr (DEEP) {
             // L3 of b+1, L2 of b+2, L1 of b+3
             if (has_next) {
-                P::load_x(coords, U0, G0);
+                P::load_x(coords, gh, U0, G0);
                 P::load_x2(coords, U1);
             }
             if (batch + 2 * stride < nbatch) {
@@ -383,8 +435,8 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
             n3 = tri_l1(inc_ptr, rec, batch + 3 * stride, nbatch, n_rows, lane);
         } else {
             // L3 of b, L2 of b+1, L1 of b+2
-            P::load_x(coords, T0, G0);
-            P::load_x(coords, T1, G1);
+            P::load_x(coords, gh, T0, G0);
+            P::load_x(coords, gh, T1, G1);
             if (has_next) {
                 P::load_ids(elems, e2d, n1.rr.x, U0);
                 P::load_ids(elems, e2d, n1.rr.y, U1);
@@ -421,8 +473,8 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
                 double m0a, k0a, m0b, k0b, ma[NO], ka[NO], mb[NO], kb[NO];
                 int ca[NO], cb[NO];
                 if constexpr (DEEP) P::complete2(T0, T1);
-                const double da = P::row(T0, G0, m0a, k0a, ca, ma, ka);
-                const double db = P::row(T1, G1, m0b, k0b, cb, mb, kb);
+                const double da = P::row(T0, G0, gh, m0a, k0a, ca, ma, ka);
+                const double db = P::row(T1, G1, gh, m0b, k0b, cb, mb, kb);
                 const bool bad_a = !(fabs(da) > 0.0 && fabs(da) < INFINITY);
                 const bool bad_b = two && !(fabs(db) > 0.0 && fabs(db) < INFINITY);
                 if (bad_a || bad_b) {
@@ -901,10 +953,20 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
             kern<<<(unsigned)(need < grid ? need : grid), TRI_TPB, 0, s>>>(
                 p.coords, p.elems, inc_ptr, p.rec + (w.win ? 0 : w.row0), w.e2d, (int)w.row0, (int)w.n_rows,
                 w.own_base, w.out_base, forms, out->row_ptr, out->col_idx, vm, vk, p.hdr, (int)w.dyn,
-                (long long)w.cap_nnz, w.win);
+                (long long)w.cap_nnz, w.win, w.gh);
             return EFEM_OK;
         };
-        const efem_status st = w.win ? launch(k_rows_tri<KT, P, MINB, true>) : launch(k_rows_tri<KT, P, MINB, false>);
+        efem_status st;
+        if constexpr (KT::D == 2) {
+            if (w.ghost) {
+                st = w.win ? launch(k_rows_tri<KT, GhostTriPolicy, MINB, true>)
+                           : launch(k_rows_tri<KT, GhostTriPolicy, MINB, false>);
+                if (st != EFEM_OK) return st;
+                EFEM_LAUNCH_CHECK();
+                return EFEM_OK;
+            }
+        }
+        st = w.win ? launch(k_rows_tri<KT, P, MINB, true>) : launch(k_rows_tri<KT, P, MINB, false>);
         if (st != EFEM_OK) return st;
     } else {
         const int fast_ids = p.n_nodes < (1ll << 27);

@@ -98,6 +98,10 @@ struct Plan {
     int32_t* fan_ptr = nullptr;      // N+1
     int32_t* fan = nullptr;          // 2T triangle ids
     unsigned long long* fan_tiles = nullptr;  // look-back tile states
+    // owned node range of a distributed plan (dist2d.cu): the fan pipeline
+    // builds rows only for nodes [own_lo, own_lo + own_n); own_n < 0: all
+    int64_t own_lo = 0, own_n = -1;
+    int32_t* node_ent = nullptr;     // optional: first row of each owned node (dist2d.cu)
     bool fan_valid = false;          // rec / inc_ptr / e2d are current from the fan pipeline
     bool want_d2n = false;
     bool exact_ne3 = false;  // NE0 3D: exact link counts (non-manifold meshes), efem_plan_set_exact
@@ -139,6 +143,15 @@ struct Plan {
     int64_t n_dofs = 0, nnz = 0;
 };
 
+// Ghost triangles of a distributed 2D assembly (dist2d.cu, assemble.cu
+// GhostTriPolicy): local triangle index e >= base is a ghost, its row values
+// at vals[(e - base) * 12 + 4 k ..]; columns are elems2dofs + col_base.
+struct GhostArgs {
+    const double* vals = nullptr;
+    int base = 0x7fffffff;
+    int col_base = 0;
+};
+
 // Rows [row0, row0 + n_rows) of a plan, written to a CSR whose entry 0 is the
 // plan's entry row_ptr[row0] = out_base; own DOF of local row i is
 // own_base + i; column ids from e2d (local or globalised).
@@ -153,6 +166,9 @@ struct RowWindow {
     // bound partition, asynchronous: row0 / n_rows / out_base / own_base come
     // from this device window (WsHeader::win); n_rows, cap_nnz are capacities
     const long long* win = nullptr;
+    // distributed 2D assembly: ghost triangles (GhostTriPolicy)
+    bool ghost = false;
+    GhostArgs gh;
 };
 
 // ---- error plumbing --------------------------------------------------------------
@@ -197,7 +213,8 @@ efem_status run_signs(Plan& p, cudaStream_t s);
 efem_status ensure_enumerated(Plan& p, cudaStream_t s);
 // 2D node-fan pipeline (fan2d.cu)
 inline bool uses_fan(const Plan& p) { return p.dim == 2; }
-efem_status launch_fan_symbolic(Plan& p, cudaStream_t s);
+efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset = true);
+efem_status launch_hdr_reset(Plan& p, cudaStream_t s);
 size_t fan_tiles_bytes(int64_t n_nodes);
 // row_ptr helpers (api.cu): 2D edges / 3D faces keep no row_ptr array, row r
 // starts at r + (m-1) inc_ptr[r]; 3D edges store it (plan row_ptr).

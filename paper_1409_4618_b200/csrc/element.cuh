@@ -7,6 +7,39 @@
 
 namespace efem {
 
+// 2D local row in the frame rotated so that vertex q0 (the vertex opposite
+// the row's edge) comes first: closed form of PAPER.md:344-363 for the
+// sign-corrected Piola-mapped RT0 basis (= NE0 in 2D):
+//   M_kl = s_k s_l (y_k . y_l + Q) / (2 |det|),  Q = sum_v |y_v|^2 / 12,
+//   K_kl = 2 s_k s_l / |det|,   y_v = x_v - centroid.
+// Unsigned values of the row: m0 = M_00, v1 = M_01, v2 = M_02 (x1 = q1,
+// x2 = q2), ck = 2 / |det|.  One definition for the numeric kernel
+// (assemble.cu tri_row) and the ghost triangles of the distributed path
+// (dist2d.cu), so both give the same bits.
+struct TriVals {
+    double det, m0, v1, v2, ck;
+};
+
+__device__ __forceinline__ TriVals tri_vals(double2 x0, double2 x1, double2 x2) {
+    TriVals V;
+    const double ax = x1.x - x0.x, ay = x1.y - x0.y;  // q1 - q0
+    const double bx = x2.x - x0.x, by = x2.y - x0.y;  // q2 - q0
+    V.det = ax * by - bx * ay;
+    const double cx = (ax + bx) * (1.0 / 3.0), cy = (ay + by) * (1.0 / 3.0);
+    const double y0x = -cx, y0y = -cy;
+    const double y1x = ax - cx, y1y = ay - cy;
+    const double y2x = bx - cx, y2y = by - cy;
+    const double n0 = y0x * y0x + y0y * y0y;
+    const double Q = (n0 + (y1x * y1x + y1y * y1y) + (y2x * y2x + y2y * y2y)) * (1.0 / 12.0);
+    const double rad = 1.0 / fabs(V.det);
+    const double cm = 0.5 * rad;
+    V.ck = 2.0 * rad;
+    V.m0 = cm * (n0 + Q);
+    V.v1 = cm * ((y0x * y1x + y0y * y1y) + Q);
+    V.v2 = cm * ((y0x * y2x + y0y * y2y) + Q);
+    return V;
+}
+
 template <class KT>
 __device__ __forceinline__ void load_g(const int32_t* __restrict__ elems, int e, int (&g)[KT::NV]) {
     if constexpr (KT::NV == 4) {

@@ -54,10 +54,13 @@ __device__ __forceinline__ void sort3(int& p, int& q, int& r) {
 // each count (atomicSub), which returns the counts to zero for the next
 // call; the order inside a fan is fixed later (ascending e).
 // ---------------------------------------------------------------------------------
+// (distributed assembly: only the fans of the owned nodes [lo, lo + n_own),
+// indexed from lo; single GPU: lo = 0, n_own = n_nodes)
 template <bool FILL>
 __global__ void __launch_bounds__(256) k_fan_bucket(const int32_t* __restrict__ elems, int64_t n_elems, int64_t n_nodes,
-                                                    int32_t* __restrict__ cnt, const int32_t* __restrict__ fan_ptr,
-                                                    int32_t* __restrict__ fan, WsHeader* hdr) {
+                                                    int64_t lo, int64_t n_own, int32_t* __restrict__ cnt,
+                                                    const int32_t* __restrict__ fan_ptr, int32_t* __restrict__ fan,
+                                                    WsHeader* hdr) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= n_elems) return;
     int p = __ldg(elems + 3 * e), q = __ldg(elems + 3 * e + 1), r = __ldg(elems + 3 * e + 2);
@@ -66,12 +69,15 @@ __global__ void __launch_bounds__(256) k_fan_bucket(const int32_t* __restrict__ 
         return;  // (skipped consistently by count and fill; the call reports EFEM_EINVAL)
     }
     sort3(p, q, r);
+    const int64_t lp = p - lo, lq = q - lo;
+    const bool op = (unsigned long long)lp < (unsigned long long)n_own;
+    const bool oq = q != p && (unsigned long long)lq < (unsigned long long)n_own;
     if constexpr (!FILL) {
-        atomicAdd(cnt + p, 1);
-        if (q != p) atomicAdd(cnt + q, 1);
+        if (op) atomicAdd(cnt + lp, 1);
+        if (oq) atomicAdd(cnt + lq, 1);
     } else {
-        fan[__ldg(fan_ptr + p) + atomicSub(cnt + p, 1) - 1] = (int)e;
-        if (q != p) fan[__ldg(fan_ptr + q) + atomicSub(cnt + q, 1) - 1] = (int)e;
+        if (op) fan[__ldg(fan_ptr + lp) + atomicSub(cnt + lp, 1) - 1] = (int)e;
+        if (oq) fan[__ldg(fan_ptr + lq) + atomicSub(cnt + lq, 1) - 1] = (int)e;
     }
 }
 
@@ -89,9 +95,10 @@ __global__ void __launch_bounds__(256) k_fan_bucket(const int32_t* __restrict__ 
 // ---------------------------------------------------------------------------------
 struct FanNodesArgs {
     const int32_t* elems;
-    const int32_t* fan_ptr;
+    const int32_t* fan_ptr;  // indexed from node lo
     int32_t* fan;  // big fans (> FAN_REG) are sorted in place here
-    int64_t n_nodes;
+    int64_t lo, n_nodes;     // owned nodes [lo, lo + n_nodes)
+    int32_t* node_ent;       // optional (n_nodes + 1): first row of each owned node
     int2* rec;
     int32_t* inc_ptr;
     int32_t* e2d;
@@ -234,9 +241,9 @@ __global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
     if (threadIdx.x == 0) s_tile = atomicAdd(&A.hdr->tile_ticket, 1);
     __syncthreads();
     const int tile = s_tile;
-    const int64_t a64 = (int64_t)tile * FAN_TPB + threadIdx.x;
-    const bool live = a64 < A.n_nodes;
-    const int a = (int)a64;
+    const int64_t l64 = (int64_t)tile * FAN_TPB + threadIdx.x;  // owned node index
+    const bool live = l64 < A.n_nodes;
+    const int a = (int)(A.lo + l64);
     int n_ent = 0, n_inst = 0, beg = 0, n = 0;
     bool bad = false, slow = false;
     unsigned key[2 * FAN_REG];
@@ -246,8 +253,8 @@ __global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
 #pragma unroll
     for (int j = 0; j < FAN_REG; ++j) ev[j] = 0;
     if (live) {
-        beg = __ldg(A.fan_ptr + a);
-        n = __ldg(A.fan_ptr + a + 1) - beg;
+        beg = __ldg(A.fan_ptr + l64);
+        n = __ldg(A.fan_ptr + l64 + 1) - beg;
         slow = n > FAN_REG;
         if (!slow) {
 #pragma unroll
@@ -334,6 +341,7 @@ __global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
     if (live) {
         int id = e_tile0 + e_off;  // first DOF of node a
         int inst = i_tile0 + (int)(off & 0x7fffffffull);
+        if (A.node_ent) A.node_ent[l64] = id;
         auto row = [&](int first, int last, int t) {
             if (stage) {
                 s_rec[id - e_tile0] = make_int2(first, last);
@@ -353,7 +361,8 @@ __global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
         } else {
             fan_edges_slow(A.elems, A.fan + beg, a, n, [&](int, int first, int last, int t) { row(first, last, min(t, 2)); });
         }
-        if (a == A.n_nodes - 1) {
+        if (l64 == A.n_nodes - 1) {
+            if (A.node_ent) A.node_ent[A.n_nodes] = id;
             A.inc_ptr[id] = inst;
             A.hdr->totals[0] = id;
             A.hdr->totals[1] = (long long)id + 2ll * inst;  // sum_i (1 + 2 t_i)
@@ -386,25 +395,40 @@ __global__ void k_fan_init(WsHeader* hdr) {
 
 // The symbolic half (K1-K3): sizes in the header totals, offsets and
 // neighbour lists in the plan's fan arrays.  Enqueue only.
-efem_status launch_fan_symbolic(Plan& p, cudaStream_t s) {
-    const int64_t N = p.n_nodes, T = p.n_elems;
+efem_status launch_hdr_reset(Plan& p, cudaStream_t s) {
     k_fan_init<<<1, 32, 0, s>>>(p.hdr);
     EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
+
+efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset) {
+    const int64_t Ng = p.n_nodes, T = p.n_elems;
+    const int64_t lo = p.own_lo, N = p.own_n < 0 ? Ng : p.own_n;  // owned nodes [lo, lo + N)
+    if (reset) {
+        k_fan_init<<<1, 32, 0, s>>>(p.hdr);
+        EFEM_LAUNCH_CHECK();
+    } else {  // (the caller reset the header; the look-back ticket restarts here)
+        EFEM_CUDA_TRY(cudaMemsetAsync(&p.hdr->tile_ticket, 0, 4, s));
+    }
     const int ntiles = (int)grid_for(N, FAN_TPB);
     if (ntiles > 0) EFEM_CUDA_TRY(cudaMemsetAsync(p.fan_tiles, 0, (size_t)ntiles * 8, s));
     if (T > 0) {
-        k_fan_bucket<false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, nullptr, nullptr, p.hdr);
+        k_fan_bucket<false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, nullptr, nullptr, p.hdr);
         EFEM_LAUNCH_CHECK();
     }
     size_t bytes = p.cub_bytes;
     EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.fan_ptr, (int)(N + 1), s));
     count_launch(2);
     if (T > 0) {
-        k_fan_bucket<true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, p.fan_ptr, p.fan, p.hdr);
+        k_fan_bucket<true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_ptr, p.fan, p.hdr);
         EFEM_LAUNCH_CHECK();
     }
-    if (N == 0) return EFEM_OK;
-    FanNodesArgs A{p.elems, p.fan_ptr, p.fan, N, p.rec, p.inc_ptr, p.e2d, p.fan_tiles, p.hdr};
+    if (N == 0) {  // no owned node: an empty row set
+        EFEM_CUDA_TRY(cudaMemsetAsync(p.inc_ptr, 0, 4, s));
+        if (p.node_ent) EFEM_CUDA_TRY(cudaMemsetAsync(p.node_ent, 0, 4, s));
+        return EFEM_OK;
+    }
+    FanNodesArgs A{p.elems, p.fan_ptr, p.fan, lo, N, p.node_ent, p.rec, p.inc_ptr, p.e2d, p.fan_tiles, p.hdr};
     k_fan_nodes<<<ntiles, FAN_TPB, 0, s>>>(A);
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;

@@ -390,3 +390,207 @@ def concat_slices(slices, entry_offsets):
         vm.append(s.vals_M.cpu().numpy())
         vk.append(s.vals_K.cpu().numpy())
     return (np.concatenate(rp), np.concatenate(ci), np.concatenate(vm), np.concatenate(vk))
+
+
+# --------------------------------------------------------------------------- element slabs over NCCL (2D)
+# efem_dist_* (dist2d.cu): the north_star multi-GPU path -- contiguous element
+# slabs, row-owned CSR slices, the off-rank contributions (ghost triangles'
+# local matrices) and column ids exchanged by NCCL inside libefem.  This
+# module only moves the 128-byte NCCL unique id between processes (through
+# torch.distributed) and marshals arguments.
+def slab_bounds(n_elems: int, world: int):
+    """Contiguous element slabs [b_r, b_{r+1}) of (nearly) equal size."""
+    return [n_elems * r // world for r in range(world + 1)]
+
+
+def _empty_csr(device):
+    z32 = torch.zeros(1, dtype=torch.int32, device=device)
+    z64 = torch.zeros(1, dtype=torch.float64, device=device)
+    return CSR(z32, z32.clone(), z64, z64.clone())
+
+
+def _slice_struct(c: CSR, n_rows: int, nnz: int):
+    return _lib.efem_csr(n_rows, nnz, c.row_ptr.data_ptr(), c.col_idx.data_ptr(), c.vals_M.data_ptr(),
+                         c.vals_K.data_ptr())
+
+
+def _alloc_slice(rows: int, nnz: int, device):
+    return CSR(torch.empty(rows + 1, dtype=torch.int32, device=device),
+               torch.empty(max(nnz, 1), dtype=torch.int32, device=device),
+               torch.empty(max(nnz, 1), dtype=torch.float64, device=device),
+               torch.empty(max(nnz, 1), dtype=torch.float64, device=device))
+
+
+def layout(elems_host, n_nodes: int, bounds, rank: int):
+    """efem_dist_layout: (lo, hi, kept, sent-to-rank list) of one rank (host only)."""
+    import numpy as _np
+
+    e = _np.ascontiguousarray(elems_host, dtype=_np.int32)
+    b = (ctypes.c_int64 * len(bounds))(*bounds)
+    P = len(bounds) - 1
+    out = (ctypes.c_int64 * (3 + P))()
+    _lib.check("efem_dist_layout", _lib.load().efem_dist_layout(e.ctypes.data_as(ctypes.c_void_p), n_nodes,
+                                                                  e.shape[0], b, P, rank, out))
+    return out[0], out[1], out[2], list(out[3:3 + P])
+
+
+class DistGroup:
+    """All ranks of one distributed 2D assembly inside this process on one
+    device (efem_dist_group_create): the exchanges are device copies.  For
+    testing the multi-rank path where one GPU exists."""
+
+    def __init__(self, coords: torch.Tensor, elems: torch.Tensor, element: int, bounds, stream=None):
+        L = _lib.load()
+        self.device = coords.device
+        self.P = len(bounds) - 1
+        self._mesh = _lib.efem_mesh(2, coords.shape[0], elems.shape[0], coords.data_ptr(), elems.data_ptr())
+        self._keep = (coords, elems)
+        self.plans = (ctypes.c_void_p * self.P)()
+        b = (ctypes.c_int64 * len(bounds))(*bounds)
+        with torch.cuda.device(self.device):
+            _lib.check("efem_dist_group_create", L.efem_dist_group_create(self.plans, self.P, ctypes.byref(self._mesh),
+                                                                          element, b, _stream(stream)))
+        self.slices = None
+
+    def close(self):
+        if self.plans is not None:
+            for p in self.plans:
+                _lib.load().efem_dist_plan_destroy(p)
+            self.plans = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self, r):
+        out = (ctypes.c_int64 * 8)()
+        _lib.check("efem_dist_info", _lib.load().efem_dist_info(self.plans[r], out))
+        return list(out)
+
+    def _step(self, slices, caps, forms, stream):
+        arr = (_lib.efem_csr * self.P)(*[_slice_struct(s, r, z) for s, (r, z) in zip(slices, caps)])
+        with torch.cuda.device(self.device):
+            _lib.check("efem_dist_assemble_group", _lib.load().efem_dist_assemble_group(self.plans, self.P, forms, arr,
+                                                                                        _stream(stream)))
+
+    def windows(self, stream=None, check=True):
+        out = []
+        for r in range(self.P):
+            w = (ctypes.c_int64 * 4)()
+            st = _lib.load().efem_dist_check(self.plans[r], w, _stream(stream))
+            if check:
+                _lib.check("efem_dist_check", st)
+            out.append((list(w), st))
+        return out
+
+    def assemble(self, forms: int = ALL, stream=None):
+        """One step of every rank; slices sized by a first size-query step."""
+        if self.slices is None:
+            empty = [_empty_csr(self.device) for _ in range(self.P)]
+            self._step(empty, [(0, 0)] * self.P, forms, stream)
+            wins = self.windows(stream, check=False)
+            self.slices = [_alloc_slice(w[1], w[3], self.device) for w, _ in wins]
+        caps = [(s.row_ptr.numel() - 1, s.col_idx.numel()) for s in self.slices]
+        self._step(self.slices, caps, forms, stream)
+        self.last = [w for w, _ in self.windows(stream)]
+        return self.slices
+
+    def concat(self):
+        """The global CSR (host numpy) from the ranks' slices, rank order."""
+        rps, cis, vms, vks = [], [], [], []
+        for s, w in zip(self.slices, self.last):
+            rows, nnz, zoff = w[1], w[3], w[2]
+            rps.append(s.row_ptr[:rows].cpu().numpy().astype(np.int64) + zoff)
+            cis.append(s.col_idx[:nnz].cpu().numpy())
+            vms.append(s.vals_M[:nnz].cpu().numpy())
+            vks.append(s.vals_K[:nnz].cpu().numpy())
+        total = self.last[-1][2] + self.last[-1][3]
+        rp = np.concatenate(rps + [np.array([total], np.int64)]).astype(np.int32)
+        return rp, np.concatenate(cis), np.concatenate(vms), np.concatenate(vks)
+
+
+def nccl_comm(rank: int, world: int, group=None):
+    """An efem_comm over the processes of a torch.distributed group: rank 0
+    draws the NCCL unique id, torch.distributed broadcasts its 128 bytes."""
+    import torch.distributed as tdist
+
+    L = _lib.load()
+    uid = (ctypes.c_ubyte * 128)()
+    if rank == 0:
+        _lib.check("efem_comm_unique_id", L.efem_comm_unique_id(uid))
+    dev = "cuda" if tdist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
+    tdist.broadcast(t, src=0, group=group)
+    raw = bytes(t.cpu().tolist())
+    uid = (ctypes.c_ubyte * 128).from_buffer_copy(raw)
+    comm = ctypes.c_void_p()
+    _lib.check("efem_comm_init", L.efem_comm_init(ctypes.byref(comm), uid, world, rank))
+    return comm
+
+
+class DistAssembler:
+    """This process's rank of a distributed 2D assembly over NCCL
+    (efem_dist_plan_create / efem_dist_assemble)."""
+
+    def __init__(self, coords: torch.Tensor, elems: torch.Tensor, element: int, elem_lo: int, elem_hi: int, comm,
+                 stream=None):
+        L = _lib.load()
+        self.device = coords.device
+        self.comm = comm
+        self._mesh = _lib.efem_mesh(2, coords.shape[0], elems.shape[0], coords.data_ptr(), elems.data_ptr())
+        self._keep = (coords, elems)
+        self.plan = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check("efem_dist_plan_create", L.efem_dist_plan_create(ctypes.byref(self.plan), ctypes.byref(self._mesh),
+                                                                        element, elem_lo, elem_hi, comm,
+                                                                        _stream(stream)))
+        self.slice = None
+        self.window = None
+
+    def info(self):
+        out = (ctypes.c_int64 * 8)()
+        _lib.check("efem_dist_info", _lib.load().efem_dist_info(self.plan, out))
+        return list(out)
+
+    def step(self, forms: int = ALL, stream=None):
+        """Enqueue one step into the current slice (asynchronous)."""
+        s = self.slice
+        c = _slice_struct(s, s.row_ptr.numel() - 1, s.col_idx.numel())
+        with torch.cuda.device(self.device):
+            _lib.check("efem_dist_assemble", _lib.load().efem_dist_assemble(self.plan, forms, ctypes.byref(c),
+                                                                            _stream(stream)))
+
+    def check(self, stream=None):
+        w = (ctypes.c_int64 * 4)()
+        with torch.cuda.device(self.device):
+            _lib.check("efem_dist_check", _lib.load().efem_dist_check(self.plan, w, _stream(stream)))
+        self.window = list(w)
+        return self.window
+
+    def assemble(self, forms: int = ALL, stream=None):
+        """One step with a synchronising check; the first call sizes the slice."""
+        if self.slice is None:
+            self.slice = _empty_csr(self.device)
+            c = _slice_struct(self.slice, 0, 0)
+            with torch.cuda.device(self.device):
+                _lib.check("efem_dist_assemble", _lib.load().efem_dist_assemble(self.plan, forms, ctypes.byref(c),
+                                                                                _stream(stream)))
+            w = (ctypes.c_int64 * 4)()
+            _lib.load().efem_dist_check(self.plan, w, _stream(stream))
+            self.slice = _alloc_slice(w[1], w[3], self.device)
+        self.step(forms, stream)
+        self.check(stream)
+        return self.slice
+
+    def close(self):
+        if self.plan:
+            _lib.load().efem_dist_plan_destroy(self.plan)
+            self.plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
