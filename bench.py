@@ -206,7 +206,7 @@ def run_efem(args, cfg):
     from paper_1409_4618_b200 import api
 
     ws, rank, local = dist_env()
-    if ws > 1:
+    if ws > 1 or args.dist:
         return run_efem_dist(args, cfg)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -322,12 +322,16 @@ def run_efem(args, cfg):
 
 
 def run_efem_dist(args, cfg):
-    """N > 1: one process per GPU, row-owned partition.  Each
-    rank builds the full mesh (untimed) and its two-hop sub-mesh (untimed
-    setup); a timed step is dist.AsyncStep (= assemble_rank_async): the rank's local
-    enumeration, the two all_gathers (per-node entity counts, per-rank nnz),
-    globalisation, the owned-row numeric kernel and the flag read-back; the
-    host half of the check (one round trip) follows each step's end event.  Time = max over ranks of the summed per-step device time."""
+    """N > 1: one process per GPU over NCCL.  2D (configs 1, 2, 5; config 5 is
+    BASELINE's 1/2/4/8-GPU sweep): efem_dist_* -- element slab per rank,
+    row-owned CSR slice, the off-rank contributions (ghost triangles' local
+    matrices) and column ids exchanged by NCCL inside libefem (dist2d.cu);
+    the mesh is fixed, so the scaling is strong.  Each rank builds the full
+    mesh and the partition's communication pattern (untimed setup).  A timed
+    step is one efem_dist_assemble into the rank's slice; its CUDA events
+    bracket the device work, the flag check follows.  Time = max over ranks
+    of the summed per-step device time.  3D configs: the owner-computes
+    partition (efem_part_*, dist.AsyncStep)."""
     import torch
     import torch.distributed as dist
 
@@ -335,21 +339,50 @@ def run_efem_dist(args, cfg):
     from paper_1409_4618_b200 import dist as pdist
 
     ws, rank, local = dist_env()
-    backend = os.environ.get("EFEM_DIST_BACKEND", "nccl")
+    if "MASTER_ADDR" not in os.environ:  # (--dist at N = 1 without torchrun)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]), RANK="0",
+                              WORLD_SIZE="1")
     n_dev = torch.cuda.device_count()
     torch.cuda.set_device(local % n_dev)
     dev = torch.device("cuda", local % n_dev)
-    dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
+    dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream()
     coords, elems = api.build_mesh(cfg["dim"], cfg["n"], cfg["alpha"], cfg["seed"], device=dev)
-    ranges = pdist.node_ranges(coords.shape[0], ws)
-    part = pdist.PartAssembler(coords, elems, cfg["element"], *ranges[rank])
-    out = None
+    T = elems.shape[0]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    out, _, _ = pdist.assemble_rank(part, ranges, out)  # sizes the slice (untimed setup)
-    step = pdist.AsyncStep(part, ranges, out, stream=stream)
+    exch = None
+    if cfg["dim"] == 2:
+        comm = pdist.nccl_comm(rank, ws)
+        bounds = pdist.slab_bounds(T, ws)
+        part = pdist.DistAssembler(coords, elems, cfg["element"], bounds[rank], bounds[rank + 1], comm)
+        part.assemble()  # sizes the slice (untimed)
+        exch = part.info()[7]
+
+        def step():
+            part.step()
+
+        def check():
+            part.check()
+        kind = "element slabs over NCCL (efem_dist_*)"
+    else:
+        ranges = pdist.node_ranges(coords.shape[0], ws)
+        part = pdist.PartAssembler(coords, elems, cfg["element"], *ranges[rank])
+        out, _, _ = pdist.assemble_rank(part, ranges, None)
+        astep = pdist.AsyncStep(part, ranges, out, stream=stream)
+
+        def step():
+            astep(check="async")
+
+        def check():
+            astep.check()
+        kind = "row-owned node ranges, owner computes (efem_part_*)"
     for _ in range(max(args.warmup, 3)):
         step()
+        check()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     l0 = api.launch_count()
@@ -359,22 +392,23 @@ def run_efem_dist(args, cfg):
         for k in range(args.steps):
             flush.fill_(k & 0xff)
             starts[k].record(stream)
-            step(check="async")
+            step()
             ends[k].record(stream)
-            step.check()  # host half of the check (wait + decode), every step, after the device window
+            check()
         torch.cuda.synchronize()
         dist.barrier()
     launches = api.launch_count() - l0
     mine = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
-    t = torch.tensor([mine], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+    t = torch.tensor([mine], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    T = elems.shape[0]
     value = T * args.steps / (total_ms * 1e-3)
     alg_bytes, _ = algorithmic_bytes(cfg)
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs") or 6650.0
     achieved = alg_bytes / (total_ms / args.steps * 1e-3) / 1e9
+    xb = torch.tensor([float(exch or 0)], dtype=torch.float64, device=dev)
+    dist.all_reduce(xb, op=dist.ReduceOp.MAX)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -383,8 +417,8 @@ def run_efem_dist(args, cfg):
             "data": "synthetic",
             "config": {"workload": cfg["name"], "element": ELEMENT_NAMES[cfg["element"]], "dim": cfg["dim"],
                        "n": cfg["n"], "jitter": cfg["alpha"], "seed": cfg["seed"], "n_elems": T,
-                       "elems_per_rank": T / ws,
-                       "parallelism": f"row-owned node ranges x{ws} ({backend})",
+                       "elems_per_rank": T / ws, "parallelism": f"{kind} x{ws}",
+                       "exchange_bytes_per_rank_step": float(xb.item()) if exch is not None else None,
                        "l2": "flushed between timed steps (512 MiB write)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
                          "frac": achieved / (peak * ws), "traffic": None,
@@ -429,6 +463,8 @@ def main():
                          "the one BASELINE sweeps over 1/2/4/8 GPUs (strong scaling: the mesh is fixed)")
     ap.add_argument("--impl", default="efem", choices=["efem", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="run the multi-GPU code path (NCCL) even at N = 1 (a one-rank communicator)")
     args = ap.parse_args()
     ws = dist_env()[0]
     if "WORLD_SIZE" in os.environ and ws != args.gpus:

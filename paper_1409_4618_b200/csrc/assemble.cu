@@ -306,7 +306,10 @@ struct GhostTriPolicy {
 //   L1 inc_ptr[i], inc_ptr[i+1], rec[i]  ->  L2 elems / elems2dofs  ->  L3 coords
 // and is overlapped across batches: while batch b is computed, the L2 loads
 // of batch b+1 and the L1 loads of batch b+2 are in flight.
-constexpr int TRI_TPB = 256;
+#ifndef EFEM_TRI_TPB
+#define EFEM_TRI_TPB 256
+#endif
+constexpr int TRI_TPB = EFEM_TRI_TPB;
 
 // Asynchronous assembly (efem_assemble_async): the row count comes from the
 // enumeration's header totals on the device; a pattern larger than the output
@@ -365,6 +368,8 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
                                                            WsHeader* hdr, int dyn, long long cap_nnz,
                                                            const long long* __restrict__ win, GhostArgs gh) {
     constexpr int M = P::M, NO = M - 1;
+    // node ids out of range (flagged by the enumeration): nothing is gathered
+    if (*(volatile const int*)&hdr->flags[F_INVALID_NODE]) return;
     int n_rows = dyn ? dyn_rows(hdr, n_rows_arg, cap_nnz) : n_rows_arg;
     if constexpr (WIN) {  // (a template flag: the common path carries none of this)
         n_rows = win_rows(hdr, win, n_rows_arg, cap_nnz);
@@ -799,7 +804,7 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                     for (int u = 0; u < 6; ++u) {
                         // rank of the column's bit among the row's: popcount of the
                         // bits below it (mask shifted up: no 64-bit subtract / and)
-                        const int pb_ = (pi >> (6 * (u - 1))) & 63;
+                        const int pb_ = u ? (pi >> (6 * (u - 1))) & 63 : 0;
                         const int slot = (u == 0 ? sab : (pb_ ? __popcll(mask << (64 - pb_)) : 0)) * st;
                         ccol[slot] = dof[u];
                         cvm[slot] += vm[u];
@@ -825,6 +830,8 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
                                                       WsHeader* hdr, int dyn, long long cap_nnz,
                                                       const long long* __restrict__ win) {
     static_assert(KT::D == 3 && !KT::FACES, "NE0 3D only");
+    // node ids out of range (flagged by the enumeration): nothing is gathered
+    if (*(volatile const int*)&hdr->flags[F_INVALID_NODE]) return;
     int n_rows = dyn ? dyn_rows(hdr, n_rows_arg, cap_nnz) : n_rows_arg;
     if (win) {
         n_rows = win_rows(hdr, win, n_rows_arg, cap_nnz);
@@ -935,7 +942,10 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
     const int32_t* row_ptr = p.row_ptr + (w.win ? 0 : w.row0);
     if constexpr (KT::D == 2 || KT::FACES) {
         using P = std::conditional_t<KT::D == 2, TriPolicy, FacePolicy>;
-        constexpr int MINB = 2;
+#ifndef EFEM_TRI_MINB
+#define EFEM_TRI_MINB 2
+#endif
+        constexpr int MINB = EFEM_TRI_MINB;
         auto launch = [&](auto kern) -> efem_status {
             // persistent grid = SMs x resident CTAs, per device (cached)
             static std::atomic<int> grids[kMaxDevices];

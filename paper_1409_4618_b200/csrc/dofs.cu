@@ -802,9 +802,11 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_write(const int32_t*
 template <class KT>
 __global__ void __launch_bounds__(256) k_elem_dofs(const int32_t* __restrict__ elems, int64_t n_elems,
                                                    const int32_t* __restrict__ ent_ptr,
-                                                   const int32_t* __restrict__ nbr, int32_t* __restrict__ e2d) {
+                                                   const int32_t* __restrict__ nbr, int32_t* __restrict__ e2d,
+                                                   const WsHeader* hdr) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= n_elems) return;
+    if (*(volatile const int*)&hdr->flags[F_INVALID_NODE]) return;  // raw ids index ent_ptr below
     int g[4];
     load_elem<KT>(elems, (int)e, g);
     int id[6];
@@ -895,7 +897,7 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     EFEM_LAUNCH_CHECK();
     if constexpr (KT::D == 3 && !KT::FACES) {
         if (T > 0) {
-            k_elem_dofs<KT><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, p.ent_ptr, p.nbr, p.e2d);
+            k_elem_dofs<KT><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, p.ent_ptr, p.nbr, p.e2d, p.hdr);
             EFEM_LAUNCH_CHECK();
         }
     }

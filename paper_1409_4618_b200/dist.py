@@ -276,6 +276,9 @@ class AsyncStep:
             part.bind(max(hi - lo for lo, hi in ranges), self.world, stream=stream)
         self.L = _lib.load()
         self.s = _stream(stream)
+        # the collectives are issued on torch's current stream: make it the
+        # stream the library calls are enqueued on, so they stay ordered
+        self.tstream = stream if stream is not None else torch.cuda.current_stream(part.device)
         self.empty = part.empty
         self.plan = None if part.empty else part.asm._plan
         self.p_owned = _ptr(part.owned_pad)
@@ -295,6 +298,10 @@ class AsyncStep:
         self.nnz_all = torch.empty(self.world, dtype=torch.int64, device=part.device)
 
     def __call__(self, check=True):
+        with torch.cuda.stream(self.tstream):
+            return self._call(check)
+
+    def _call(self, check):
         import torch.distributed as dist
 
         L, ck = self.L, _lib.check

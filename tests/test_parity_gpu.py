@@ -169,6 +169,29 @@ def test_invalid_node_id_reported(api):
     assert ei.value.status == -1
 
 
+@pytest.mark.parametrize("dim,element", KINDS, ids=KIND_IDS)
+@pytest.mark.parametrize("bad", [-5, 1 << 30], ids=["negative", "2^30"])
+@pytest.mark.parametrize("path", ["sync", "async"])
+def test_out_of_range_node_ids_reported(api, dim, element, bad, path):
+    """A node id outside [0, n_nodes) is EFEM_EINVAL on every path, never an
+    illegal address: the kernels after the enumeration's flag return early."""
+    rc, re = ora.build_mesh(dim, 3, 0.1, 0)
+    asm = api.Assembler(torch.from_numpy(rc).cuda(), torch.from_numpy(re).cuda(), element)
+    good = asm.assemble()
+    e = torch.from_numpy(re).cuda()
+    e[len(re) // 2, 1] = bad
+    asm2 = api.Assembler(torch.from_numpy(rc).cuda(), e, element)
+    with pytest.raises(api._lib.EfemError) as ei:
+        if path == "sync":
+            asm2.assemble()
+        else:
+            asm2.assemble_async(asm.alloc_csr(good.n_rows, good.nnz))
+            asm2.check()
+    assert ei.value.status == -1
+    torch.cuda.synchronize()  # the context is intact
+    assert torch.equal(asm.assemble().col_idx, good.col_idx)
+
+
 def _bowtie_tets():
     """Two tets sharing only the edge (0, 1): a non-manifold fan (its link is
     two disjoint segments)."""
