@@ -6,7 +6,7 @@ cfgs=${2:-"4"}
 mkdir -p gpurun_out
 for c in $cfgs; do
   for n in $names; do
-    cp variants/$n/libefem.so paper_1409_4618_b200/libefem.so
+    cp vbuild/$n/libefem.so paper_1409_4618_b200/libefem.so
     timeout 300 python tools/time_numeric.py --config $c --tag $n 2>&1 | tail -1
   done
 done

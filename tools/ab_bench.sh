@@ -2,7 +2,7 @@
 # A/B of prebuilt variants through bench.py (graph step):  tools/ab_bench.sh "base A" "2 5"
 for c in ${2:-2}; do
   for n in ${1:-base A}; do
-    cp variants/$n/libefem.so paper_1409_4618_b200/libefem.so
+    cp vbuild/$n/libefem.so paper_1409_4618_b200/libefem.so
     timeout 300 python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "
 import json,sys
 d=json.loads([l for l in sys.stdin if l.startswith('{')][-1]); print('cfg$c $n', round(d['ms_per_step'],4), d['phase_ms'])"

@@ -11,7 +11,7 @@ sys.path.insert(0, ROOT)
 from paper_1409_4618_b200 import build as b  # noqa: E402
 
 name, extra = sys.argv[1], sys.argv[2:]
-out = os.path.join(ROOT, "variants", name)
+out = os.path.join(ROOT, "vbuild", name)
 os.makedirs(out, exist_ok=True)
 objs = []
 
