@@ -592,7 +592,7 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                                              bool& done) {
     constexpr int st = SM ? NE3_LD : 1;
     uint32_t key[16];
-    int inst[TM], roles[TM];
+    int inst[TM], roles[TM], cv[TM], dv[TM];  // cv / dv: each tet's two link vertices (c, d)
     int a = 0, b = 0;
     // all index loads first, then all element loads: two round trips
     // (slots j >= t repeat the last incidence and are masked below)
@@ -653,8 +653,10 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
         const int e5 = (int)((tw >> (16 * (ti & 3))) & 0x7fffull);
         roles[j] = lc | (ld << 2) | (e5 << 4);
         const bool live = j < t;
-        key[2 * j] = live ? (((uint32_t)sel4p(g01, g23, lc) << 5) | (uint32_t)(2 * j)) : 0xffffffffu;
-        key[2 * j + 1] = live ? (((uint32_t)sel4p(g01, g23, ld) << 5) | (uint32_t)(2 * j + 1)) : 0xffffffffu;
+        cv[j] = sel4p(g01, g23, lc);
+        dv[j] = sel4p(g01, g23, ld);
+        key[2 * j] = live ? (((uint32_t)cv[j] << 5) | (uint32_t)(2 * j)) : 0xffffffffu;
+        key[2 * j + 1] = live ? (((uint32_t)dv[j] << 5) | (uint32_t)(2 * j + 1)) : 0xffffffffu;
     }
 #pragma unroll
     for (int x = 2 * TM; x < 14; ++x) key[x] = 0xffffffffu;  // (unused slots when TM < 7)
@@ -742,12 +744,8 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                 if (j < t) {
                     const int e = inst[j] >> 3;
                     const int rl = roles[j];
-                    const int lc = rl & 3, ld = (rl >> 2) & 3, e5 = rl >> 4;
-                    int g[4];
-                    load_g<KT>(elems, e, g);
-                    const unsigned long long h01 = ((unsigned long long)(uint32_t)g[1] << 32) | (uint32_t)g[0];
-                    const unsigned long long h23 = ((unsigned long long)(uint32_t)g[3] << 32) | (uint32_t)g[2];
-                    const int c = sel4p(h01, h23, lc), d = sel4p(h01, h23, ld);
+                    const int e5 = rl >> 4;
+                    const int c = cv[j], d = dv[j];  // (kept from the first pass: no second tet load)
                     double e1[3], e2[3], e3[3];
 #pragma unroll
                     for (int cc = 0; cc < 3; ++cc) {
