@@ -379,6 +379,8 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
             own_base = (int)win[4];
             rec += row0;
             inc_ptr += row0;
+            // distributed path: elems2dofs held relative to the rank's first row
+            if constexpr (P::GHOST) gh.col_base = own_base;
         }
     }
     if (n_rows <= 0) {

@@ -167,17 +167,13 @@ __global__ void k_respond(const int2* __restrict__ keys, int64_t n, const int32_
     ids[i] = id;
 }
 
-// elems2dofs of the held triangles in global ids: the owned entries (local
-// ids from the fan pass) shifted by the rank's first row, then the requested
-// entries overwritten by the owners' answers
-__global__ void k_shift(int32_t* __restrict__ e2d, int64_t n, const long long* __restrict__ win) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) e2d[i] += (int)win[4];
-}
+// elems2dofs of the held triangles relative to the rank's first row (the
+// row kernel adds it back): the owned entries are the fan pass's local ids,
+// the requested ones the owners' answers (global ids) shifted down
 __global__ void k_fill(int32_t* __restrict__ e2d, const int32_t* __restrict__ slots, const int32_t* __restrict__ ids,
-                       int64_t n) {
+                       int64_t n, const long long* __restrict__ win) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) e2d[__ldg(slots + i)] = __ldg(ids + i);
+    if (i < n) e2d[__ldg(slots + i)] = __ldg(ids + i) - (int)win[4];
 }
 
 template <class T>
@@ -216,12 +212,25 @@ struct DistPlan {
     efem_plan plan = nullptr;
     efem_csr cap{};  // capacities of the last step's slice
     bool stepped = false;
+    // the step as one CUDA graph (kernels and NCCL calls), captured on the
+    // plan's own stream and replayed with event handshakes; keyed by the slice
+    cudaStream_t gs = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    efem_csr gkey{};
+    unsigned gforms = 0;
+    bool graph_failed = false;
+    int64_t graph_launches = 0;
 
     Plan& p() { return *reinterpret_cast<Plan*>(plan); }
     int owner(int64_t v) const {
         return (int)(std::upper_bound(lo.begin(), lo.end(), v) - lo.begin()) - 1;
     }
     ~DistPlan() {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (ev_in) cudaEventDestroy(ev_in);
+        if (ev_out) cudaEventDestroy(ev_out);
+        if (gs) cudaStreamDestroy(gs);
         if (plan) efem_plan_destroy(plan);
         for (void* q : {(void*)keep, (void*)send_tris, (void*)sendA, (void*)recvA, (void*)held, (void*)gvals,
                         (void*)req_slots, (void*)req_ids, (void*)resp_keys, (void*)resp_ids, (void*)totals,
@@ -476,13 +485,9 @@ efem_status ph_respond(DistPlan& D, cudaStream_t s) {
 
 efem_status ph_numeric(DistPlan& D, unsigned forms, efem_csr* slice, cudaStream_t s) {
     Plan& p = D.p();
-    if (D.n_held > 0) {
-        k_shift<<<grid_for(3 * D.n_held, 256), 256, 0, s>>>(p.e2d, 3 * D.n_held, p.hdr->win);
-        EFEM_LAUNCH_CHECK();
-    }
     const int64_t nr = D.req_off[D.P];
     if (nr > 0) {
-        k_fill<<<grid_for(nr, 256), 256, 0, s>>>(p.e2d, D.req_slots, D.req_ids, nr);
+        k_fill<<<grid_for(nr, 256), 256, 0, s>>>(p.e2d, D.req_slots, D.req_ids, nr, p.hdr->win);
         EFEM_LAUNCH_CHECK();
     }
     D.cap = *slice;
@@ -499,7 +504,7 @@ efem_status ph_numeric(DistPlan& D, unsigned forms, efem_csr* slice, cudaStream_
     w.ghost = true;
     w.gh.vals = D.gvals;
     w.gh.base = (int)D.n_keep;
-    w.gh.col_base = 0;
+    w.gh.col_base = 0;  // (set from the device window in the kernel)
     return launch_rows_any(p, forms, slice, w, s);
 }
 
@@ -784,17 +789,60 @@ efem_status efem_dist_assemble(efem_dist_plan plan, unsigned forms, efem_csr* sl
         return EFEM_EINVAL;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    efem_status st;
-    // A: ghost local matrices to the row owners
-    if ((st = ph_pack(*D, s)) != EFEM_OK) return st;
-    if ((st = nccl_alltoallv(*D, D->sendA, D->send_off, D->recvA, D->recv_off, REC_D * 8, s)) != EFEM_OK) return st;
-    if ((st = ph_symbolic(*D, s)) != EFEM_OK) return st;
-    // totals: {rows, entries} of every rank
-    EFEM_NCCL_TRY(ncclAllGather(D->totals + 2 * D->rank, D->totals, 2, ncclInt64, D->comm->nccl, s));
-    if ((st = ph_respond(*D, s)) != EFEM_OK) return st;
-    // B: column ids answered by their owners
-    if ((st = nccl_alltoallv(*D, D->resp_ids, D->resp_off, D->req_ids, D->req_off, 4, s)) != EFEM_OK) return st;
-    return ph_numeric(*D, forms, slice, s);
+    auto enqueue = [&](cudaStream_t q) -> efem_status {
+        efem_status st;
+        // A: ghost local matrices to the row owners
+        if ((st = ph_pack(*D, q)) != EFEM_OK) return st;
+        if ((st = nccl_alltoallv(*D, D->sendA, D->send_off, D->recvA, D->recv_off, REC_D * 8, q)) != EFEM_OK)
+            return st;
+        if ((st = ph_symbolic(*D, q)) != EFEM_OK) return st;
+        // totals: {rows, entries} of every rank
+        EFEM_NCCL_TRY(ncclAllGather(D->totals + 2 * D->rank, D->totals, 2, ncclInt64, D->comm->nccl, q));
+        if ((st = ph_respond(*D, q)) != EFEM_OK) return st;
+        // B: column ids answered by their owners
+        if ((st = nccl_alltoallv(*D, D->resp_ids, D->resp_off, D->req_ids, D->req_off, 4, q)) != EFEM_OK) return st;
+        return ph_numeric(*D, forms, slice, q);
+    };
+    const bool same = D->graph && D->gforms == forms && !std::memcmp(&D->gkey, slice, sizeof(efem_csr));
+    if (!same && D->graph) {
+        cudaGraphExecDestroy(D->graph);
+        D->graph = nullptr;
+    }
+    if (!D->graph && !D->graph_failed && !debug_sync()) {
+        bool ok = D->gs != nullptr;
+        if (!ok)
+            ok = cudaStreamCreateWithFlags(&D->gs, cudaStreamNonBlocking) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&D->ev_in, cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&D->ev_out, cudaEventDisableTiming) == cudaSuccess;
+        cudaGraph_t g = nullptr;
+        if (ok && cudaStreamBeginCapture(D->gs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            const int64_t l0 = efem_launch_count();
+            const efem_status e = enqueue(D->gs);
+            const cudaError_t ee = cudaStreamEndCapture(D->gs, &g);
+            D->graph_launches = efem_launch_count() - l0;
+            count_launch(-(int)D->graph_launches);  // counted at replay
+            if (e == EFEM_OK && ee == cudaSuccess && cudaGraphInstantiate(&D->graph, g, 0) == cudaSuccess) {
+                D->gkey = *slice;
+                D->gforms = forms;
+            } else {
+                D->graph = nullptr;
+                D->graph_failed = true;  // (enqueue directly from now on)
+            }
+            if (g) cudaGraphDestroy(g);
+        }
+        cudaGetLastError();
+    }
+    if (D->graph) {
+        D->cap = *slice;
+        EFEM_CUDA_TRY(cudaEventRecord(D->ev_in, s));
+        EFEM_CUDA_TRY(cudaStreamWaitEvent(D->gs, D->ev_in, 0));
+        EFEM_CUDA_TRY(cudaGraphLaunch(D->graph, D->gs));
+        count_launch((int)D->graph_launches);
+        EFEM_CUDA_TRY(cudaEventRecord(D->ev_out, D->gs));
+        EFEM_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_out, 0));
+        return EFEM_OK;
+    }
+    return enqueue(s);
 }
 
 efem_status efem_dist_assemble_group(efem_dist_plan* plans, int nranks, unsigned forms, efem_csr* slices,

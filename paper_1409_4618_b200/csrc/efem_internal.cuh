@@ -145,7 +145,8 @@ struct Plan {
 
 // Ghost triangles of a distributed 2D assembly (dist2d.cu, assemble.cu
 // GhostTriPolicy): local triangle index e >= base is a ghost, its row values
-// at vals[(e - base) * 12 + 4 k ..]; columns are elems2dofs + col_base.
+// at vals[(e - base) * 12 + 4 k ..]; columns are elems2dofs + col_base (with
+// a device row window: col_base = the window's global first row).
 struct GhostArgs {
     const double* vals = nullptr;
     int base = 0x7fffffff;
