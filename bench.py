@@ -133,6 +133,26 @@ def dist_env():
 _ORACLE_MESH = {}
 
 
+# FP64 flops of the NE0-3D row kernel per (row, tet) pair of the fast path
+# (k_rows_ne3, assemble.cu: tet edge vectors 9, three area normals 27, det 5,
+# fourth normal 6, seven Gram dot products 35, 1/|det| and the two scales 5,
+# six mass and six curl-curl values 50, the twelve accumulations 12), and the
+# measured B200 FP64 FMA peak (tools/fp64_peak.cu, profiles/r2/fp64_peak.txt).
+NE3_FLOPS_PER_ROW_TET = 149
+FP64_PEAK_TFLOPS = 34.2
+
+
+def fp64_line(cfg, T, num_ms):
+    """The NE0-3D numeric kernel against the FP64 ALU (it is instruction /
+    ALU bound, not HBM bound): flops = 149 per (row, tet) x 6 T pairs."""
+    if not (cfg["dim"] == 3 and cfg["element"] == 1):
+        return None
+    fl = NE3_FLOPS_PER_ROW_TET * 6 * T
+    tf = fl / (num_ms * 1e-3) / 1e12
+    return {"bound": "alu", "kernel": "k_rows_ne3", "flops": fl, "achieved": tf, "peak": FP64_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": tf / FP64_PEAK_TFLOPS, "peak_source": "measured, tools/fp64_peak.cu"}
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -311,6 +331,7 @@ def run_efem(args, cfg):
                      "numeric_kernel": {"kernel": ("k_rows_ne3" if (cfg["dim"] == 3 and cfg["element"] == 1)
                                                    else "k_rows_tri") + " (the numeric call alone)",
                                         "ms": num_ms, "achieved": num_gbs, "frac": num_gbs / peak}},
+        "fp64": fp64_line(cfg, T, num_ms),
         "e2e": {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clk.summary(),
