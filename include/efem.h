@@ -162,11 +162,13 @@ efem_status efem_plan_set_exact(efem_plan plan, int exact);
  * a second call on the same plan only copies the tables out. */
 efem_status efem_enumerate_dofs(efem_plan plan, efem_dofs* out, efem_stream_t stream);
 
-/* Symbolic assembly: DOF enumeration (if not yet done) + CSR sparsity pattern
- * sizes: the structural pattern is the union over elements of
- * dofs(K) x dofs(K) (reading C9).  Synchronising (reads nnz
- * back).  If row_ptr != NULL it receives the n_rows+1 row offsets.  Returns
- * EFEM_EOVERFLOW when nnz >= 2^31. */
+/* Symbolic assembly: DOF enumeration + CSR sparsity pattern sizes, always
+ * recomputed from the mesh arrays (the mesh may have changed since the last
+ * call; 2D: the node-fan pipeline, 3D: the bucket pipeline): the structural
+ * pattern is the union over elements of dofs(K) x dofs(K) (PAPER.md:696,
+ * reading C9).  Synchronising (reads n_rows / nnz back).  If row_ptr != NULL
+ * it receives the n_rows+1 row offsets.  Returns EFEM_EOVERFLOW when
+ * nnz >= 2^31. */
 efem_status efem_assemble_symbolic(efem_plan plan, int64_t* n_rows, int64_t* nnz, int32_t* row_ptr,
                                    efem_stream_t stream);
 
