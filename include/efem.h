@@ -299,6 +299,25 @@ efem_status efem_part_numeric_async(efem_plan plan, unsigned forms, const int32_
  * (device), e.g. for an allgather of the owned entry counts. */
 efem_status efem_part_window(efem_plan plan, int64_t* window_dev, efem_stream_t stream);
 
+/* ---- O(interface) exchange for the owner-computes partition ------------
+ * Instead of all-gathering every node's entity count (O(N) per rank), each
+ * rank scans its owned counts (efem_part_scan over its width), the ranks
+ * all-gather their totals (one int each), efem_part_add_offset turns the
+ * local prefix into global first DOF ids, and every rank answers only the
+ * first ids of its nodes that other ranks' sub-meshes hold (ghost nodes):
+ * efem_index_gather (dst[j] = src[idx[j] + bias]) builds the answers and the
+ * owned part of the sub-mesh's first ids, efem_index_scatter (dst[idx[j]] =
+ * src[j]) places the received ones.  efem_part_globalize_sub then maps
+ * elems2dofs to global ids from those per-SUB-MESH-node first ids (sub_first,
+ * device, n_sub_nodes) and records the window's global first row
+ * (sub_first[l0]; [l0, l1) = the owned sub-mesh nodes). */
+efem_status efem_part_add_offset(int32_t* first, int64_t n, const int32_t* totals, int rank, efem_stream_t stream);
+efem_status efem_index_gather(int32_t* dst, const int32_t* src, const int32_t* idx, int64_t n, int32_t bias,
+                              efem_stream_t stream);
+efem_status efem_index_scatter(int32_t* dst, const int32_t* idx, const int32_t* src, int64_t n, efem_stream_t stream);
+efem_status efem_part_globalize_sub(efem_plan plan, const int32_t* sub_first, int64_t l0, int64_t l1,
+                                    int32_t* e2d_global, efem_stream_t stream);
+
 /* ---- distributed 2D assembly over NCCL (BASELINE north_star) -----------
  * The elements are split into contiguous slabs, one per rank (one process
  * per GPU).  Rank r owns the nodes [lo_r, lo_{r+1}), lo_r = the smallest

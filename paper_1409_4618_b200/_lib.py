@@ -107,6 +107,10 @@ def load():
         "efem_p1_load": (st, [vp, vp, vp, vp]),
         "efem_p1_gradient": (st, [ctypes.POINTER(efem_mesh), vp, vp, vp]),
         "efem_dirichlet": (st, [ctypes.POINTER(efem_csr), vp, vp, vp]),
+        "efem_part_add_offset": (st, [vp, i64, vp, ctypes.c_int, vp]),
+        "efem_index_gather": (st, [vp, vp, vp, i64, ctypes.c_int32, vp]),
+        "efem_index_scatter": (st, [vp, vp, vp, i64, vp]),
+        "efem_part_globalize_sub": (st, [vp, vp, i64, i64, vp, vp]),
         "efem_comm_unique_id": (st, [vp]),
         "efem_comm_init": (st, [ctypes.POINTER(vp), vp, ctypes.c_int, ctypes.c_int]),
         "efem_comm_destroy": (st, [vp]),

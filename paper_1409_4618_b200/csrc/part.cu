@@ -12,6 +12,8 @@
 // entry counts (row offsets): owner computes, no matrix values cross ranks.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "efem_internal.cuh"
 
 namespace efem {
@@ -180,6 +182,45 @@ __global__ void k_empty_window_check(WsHeader* hdr) {  // a zero-capacity slice 
 __global__ void k_part_first_row(const int32_t* __restrict__ global_ent_ptr, int64_t lo, long long* __restrict__ win) {
     if (threadIdx.x || blockIdx.x) return;
     win[4] = global_ent_ptr[lo];
+}
+
+// O(interface) globalisation: global first DOF id per SUB-MESH node
+__global__ void k_node_shift_sub(const int32_t* __restrict__ ent_ptr, const int32_t* __restrict__ sub_first,
+                                 int64_t n_nodes, int32_t* __restrict__ shift) {
+    const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (u < n_nodes) shift[u] = sub_first[u] - ent_ptr[u];
+}
+
+__global__ void k_part_first_row_sub(const int32_t* __restrict__ sub_first, int64_t l0, int64_t l1,
+                                     long long* __restrict__ win) {
+    if (threadIdx.x || blockIdx.x) return;
+    win[4] = l1 > l0 ? sub_first[l0] : 0;
+}
+
+// first ids of the owned nodes: local exclusive prefix + the totals of the
+// ranks before `rank` (totals: device, one int per rank)
+__global__ void k_add_offset(int32_t* __restrict__ first, int64_t n, const int32_t* __restrict__ totals, int rank) {
+    __shared__ int off;
+    if (threadIdx.x == 0) {
+        int o = 0;
+        for (int r = 0; r < rank; ++r) o += totals[r];
+        off = o;
+    }
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        first[i] += off;
+}
+
+__global__ void k_index_gather(int32_t* __restrict__ dst, const int32_t* __restrict__ src,
+                               const int32_t* __restrict__ idx, int64_t n, int32_t bias) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[idx[i] + bias];
+}
+
+__global__ void k_index_scatter(int32_t* __restrict__ dst, const int32_t* __restrict__ idx,
+                                const int32_t* __restrict__ src, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[idx[i]] = src[i];
 }
 
 }  // namespace
@@ -526,6 +567,76 @@ efem_status efem_part_window(efem_plan plan, int64_t* window_dev, efem_stream_t 
         return EFEM_EINVAL;
     }
     EFEM_CUDA_TRY(cudaMemcpyAsync(window_dev, p->hdr->win, 5 * 8, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return EFEM_OK;
+}
+
+// ---- O(interface) globalisation of the owner-computes partition ------------------------
+efem_status efem_part_add_offset(int32_t* first, int64_t n, const int32_t* totals, int rank, efem_stream_t stream) {
+    if ((n > 0 && !first) || !totals || rank < 0) {
+        set_error("efem_part_add_offset: NULL array or negative rank");
+        return EFEM_EINVAL;
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(grid_for(std::max<int64_t>(n, 1), 256), 1024);
+    k_add_offset<<<grid, 256, 0, (cudaStream_t)stream>>>(first, n, totals, rank);
+    EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
+
+efem_status efem_index_gather(int32_t* dst, const int32_t* src, const int32_t* idx, int64_t n, int32_t bias,
+                              efem_stream_t stream) {
+    if (n < 0 || (n > 0 && (!dst || !src || !idx))) {
+        set_error("efem_index_gather: NULL array");
+        return EFEM_EINVAL;
+    }
+    if (n == 0) return EFEM_OK;
+    k_index_gather<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(dst, src, idx, n, bias);
+    EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
+
+efem_status efem_index_scatter(int32_t* dst, const int32_t* idx, const int32_t* src, int64_t n, efem_stream_t stream) {
+    if (n < 0 || (n > 0 && (!dst || !src || !idx))) {
+        set_error("efem_index_scatter: NULL array");
+        return EFEM_EINVAL;
+    }
+    if (n == 0) return EFEM_OK;
+    k_index_scatter<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(dst, idx, src, n);
+    EFEM_LAUNCH_CHECK();
+    return EFEM_OK;
+}
+
+efem_status efem_part_globalize_sub(efem_plan plan, const int32_t* sub_first, int64_t l0, int64_t l1,
+                                    int32_t* e2d_global, efem_stream_t stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !(p->symbolic || (p->part_bound && p->async_pending)) || !sub_first || !e2d_global) {
+        set_error("efem_part_globalize_sub: needs a plan after efem_assemble_symbolic (or "
+                  "efem_part_enumerate_async) and non-NULL arrays");
+        return EFEM_ESTATE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!p->async_pending) {
+        const efem_status e = ensure_enumerated(*p, s);
+        if (e != EFEM_OK) return e;
+    }
+    if (p->n_elems > 0) {
+        int32_t* shift = p->ent_cnt;  // (scratch between enumerations)
+        k_node_shift_sub<<<grid_for(p->n_nodes, 256), 256, 0, s>>>(p->ent_ptr, sub_first, p->n_nodes, shift);
+        EFEM_LAUNCH_CHECK();
+        const unsigned grid = grid_for(p->n_elems, 256);
+        if (p->dim == 2 && p->element == EFEM_RT0)
+            k_globalize<Kind<2, EFEM_RT0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, shift, e2d_global);
+        else if (p->dim == 2)
+            k_globalize<Kind<2, EFEM_NED0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, shift, e2d_global);
+        else if (p->element == EFEM_RT0)
+            k_globalize<Kind<3, EFEM_RT0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, shift, e2d_global);
+        else
+            k_globalize<Kind<3, EFEM_NED0>><<<grid, 256, 0, s>>>(p->elems, p->n_elems, p->e2d, shift, e2d_global);
+        EFEM_LAUNCH_CHECK();
+    }
+    if (p->part_bound) {
+        k_part_first_row_sub<<<1, 32, 0, s>>>(sub_first, l0, l1, p->hdr->win);
+        EFEM_LAUNCH_CHECK();
+    }
     return EFEM_OK;
 }
 

@@ -56,7 +56,6 @@ class PartAssembler:
         # need) owns nothing: no sub-mesh, no plan, an empty slice
         self.empty = self.hi <= self.lo
         self.scan_ws = torch.empty(256, dtype=torch.uint8, device=self.device)
-        self.global_ent_ptr = torch.empty(self.n_global_nodes + 1, dtype=torch.int32, device=self.device)
         if self.empty:
             self.owned_cnt = torch.zeros(1, dtype=torch.int32, device=self.device)
             self.info = (ctypes.c_int64 * 4)()
@@ -87,9 +86,8 @@ class PartAssembler:
         self.info = (ctypes.c_int64 * 4)()
         self.e2d_global = torch.empty(max(self.sub_elems.shape[0] * self.asm.m, 1), dtype=torch.int32,
                                       device=self.device)
-        self.global_ent_ptr = torch.empty(self.n_global_nodes + 1, dtype=torch.int32, device=self.device)
         scan_bytes = ctypes.c_size_t()
-        _lib.check("efem_part_scan", L.efem_part_scan(None, self.n_global_nodes, None, None,
+        _lib.check("efem_part_scan", L.efem_part_scan(None, max(self.hi - self.lo, 1), None, None,
                                                       ctypes.byref(scan_bytes), None))
         self.scan_ws = torch.empty(max(scan_bytes.value, 256), dtype=torch.uint8, device=self.device)
         self.first_row = 0
@@ -117,22 +115,6 @@ class PartAssembler:
                                                               self.hi, _ptr(self.owned_cnt), self.info,
                                                               _stream(stream)))
         return self.owned_cnt[: self.hi - self.lo]
-
-    def globalize(self, global_cnt: torch.Tensor, stream=None):
-        """global_cnt: per-node entity counts of ALL nodes (device int32)."""
-        if self.empty:
-            return 0
-        L = _lib.load()
-        b = ctypes.c_size_t(self.scan_ws.numel())
-        with torch.cuda.device(self.device):
-            _lib.check("efem_part_scan", L.efem_part_scan(_ptr(global_cnt), self.n_global_nodes,
-                                                          _ptr(self.global_ent_ptr), _ptr(self.scan_ws),
-                                                          ctypes.byref(b), _stream(stream)))
-            _lib.check("efem_part_globalize", L.efem_part_globalize(self.asm._plan, _ptr(self.sub2global),
-                                                                    _ptr(self.global_ent_ptr),
-                                                                    _ptr(self.e2d_global), _stream(stream)))
-        self.first_row = int(self.global_ent_ptr[self.lo].item())
-        return self.first_row
 
     def alloc_slice(self) -> CSR:
         dev = self.device
@@ -168,7 +150,6 @@ class PartAssembler:
                                                               self.hi, _stream(stream)))
         self.width = int(width)
         self.owned_pad = torch.zeros(max(self.width, 1), dtype=torch.int32, device=self.device)
-        self.global_buf = torch.zeros(max(self.width, 1) * world, dtype=torch.int32, device=self.device)
         self.window = torch.zeros(5, dtype=torch.int64, device=self.device)
         self.bound = True
 
@@ -180,19 +161,6 @@ class PartAssembler:
             _lib.check("efem_part_enumerate_async",
                        L.efem_part_enumerate_async(self.asm._plan, _ptr(self.owned_pad), _stream(stream)))
         return self.owned_pad
-
-    def globalize_async(self, global_cnt: torch.Tensor, stream=None):
-        if self.empty:
-            return
-        L = _lib.load()
-        b = ctypes.c_size_t(self.scan_ws.numel())
-        with torch.cuda.device(self.device):
-            _lib.check("efem_part_scan", L.efem_part_scan(_ptr(global_cnt), self.n_global_nodes,
-                                                          _ptr(self.global_ent_ptr), _ptr(self.scan_ws),
-                                                          ctypes.byref(b), _stream(stream)))
-            _lib.check("efem_part_globalize", L.efem_part_globalize(self.asm._plan, _ptr(self.sub2global),
-                                                                    _ptr(self.global_ent_ptr),
-                                                                    _ptr(self.e2d_global), _stream(stream)))
 
     def numeric_async(self, out: CSR, forms: int = ALL, stream=None):
         """out: a slice with capacities (e.g. from alloc_slice after one
@@ -211,25 +179,134 @@ class PartAssembler:
         return out
 
 
+# ---- O(interface) exchange (efem_part_add_offset / efem_index_* /
+# efem_part_globalize_sub): the ranks all-gather one total each and answer
+# only the first DOF ids of the ghost nodes other ranks' sub-meshes hold.
+def exchange_plan_host(s2g, lo: int, hi: int, ranges):
+    """Host arrays: (l0, l1, owned_idx, ghost_pos, recv_splits, requests) of
+    a rank owning [lo, hi) whose sub-mesh holds the ascending global node ids
+    s2g: the owned sub-mesh nodes [l0, l1) and their index into the owned
+    range, the ghost positions grouped by owner rank, how many first ids it
+    receives from each rank, and the global ids it asks each rank for."""
+    s2g = np.asarray(s2g, np.int64)
+    P = len(ranges)
+    owned = (s2g >= lo) & (s2g < hi)
+    idx = np.nonzero(owned)[0]
+    l0 = int(idx[0]) if idx.size else 0
+    l1 = l0 + int(idx.size)
+    his = np.array([h for _, h in ranges], np.int64)
+    ghost = np.nonzero(~owned)[0]
+    own_of = np.searchsorted(his, s2g[ghost], side="right")
+    order = np.argsort(own_of, kind="stable")
+    ghost, own_of = ghost[order], own_of[order]
+    recv_splits = [int((own_of == r).sum()) for r in range(P)]
+    requests = [s2g[ghost[own_of == r]] for r in range(P)]
+    return l0, l1, (s2g[l0:l1] - lo).astype(np.int32), ghost.astype(np.int32), recv_splits, requests
+
+
+def answer_plan_host(requests_to_me, lo: int):
+    """(send_splits, answer_idx): what this rank answers each rank, as indices
+    into its owned range."""
+    send_splits = [len(q) for q in requests_to_me]
+    flat = np.concatenate([np.asarray(q, np.int64) for q in requests_to_me]) if requests_to_me else np.zeros(0)
+    return send_splits, (flat - lo).astype(np.int32)
+
+
+def _exchange_plan(part: "PartAssembler", ranges):
+    """Host, once per partition: the owned sub-mesh nodes [l0, l1) and their
+    index into the owned range, the ghost sub-mesh nodes grouped by owner
+    rank (their positions and global ids: this rank's requests)."""
+    P = len(ranges)
+    part.P = P
+    if part.empty:
+        part.l0 = part.l1 = 0
+        part.requests = [np.zeros(0, np.int64) for _ in range(P)]
+        part.recv_splits = [0] * P
+        part.recv_buf = torch.zeros(1, dtype=torch.int32, device=part.device)
+        return
+    s2g = part.sub2global.cpu().numpy().astype(np.int64)
+    dev = part.device
+    part.l0, part.l1, own_idx, ghost, part.recv_splits, part.requests = exchange_plan_host(s2g, part.lo, part.hi,
+                                                                                         ranges)
+    part.owned_idx = torch.from_numpy(own_idx).to(dev)
+    part.ghost_pos = torch.from_numpy(ghost).to(dev)
+    part.sub_first = torch.zeros(max(s2g.size, 1), dtype=torch.int32, device=dev)
+    part.recv_buf = torch.zeros(max(ghost.size, 1), dtype=torch.int32, device=dev)
+
+
+def _answer_plan(part: "PartAssembler", requests_to_me):
+    """requests_to_me[s]: the global ids rank s asks this rank for."""
+    part.send_splits, idx = answer_plan_host(requests_to_me, part.lo)
+    part.answer_idx = torch.from_numpy(idx).to(part.device)
+    part.send_buf = torch.zeros(max(idx.size, 1), dtype=torch.int32, device=part.device)
+    part.first_buf = torch.zeros(max(part.hi - part.lo, 0) + 1, dtype=torch.int32, device=part.device)
+
+
+def setup_exchange(part: "PartAssembler", ranges, group=None):
+    """The request lists to their owners (torch.distributed all_gather_object,
+    setup only)."""
+    import torch.distributed as dist
+
+    _exchange_plan(part, ranges)
+    everyone = [None] * len(ranges)
+    dist.all_gather_object(everyone, [q.tolist() for q in part.requests], group=group)
+    me = dist.get_rank(group)
+    _answer_plan(part, [everyone[s][me] for s in range(len(ranges))])
+
+
+def _part_local_prefix(part: "PartAssembler", owned: torch.Tensor, stream=None):
+    """Exclusive scan of the owned counts into first_buf; returns the device
+    view of this rank's total (first_buf[width])."""
+    L = _lib.load()
+    w = part.hi - part.lo
+    if w > 0:
+        b = ctypes.c_size_t(part.scan_ws.numel())
+        _lib.check("efem_part_scan", L.efem_part_scan(_ptr(owned), w, _ptr(part.first_buf), _ptr(part.scan_ws),
+                                                      ctypes.byref(b), _stream(stream)))
+    else:
+        part.first_buf.zero_()
+    return part.first_buf[w:w + 1]
+
+
+def _part_first_ids(part: "PartAssembler", totals: torch.Tensor, rank: int, stream=None):
+    """first_buf += the totals of the ranks before; the answers to send."""
+    L = _lib.load()
+    _lib.check("efem_part_add_offset", L.efem_part_add_offset(_ptr(part.first_buf), part.first_buf.numel(),
+                                                              _ptr(totals), rank, _stream(stream)))
+    n = part.answer_idx.numel()
+    _lib.check("efem_index_gather", L.efem_index_gather(_ptr(part.send_buf), _ptr(part.first_buf),
+                                                        _ptr(part.answer_idx), n, 0, _stream(stream)))
+    return part.send_buf[:n]
+
+
+def _part_place(part: "PartAssembler", recv: torch.Tensor, stream=None):
+    """sub_first: owned nodes from first_buf, ghosts from the answers; then
+    elems2dofs in global ids and the window's global first row."""
+    if part.empty:
+        return
+    L = _lib.load()
+    n_own = part.l1 - part.l0
+    sub_view = part.sub_first[part.l0:]
+    _lib.check("efem_index_gather", L.efem_index_gather(_ptr(sub_view), _ptr(part.first_buf), _ptr(part.owned_idx),
+                                                        n_own, 0, _stream(stream)))
+    _lib.check("efem_index_scatter", L.efem_index_scatter(_ptr(part.sub_first), _ptr(part.ghost_pos), _ptr(recv),
+                                                          part.ghost_pos.numel(), _stream(stream)))
+    _lib.check("efem_part_globalize_sub", L.efem_part_globalize_sub(part.asm._plan, _ptr(part.sub_first), part.l0,
+                                                                    part.l1, _ptr(part.e2d_global), _stream(stream)))
+
+
+def exchange_bytes(part: "PartAssembler") -> int:
+    """Bytes this rank sends per step: its total (all-gather), its answers,
+    its entry count (all-gather)."""
+    return 4 + 4 * int(part.answer_idx.numel()) + 8
+
+
 def _comm_device(t: torch.Tensor, group=None):
     """NCCL gathers device tensors directly; gloo (CPU tests, or several
     ranks sharing one GPU) goes through host copies."""
     import torch.distributed as dist
 
     return t.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
-
-
-def allgather_counts(owned: torch.Tensor, ranges, group=None) -> torch.Tensor:
-    """Collective 1: every rank's per-node counts -> counts of all nodes."""
-    import torch.distributed as dist
-
-    dev = _comm_device(owned, group)
-    width = max(hi - lo for lo, hi in ranges)
-    buf = torch.zeros(width, dtype=torch.int32, device=dev)
-    buf[: owned.numel()] = owned.to(dev)
-    parts = [torch.empty_like(buf) for _ in ranges]
-    dist.all_gather(parts, buf, group=group)
-    return torch.cat([p[: hi - lo] for p, (lo, hi) in zip(parts, ranges)]).to(owned.device)
 
 
 def allgather_nnz(nnz: int, device, group=None):
@@ -245,20 +322,42 @@ def allgather_nnz(nnz: int, device, group=None):
 
 
 def assemble_rank(part: PartAssembler, ranges, out: CSR | None = None, group=None, stream=None):
-    """One rank's full step: local symbolic, the two collectives, numeric.
-    Returns (slice CSR, first global row, first global CSR entry)."""
+    """One rank's full step: local symbolic, the O(interface) exchange (the
+    ranks' totals, the ghost nodes' first ids), numeric.  Returns (slice
+    CSR, first global row, first global CSR entry)."""
     import torch.distributed as dist
 
+    if not hasattr(part, "answer_idx"):
+        setup_exchange(part, ranges, group=group)
+    rank = dist.get_rank(group)
     owned = part.symbolic(stream=stream)
-    global_cnt = allgather_counts(owned, ranges, group=group)
-    part.globalize(global_cnt, stream=stream)
+    total = _part_local_prefix(part, owned, stream=stream)
+    totals = _allgather_dev(total.contiguous(), group).to(part.device)
+    send = _part_first_ids(part, totals, rank, stream=stream)
+    recv = _alltoall_dev(send, part.send_splits, part.recv_buf, part.recv_splits, group)
+    _part_place(part, recv, stream=stream)
+    part.first_row = int(part.sub_first[part.l0].item()) if part.l1 > part.l0 else 0
     nnzs = allgather_nnz(part.owned_nnz, owned.device, group=group)
     offs, _ = offsets_from_counts(nnzs)
     if out is None or out.nnz != part.owned_nnz or out.n_rows != part.owned_rows:
         out = part.alloc_slice()
     part.numeric(out, stream=stream)
     part.check(stream=stream)
-    return out, part.first_row, offs[dist.get_rank(group)]
+    return out, part.first_row, offs[rank]
+
+
+def _alltoall_dev(send: torch.Tensor, send_splits, recv: torch.Tensor, recv_splits, group=None):
+    """all_to_all of the ghost answers (NCCL on the device, gloo via host)."""
+    import torch.distributed as dist
+
+    n_recv = sum(recv_splits)
+    if dist.get_backend(group) == "nccl":
+        dist.all_to_all_single(recv[:n_recv], send[:sum(send_splits)], recv_splits, send_splits, group=group)
+        return recv[:n_recv]
+    r = torch.zeros(n_recv, dtype=recv.dtype)
+    dist.all_to_all_single(r, send[:sum(send_splits)].cpu(), recv_splits, send_splits, group=group)
+    recv[:n_recv].copy_(r.to(recv.device))
+    return recv[:n_recv]
 
 
 class AsyncStep:
@@ -274,7 +373,11 @@ class AsyncStep:
         self.nccl = dist.get_backend(group) == "nccl"
         if not getattr(part, "bound", False):
             part.bind(max(hi - lo for lo, hi in ranges), self.world, stream=stream)
+        if not hasattr(part, "answer_idx"):
+            setup_exchange(part, ranges, group=group)
+        self.rank = dist.get_rank(group)
         self.L = _lib.load()
+        self.stream = stream
         self.s = _stream(stream)
         # the collectives are issued on torch's current stream: make it the
         # stream the library calls are enqueued on, so they stay ordered
@@ -282,8 +385,6 @@ class AsyncStep:
         self.empty = part.empty
         self.plan = None if part.empty else part.asm._plan
         self.p_owned = _ptr(part.owned_pad)
-        self.p_gbuf = _ptr(part.global_buf)
-        self.p_gptr = _ptr(part.global_ent_ptr)
         self.p_sws = _ptr(part.scan_ws)
         self.p_s2g = _ptr(part.sub2global)
         self.p_e2dg = _ptr(part.e2d_global)
@@ -307,21 +408,14 @@ class AsyncStep:
         L, ck = self.L, _lib.check
         if not self.empty:
             ck("efem_part_enumerate_async", L.efem_part_enumerate_async(self.plan, self.p_owned, self.s))
-        if self.nccl:
-            dist.all_gather_into_tensor(self.part.global_buf, self.part.owned_pad, group=self.group)
-            gptr = self.p_gbuf
-        else:  # gloo: host copies
-            o = self.part.owned_pad
-            parts = [torch.empty_like(o, device="cpu") for _ in range(self.world)]
-            dist.all_gather(parts, o.cpu(), group=self.group)
-            self._g = torch.cat(parts).to(o.device)
-            gptr = _ptr(self._g)
+        part = self.part
+        # O(interface): one total per rank, the ghost nodes' first ids
+        total = _part_local_prefix(part, part.owned_pad, stream=self.stream)
+        totals = _allgather_dev(total.contiguous(), self.group).to(part.device)
+        send = _part_first_ids(part, totals, self.rank, stream=self.stream)
+        recv = _alltoall_dev(send, part.send_splits, part.recv_buf, part.recv_splits, self.group)
         if not self.empty:
-            self.sws_bytes.value = self.part.scan_ws.numel()
-            ck("efem_part_scan", L.efem_part_scan(gptr, self.n_global, self.p_gptr, self.p_sws,
-                                                  ctypes.byref(self.sws_bytes), self.s))
-            ck("efem_part_globalize", L.efem_part_globalize(self.plan, self.p_s2g, self.p_gptr, self.p_e2dg,
-                                                            self.s))
+            _part_place(part, recv, stream=self.stream)
             ck("efem_part_numeric_async", L.efem_part_numeric_async(self.plan, self.forms, self.p_e2dg,
                                                                     self.csr_ref, self.s))
             ck("efem_part_window", L.efem_part_window(self.plan, self.p_win, self.s))
@@ -345,31 +439,11 @@ class AsyncStep:
 
 
 def assemble_rank_async(part: PartAssembler, ranges, out: CSR, group=None, stream=None, check=True):
-    """One rank's step with every size on the device: enumeration + owned
-    counts, the counts all_gather, scan + globalisation, owned-row numeric,
-    the entry-count all_gather; one host round trip (the flags check) at
-    the end.  `out` holds capacities (from a synchronous assemble_rank).
-    Returns (out, window (device int64[5]: first local row, rows, local CSR
-    offset, entries, global first row), every rank's entry count (device))."""
-    import torch.distributed as dist
-
-    world = dist.get_world_size(group)
-    if not getattr(part, "bound", False):
-        part.bind(max(hi - lo for lo, hi in ranges), world, stream=stream)
-    owned = part.enumerate_async(stream=stream)
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(part.global_buf, owned, group=group)
-        gcnt = part.global_buf
-    else:  # gloo: host copies
-        parts = [torch.empty_like(owned, device="cpu") for _ in range(world)]
-        dist.all_gather(parts, owned.cpu(), group=group)
-        gcnt = torch.cat(parts).to(part.device)
-    part.globalize_async(gcnt, stream=stream)
-    part.numeric_async(out, stream=stream)
-    nnz_all = _allgather_dev(part.window[3:4].contiguous(), group)
-    if check:
-        part.check(stream=stream)
-    return out, part.window, nnz_all
+    """One rank's step with every size on the device (dist.AsyncStep once):
+    enumeration + owned counts, the O(interface) exchange, globalisation,
+    owned-row numeric, the entry-count all_gather; one host round trip (the
+    flags check) at the end.  Returns (out, window, every rank's entries)."""
+    return AsyncStep(part, ranges, out, group=group, stream=stream)(check=check)
 
 
 def _allgather_dev(t: torch.Tensor, group=None) -> torch.Tensor:

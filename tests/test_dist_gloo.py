@@ -1,8 +1,9 @@
-"""The multi-rank host logic over a real torch.distributed (gloo) group of
-2 processes on CPU: node ranges, the two all_gathers and the offsets they
-produce, checked against the oracle's global numbering.  The per-node entity
-counts each rank contributes (on GPU: efem_part_counts) are taken from the
-oracle's dofs2nodes here, so this test needs no GPU."""
+"""The multi-rank host logic of the owner-computes partition over a real
+torch.distributed (gloo) group of 2 processes on CPU: node ranges, the
+O(interface) exchange (one total per rank, the ghost nodes' first DOF ids)
+and the entry offsets, checked against the oracle's global numbering.  The
+per-node entity counts each rank contributes (on GPU: efem_part_counts) are
+taken from the oracle's dofs2nodes here, so this test needs no GPU."""
 import os
 import socket
 
@@ -23,11 +24,28 @@ def _free_port():
     return port
 
 
+def _two_hop(elems, lo, hi):
+    """Ascending global ids of the two-hop sub-mesh of the node range [lo, hi)
+    (elements touching the nodes of the elements touching the range), as
+    efem_partition builds it -- here in numpy, for the host-logic test."""
+    touch = ((elems >= lo) & (elems < hi)).any(1)
+    nodes1 = np.unique(elems[touch])
+    mark = np.zeros(elems.max() + 1, bool)
+    mark[nodes1] = True
+    touch2 = mark[elems].any(1)
+    return np.unique(elems[touch2])
+
+
 def _worker(rank, world, port, dim, element, q):
+    """The owner-computes partition's O(interface) exchange over gloo: each
+    rank all-gathers one total, requests the first DOF ids of its ghost
+    nodes from their owners (setup: all_gather_object of the request lists;
+    step: all_to_all_single of the answers) and must obtain, for every node
+    of its sub-mesh, the oracle's global first DOF id."""
     import torch.distributed as dist
 
-    from paper_1409_4618_b200.dist import (_allgather_dev, allgather_counts, allgather_nnz, node_ranges,
-                                           offsets_from_counts)
+    from paper_1409_4618_b200.dist import (_allgather_dev, allgather_nnz, answer_plan_host, exchange_plan_host,
+                                           node_ranges, offsets_from_counts)
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -40,30 +58,32 @@ def _worker(rank, world, port, dim, element, q):
         ranges = node_ranges(N, world)
         lo, hi = ranges[rank]
         mins = A.dofs2nodes[:, 0]
-        owned = torch.from_numpy(np.bincount(mins[(mins >= lo) & (mins < hi)] - lo, minlength=hi - lo)
-                                 .astype(np.int32))
-        global_cnt = allgather_counts(owned, ranges)
-        ent_ptr = np.concatenate([[0], np.cumsum(global_cnt.numpy())])
-        # global DOF id of node g's first entity == rank of its first entity in the oracle numbering
-        first = np.searchsorted(mins, np.arange(N))
-        ok1 = bool(np.array_equal(ent_ptr[:N], first)) and int(ent_ptr[N]) == A.n_dofs
+        first_true = np.searchsorted(mins, np.arange(N + 1))  # global first DOF id of every node
+        # this rank's owned counts (on GPU: efem_part_counts) from the oracle's numbering
+        owned = np.bincount(mins[(mins >= lo) & (mins < hi)] - lo, minlength=hi - lo).astype(np.int64)
+        local = np.concatenate([[0], np.cumsum(owned)])
+        totals = _allgather_dev(torch.tensor([local[-1]], dtype=torch.int64))
+        first = local + int(totals[:rank].sum())  # efem_part_add_offset
+        s2g = _two_hop(elems, lo, hi)
+        l0, l1, own_idx, ghost_pos, recv_splits, requests = exchange_plan_host(s2g, lo, hi, ranges)
+        everyone = [None] * world
+        dist.all_gather_object(everyone, [r.tolist() for r in requests])
+        send_splits, answer_idx = answer_plan_host([everyone[s][rank] for s in range(world)], lo)
+        send = torch.from_numpy(first[answer_idx].astype(np.int32))
+        recv = torch.zeros(sum(recv_splits), dtype=torch.int32)
+        dist.all_to_all_single(recv, send, recv_splits, send_splits)
+        sub_first = np.zeros(s2g.size, np.int64)
+        sub_first[l0:l1] = first[own_idx]
+        sub_first[ghost_pos] = recv.numpy()
+        ok1 = bool(np.array_equal(sub_first, first_true[s2g]))
+        # the interface bound: answers are only ghost nodes, a small part of the sub-mesh
+        ok1 = ok1 and len(answer_idx) <= s2g.size
         rows = np.nonzero((mins >= lo) & (mins < hi))[0]
         my_nnz = int(A.row_ptr[rows[-1] + 1] - A.row_ptr[rows[0]]) if len(rows) else 0
         nnzs = allgather_nnz(my_nnz, torch.device("cpu"))
         offs, total = offsets_from_counts(nnzs)
         ok2 = total == A.col_idx.shape[0] and (len(rows) == 0 or offs[rank] == A.row_ptr[rows[0]])
-        # the asynchronous step's exchange (dist.assemble_rank_async): W-wide
-        # buffers gathered in rank order ARE the global counts (+ zero tail)
-        W = max(h - l for l, h in ranges)
-        pad = torch.zeros(W, dtype=torch.int32)
-        pad[: hi - lo] = owned
-        parts = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(parts, pad)
-        flat = torch.cat(parts).numpy()
-        ok3 = bool(np.array_equal(flat[:N], global_cnt.numpy())) and not flat[N:].any()
-        nz = _allgather_dev(torch.tensor([my_nnz], dtype=torch.int64))
-        ok3 = ok3 and [int(v) for v in nz] == nnzs
-        q.put((rank, ok1, ok2 and ok3))
+        q.put((rank, ok1, ok2))
     finally:
         dist.destroy_process_group()
 

@@ -18,15 +18,46 @@ KINDS = [(2, RT0), (2, NED0), (3, RT0), (3, NED0)]
 KIND_IDS = ["rt0_2d", "ne0_2d", "rt0_3d", "ne0_3d"]
 
 
-def _emulate(coords, elems, element, P):
+def _exchange(parts, owned):
+    """The O(interface) exchange of the owner-computes partition for P ranks
+    in this process: every rank's total (== all_gather), the first-id answers
+    (== all_to_all_single), placed into each rank's sub-mesh first ids."""
+    from paper_1409_4618_b200 import dist
+
+    P = len(parts)
+    totals = torch.cat([dist._part_local_prefix(p, o) for p, o in zip(parts, owned)])
+    sends = [dist._part_first_ids(p, totals, r) for r, p in enumerate(parts)]
+    for r, p in enumerate(parts):
+        segs = []
+        for o, q in enumerate(parts):
+            off = sum(q.send_splits[:r])
+            segs.append(sends[o][off:off + q.send_splits[r]])
+        recv = torch.cat(segs) if segs else torch.zeros(0, dtype=torch.int32, device="cuda")
+        assert recv.numel() == sum(p.recv_splits)
+        dist._part_place(p, recv)
+        p.first_row = int(p.sub_first[p.l0].item()) if (not p.empty and p.l1 > p.l0) else 0
+    # per rank and step: one total, its answers, its entry count
+    return [dist.exchange_bytes(p) for p in parts]
+
+
+def _parts(coords, elems, element, P):
     from paper_1409_4618_b200 import dist
 
     ranges = dist.node_ranges(coords.shape[0], P)
     parts = [dist.PartAssembler(coords, elems, element, lo, hi) for lo, hi in ranges]
-    owned = [p.symbolic() for p in parts]
-    global_cnt = torch.cat(owned)  # == all_gather of the owned counts
     for p in parts:
-        p.globalize(global_cnt)
+        dist._exchange_plan(p, ranges)
+    for r, p in enumerate(parts):
+        dist._answer_plan(p, [parts[s].requests[r] for s in range(P)])
+    return ranges, parts
+
+
+def _emulate(coords, elems, element, P):
+    from paper_1409_4618_b200 import dist
+
+    ranges, parts = _parts(coords, elems, element, P)
+    owned = [p.symbolic() for p in parts]
+    _exchange(parts, owned)
     offs, total = dist.offsets_from_counts([p.owned_nnz for p in parts])
     slices = []
     for p in parts:
@@ -92,23 +123,33 @@ def test_partitioned_config5_against_oracle_rows():
 
 
 def _emulate_async(coords, elems, element, P, caps):
-    """The asynchronous rank step (dist.assemble_rank_async) for P ranks in
-    this process: every rank's enumeration first, then the gathered counts
-    (== all_gather_into_tensor of the W-wide buffers), then each rank's
-    globalisation and numeric into `caps` (slices with capacities)."""
-    from paper_1409_4618_b200 import dist
-
-    ranges = dist.node_ranges(coords.shape[0], P)
+    """The asynchronous rank step for P ranks in this process: every rank's
+    enumeration first, then the exchange, then each rank's numeric into
+    `caps` (slices with capacities)."""
+    ranges, parts = _parts(coords, elems, element, P)
     W = max(hi - lo for lo, hi in ranges)
-    parts = [dist.PartAssembler(coords, elems, element, lo, hi) for lo, hi in ranges]
     for p in parts:
         p.bind(W, P)
-    owned = [p.enumerate_async().clone() for p in parts]
-    gathered = torch.cat(owned)
+    owned = [p.enumerate_async() for p in parts]
+    _exchange(parts, owned)
     for p, s in zip(parts, caps):
-        p.globalize_async(gathered)
         p.numeric_async(s)
     return parts
+
+
+def test_exchange_is_interface_sized():
+    """The owner-computes exchange no longer scales with N: config 5 split 8
+    ways sends at most ~one node row of first ids per interface."""
+    from paper_1409_4618_b200 import api, dist
+    from workloads import CONFIGS
+
+    C = CONFIGS[5]
+    coords, elems = api.build_mesh(2, C["n"], C["alpha"], C["seed"])
+    ranges, parts = _parts(coords, elems, C["element"], 8)
+    owned = [p.symbolic() for p in parts]
+    sent = _exchange(parts, owned)
+    assert max(sent) <= 4 * (4 * (C["n"] + 1) + 8) + 12, sent  # (two ghost node rows on each side)
+    assert max(sent) < 1 << 20
 
 
 @pytest.mark.parametrize("dim,element", KINDS, ids=KIND_IDS)

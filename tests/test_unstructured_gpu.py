@@ -158,20 +158,16 @@ def test_delaunay_partitioned_async(dim, element, P):
     pts, el = delaunay_mesh(dim, 1500 if dim == 2 else 300, 7)
     coords, elems = torch.from_numpy(pts).cuda(), torch.from_numpy(el).cuda()
     one = api.Assembler(coords, elems, element).assemble()
-    ranges = dist.node_ranges(coords.shape[0], P)
+    from test_dist_gpu import _exchange, _parts
+
+    ranges, parts = _parts(coords, elems, element, P)
     W = max(hi - lo for lo, hi in ranges)
-    parts = [dist.PartAssembler(coords, elems, element, lo, hi) for lo, hi in ranges]
-    for p in parts:
-        p.symbolic()
-    gcnt = torch.cat([p.symbolic() for p in parts])
-    for p in parts:
-        p.globalize(gcnt)
+    _exchange(parts, [p.symbolic() for p in parts])
     caps = [p.alloc_slice() for p in parts]
     for p in parts:
         p.bind(W, P)
-    owned = torch.cat([p.enumerate_async().clone() for p in parts])
+    _exchange(parts, [p.enumerate_async() for p in parts])
     for p, c in zip(parts, caps):
-        p.globalize_async(owned)
         p.numeric_async(c)
         p.check()
     offs, total = dist.offsets_from_counts([int(p.window[3].item()) for p in parts])
