@@ -204,18 +204,17 @@ __device__ __forceinline__ void sort_keys(unsigned (&key)[2 * FAN_REG]) {
 
 // walk the sorted keys: row(first, last, t) per run of equal b, the run's
 // instances e << 3 | k ordered by element
+// (sev: the fan's element ids in shared memory, sev[j * FAN_TPB]: one load
+// per key instead of a select chain over the register array)
 template <int C, class R>
-__device__ __forceinline__ void key_runs(const unsigned (&key)[2 * FAN_REG], const int (&ev)[FAN_REG], R&& row) {
+__device__ __forceinline__ void key_runs(const unsigned (&key)[2 * FAN_REG], const int* sev, R&& row) {
     int first = 0, last = 0, t = 0;
     unsigned prev = KEY_NONE;
 #pragma unroll
     for (int x = 0; x < C; ++x) {
         const unsigned k = key[x];
         if (k == KEY_NONE) continue;
-        const int j = (k >> 2) & 7;
-        int e = ev[0];
-#pragma unroll
-        for (int q = 1; q < FAN_REG; ++q) e = j == q ? ev[q] : e;
+        const int e = sev[((k >> 2) & 7) * FAN_TPB];
         const int inst = (e << 3) | (int)(k & 3);
         if ((k >> 5) != (prev >> 5)) {
             if (t) row(first, last, t);
@@ -238,6 +237,7 @@ __global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
     __shared__ unsigned long long s_excl;
     __shared__ int2 s_rec[FAN_REC_STAGE];
     __shared__ int s_inc[FAN_REC_STAGE];
+    __shared__ int s_ev[FAN_REG * FAN_TPB];  // the fan's element ids, [j * FAN_TPB + thread]
     if (threadIdx.x == 0) s_tile = atomicAdd(&A.hdr->tile_ticket, 1);
     __syncthreads();
     const int tile = s_tile;
@@ -259,6 +259,9 @@ __global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
         if (!slow) {
 #pragma unroll
             for (int j = 0; j < FAN_REG; ++j) ev[j] = j < n ? A.fan[beg + j] : 0;
+#pragma unroll
+            for (int j = 0; j < FAN_REG; ++j)
+                if (j < n) s_ev[j * FAN_TPB + threadIdx.x] = ev[j];
 #pragma unroll
             for (int j = 0; j < FAN_REG; ++j) {
                 if (j < n) {
@@ -356,8 +359,8 @@ __global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
             inst += t;
         };
         if (!slow) {
-            if (n <= FAN_REG / 2) key_runs<FAN_REG>(key, ev, row);
-            else key_runs<2 * FAN_REG>(key, ev, row);
+            if (n <= FAN_REG / 2) key_runs<FAN_REG>(key, s_ev + threadIdx.x, row);
+            else key_runs<2 * FAN_REG>(key, s_ev + threadIdx.x, row);
         } else {
             fan_edges_slow(A.elems, A.fan + beg, a, n, [&](int, int first, int last, int t) { row(first, last, min(t, 2)); });
         }
