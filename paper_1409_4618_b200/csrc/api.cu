@@ -112,6 +112,7 @@ efem_status flags_status(const Plan& p) {
 efem_status read_flags(Plan& p, cudaStream_t s) {
     EFEM_CUDA_TRY(cudaMemcpyAsync(p.h_hdr, p.hdr, sizeof(WsHeader), cudaMemcpyDeviceToHost, s));
     EFEM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (uses_fan(p)) p.fan_small = p.h_hdr->fan_big == 0;  // (a performance hint only)
     return flags_status(p);
 }
 

@@ -32,7 +32,7 @@ struct WsHeader {
     // entries, global id of the first row
     long long win[6];
     int tile_ticket;  // dynamic tile ids of the look-back scans (fan2d.cu)
-    int pad2;
+    int fan_big;      // the last fan pass saw a node fan of > FAN_SMALL triangles (fan2d.cu)
 };
 
 // Instance words e << 3 | k (element e < 2^27, local entity k); the two top
@@ -103,6 +103,7 @@ struct Plan {
     int64_t own_lo = 0, own_n = -1;
     int32_t* node_ent = nullptr;     // optional: first row of each owned node (dist2d.cu)
     bool fan_valid = false;          // rec / inc_ptr / e2d are current from the fan pipeline
+    bool fan_small = false;          // the last read-back saw no fan above FAN_SMALL (fan2d.cu kernel choice)
     bool want_d2n = false;
     bool exact_ne3 = false;  // NE0 3D: exact link counts (non-manifold meshes), efem_plan_set_exact
     void* cub_tmp = nullptr;

@@ -35,7 +35,16 @@ namespace efem {
 namespace {
 
 constexpr int FAN_TPB = 128;
-constexpr int FAN_REG = 8;                   // fast path: fan size and neighbour count per node
+// Register fast path: fans of <= FR triangles, 2 FR key registers.  FR = 8
+// covers every node of the meshes in the tests but one in a thousand; FR = 4
+// (all 2D triangulations average 4) leaves registers for 12 CTAs / SM and is
+// launched when the previous fan pass of the plan saw no larger fan (a
+// larger one then takes the slow path: same result, slower).
+constexpr int FAN_REG = 8;
+constexpr int FAN_SMALL = 4;
+#ifndef EFEM_FAN_MINB
+#define EFEM_FAN_MINB 12
+#endif
 constexpr unsigned long long TS_AGG = 1ull << 62, TS_PRE = 2ull << 62, TS_VAL = (1ull << 62) - 1;
 
 __device__ __forceinline__ bool invalid_node(int v, int64_t n) { return (unsigned long long)(unsigned)v >= (unsigned long long)n; }
@@ -184,8 +193,8 @@ constexpr int FAN_REC_STAGE = FAN_TPB * 4;  // staged rows per tile
 constexpr unsigned KEY_NONE = 0xffffffffu;
 constexpr int KEY_DMAX = 1 << 27;
 
-template <int C>
-__device__ __forceinline__ void sort_keys(unsigned (&key)[2 * FAN_REG]) {
+template <int C, int K2>
+__device__ __forceinline__ void sort_keys(unsigned (&key)[K2]) {
 #pragma unroll
     for (int kk = 2; kk <= C; kk <<= 1)
 #pragma unroll
@@ -206,8 +215,8 @@ __device__ __forceinline__ void sort_keys(unsigned (&key)[2 * FAN_REG]) {
 // instances e << 3 | k ordered by element
 // (sev: the fan's element ids in shared memory, sev[j * FAN_TPB]: one load
 // per key instead of a select chain over the register array)
-template <int C, class R>
-__device__ __forceinline__ void key_runs(const unsigned (&key)[2 * FAN_REG], const int* sev, R&& row) {
+template <int C, int K2, class R>
+__device__ __forceinline__ void key_runs(const unsigned (&key)[K2], const int* sev, R&& row) {
     int first = 0, last = 0, t = 0;
     unsigned prev = KEY_NONE;
 #pragma unroll
@@ -230,15 +239,20 @@ __device__ __forceinline__ void key_runs(const unsigned (&key)[2 * FAN_REG], con
     if (t) row(first, last, t);
 }
 
-__global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
+template <int FR>
+__global__ void __launch_bounds__(FAN_TPB, EFEM_FAN_MINB) k_fan_nodes(FanNodesArgs A) {
     using BlockScan = cub::BlockScan<unsigned long long, FAN_TPB>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
     __shared__ int s_tile;
     __shared__ unsigned long long s_excl;
     __shared__ int2 s_rec[FAN_REC_STAGE];
     __shared__ int s_inc[FAN_REC_STAGE];
-    __shared__ int s_ev[FAN_REG * FAN_TPB];  // the fan's element ids, [j * FAN_TPB + thread]
-    if (threadIdx.x == 0) s_tile = atomicAdd(&A.hdr->tile_ticket, 1);
+    __shared__ int s_ev[FR * FAN_TPB];  // the fan's element ids, [j * FAN_TPB + thread]
+    __shared__ int s_big;
+    if (threadIdx.x == 0) {
+        s_tile = atomicAdd(&A.hdr->tile_ticket, 1);
+        s_big = 0;
+    }
     __syncthreads();
     const int tile = s_tile;
     const int64_t l64 = (int64_t)tile * FAN_TPB + threadIdx.x;  // owned node index
@@ -246,24 +260,25 @@ __global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
     const int a = (int)(A.lo + l64);
     int n_ent = 0, n_inst = 0, beg = 0, n = 0;
     bool bad = false, slow = false;
-    unsigned key[2 * FAN_REG];
-    int ev[FAN_REG];
+    unsigned key[2 * FR];
+    int ev[FR];
 #pragma unroll
-    for (int x = 0; x < 2 * FAN_REG; ++x) key[x] = KEY_NONE;
+    for (int x = 0; x < 2 * FR; ++x) key[x] = KEY_NONE;
 #pragma unroll
-    for (int j = 0; j < FAN_REG; ++j) ev[j] = 0;
+    for (int j = 0; j < FR; ++j) ev[j] = 0;
     if (live) {
         beg = __ldg(A.fan_ptr + l64);
         n = __ldg(A.fan_ptr + l64 + 1) - beg;
-        slow = n > FAN_REG;
+        slow = n > FR;
+        if (n > FAN_SMALL) s_big = 1;  // (for the next launch's choice of FR)
         if (!slow) {
 #pragma unroll
-            for (int j = 0; j < FAN_REG; ++j) ev[j] = j < n ? A.fan[beg + j] : 0;
+            for (int j = 0; j < FR; ++j) ev[j] = j < n ? A.fan[beg + j] : 0;
 #pragma unroll
-            for (int j = 0; j < FAN_REG; ++j)
+            for (int j = 0; j < FR; ++j)
                 if (j < n) s_ev[j * FAN_TPB + threadIdx.x] = ev[j];
 #pragma unroll
-            for (int j = 0; j < FAN_REG; ++j) {
+            for (int j = 0; j < FR; ++j) {
                 if (j < n) {
                     int g0, g1, g2;
                     load_tri(A.elems, ev[j], g0, g1, g2);
@@ -289,8 +304,8 @@ __global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
                     if (x >= 2) bad |= v && (key[x] >> 5) == (key[x - 2] >> 5);  // an edge in three triangles
                 }
             };
-            if (n <= FAN_REG / 2) count(std::integral_constant<int, FAN_REG>{});
-            else count(std::integral_constant<int, 2 * FAN_REG>{});
+            if (n <= FR / 2) count(std::integral_constant<int, FR>{});
+            else count(std::integral_constant<int, 2 * FR>{});
         } else {
             fan_sort_inplace(A.fan + beg, n);
             fan_edges_slow(A.elems, A.fan + beg, a, n, [&](int, int, int, int t) {
@@ -336,6 +351,7 @@ __global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
         if (threadIdx.x == 0) s_excl = excl;
     }
     __syncthreads();
+    if (threadIdx.x == 0 && s_big && !__ldg(&A.hdr->fan_big)) atomicOr(&A.hdr->fan_big, 1);
     const unsigned long long base = s_excl;
     const int e_tile0 = (int)(base >> 31), i_tile0 = (int)(base & 0x7fffffffull);
     const int e_off = (int)(off >> 31);
@@ -359,8 +375,8 @@ __global__ void __launch_bounds__(FAN_TPB) k_fan_nodes(FanNodesArgs A) {
             inst += t;
         };
         if (!slow) {
-            if (n <= FAN_REG / 2) key_runs<FAN_REG>(key, s_ev + threadIdx.x, row);
-            else key_runs<2 * FAN_REG>(key, s_ev + threadIdx.x, row);
+            if (n <= FR / 2) key_runs<FR>(key, s_ev + threadIdx.x, row);
+            else key_runs<2 * FR>(key, s_ev + threadIdx.x, row);
         } else {
             fan_edges_slow(A.elems, A.fan + beg, a, n, [&](int, int first, int last, int t) { row(first, last, min(t, 2)); });
         }
@@ -391,6 +407,7 @@ __global__ void k_fan_init(WsHeader* hdr) {
         hdr->totals[0] = 0;
         hdr->totals[1] = 0;
         hdr->tile_ticket = 0;
+        hdr->fan_big = 0;
     }
 }
 
@@ -432,7 +449,8 @@ efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset) {
         return EFEM_OK;
     }
     FanNodesArgs A{p.elems, p.fan_ptr, p.fan, lo, N, p.node_ent, p.rec, p.inc_ptr, p.e2d, p.fan_tiles, p.hdr};
-    k_fan_nodes<<<ntiles, FAN_TPB, 0, s>>>(A);
+    if (p.fan_small) k_fan_nodes<FAN_SMALL><<<ntiles, FAN_TPB, 0, s>>>(A);
+    else k_fan_nodes<FAN_REG><<<ntiles, FAN_TPB, 0, s>>>(A);
     EFEM_LAUNCH_CHECK();
     return EFEM_OK;
 }

@@ -267,3 +267,64 @@ def test_ne3_sliver_rows_against_exact_rationals():
             assert e_ora <= bound, (int(r), e_gpu, e_ora, bound)
             worst = max(worst, e_gpu * qmin_row[r] ** 2 / eps)
     print(f"worst GPU error x q^2 / eps over the sliver rows: {worst:.3g}")
+
+
+def _max_fan(el, n_nodes):
+    """Largest node fan of the 2D fan pipeline: triangles in which the node
+    is the smallest or the middle vertex."""
+    s = np.sort(el, axis=1)
+    return int(np.bincount(s[:, :2].ravel(), minlength=n_nodes).max())
+
+
+@pytest.mark.parametrize("element", [RT0, NED0], ids=["rt0_2d", "ne0_2d"])
+def test_fan_register_path_choice_on_swapped_mesh(element):
+    """The fan pass launches its 4-triangle register kernel when the plan's
+    previous pass saw no larger fan (fan2d.cu FAN_SMALL).  Swap a relabelled
+    copy of the mesh (same sizes, fans of up to 6+ triangles) into the plan's
+    buffers: the 4-kernel's slow path for the big fans, the synchronous and
+    the graph-replayed asynchronous path, and the next call (back on the
+    8-kernel) must all give the CSR of a fresh plan, bit for bit."""
+    from paper_1409_4618_b200 import api
+    coords, elems = api.build_mesh(2, 48, 0.2, 11)
+    n_nodes = coords.shape[0]
+    el1 = elems.cpu().numpy()
+    assert _max_fan(el1, n_nodes) <= 4
+    rng = np.random.default_rng(5)
+    perm = rng.permutation(n_nodes)  # new id of node i: perm[i]
+    c2 = torch.empty_like(coords)
+    c2[torch.from_numpy(perm).to(coords.device)] = coords
+    e2 = torch.from_numpy(perm[el1].astype(np.int32)).to(elems.device)
+    assert _max_fan(e2.cpu().numpy(), n_nodes) > 4
+
+    ref = api.Assembler(c2.clone(), e2.clone(), element).assemble()
+
+    asm = api.Assembler(coords, elems, element)
+    asm.symbolic()                      # structured mesh: the next fan pass takes the 4-kernel
+    out = asm.alloc_csr()
+    asm.assemble_async(out, api.ALL)    # graph captured with the 4-kernel
+    asm.check()
+    asm.coords.copy_(c2)
+    asm.elems.copy_(e2)
+    outs = []
+    asm.symbolic()                      # synchronous, 4-kernel, on the swapped mesh
+    o = asm.alloc_csr()
+    asm.numeric(o, api.ALL)
+    asm.check()
+    outs.append(o)
+    asm.assemble_async(out, api.ALL)    # replay of the 4-kernel graph on the swapped mesh
+    asm.check()
+    outs.append(_csr_copy(out))
+    asm.symbolic()                      # the 8-kernel (this mesh's fans were seen)
+    o = asm.alloc_csr()
+    asm.numeric(o, api.ALL)
+    asm.check()
+    outs.append(o)
+    for o in outs:
+        for a, b in ((o.row_ptr, ref.row_ptr), (o.col_idx, ref.col_idx), (o.vals_M, ref.vals_M),
+                     (o.vals_K, ref.vals_K)):
+            assert torch.equal(a, b)
+
+
+def _csr_copy(c):
+    from paper_1409_4618_b200 import api
+    return api.CSR(c.row_ptr.clone(), c.col_idx.clone(), c.vals_M.clone(), c.vals_K.clone())
