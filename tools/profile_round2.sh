@@ -16,7 +16,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_launches.log 2>&1; echo "launches rc=$?"
 for c in 2 3 4 5; do
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum \
-      --clock-control none --csv --log-file $O/step_cfg$c.csv python tools/profile_step.py --config $c --reps 1 \
+      --clock-control none --profile-from-start off --csv --log-file $O/step_cfg$c.csv \
+      python tools/profile_step.py --config $c --reps 1 --warm 1 \
       > /dev/null 2>&1; echo "step c$c rc=$?"
 done
 for spec in "5 k_rows_tri cfg5_k_rows_tri" "5 k_fan_nodes cfg5_k_fan_nodes" "2 k_rows_tri cfg2_k_rows_tri" \
