@@ -859,6 +859,9 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     const BucketArrays barr{p.bkey, p.binst, p.bx};
     k_init<<<1, 32, 0, s>>>(p.hdr);
     EFEM_LAUNCH_CHECK();
+    // (2D plans: the node-fan pipeline's one-pass fill leaves its counts in
+    // cnt; 3D plans keep the invariant that every fill returns them to zero)
+    if (KT::D == 2) EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (size_t)(N + 1) * 4, s));
     if (T > 0) {
         k_bucket<KT, false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, nullptr, BucketArrays{}, p.hdr);
         EFEM_LAUNCH_CHECK();

@@ -19,6 +19,7 @@ enum : int {
     F_CAPACITY = 1,      // a per-thread list overflowed
     F_ROW_MISMATCH = 2,  // numeric row length != symbolic row length (internal error)
     F_DEGENERATE = 3,    // det B_K == 0 or non-finite
+    F_FAN_OVER = 4,      // (internal, not an error) a node fan overflowed the fixed-capacity fill (fan2d.cu)
     F_NFLAGS = 8
 };
 
@@ -98,6 +99,8 @@ struct Plan {
     int32_t* fan_ptr = nullptr;      // N+1
     int32_t* fan = nullptr;          // 2T triangle ids
     unsigned long long* fan_tiles = nullptr;  // look-back tile states
+    int32_t* fan_fix = nullptr;      // N * FAN_FIXC: fixed-capacity fans (one-pass fill)
+    int32_t* fan_csum = nullptr;     // tile sums of the fallback scan of the fan counts
     // owned node range of a distributed plan (dist2d.cu): the fan pipeline
     // builds rows only for nodes [own_lo, own_lo + own_n); own_n < 0: all
     int64_t own_lo = 0, own_n = -1;
@@ -218,6 +221,7 @@ inline bool uses_fan(const Plan& p) { return p.dim == 2; }
 efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset = true);
 efem_status launch_hdr_reset(Plan& p, cudaStream_t s);
 size_t fan_tiles_bytes(int64_t n_nodes);
+constexpr int FAN_FIXC = 8;  // largest fixed fan capacity (fan2d.cu)
 // row_ptr helpers (api.cu): 2D edges / 3D faces keep no row_ptr array, row r
 // starts at r + (m-1) inc_ptr[r]; 3D edges store it (plan row_ptr).
 bool row_ptr_stored(const Plan& p);
