@@ -41,7 +41,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
     size_t hdr, cnt, ent_cnt, bucket_ptr, bucket, bkey, binst, bx, nbr, e2d, inc_ptr, row_ptr, rec, d2n, ent_ptr, nnz_cnt, tiles, totals, cub, total;
-    size_t fan_ptr, fan, fan_tiles, fan_fix, fan_csum;
+    size_t fan_ptr, fan, fan_tiles, fan_fix, fan_csum, ne3_fan, ne3_fcnt;
 };
 
 Layout layout(const Plan& p, size_t cub_bytes) {
@@ -81,6 +81,8 @@ Layout layout(const Plan& p, size_t cub_bytes) {
     L.fan_tiles = take(fan ? fan_tiles_bytes(p.n_nodes) : 8);
     L.fan_fix = take(fan ? (size_t)p.n_nodes * FAN_FIXC * 4 : 4);
     L.fan_csum = take(fan ? ((size_t)p.n_nodes / 2048 + 2) * 4 : 4);
+    L.ne3_fan = take(ne3 ? (size_t)p.n_nodes * 24 * 4 : 4);  // (NE3_FAN_C, dofs.cu)
+    L.ne3_fcnt = take(ne3 ? (size_t)p.n_nodes * 4 : 4);
     L.total = off;
     return L;
 }
@@ -443,6 +445,8 @@ efem_status efem_plan_set_workspace(efem_plan plan, void* ws, size_t ws_bytes) {
     p->fan_tiles = reinterpret_cast<unsigned long long*>(b + L.fan_tiles);
     p->fan_fix = reinterpret_cast<int32_t*>(b + L.fan_fix);
     p->fan_csum = reinterpret_cast<int32_t*>(b + L.fan_csum);
+    p->ne3_fan = reinterpret_cast<int32_t*>(b + L.ne3_fan);
+    p->ne3_fcnt = reinterpret_cast<int32_t*>(b + L.ne3_fcnt);
     p->fan_valid = false;
     p->enumerated = p->symbolic = false;
     // counters that must start at zero (the fill pass restores cnt to zero;

@@ -120,12 +120,10 @@ template <class KT>
 constexpr int KS = KT::D == 3 ? 2 : 1;  // key stride in u64 words
 
 template <class KT, bool FILL>
-__global__ void __launch_bounds__(256) k_bucket(const int32_t* __restrict__ elems, int64_t n_elems, int64_t n_nodes,
-                                                int32_t* __restrict__ cnt, const int32_t* __restrict__ bucket_ptr,
-                                                BucketArrays B, WsHeader* hdr) {
+__device__ __forceinline__ void bucket_one(const int32_t* __restrict__ elems, int64_t e, int64_t n_nodes,
+                                           int32_t* __restrict__ cnt, const int32_t* __restrict__ bucket_ptr,
+                                           BucketArrays B, WsHeader* hdr) {
     constexpr int M = KT::M;
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= n_elems) return;
     int g[KT::NV];
     load_elem<KT>(elems, (int)e, g);
     bool bad = false;
@@ -184,6 +182,65 @@ __global__ void __launch_bounds__(256) k_bucket(const int32_t* __restrict__ elem
             }
         }
     }
+}
+
+template <class KT, bool FILL>
+__global__ void __launch_bounds__(256) k_bucket(const int32_t* __restrict__ elems, int64_t n_elems, int64_t n_nodes,
+                                                int32_t* __restrict__ cnt, const int32_t* __restrict__ bucket_ptr,
+                                                BucketArrays B, WsHeader* hdr) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n_elems) return;
+    bucket_one<KT, FILL>(elems, e, n_nodes, cnt, bucket_ptr, B, hdr);
+}
+
+// ---------------------------------------------------------------------------------
+// NE0 3D, one pass over the tets: the instance counts of the bucket layout
+// (as k_bucket<count>) plus each tet's id in FIXED-capacity fans of its three
+// smallest vertices (the nodes whose edges it holds): the node pass then
+// gathers the tets instead of reading 16-byte instance records, and the
+// record fill disappears.  A fan over C tets, or a tet with repeated (or
+// out-of-range, counted as node 0) vertices, sets F_FAN_OVER: the record
+// fill (k_bucket_cond) then runs on the device and the node pass reads the
+// records, exactly the counting-sort path.
+// ---------------------------------------------------------------------------------
+constexpr int NE3_FAN_C = 24;  // fan slots per node (structured tet meshes: 18)
+
+__global__ void __launch_bounds__(256) k_fill_fan3(const int32_t* __restrict__ elems, int64_t n_elems, int64_t n_nodes,
+                                                   int32_t* __restrict__ cnt, int32_t* __restrict__ fcnt,
+                                                   int32_t* __restrict__ fan, WsHeader* hdr) {
+    using KT = Kind<3, EFEM_NED0>;
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n_elems) return;
+    bucket_one<KT, false>(elems, e, n_nodes, cnt, nullptr, BucketArrays{}, hdr);  // instance counts
+    int g[4];
+    load_elem<KT>(elems, (int)e, g);
+    bool over = false;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) over |= (unsigned)g[v] >= (unsigned long long)n_nodes;
+    over |= g[0] == g[1] || g[0] == g[2] || g[0] == g[3] || g[1] == g[2] || g[1] == g[3] || g[2] == g[3];
+    if (!over) {
+        const int mx = max(max(g[0], g[1]), max(g[2], g[3]));
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            if (g[v] != mx) {  // one of the three smallest
+                const int k = atomicAdd(fcnt + g[v], 1);
+                if (k < NE3_FAN_C) fan[(int64_t)g[v] * NE3_FAN_C + k] = (int)e;
+                else over = true;
+            }
+        }
+    }
+    if (over) atomicOr(&hdr->flags[F_FAN_OVER], 1);
+}
+
+// the record fill of the counting-sort path, only after an overflow
+template <class KT>
+__global__ void __launch_bounds__(256) k_bucket_cond(const int32_t* __restrict__ elems, int64_t n_elems,
+                                                     int64_t n_nodes, int32_t* __restrict__ cnt,
+                                                     const int32_t* __restrict__ bucket_ptr, BucketArrays B,
+                                                     WsHeader* hdr) {
+    if (!__ldg(&hdr->flags[F_FAN_OVER])) return;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_elems; e += (int64_t)gridDim.x * blockDim.x)
+        bucket_one<KT, true>(elems, e, n_nodes, cnt, bucket_ptr, B, hdr);
 }
 
 // ---------------------------------------------------------------------------------
@@ -410,6 +467,150 @@ __device__ __forceinline__ bool node_group_ne3(const BucketArrays& B, int32_t* _
     return true;
 }
 
+// local edge of the local vertex pair (p, q), p != q: nibble 4 p + q
+constexpr unsigned long long NE3_LOCAL_EDGE = 0x452403153002100ull;
+
+// 3D edges, fan mode: node_group_ne3 over the node's fan tets (gathered)
+// instead of its instance records -- instance (a, b) for every vertex b > a
+// of a fan tet, inst = e << 3 | local edge, link-edge xor c ^ d = the tet's
+// xor ^ a ^ b.  Same outputs (grouped words, BND / RUN flags, b's in x).
+template <class KT, int DC>
+__device__ __forceinline__ bool node_group_ne3_fan(const int32_t* __restrict__ elems, const int32_t* __restrict__ fl,
+                                                   int nf, int32_t* __restrict__ gb, int32_t* __restrict__ bx, int a,
+                                                   int* s_grp, int& n_ent, int& n_nnz) {
+    constexpr int TPB = NodeCaps<KT>::TPB;
+    static_assert(DC <= NodeCaps<KT>::DCAP, "shared scratch sized for DCAP groups");
+    int* Cur = s_grp + threadIdx.x;
+    int* X = Cur + NodeCaps<KT>::DCAP * TPB;
+    int D[DC], C[DC];
+#pragma unroll
+    for (int q = 0; q < DC; ++q) {
+        D[q] = INT_MAX;
+        C[q] = 0;
+    }
+    int nd = 0;
+    bool over = false;
+    constexpr int U = 4;  // tets gathered ahead of use
+    for (int f0 = 0; f0 < nf; f0 += U) {
+        int4 tq[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            tq[u] = f0 + u < nf ? __ldg(reinterpret_cast<const int4*>(elems) + __ldg(fl + f0 + u))
+                                : make_int4(-1, -1, -1, -1);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int gv[4] = {tq[u].x, tq[u].y, tq[u].z, tq[u].w};
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int b = gv[v];
+                if (b <= a) continue;
+                int lt = 0;
+                bool found = false;
+#pragma unroll
+                for (int q = 0; q < DC; ++q) {
+                    lt += D[q] < b;
+                    found |= D[q] == b;
+                }
+                if (found) {
+#pragma unroll
+                    for (int q = 0; q < DC; ++q) C[q] += q == lt;
+                } else if (nd == DC) {
+                    over = true;
+                } else {
+#pragma unroll
+                    for (int q = DC - 1; q > 0; --q) {
+                        D[q] = q > lt ? D[q - 1] : (q == lt ? b : D[q]);
+                        C[q] = q > lt ? C[q - 1] : (q == lt ? 1 : C[q]);
+                    }
+                    D[0] = lt == 0 ? b : D[0];
+                    C[0] = lt == 0 ? 1 : C[0];
+                    ++nd;
+                }
+            }
+        }
+    }
+    if (over) return false;
+    int S[DC];
+    int off = 0;
+#pragma unroll
+    for (int q = 0; q < DC; ++q) {
+        S[q] = off;
+        if (q < nd) {
+            Cur[q * TPB] = off;
+            X[q * TPB] = 0;
+        }
+        off += C[q];
+    }
+    for (int f0 = 0; f0 < nf; f0 += U) {
+        int ev[U];
+        int4 tq[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ev[u] = f0 + u < nf ? __ldg(fl + f0 + u) : 0;
+            tq[u] = f0 + u < nf ? __ldg(reinterpret_cast<const int4*>(elems) + ev[u]) : make_int4(-1, -1, -1, -1);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int gv[4] = {tq[u].x, tq[u].y, tq[u].z, tq[u].w};
+            const int la = gv[0] == a ? 0 : (gv[1] == a ? 1 : (gv[2] == a ? 2 : 3));
+            const int xr = gv[0] ^ gv[1] ^ gv[2] ^ gv[3];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int b = gv[v];
+                if (b <= a) continue;
+                int g = 0, st = 0;
+#pragma unroll
+                for (int q = 0; q < DC; ++q) g += D[q] < b;  // b present: its group index
+#pragma unroll
+                for (int q = 0; q < DC; ++q) st = q == g ? S[q] : st;
+                const int pos = Cur[g * TPB];
+                Cur[g * TPB] = pos + 1;
+                X[g * TPB] ^= xr ^ a ^ b;  // c ^ d of this tet
+                const int k = (int)((NE3_LOCAL_EDGE >> (4 * (la * 4 + v))) & 15ull);
+                gb[pos] = (int)((uint32_t)((ev[u] << 3) | k) | (pos == st ? RUN_FLAG : 0u));
+            }
+        }
+    }
+    int nnz = 0;
+#pragma unroll
+    for (int q = 0; q < DC; ++q) {
+        if (q < nd) {
+            const int st = S[q];
+            const bool bnd = X[q * TPB] != 0;  // open link path: L = t + 1
+            if (bnd) atomicOr(gb + st, (int)BND_FLAG);
+            bx[q] = D[q];  // compact: group q's b
+            nnz += 1 + 3 * C[q] + 2 * (int)bnd;
+        }
+    }
+    n_ent = nd;
+    n_nnz = nnz;
+    return true;
+}
+
+// fan mode, a node the register path cannot take (more distinct neighbours
+// than DCAP, or exact link counts): its instance records {b << 32 | inst,
+// tet xor} written into its bucket range of the key array, for the generic
+// sort that follows
+__device__ __forceinline__ void ne3_fan_records(const int32_t* __restrict__ elems, const int32_t* __restrict__ fl,
+                                                int nf, int a, uint64_t* __restrict__ key, int64_t beg) {
+    int j = 0;
+    for (int f = 0; f < nf; ++f) {
+        const int e = __ldg(fl + f);
+        const int4 t = __ldg(reinterpret_cast<const int4*>(elems) + e);
+        const int gv[4] = {t.x, t.y, t.z, t.w};
+        const int la = gv[0] == a ? 0 : (gv[1] == a ? 1 : (gv[2] == a ? 2 : 3));
+        const int xr = gv[0] ^ gv[1] ^ gv[2] ^ gv[3];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            if (gv[v] <= a) continue;
+            const int k = (int)((NE3_LOCAL_EDGE >> (4 * (la * 4 + v))) & 15ull);
+            key[(beg + j) * 2] = ((uint64_t)(uint32_t)gv[v] << 32) | (uint32_t)((e << 3) | k);
+            key[(beg + j) * 2 + 1] = (uint64_t)(uint32_t)xr;
+            ++j;
+        }
+    }
+}
+
 // 3D faces: group the node's instances by face key (mid << 32 | hi) with the
 // sorted distinct list and counts in registers (as node_group_ne3), counting
 // scatter, then each face's two tets in element order.  Returns false when
@@ -559,7 +760,9 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
                                                                   int64_t n_nodes, int32_t* __restrict__ ent_cnt,
                                                                   int32_t* __restrict__ nnz_cnt, int exact,
                                                                   int32_t* __restrict__ ent_bsum,
-                                                                  int32_t* __restrict__ nnz_bsum) {
+                                                                  int32_t* __restrict__ nnz_bsum,
+                                                                  const int32_t* __restrict__ fan,
+                                                                  const int32_t* __restrict__ fcnt, WsHeader* hdr) {
     constexpr bool NE3 = KT::D == 3 && !KT::FACES;
     constexpr int TPB = NodeCaps<KT>::TPB;
     constexpr int DCAP = NodeCaps<KT>::DCAP;
@@ -569,6 +772,13 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
     __shared__ int s_inst[1];
     __shared__ int s_grp[NE3 ? 2 * DCAP * TPB : 1];
     __shared__ int s_cur[KT::FACES ? 16 * TPB : 1];
+    // NE3 fan mode (fan != NULL and no overflow): the node's tets come from
+    // its fixed-capacity fan (k_fill_fan3), not from instance records.  (The
+    // flag is read once per CTA.)
+    __shared__ int s_fan;
+    if (NE3 && threadIdx.x == 0) s_fan = fan && !*(volatile const int*)&hdr->flags[F_FAN_OVER];
+    __syncthreads();
+    const bool fanmode = NE3 && s_fan;
     const int64_t a64 = (int64_t)blockIdx.x * TPB + threadIdx.x;
     int n_ent = 0, n_nnz = 0;
     if (a64 < n_nodes) {
@@ -617,8 +827,19 @@ __global__ void __launch_bounds__(NodeCaps<KT>::TPB) k_node_count(const int32_t*
             node_sort_generic<KT, false>(B, gb, beg, n, s_key, s_inst, n_ent);
     } else {
         // (8 distinct larger neighbours cover structured tet meshes; 12, then a generic sort)
-        if (exact || (!node_group_ne3<KT, 8>(B, gb, beg, n, a, s_grp, n_ent, n_nnz) &&
-                      !node_group_ne3<KT, NodeCaps<KT>::DCAP>(B, gb, beg, n, a, s_grp, n_ent, n_nnz))) {
+        bool done;
+        if (fanmode) {
+            const int32_t* fl = fan + (int64_t)a * NE3_FAN_C;
+            const int nf = __ldg(fcnt + a);
+            done = !exact && (node_group_ne3_fan<KT, 8>(elems, fl, nf, gb, B.x + beg, a, s_grp, n_ent, n_nnz) ||
+                              node_group_ne3_fan<KT, NodeCaps<KT>::DCAP>(elems, fl, nf, gb, B.x + beg, a, s_grp,
+                                                                         n_ent, n_nnz));
+            if (!done) ne3_fan_records(elems, fl, nf, a, B.key, beg);  // for the generic sort below
+        } else {
+            done = !exact && (node_group_ne3<KT, 8>(B, gb, beg, n, a, s_grp, n_ent, n_nnz) ||
+                              node_group_ne3<KT, NodeCaps<KT>::DCAP>(B, gb, beg, n, a, s_grp, n_ent, n_nnz));
+        }
+        if (!done) {
             n_ent = 0;
             n_nnz = 0;
             // (the NE3 instantiation has no key smem: sort in global memory)
@@ -859,17 +1080,37 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     const BucketArrays barr{p.bkey, p.binst, p.bx};
     k_init<<<1, 32, 0, s>>>(p.hdr);
     EFEM_LAUNCH_CHECK();
+#ifndef EFEM_NE3_FAN
+#define EFEM_NE3_FAN 1
+#endif
+    // NE0 3D: one-pass fan fill (k_fill_fan3); exact link counts keep the
+    // record path
+    constexpr bool NE3 = KT::D == 3 && !KT::FACES;
+    const bool fan3 = NE3 && EFEM_NE3_FAN && !p.exact_ne3 && N > 0;
     // (2D plans: the node-fan pipeline's one-pass fill leaves its counts in
     // cnt; 3D plans keep the invariant that every fill returns them to zero)
-    if (KT::D == 2) EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (size_t)(N + 1) * 4, s));
+    // (the 2D fan pipeline's one-pass fill and the NE3 fan fill leave their
+    // counts in cnt -- and an NE3 plan switches between that and the record
+    // path with efem_plan_set_exact; the counting-sort fills return them to zero)
+    if (KT::D == 2 || NE3) EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (size_t)(N + 1) * 4, s));
+    if (fan3) EFEM_CUDA_TRY(cudaMemsetAsync(p.ne3_fcnt, 0, (size_t)N * 4, s));
     if (T > 0) {
-        k_bucket<KT, false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, nullptr, BucketArrays{}, p.hdr);
+        if (fan3)
+            k_fill_fan3<<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, p.ne3_fcnt, p.ne3_fan, p.hdr);
+        else
+            k_bucket<KT, false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, nullptr, BucketArrays{}, p.hdr);
         EFEM_LAUNCH_CHECK();
     }
     EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.cnt, p.bucket_ptr, (int)(N + 1), s));
     count_launch(2);
     if (T > 0) {
-        k_bucket<KT, true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, p.bucket_ptr, barr, p.hdr);
+        if (fan3) {  // the record fill only after an overflow (exits at once otherwise)
+            int sms = 148, dev = 0;
+            if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            k_bucket_cond<KT><<<8 * sms, 256, 0, s>>>(p.elems, T, N, p.cnt, p.bucket_ptr, barr, p.hdr);
+        } else {
+            k_bucket<KT, true><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, N, p.cnt, p.bucket_ptr, barr, p.hdr);
+        }
         EFEM_LAUNCH_CHECK();
     }
     if (N == 0) {
@@ -882,7 +1123,8 @@ efem_status run_enumerate_kt(Plan& p, cudaStream_t s) {
     constexpr int TPB = NodeCaps<KT>::TPB;
     const int nb = (int)grid_for(N, TPB);
     k_node_count<KT><<<nb, TPB, 0, s>>>(p.elems, p.bucket_ptr, barr, p.bucket, N, p.ent_cnt, p.nnz_cnt,
-                                         (int)p.exact_ne3, p.ent_bsum, p.nnz_bsum);
+                                         (int)p.exact_ne3, p.ent_bsum, p.nnz_bsum, fan3 ? p.ne3_fan : nullptr,
+                                         p.ne3_fcnt, p.hdr);
     EFEM_LAUNCH_CHECK();
     // scans over the CTA tiles' totals only (the write pass finishes per node)
     EFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(p.cub_tmp, bytes, p.ent_bsum, p.ent_bpre, nb + 1, s));

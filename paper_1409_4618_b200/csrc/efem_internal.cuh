@@ -101,6 +101,8 @@ struct Plan {
     unsigned long long* fan_tiles = nullptr;  // look-back tile states
     int32_t* fan_fix = nullptr;      // N * FAN_FIXC: fixed-capacity fans (one-pass fill)
     int32_t* fan_csum = nullptr;     // tile sums of the fallback scan of the fan counts
+    int32_t* ne3_fan = nullptr;      // NE0 3D: N * 24 fixed-capacity tet fans (dofs.cu k_fill_fan3)
+    int32_t* ne3_fcnt = nullptr;     // their counts
     // owned node range of a distributed plan (dist2d.cu): the fan pipeline
     // builds rows only for nodes [own_lo, own_lo + own_n); own_n < 0: all
     int64_t own_lo = 0, own_n = -1;

@@ -282,6 +282,7 @@ __device__ __noinline__ bool row_generic(const double* __restrict__ coords, cons
     constexpr int WCAP = RowCaps<KT>::WCAP;
     constexpr int D = KT::D, NV = KT::NV, M = KT::M;
     bool ok = t <= EFEM_MAX_ROW_ELEMS;
+    bool cap = !ok;  // a per-thread capacity (not a mesh defect): reported as EFEM_ECAPACITY
     const int nt = ok ? t : EFEM_MAX_ROW_ELEMS;
     // the row's instances in ascending element order (fixed summation order)
     int ord[EFEM_MAX_ROW_ELEMS];
@@ -307,7 +308,7 @@ __device__ __noinline__ bool row_generic(const double* __restrict__ coords, cons
             int q = nw;
             while (q > 0 && W[q - 1] > x) --q;
             if (q > 0 && W[q - 1] == x) continue;
-            if (nw >= WCAP) { ok = false; continue; }
+            if (nw >= WCAP) { ok = false; cap = true; continue; }
             for (int u = nw; u > q; --u) W[u] = W[u - 1];
             W[q] = x;
             ++nw;
@@ -339,6 +340,7 @@ __device__ __noinline__ bool row_generic(const double* __restrict__ coords, cons
     }
     const int ncol = mk.finish();
     ok &= ncol == rlen;
+    if (cap) atomicOr(&hdr->flags[F_CAPACITY], 1);
     if (!ok) return false;
     for (int q = 0; q < rlen; ++q) {
         vm[q * st] = 0.0;

@@ -328,3 +328,45 @@ def test_fan_register_path_choice_on_swapped_mesh(element):
 def _csr_copy(c):
     from paper_1409_4618_b200 import api
     return api.CSR(c.row_ptr.clone(), c.col_idx.clone(), c.vals_M.clone(), c.vals_K.clone())
+
+
+def edge_ring_mesh(k, rings=1):
+    """rings x k tets (0, p, r_i, r_(i+1) mod k) around the edges (0, p), p the
+    pole of each ring (ring 1 above node 0, ring 2 below): node 0 is the
+    smallest vertex of all of them (its fan in the NE0-3D enumeration), with
+    rings * (k + 1) distinct larger neighbours, and each edge (0, p) has k tets."""
+    pts, el = [[0.0, 0.0, 0.0]], []
+    for r in range(rings):
+        z = 0.3 if r == 0 else -0.3
+        pole = len(pts)
+        pts.append([0.0, 0.0, 2 * z])
+        th = 2 * np.pi * (np.arange(k) + 0.5 * r) / k
+        ring = len(pts)
+        pts += [[np.cos(t), np.sin(t), z] for t in th]
+        el += [[0, pole, ring + i, ring + (i + 1) % k] for i in range(k)]
+    return np.ascontiguousarray(np.array(pts)), np.array(el, np.int32)
+
+
+@pytest.mark.parametrize("element", [RT0, NED0], ids=["rt0", "ne0"])
+@pytest.mark.parametrize("k,rings", [(9, 1), (20, 1), (15, 2)], ids=["k9", "k20", "k15x2"])
+def test_edge_ring_parity(element, k, rings):
+    """NE0 3D fan enumeration (dofs.cu k_fill_fan3): k = 20 keeps node 0's
+    fan within the 24 fixed slots but its 21 larger neighbours beyond the
+    register lists (the fan-mode generic path, records built from the fan);
+    two rings of 15 overflow the slots (the on-device record fallback);
+    k = 9 the register path with a row of 9 tets (row_generic in the
+    numeric kernel)."""
+    pts, el = edge_ring_mesh(k, rings)
+    _check(3, element, pts, el, f"edge ring k={k} x{rings}")
+
+
+def test_edge_ring_capacity_reported():
+    """An NE0-3D row whose tets have more than 21 link vertices exceeds
+    row_generic's per-thread list (|W| <= 23): EFEM_ECAPACITY, not wrong values
+    and not a non-conformity report."""
+    from paper_1409_4618_b200 import _lib, api
+    pts, el = edge_ring_mesh(30)
+    asm = api.Assembler(torch.from_numpy(pts).cuda(), torch.from_numpy(el).cuda(), NED0)
+    with pytest.raises(_lib.EfemError) as ex:
+        asm.assemble()
+    assert ex.value.status == -8  # EFEM_ECAPACITY (include/efem.h)
