@@ -490,7 +490,10 @@ __device__ __forceinline__ bool node_group_ne3_fan(const int32_t* __restrict__ e
     }
     int nd = 0;
     bool over = false;
-    constexpr int U = 4;  // tets gathered ahead of use
+    // tets gathered ahead of use (2: U = 1 / 4 / 8 measured 9 % / 14 % / 27 %
+    // slower on the config-4 symbolic phase -- fewer unrolled compare chains
+    // in flight beat deeper prefetch here)
+    constexpr int U = 2;
     for (int f0 = 0; f0 < nf; f0 += U) {
         int4 tq[U];
 #pragma unroll
