@@ -1,6 +1,6 @@
 // fan2d.cu -- the symbolic half of the 2D hot path (RT0 and NE0 on
 // triangles) as a node-fan pipeline: DOF enumeration and the sparsity
-// pattern's row structure in three kernels.
+// pattern's row structure in two kernels (plus an on-device fallback).
 //
 // The method (Sec. 2.4; 671-696, Sec. 3.2): global edge
 // DOFs numbered by the lexicographic rank of their sorted node pair (reading
@@ -10,10 +10,15 @@
 // the triangles in which a is the smallest or the middle vertex (exactly the
 // triangles holding an edge whose smaller node is a).
 //
-//   k_fan_bucket<count>  per triangle (p < q < r): one atomic at p and at q
-//   CUB scan             -> fan_ptr
-//   k_fan_bucket<fill>   per triangle: its id into the fans of p and q
-//   k_fan_nodes          per node: the owned edges as sorted (b, element,
+//   k_fan_fill_fixed     per triangle (p < q < r): one atomic at p and at q,
+//                        whose return value is the slot of the triangle id
+//                        in the node's C fixed fan slots (C = 4 or 8)
+//   (fallback)           only when a fan overflows C (F_FAN_OVER): a scan
+//                        of the counts -> fan_ptr and the counting-sort
+//                        fill (k_cscan_*, k_fan_fill_cond: they exit at
+//                        once otherwise; the plain count / scan / fill
+//                        sequence with EFEM_FAN_FIXED=0)
+//   k_fan_nodes<FR>      per node: the owned edges as sorted (b, element,
 //                        local edge) keys in registers; DOF ids and instance
 //                        offsets by a single-pass decoupled look-back over
 //                        node tiles; row records, incidence offsets and
