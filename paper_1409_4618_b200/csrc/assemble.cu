@@ -712,20 +712,15 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
         ok = __popcll(mask) == rlen;
         done = true;
         if (ok) {
-            if constexpr (SM) {  // rlen <= NE3_SLOTS when staged: predicated, no loop
-#pragma unroll
-                for (int q = 0; q < NE3_SLOTS; ++q)
-                    if (q < rlen) {
-                        cvm[q * st] = 0.0;
-                        cvk[q * st] = 0.0;
-                    }
-            } else {
-                for (int q = 0; q < rlen; ++q) {
-                    cvm[q * st] = 0.0;
-                    cvk[q * st] = 0.0;
-                }
-            }
+            // Accumulation with fewer shared-memory accesses (their slots are
+            // data dependent, so most of them meet bank conflicts): the own
+            // column ab, held by every tet, sums in registers; every other
+            // column is stored by its first tet (0.0 + v, what a zeroed
+            // accumulator would hold) and read-modify-written by the later
+            // ones -- the same sums in the same order, bit for bit.
             const int sab = __popcll(mask & ((1ull << iab) - 1ull));
+            unsigned long long seen = 1ull << iab;
+            double dm = 0.0, dk = 0.0;
             // role frame: vertices ordered (a, b, c, d), a < b the row's
             // edge.  The globally oriented Whitney basis of edge {x, y}
             // is sigma_xy (l_x grad l_y - l_y grad l_x), sigma_xy = +1
@@ -796,22 +791,29 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
                     // DOF ids of the role pairs ac ad bc bd cd (local edge ids packed with
                     // the roles in the first pass)
                     const int32_t* de = e2d + e * 6;
-                    const int dof[6] = {own_base + i, __ldg(de + (e5 & 7)), __ldg(de + ((e5 >> 3) & 7)),
-                                        __ldg(de + ((e5 >> 6) & 7)), __ldg(de + ((e5 >> 9) & 7)),
-                                        __ldg(de + ((e5 >> 12) & 7))};
                     const int pi = pidx[j];
+                    dm += vm[0];
+                    dk += vk[0];
 #pragma unroll
-                    for (int u = 0; u < 6; ++u) {
+                    for (int u = 1; u < 6; ++u) {
                         // rank of the column's bit among the row's: popcount of the
                         // bits below it (mask shifted up: no 64-bit subtract / and)
-                        const int pb_ = u ? (pi >> (6 * (u - 1))) & 63 : 0;
-                        const int slot = (u == 0 ? sab : (pb_ ? __popcll(mask << (64 - pb_)) : 0)) * st;
-                        ccol[slot] = dof[u];
-                        cvm[slot] += vm[u];
-                        cvk[slot] += vk[u];
+                        const int pb_ = (pi >> (6 * (u - 1))) & 63;
+                        const int slot = (pb_ ? __popcll(mask << (64 - pb_)) : 0) * st;
+                        const unsigned long long bit = 1ull << pb_;
+                        const bool first = !(seen & bit);
+                        seen |= bit;
+                        if (first) ccol[slot] = __ldg(de + ((e5 >> (3 * (u - 1))) & 7));
+                        const double om = first ? 0.0 : cvm[slot];
+                        const double ok_ = first ? 0.0 : cvk[slot];
+                        cvm[slot] = om + vm[u];
+                        cvk[slot] = ok_ + vk[u];
                     }
                 }
             }
+            ccol[sab * st] = own_base + i;
+            cvm[sab * st] = dm;
+            cvk[sab * st] = dk;
         }
     }
 }
