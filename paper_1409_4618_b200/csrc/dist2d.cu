@@ -219,6 +219,7 @@ struct DistPlan {
     cudaGraphExec_t graph = nullptr;
     efem_csr gkey{};
     unsigned gforms = 0;
+    bool gfan_small = false;  // the fan-pass register path the graph was captured with
     bool graph_failed = false;
     int64_t graph_launches = 0;
 
@@ -513,6 +514,7 @@ efem_status check_one(DistPlan& D, int64_t* window, cudaStream_t s) {
     WsHeader h;
     EFEM_CUDA_TRY(cudaMemcpyAsync(&h, p.hdr, sizeof(WsHeader), cudaMemcpyDeviceToHost, s));
     EFEM_CUDA_TRY(cudaStreamSynchronize(s));
+    p.fan_small = h.fan_big == 0;  // (the fan pass's register path for the next step)
     if (window) {
         window[0] = h.win[4];  // global id of the first row
         window[1] = h.win[1];  // rows
@@ -803,7 +805,8 @@ efem_status efem_dist_assemble(efem_dist_plan plan, unsigned forms, efem_csr* sl
         if ((st = nccl_alltoallv(*D, D->resp_ids, D->resp_off, D->req_ids, D->req_off, 4, q)) != EFEM_OK) return st;
         return ph_numeric(*D, forms, slice, q);
     };
-    const bool same = D->graph && D->gforms == forms && !std::memcmp(&D->gkey, slice, sizeof(efem_csr));
+    const bool same = D->graph && D->gforms == forms && !std::memcmp(&D->gkey, slice, sizeof(efem_csr)) &&
+                      D->gfan_small == D->p().fan_small;
     if (!same && D->graph) {
         cudaGraphExecDestroy(D->graph);
         D->graph = nullptr;
@@ -824,6 +827,7 @@ efem_status efem_dist_assemble(efem_dist_plan plan, unsigned forms, efem_csr* sl
             if (e == EFEM_OK && ee == cudaSuccess && cudaGraphInstantiate(&D->graph, g, 0) == cudaSuccess) {
                 D->gkey = *slice;
                 D->gforms = forms;
+                D->gfan_small = D->p().fan_small;
             } else {
                 D->graph = nullptr;
                 D->graph_failed = true;  // (enqueue directly from now on)
