@@ -106,7 +106,7 @@ struct TriPolicy {
     __device__ __forceinline__ static void load_x(const double* __restrict__ coords, const GhostArgs&, Ids& I, Geo&) {
         tri_load_x(coords, I);
     }
-    __device__ __forceinline__ static double row(const Ids& I, const Geo&, const GhostArgs&, double& m0, double& k0,
+    __device__ __forceinline__ static double row(const Ids& I, const Geo&, const GhostArgs&, int, double& m0, double& k0,
                                                  int (&c)[2], double (&m)[2], double (&k)[2]) {
         c[0] = I.d1;
         c[1] = I.d2;
@@ -167,7 +167,7 @@ struct FacePolicy {
 #pragma unroll
             for (int c = 0; c < 3; ++c) G.x[v][c] = __ldg(coords + (int64_t)g[v] * 3 + c);
     }
-    __device__ __forceinline__ static double row(const Ids& I, const Geo& G, const GhostArgs&, double& m0,
+    __device__ __forceinline__ static double row(const Ids& I, const Geo& G, const GhostArgs&, int, double& m0,
                                                  double& k0, int (&c)[3], double (&m)[3], double (&kv)[3]) {
         const int g[4] = {I.g.x, I.g.y, I.g.z, I.g.w};
         const int d[4] = {I.d.x, I.d.y, I.d.z, I.d.w};
@@ -251,49 +251,29 @@ struct FacePolicy {
     }
 };
 
-// 2D with ghost triangles (distributed assembly): every triangle loaded in
-// full (no shared-edge shortcut), a ghost's row values read from the
-// received buffer instead of computed, columns shifted by col_base.
-struct GhostTriPolicy {
-    static constexpr int M = 3;
-    static constexpr bool DEEP = false;
+// 2D with ghost triangles (distributed assembly, dist2d.cu; see above): the
+// policy runs on TriPolicy's four-stage pipeline with the shared-edge loads
+// (coordinates are loaded for every triangle -- the mesh is whole on every
+// rank -- so the second triangle completes from the first); a ghost's values,
+// rare (interface rows only), are read when its row is computed.  Columns
+// are elems2dofs + col_base.
+struct GhostDeepPolicy : TriPolicy {
     static constexpr bool GHOST = true;
-    struct Ids {
-        Tri t;
-        int e, k;
-    };
-    struct Geo {
-        double2 gv0, gv1;  // ghost: {M_kk, M_k,k+1}, {M_k,k+2, 2/|det|}
-    };
-    __device__ __forceinline__ static void load_ids(const int32_t* __restrict__ elems,
-                                                    const int32_t* __restrict__ e2d, int inst, Ids& I) {
-        tri_load_ids(elems, e2d, inst, I.t);
-        I.e = inst >> 3;
-        I.k = inst & 7;
-    }
-    __device__ __forceinline__ static void load_x(const double* __restrict__ coords, const GhostArgs& gh, Ids& I,
-                                                  Geo& G) {
-        if (I.e >= gh.base) {
-            const double2* v = reinterpret_cast<const double2*>(gh.vals + (int64_t)(I.e - gh.base) * 12 + 4 * I.k);
-            G.gv0 = __ldg(v);
-            G.gv1 = __ldg(v + 1);
-        } else {
-            tri_load_x(coords, I.t);
-        }
-    }
-    __device__ __forceinline__ static double row(const Ids& I, const Geo& G, const GhostArgs& gh, double& m0,
+    __device__ __forceinline__ static double row(const Ids& I, const Geo&, const GhostArgs& gh, int inst, double& m0,
                                                  double& k0, int (&c)[2], double (&m)[2], double (&k)[2]) {
-        c[0] = I.t.d1 + gh.col_base;
-        c[1] = I.t.d2 + gh.col_base;
-        if (I.e < gh.base) return tri_row(I.t, m0, k0, m[0], k[0], m[1], k[1]);
-        const Tri& T = I.t;
-        const bool so = T.q1 < T.q2;
-        const bool sg1 = so == (T.q2 < T.q0), sg2 = so == (T.q0 < T.q1);
-        const double ck = G.gv1.y;
-        m0 = G.gv0.x;
+        c[0] = I.d1 + gh.col_base;
+        c[1] = I.d2 + gh.col_base;
+        const int e = inst >> 3;
+        if (e < gh.base) return tri_row(I, m0, k0, m[0], k[0], m[1], k[1]);
+        const double2* v = reinterpret_cast<const double2*>(gh.vals + (int64_t)(e - gh.base) * 12 + 4 * (inst & 7));
+        const double2 gv0 = __ldg(v), gv1 = __ldg(v + 1);
+        const bool so = I.q1 < I.q2;
+        const bool sg1 = so == (I.q2 < I.q0), sg2 = so == (I.q0 < I.q1);
+        const double ck = gv1.y;
+        m0 = gv0.x;
         k0 = ck;
-        m[0] = sg1 ? G.gv0.y : -G.gv0.y;
-        m[1] = sg2 ? G.gv1.x : -G.gv1.x;
+        m[0] = sg1 ? gv0.y : -gv0.y;
+        m[1] = sg2 ? gv1.x : -gv1.x;
         k[0] = sg1 ? ck : -ck;
         k[1] = sg2 ? ck : -ck;
         return 1.0;  // (the sending rank checked the determinant)
@@ -480,8 +460,8 @@ __global__ void __launch_bounds__(TRI_TPB, MINB) k_rows_tri(const double* __rest
                 double m0a, k0a, m0b, k0b, ma[NO], ka[NO], mb[NO], kb[NO];
                 int ca[NO], cb[NO];
                 if constexpr (DEEP) P::complete2(T0, T1);
-                const double da = P::row(T0, G0, gh, m0a, k0a, ca, ma, ka);
-                const double db = P::row(T1, G1, gh, m0b, k0b, cb, mb, kb);
+                const double da = P::row(T0, G0, gh, c1.rr.x, m0a, k0a, ca, ma, ka);
+                const double db = P::row(T1, G1, gh, c1.rr.y, m0b, k0b, cb, mb, kb);
                 const bool bad_a = !(fabs(da) > 0.0 && fabs(da) < INFINITY);
                 const bool bad_b = two && !(fabs(db) > 0.0 && fabs(db) < INFINITY);
                 if (bad_a || bad_b) {
@@ -971,8 +951,8 @@ efem_status launch_rows(Plan& p, unsigned forms, efem_csr* out, const RowWindow&
         efem_status st;
         if constexpr (KT::D == 2) {
             if (w.ghost) {
-                st = w.win ? launch(k_rows_tri<KT, GhostTriPolicy, MINB, true>)
-                           : launch(k_rows_tri<KT, GhostTriPolicy, MINB, false>);
+                st = w.win ? launch(k_rows_tri<KT, GhostDeepPolicy, MINB, true>)
+                           : launch(k_rows_tri<KT, GhostDeepPolicy, MINB, false>);
                 if (st != EFEM_OK) return st;
                 EFEM_LAUNCH_CHECK();
                 return EFEM_OK;

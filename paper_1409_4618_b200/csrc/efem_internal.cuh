@@ -150,7 +150,7 @@ struct Plan {
 };
 
 // Ghost triangles of a distributed 2D assembly (dist2d.cu, assemble.cu
-// GhostTriPolicy): local triangle index e >= base is a ghost, its row values
+// GhostDeepPolicy): local triangle index e >= base is a ghost, its row values
 // at vals[(e - base) * 12 + 4 k ..]; columns are elems2dofs + col_base (with
 // a device row window: col_base = the window's global first row).
 struct GhostArgs {
@@ -173,7 +173,7 @@ struct RowWindow {
     // bound partition, asynchronous: row0 / n_rows / out_base / own_base come
     // from this device window (WsHeader::win); n_rows, cap_nnz are capacities
     const long long* win = nullptr;
-    // distributed 2D assembly: ghost triangles (GhostTriPolicy)
+    // distributed 2D assembly: ghost triangles (GhostDeepPolicy)
     bool ghost = false;
     GhostArgs gh;
 };
