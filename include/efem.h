@@ -345,7 +345,9 @@ efem_status efem_comm_init(efem_comm* comm, const unsigned char* id, int nranks,
 efem_status efem_comm_destroy(efem_comm comm);
 
 /* Setup of one rank (collective, synchronising, untimed): mesh = the whole
- * mesh in this rank's device memory (dim 2; kept by pointer), the rank's
+ * mesh in this rank's device memory (dim 2; kept by pointer: coordinates are
+ * read at every step, the connectivity at this setup -- it fixes the plan's
+ * communication pattern, so it must not change afterwards), the rank's
  * slab [elem_lo, elem_hi) of it, comm from efem_comm_init.  Computes the node
  * ranges and the communication pattern (which triangles go to which rank,
  * which column ids each rank answers) and allocates the plan's own device

@@ -435,6 +435,13 @@ efem_status finish_setup(DistPlan& D, const std::vector<int32_t>& keep, const st
     p.own_lo = D.lo[D.rank];
     p.own_n = D.lo[D.rank + 1] - D.lo[D.rank];
     p.node_ent = D.node_ent;
+    // the slab's kept triangles into the held array, once: the connectivity
+    // (and with it this setup's classification) is fixed for the plan's life;
+    // coordinates are read every step
+    if (D.n_keep > 0) {
+        k_gather_kept<<<grid_for(D.n_keep, 256), 256, 0, s>>>(D.elems, D.keep, D.n_keep, D.held);
+        EFEM_LAUNCH_CHECK();
+    }
     EFEM_CUDA_TRY(cudaStreamSynchronize(s));
     return EFEM_OK;
 }
@@ -446,10 +453,6 @@ efem_status ph_pack(DistPlan& D, cudaStream_t s) {
     // a degenerate ghost flagged by the pack survives to the check
     efem_status st = launch_hdr_reset(p, s);
     if (st != EFEM_OK) return st;
-    if (D.n_keep > 0) {
-        k_gather_kept<<<grid_for(D.n_keep, 256), 256, 0, s>>>(D.elems, D.keep, D.n_keep, D.held);
-        EFEM_LAUNCH_CHECK();
-    }
     const int64_t ns = D.send_off[D.P];
     if (ns > 0) {
         k_ghost_pack<<<grid_for(ns, 256), 256, 0, s>>>(D.coords, D.elems, D.send_tris, ns, D.sendA, p.hdr);
