@@ -119,19 +119,33 @@ __global__ void __launch_bounds__(256) k_fan_fill_fixed(const int32_t* __restric
                                                         int32_t* __restrict__ cnt, int32_t* __restrict__ fan_fix,
                                                         WsHeader* hdr) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= n_elems) return;
-    int p = __ldg(elems + 3 * e), q = __ldg(elems + 3 * e + 1), r = __ldg(elems + 3 * e + 2);
-    if (invalid_node(p, n_nodes) || invalid_node(q, n_nodes) || invalid_node(r, n_nodes)) {
-        atomicOr(&hdr->flags[F_INVALID_NODE], 1);
-        return;
+    // lanes 2i, 2i+1 whose triangles share their smallest vertex (the two
+    // triangles of a structured cell) take their two slots there with one
+    // atomic; slot order inside a fan is immaterial (k_fan_nodes sorts)
+    bool ok = e < n_elems;
+    int p = 0, q = 0, r = 0;
+    if (ok) {
+        p = __ldg(elems + 3 * e);
+        q = __ldg(elems + 3 * e + 1);
+        r = __ldg(elems + 3 * e + 2);
+        if (invalid_node(p, n_nodes) || invalid_node(q, n_nodes) || invalid_node(r, n_nodes)) {
+            atomicOr(&hdr->flags[F_INVALID_NODE], 1);
+            ok = false;
+        }
     }
     sort3(p, q, r);
     const int64_t lp = p - lo, lq = q - lo;
-    const bool op = (unsigned long long)lp < (unsigned long long)n_own;
-    const bool oq = q != p && (unsigned long long)lq < (unsigned long long)n_own;
+    const bool op = ok && (unsigned long long)lp < (unsigned long long)n_own;
+    const bool oq = ok && q != p && (unsigned long long)lq < (unsigned long long)n_own;
+    const int lane = threadIdx.x & 31;
+    const int kp = op ? (int)lp : -1 - lane;  // (never equal across lanes unless both own p)
+    const bool pair = __shfl_xor_sync(0xffffffffu, kp, 1) == kp;
+    int base = 0;
+    if (pair && !(lane & 1)) base = atomicAdd(cnt + lp, 2);
+    base = __shfl_xor_sync(0xffffffffu, base, 1) + base;  // (the even lane's value; the odd lane's is 0)
     bool over = false;
     if (op) {
-        const int k = atomicAdd(cnt + lp, 1);
+        const int k = pair ? base + (lane & 1) : atomicAdd(cnt + lp, 1);
         if (k < C) fan_fix[lp * C + k] = (int)e;
         else over = true;
     }
@@ -403,6 +417,20 @@ __global__ void __launch_bounds__(FAN_TPB, EFEM_FAN_MINB) k_fan_nodes(FanNodesAr
     const bool csr = s_csr;  // (uniform over the launch)
     int32_t* const fbase = csr ? A.fan : A.fan_fix;
     if (live) {
+        // fixed slots of this launch's width: all FR slots as 16-byte loads,
+        // issued with the count load (slots past the count are ignored)
+        const bool vec = !csr && A.fix_c == FR;
+        if (vec) {
+            const int4* p4 = reinterpret_cast<const int4*>(A.fan_fix + l64 * FR);
+#pragma unroll
+            for (int q = 0; q < FR / 4; ++q) {
+                const int4 v = __ldg(p4 + q);
+                ev[4 * q] = v.x;
+                ev[4 * q + 1] = v.y;
+                ev[4 * q + 2] = v.z;
+                ev[4 * q + 3] = v.w;
+            }
+        }
         if (csr) {
             beg = __ldg(A.fan_ptr + l64);
             n = __ldg(A.fan_ptr + l64 + 1) - beg;
@@ -413,8 +441,10 @@ __global__ void __launch_bounds__(FAN_TPB, EFEM_FAN_MINB) k_fan_nodes(FanNodesAr
         slow = n > FR;
         if (n > FAN_SMALL) s_big = 1;  // (for the next launch's choice of FR)
         if (!slow) {
+            if (!vec) {
 #pragma unroll
-            for (int j = 0; j < FR; ++j) ev[j] = j < n ? fbase[beg + j] : 0;
+                for (int j = 0; j < FR; ++j) ev[j] = j < n ? fbase[beg + j] : 0;
+            }
 #pragma unroll
             for (int j = 0; j < FR; ++j)
                 if (j < n) s_ev[j * FAN_TPB + threadIdx.x] = ev[j];
