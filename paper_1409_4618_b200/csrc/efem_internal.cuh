@@ -32,7 +32,6 @@ struct WsHeader {
     // device: first local row, rows, local CSR offset of the first row,
     // entries, global id of the first row
     long long win[6];
-    int tile_ticket;  // dynamic tile ids of the look-back scans (fan2d.cu)
     int fan_big;      // the last fan pass saw a node fan of > FAN_SMALL triangles (fan2d.cu)
 };
 

@@ -384,37 +384,29 @@ __device__ __forceinline__ void key_runs(const unsigned (&key)[K2], const int* s
 
 template <int FR>
 __global__ void __launch_bounds__(FAN_TPB, EFEM_FAN_MINB) k_fan_nodes(FanNodesArgs A) {
-    using BlockScan = cub::BlockScan<unsigned long long, FAN_TPB>;
+    using BlockScan = cub::BlockScan<unsigned long long, FAN_TPB, cub::BLOCK_SCAN_WARP_SCANS>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
-    __shared__ int s_tile;
     __shared__ unsigned long long s_excl;
     __shared__ int2 s_rec[FAN_REC_STAGE];
     __shared__ int s_inc[FAN_REC_STAGE];
     __shared__ int s_ev[FR * FAN_TPB];  // the fan's element ids, [j * FAN_TPB + thread]
-    __shared__ int s_big;
-    __shared__ int s_csr;
-    if (threadIdx.x == 0) {
-        s_tile = atomicAdd(&A.hdr->tile_ticket, 1);
-        s_big = 0;
-        // fans: fixed-capacity slots, or (no capacity / an overflow) the
-        // counting-sort fans.  (Read once per CTA: one header word read by
-        // every warp queues its requests at one L2 slice.)
-        s_csr = A.fix_c == 0 || *(volatile const int*)&A.hdr->flags[F_FAN_OVER];
-    }
-    __syncthreads();
-    const int tile = s_tile;
+    // tiles in launch order (CTAs are dispatched in blockIdx order, so every
+    // predecessor a tile waits on is resident or done -- as CUB's single-pass
+    // scans); the overflow flag through the read-only path (one L1 line per
+    // SM): no ticket round trip and no barrier before the loads
+    const int tile = blockIdx.x;
+    const bool csr = A.fix_c == 0 || __ldg(&A.hdr->flags[F_FAN_OVER]);
     const int64_t l64 = (int64_t)tile * FAN_TPB + threadIdx.x;  // owned node index
     const bool live = l64 < A.n_nodes;
     const int a = (int)(A.lo + l64);
     int n_ent = 0, n_inst = 0, beg = 0, n = 0;
-    bool bad = false, slow = false;
+    bool bad = false, slow = false, big = false;
     unsigned key[2 * FR];
     int ev[FR];
 #pragma unroll
     for (int x = 0; x < 2 * FR; ++x) key[x] = KEY_NONE;
 #pragma unroll
     for (int j = 0; j < FR; ++j) ev[j] = 0;
-    const bool csr = s_csr;  // (uniform over the launch)
     int32_t* const fbase = csr ? A.fan : A.fan_fix;
     if (live) {
         // fixed slots of this launch's width: all FR slots as 16-byte loads,
@@ -439,7 +431,7 @@ __global__ void __launch_bounds__(FAN_TPB, EFEM_FAN_MINB) k_fan_nodes(FanNodesAr
             n = __ldg(A.cnt + l64);
         }
         slow = n > FR;
-        if (n > FAN_SMALL) s_big = 1;  // (for the next launch's choice of FR)
+        big = n > FAN_SMALL;  // (for the next launch's choice of FR)
         if (!slow) {
             if (!vec) {
 #pragma unroll
@@ -522,7 +514,8 @@ __global__ void __launch_bounds__(FAN_TPB, EFEM_FAN_MINB) k_fan_nodes(FanNodesAr
         if (threadIdx.x == 0) s_excl = excl;
     }
     __syncthreads();
-    if (threadIdx.x == 0 && s_big && !__ldg(&A.hdr->fan_big)) atomicOr(&A.hdr->fan_big, 1);
+    if (__any_sync(0xffffffffu, big) && (threadIdx.x & 31) == 0 && !__ldg(&A.hdr->fan_big))
+        atomicOr(&A.hdr->fan_big, 1);
     const unsigned long long base = s_excl;
     const int e_tile0 = (int)(base >> 31), i_tile0 = (int)(base & 0x7fffffffull);
     const int e_off = (int)(off >> 31);
@@ -578,7 +571,6 @@ __global__ void k_fan_init(WsHeader* hdr) {
         hdr->bad_element = ~0ull;
         hdr->totals[0] = 0;
         hdr->totals[1] = 0;
-        hdr->tile_ticket = 0;
         hdr->fan_big = 0;
     }
 }
@@ -599,9 +591,7 @@ efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset) {
     if (reset) {
         k_fan_init<<<1, 32, 0, s>>>(p.hdr);
         EFEM_LAUNCH_CHECK();
-    } else {  // (the caller reset the header; the look-back ticket restarts here)
-        EFEM_CUDA_TRY(cudaMemsetAsync(&p.hdr->tile_ticket, 0, 4, s));
-    }
+    }  // (else the caller reset the header)
     const int ntiles = (int)grid_for(N, FAN_TPB);
     if (ntiles > 0) EFEM_CUDA_TRY(cudaMemsetAsync(p.fan_tiles, 0, (size_t)ntiles * 8, s));
 #ifndef EFEM_FAN_FIXED
