@@ -12,7 +12,8 @@
 //
 //   k_fan_fill_fixed     per triangle (p < q < r): one atomic at p and at q,
 //                        whose return value is the slot of the triangle id
-//                        in the node's C fixed fan slots (C = 4 or 8)
+//                        in the node's C fixed fan slots (C = 4 or 8); two
+//                        triangles per thread, one atomic for a shared p
 //   (fallback)           only when a fan overflows C (F_FAN_OVER): a scan
 //                        of the counts -> fan_ptr and the counting-sort
 //                        fill (k_cscan_*, k_fan_fill_cond: they exit at
@@ -113,47 +114,57 @@ __global__ void __launch_bounds__(256) k_fan_bucket(const int32_t* __restrict__ 
 // in the fan pass made its loads wait on the stores, 0.67 -> 1.55 ms; the
 // fallback's fill counts them down to zero).
 // ---------------------------------------------------------------------------------
+// two consecutive triangles per thread (24 contiguous bytes, three 8-byte
+// loads when the element array is 8-byte aligned); a shared smallest vertex
+// takes both slots with one atomic
+template <int C>
+__device__ __forceinline__ void fill_put(int32_t* __restrict__ fan_fix, int64_t l, int k, int e, bool& over) {
+    if (k < C) fan_fix[l * C + k] = e;
+    else over = true;
+}
 template <int C>
 __global__ void __launch_bounds__(256) k_fan_fill_fixed(const int32_t* __restrict__ elems, int64_t n_elems,
-                                                        int64_t n_nodes, int64_t lo, int64_t n_own,
-                                                        int32_t* __restrict__ cnt, int32_t* __restrict__ fan_fix,
-                                                        WsHeader* hdr) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    // lanes 2i, 2i+1 whose triangles share their smallest vertex (the two
-    // triangles of a structured cell) take their two slots there with one
-    // atomic; slot order inside a fan is immaterial (k_fan_nodes sorts)
-    bool ok = e < n_elems;
-    int p = 0, q = 0, r = 0;
-    if (ok) {
-        p = __ldg(elems + 3 * e);
-        q = __ldg(elems + 3 * e + 1);
-        r = __ldg(elems + 3 * e + 2);
-        if (invalid_node(p, n_nodes) || invalid_node(q, n_nodes) || invalid_node(r, n_nodes)) {
-            atomicOr(&hdr->flags[F_INVALID_NODE], 1);
-            ok = false;
-        }
+                                                         int64_t n_nodes, int64_t lo, int64_t n_own,
+                                                         int32_t* __restrict__ cnt, int32_t* __restrict__ fan_fix,
+                                                         WsHeader* hdr) {
+    const int64_t e0 = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    if (e0 >= n_elems) return;
+    int v[6];
+    const bool two = e0 + 1 < n_elems;
+    if (two && !(reinterpret_cast<uintptr_t>(elems) & 7)) {
+        const int2* p2 = reinterpret_cast<const int2*>(elems + 3 * e0);
+        const int2 x = __ldg(p2), y = __ldg(p2 + 1), z = __ldg(p2 + 2);
+        v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y; v[4] = z.x; v[5] = z.y;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 6; ++j) v[j] = (j < 3 || two) ? __ldg(elems + 3 * e0 + j) : 0;
     }
-    sort3(p, q, r);
-    const int64_t lp = p - lo, lq = q - lo;
-    const bool op = ok && (unsigned long long)lp < (unsigned long long)n_own;
-    const bool oq = ok && q != p && (unsigned long long)lq < (unsigned long long)n_own;
-    const int lane = threadIdx.x & 31;
-    const int kp = op ? (int)lp : -1 - lane;  // (never equal across lanes unless both own p)
-    const bool pair = __shfl_xor_sync(0xffffffffu, kp, 1) == kp;
-    int base = 0;
-    if (pair && !(lane & 1)) base = atomicAdd(cnt + lp, 2);
-    base = __shfl_xor_sync(0xffffffffu, base, 1) + base;  // (the even lane's value; the odd lane's is 0)
+    bool ok0 = !(invalid_node(v[0], n_nodes) || invalid_node(v[1], n_nodes) || invalid_node(v[2], n_nodes));
+    bool ok1 = two && !(invalid_node(v[3], n_nodes) || invalid_node(v[4], n_nodes) || invalid_node(v[5], n_nodes));
+    if (!ok0 || (two && !ok1)) atomicOr(&hdr->flags[F_INVALID_NODE], 1);
+    sort3(v[0], v[1], v[2]);
+    sort3(v[3], v[4], v[5]);
+    const int64_t lp0 = v[0] - lo, lq0 = v[1] - lo, lp1 = v[3] - lo, lq1 = v[4] - lo;
+    const bool op0 = ok0 && (unsigned long long)lp0 < (unsigned long long)n_own;
+    const bool oq0 = ok0 && v[1] != v[0] && (unsigned long long)lq0 < (unsigned long long)n_own;
+    const bool op1 = ok1 && (unsigned long long)lp1 < (unsigned long long)n_own;
+    const bool oq1 = ok1 && v[4] != v[3] && (unsigned long long)lq1 < (unsigned long long)n_own;
+    const bool pair = op0 && op1 && lp0 == lp1;
+    int kp0 = 0, kp1 = 0, kq0 = 0, kq1 = 0;
+    if (pair) {
+        kp0 = atomicAdd(cnt + lp0, 2);
+        kp1 = kp0 + 1;
+    } else {
+        if (op0) kp0 = atomicAdd(cnt + lp0, 1);
+        if (op1) kp1 = atomicAdd(cnt + lp1, 1);
+    }
+    if (oq0) kq0 = atomicAdd(cnt + lq0, 1);
+    if (oq1) kq1 = atomicAdd(cnt + lq1, 1);
     bool over = false;
-    if (op) {
-        const int k = pair ? base + (lane & 1) : atomicAdd(cnt + lp, 1);
-        if (k < C) fan_fix[lp * C + k] = (int)e;
-        else over = true;
-    }
-    if (oq) {
-        const int k = atomicAdd(cnt + lq, 1);
-        if (k < C) fan_fix[lq * C + k] = (int)e;
-        else over = true;
-    }
+    if (op0) fill_put<C>(fan_fix, lp0, kp0, (int)e0, over);
+    if (op1) fill_put<C>(fan_fix, lp1, kp1, (int)e0 + 1, over);
+    if (oq0) fill_put<C>(fan_fix, lq0, kq0, (int)e0, over);
+    if (oq1) fill_put<C>(fan_fix, lq1, kq1, (int)e0 + 1, over);
     if (over) atomicOr(&hdr->flags[F_FAN_OVER], 1);
 }
 
@@ -604,9 +615,10 @@ efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset) {
         EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (size_t)N * 4, s));
         if (T > 0) {
             if (fix_c == 4)
-                k_fan_fill_fixed<4><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix, p.hdr);
+                k_fan_fill_fixed<4><<<grid_for((T + 1) / 2, 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
+                                                                                p.hdr);
             else
-                k_fan_fill_fixed<FAN_FIXC><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
+                k_fan_fill_fixed<FAN_FIXC><<<grid_for((T + 1) / 2, 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
                                                                               p.hdr);
             EFEM_LAUNCH_CHECK();
         }
