@@ -393,106 +393,132 @@ __device__ __forceinline__ void key_runs(const unsigned (&key)[K2], const int* s
     if (t) row(first, last, t);
 }
 
+#ifndef EFEM_FAN_NPT
+#define EFEM_FAN_NPT 1
+#endif
+#ifndef EFEM_FAN_MINB2
+#define EFEM_FAN_MINB2 8
+#endif
+constexpr int FAN_NPT = EFEM_FAN_NPT;  // owned nodes per thread (blocked: thread x holds nodes NPT x .. NPT x + NPT - 1)
+constexpr int FAN_TILE = FAN_TPB * FAN_NPT;
+
 template <int FR>
-__global__ void __launch_bounds__(FAN_TPB, EFEM_FAN_MINB) k_fan_nodes(FanNodesArgs A) {
+__global__ void __launch_bounds__(FAN_TPB, FAN_NPT == 1 ? EFEM_FAN_MINB : EFEM_FAN_MINB2) k_fan_nodes(FanNodesArgs A) {
+    constexpr int NPT = FAN_NPT;
     using BlockScan = cub::BlockScan<unsigned long long, FAN_TPB, cub::BLOCK_SCAN_WARP_SCANS>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
     __shared__ unsigned long long s_excl;
-    __shared__ int2 s_rec[FAN_REC_STAGE];
-    __shared__ int s_inc[FAN_REC_STAGE];
-    __shared__ int s_ev[FR * FAN_TPB];  // the fan's element ids, [j * FAN_TPB + thread]
+    __shared__ int2 s_rec[FAN_REC_STAGE * NPT];
+    __shared__ int s_inc[FAN_REC_STAGE * NPT];
+    __shared__ int s_ev[NPT * FR * FAN_TPB];  // the fans' element ids, [(h FR + j) FAN_TPB + thread]
     // tiles in launch order (CTAs are dispatched in blockIdx order, so every
     // predecessor a tile waits on is resident or done -- as CUB's single-pass
     // scans); the overflow flag through the read-only path (one L1 line per
     // SM): no ticket round trip and no barrier before the loads
     const int tile = blockIdx.x;
     const bool csr = A.fix_c == 0 || __ldg(&A.hdr->flags[F_FAN_OVER]);
-    const int64_t l64 = (int64_t)tile * FAN_TPB + threadIdx.x;  // owned node index
-    const bool live = l64 < A.n_nodes;
-    const int a = (int)(A.lo + l64);
-    int n_ent = 0, n_inst = 0, beg = 0, n = 0;
-    bool bad = false, slow = false, big = false;
-    unsigned key[2 * FR];
-    int ev[FR];
+    const int64_t l0 = (int64_t)tile * FAN_TILE + (int64_t)threadIdx.x * NPT;  // first owned node index
+    int n_ent[NPT], n_inst[NPT], beg[NPT], n[NPT];
+    bool slow[NPT];
+    bool bad = false, big = false;
+    unsigned key[NPT][2 * FR];
+    int ev[NPT][FR];
 #pragma unroll
-    for (int x = 0; x < 2 * FR; ++x) key[x] = KEY_NONE;
+    for (int h = 0; h < NPT; ++h) {
+        n_ent[h] = n_inst[h] = beg[h] = n[h] = 0;
+        slow[h] = false;
 #pragma unroll
-    for (int j = 0; j < FR; ++j) ev[j] = 0;
+        for (int x = 0; x < 2 * FR; ++x) key[h][x] = KEY_NONE;
+#pragma unroll
+        for (int j = 0; j < FR; ++j) ev[h][j] = 0;
+    }
     int32_t* const fbase = csr ? A.fan : A.fan_fix;
-    if (live) {
-        // fixed slots of this launch's width: all FR slots as 16-byte loads,
-        // issued with the count load (slots past the count are ignored)
-        const bool vec = !csr && A.fix_c == FR;
-        if (vec) {
-            const int4* p4 = reinterpret_cast<const int4*>(A.fan_fix + l64 * FR);
+    // fixed slots of this launch's width: all FR slots as 16-byte loads,
+    // issued with the count load (slots past the count are ignored)
+    const bool vec = !csr && A.fix_c == FR;
 #pragma unroll
-            for (int q = 0; q < FR / 4; ++q) {
-                const int4 v = __ldg(p4 + q);
-                ev[4 * q] = v.x;
-                ev[4 * q + 1] = v.y;
-                ev[4 * q + 2] = v.z;
-                ev[4 * q + 3] = v.w;
+    for (int h = 0; h < NPT; ++h) {
+        const int64_t l64 = l0 + h;
+        if (l64 < A.n_nodes) {
+            if (vec) {
+                const int4* p4 = reinterpret_cast<const int4*>(A.fan_fix + l64 * FR);
+#pragma unroll
+                for (int q = 0; q < FR / 4; ++q) {
+                    const int4 v = __ldg(p4 + q);
+                    ev[h][4 * q] = v.x;
+                    ev[h][4 * q + 1] = v.y;
+                    ev[h][4 * q + 2] = v.z;
+                    ev[h][4 * q + 3] = v.w;
+                }
+            }
+            if (csr) {
+                beg[h] = __ldg(A.fan_ptr + l64);
+                n[h] = __ldg(A.fan_ptr + l64 + 1) - beg[h];
+            } else {
+                beg[h] = (int)l64 * A.fix_c;
+                n[h] = __ldg(A.cnt + l64);
             }
         }
-        if (csr) {
-            beg = __ldg(A.fan_ptr + l64);
-            n = __ldg(A.fan_ptr + l64 + 1) - beg;
-        } else {
-            beg = (int)l64 * A.fix_c;
-            n = __ldg(A.cnt + l64);
-        }
-        slow = n > FR;
-        big = n > FAN_SMALL;  // (for the next launch's choice of FR)
-        if (!slow) {
+    }
+#pragma unroll
+    for (int h = 0; h < NPT; ++h) {
+        const int64_t l64 = l0 + h;
+        if (l64 >= A.n_nodes) continue;
+        const int a = (int)(A.lo + l64);
+        const int nh = n[h];
+        slow[h] = nh > FR;
+        big |= nh > FAN_SMALL;  // (for the next launch's choice of FR)
+        if (!slow[h]) {
             if (!vec) {
 #pragma unroll
-                for (int j = 0; j < FR; ++j) ev[j] = j < n ? fbase[beg + j] : 0;
+                for (int j = 0; j < FR; ++j) ev[h][j] = j < nh ? fbase[beg[h] + j] : 0;
             }
 #pragma unroll
             for (int j = 0; j < FR; ++j)
-                if (j < n) s_ev[j * FAN_TPB + threadIdx.x] = ev[j];
+                if (j < nh) s_ev[(h * FR + j) * FAN_TPB + threadIdx.x] = ev[h][j];
 #pragma unroll
             for (int j = 0; j < FR; ++j) {
-                if (j < n) {
+                if (j < nh) {
                     int g0, g1, g2;
-                    load_tri(A.elems, ev[j], g0, g1, g2);
+                    load_tri(A.elems, ev[h][j], g0, g1, g2);
                     const int la = g0 == a ? 0 : (g1 == a ? 1 : 2);
                     const int w1 = la == 0 ? 1 : 0, w2 = la == 2 ? 1 : 2;  // the two other positions
                     const int v1 = w1 == 0 ? g0 : g1, v2 = w2 == 1 ? g1 : g2;
                     // (a vertex id above a by 2^27 or more takes the slow path)
-                    slow |= (v1 > a && v1 - a >= KEY_DMAX) || (v2 > a && v2 - a >= KEY_DMAX);
-                    if (v1 > a) key[2 * j] = ((unsigned)(v1 - a) << 5) | (j << 2) | (unsigned)(3 - la - w1);
-                    if (v2 > a) key[2 * j + 1] = ((unsigned)(v2 - a) << 5) | (j << 2) | (unsigned)(3 - la - w2);
+                    slow[h] |= (v1 > a && v1 - a >= KEY_DMAX) || (v2 > a && v2 - a >= KEY_DMAX);
+                    if (v1 > a) key[h][2 * j] = ((unsigned)(v1 - a) << 5) | (j << 2) | (unsigned)(3 - la - w1);
+                    if (v2 > a) key[h][2 * j + 1] = ((unsigned)(v2 - a) << 5) | (j << 2) | (unsigned)(3 - la - w2);
                 }
             }
         }
-        if (!slow) {
+        if (!slow[h]) {
             auto count = [&](auto cmax) {
                 constexpr int CM = decltype(cmax)::value;
-                sort_keys<CM>(key);
+                sort_keys<CM>(key[h]);
 #pragma unroll
                 for (int x = 0; x < CM; ++x) {
-                    const bool v = key[x] != KEY_NONE;
-                    n_inst += v;
-                    n_ent += v && (x == 0 || (key[x] >> 5) != (key[x - 1] >> 5));
-                    if (x >= 2) bad |= v && (key[x] >> 5) == (key[x - 2] >> 5);  // an edge in three triangles
+                    const bool v = key[h][x] != KEY_NONE;
+                    n_inst[h] += v;
+                    n_ent[h] += v && (x == 0 || (key[h][x] >> 5) != (key[h][x - 1] >> 5));
+                    if (x >= 2) bad |= v && (key[h][x] >> 5) == (key[h][x - 2] >> 5);  // an edge in three triangles
                 }
             };
-            if (n <= FR / 2) count(std::integral_constant<int, FR>{});
+            if (nh <= FR / 2) count(std::integral_constant<int, FR>{});
             else count(std::integral_constant<int, 2 * FR>{});
         } else {
-            fan_sort_inplace(fbase + beg, n);
-            fan_edges_slow(A.elems, fbase + beg, a, n, [&](int, int, int, int t) {
-                ++n_ent;
-                n_inst += t;
+            fan_sort_inplace(fbase + beg[h], nh);
+            fan_edges_slow(A.elems, fbase + beg[h], a, nh, [&](int, int, int, int t) {
+                ++n_ent[h];
+                n_inst[h] += t;
                 bad |= t > 2;
             });
         }
-        if (bad) atomicOr(&A.hdr->flags[F_ROW_MISMATCH], 1);
     }
+    if (bad) atomicOr(&A.hdr->flags[F_ROW_MISMATCH], 1);
     // tile prefix of (entities << 31 | instances)
-    const unsigned long long mine = ((unsigned long long)n_ent << 31) | (unsigned long long)n_inst;
-    unsigned long long off, agg;
+    unsigned long long mine[NPT], off[NPT], agg;
+#pragma unroll
+    for (int h = 0; h < NPT; ++h) mine[h] = ((unsigned long long)n_ent[h] << 31) | (unsigned long long)n_inst[h];
     BlockScan(scan_tmp).ExclusiveSum(mine, off, agg);
     if (threadIdx.x < 32) {
         // decoupled look-back (warp 0): publish the aggregate, sum the
@@ -529,12 +555,15 @@ __global__ void __launch_bounds__(FAN_TPB, EFEM_FAN_MINB) k_fan_nodes(FanNodesAr
         atomicOr(&A.hdr->fan_big, 1);
     const unsigned long long base = s_excl;
     const int e_tile0 = (int)(base >> 31), i_tile0 = (int)(base & 0x7fffffffull);
-    const int e_off = (int)(off >> 31);
     const int e_tot = (int)(agg >> 31);
-    const bool stage = e_tot <= FAN_REC_STAGE;
-    if (live) {
-        int id = e_tile0 + e_off;  // first DOF of node a
-        int inst = i_tile0 + (int)(off & 0x7fffffffull);
+    const bool stage = e_tot <= FAN_REC_STAGE * NPT;
+#pragma unroll
+    for (int h = 0; h < NPT; ++h) {
+        const int64_t l64 = l0 + h;
+        if (l64 >= A.n_nodes) continue;
+        const int a = (int)(A.lo + l64);
+        int id = e_tile0 + (int)(off[h] >> 31);  // first DOF of node a
+        int inst = i_tile0 + (int)(off[h] & 0x7fffffffull);
         if (A.node_ent) A.node_ent[l64] = id;
         auto row = [&](int first, int last, int t) {
             if (stage) {
@@ -549,11 +578,12 @@ __global__ void __launch_bounds__(FAN_TPB, EFEM_FAN_MINB) k_fan_nodes(FanNodesAr
             ++id;
             inst += t;
         };
-        if (!slow) {
-            if (n <= FR / 2) key_runs<FR>(key, s_ev + threadIdx.x, row);
-            else key_runs<2 * FR>(key, s_ev + threadIdx.x, row);
+        if (!slow[h]) {
+            const int* sev = s_ev + h * FR * FAN_TPB + threadIdx.x;
+            if (n[h] <= FR / 2) key_runs<FR>(key[h], sev, row);
+            else key_runs<2 * FR>(key[h], sev, row);
         } else {
-            fan_edges_slow(A.elems, fbase + beg, a, n,
+            fan_edges_slow(A.elems, fbase + beg[h], a, n[h],
                            [&](int, int first, int last, int t) { row(first, last, min(t, 2)); });
         }
         if (l64 == A.n_nodes - 1) {
@@ -603,7 +633,7 @@ efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset) {
         k_fan_init<<<1, 32, 0, s>>>(p.hdr);
         EFEM_LAUNCH_CHECK();
     }  // (else the caller reset the header)
-    const int ntiles = (int)grid_for(N, FAN_TPB);
+    const int ntiles = (int)grid_for(N, FAN_TILE);
     if (ntiles > 0) EFEM_CUDA_TRY(cudaMemsetAsync(p.fan_tiles, 0, (size_t)ntiles * 8, s));
 #ifndef EFEM_FAN_FIXED
 #define EFEM_FAN_FIXED 1
