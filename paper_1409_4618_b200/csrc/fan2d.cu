@@ -114,9 +114,14 @@ __global__ void __launch_bounds__(256) k_fan_bucket(const int32_t* __restrict__ 
 // in the fan pass made its loads wait on the stores, 0.67 -> 1.55 ms; the
 // fallback's fill counts them down to zero).
 // ---------------------------------------------------------------------------------
-// two consecutive triangles per thread (24 contiguous bytes, three 8-byte
-// loads when the element array is 8-byte aligned); a shared smallest vertex
-// takes both slots with one atomic
+// 2 NP consecutive triangles per thread (NP pairs; 24 NP contiguous bytes
+// as 8- or 16-byte loads when the element array is aligned), all atomics
+// issued before the slot stores; the two triangles of a pair sharing their
+// smallest vertex (a structured cell) take both slots with one atomic
+#ifndef EFEM_FILL_NP
+#define EFEM_FILL_NP 1
+#endif
+constexpr int FILL_NP = EFEM_FILL_NP;
 template <int C>
 __device__ __forceinline__ void fill_put(int32_t* __restrict__ fan_fix, int64_t l, int k, int e, bool& over) {
     if (k < C) fan_fix[l * C + k] = e;
@@ -127,44 +132,66 @@ __global__ void __launch_bounds__(256) k_fan_fill_fixed(const int32_t* __restric
                                                          int64_t n_nodes, int64_t lo, int64_t n_own,
                                                          int32_t* __restrict__ cnt, int32_t* __restrict__ fan_fix,
                                                          WsHeader* hdr) {
-    const int64_t e0 = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    constexpr int NP = FILL_NP, NT = 2 * NP;
+    const int64_t e0 = NT * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
     if (e0 >= n_elems) return;
-    int v[6];
-    const bool two = e0 + 1 < n_elems;
-    if (two && !(reinterpret_cast<uintptr_t>(elems) & 7)) {
+    int v[3 * NT];
+    const bool full = e0 + NT <= n_elems;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(elems);
+    if (full && NT % 4 == 0 && !(al & 15)) {
+        const int4* p4 = reinterpret_cast<const int4*>(elems + 3 * e0);
+#pragma unroll
+        for (int q = 0; q < 3 * NT / 4; ++q) {
+            const int4 x = __ldg(p4 + q);
+            v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+        }
+    } else if (full && !(al & 7)) {
         const int2* p2 = reinterpret_cast<const int2*>(elems + 3 * e0);
-        const int2 x = __ldg(p2), y = __ldg(p2 + 1), z = __ldg(p2 + 2);
-        v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y; v[4] = z.x; v[5] = z.y;
+#pragma unroll
+        for (int q = 0; q < 3 * NT / 2; ++q) {
+            const int2 x = __ldg(p2 + q);
+            v[2 * q] = x.x; v[2 * q + 1] = x.y;
+        }
     } else {
 #pragma unroll
-        for (int j = 0; j < 6; ++j) v[j] = (j < 3 || two) ? __ldg(elems + 3 * e0 + j) : 0;
+        for (int j = 0; j < 3 * NT; ++j) v[j] = e0 + j / 3 < n_elems ? __ldg(elems + 3 * e0 + j) : 0;
     }
-    bool ok0 = !(invalid_node(v[0], n_nodes) || invalid_node(v[1], n_nodes) || invalid_node(v[2], n_nodes));
-    bool ok1 = two && !(invalid_node(v[3], n_nodes) || invalid_node(v[4], n_nodes) || invalid_node(v[5], n_nodes));
-    if (!ok0 || (two && !ok1)) atomicOr(&hdr->flags[F_INVALID_NODE], 1);
-    sort3(v[0], v[1], v[2]);
-    sort3(v[3], v[4], v[5]);
-    const int64_t lp0 = v[0] - lo, lq0 = v[1] - lo, lp1 = v[3] - lo, lq1 = v[4] - lo;
-    const bool op0 = ok0 && (unsigned long long)lp0 < (unsigned long long)n_own;
-    const bool oq0 = ok0 && v[1] != v[0] && (unsigned long long)lq0 < (unsigned long long)n_own;
-    const bool op1 = ok1 && (unsigned long long)lp1 < (unsigned long long)n_own;
-    const bool oq1 = ok1 && v[4] != v[3] && (unsigned long long)lq1 < (unsigned long long)n_own;
-    const bool pair = op0 && op1 && lp0 == lp1;
-    int kp0 = 0, kp1 = 0, kq0 = 0, kq1 = 0;
-    if (pair) {
-        kp0 = atomicAdd(cnt + lp0, 2);
-        kp1 = kp0 + 1;
-    } else {
-        if (op0) kp0 = atomicAdd(cnt + lp0, 1);
-        if (op1) kp1 = atomicAdd(cnt + lp1, 1);
+    bool inval = false;
+    bool op[NT], oq[NT];
+    int64_t lp[NT], lq[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+        const bool in = e0 + i < n_elems;
+        const bool ok = in && !(invalid_node(v[3 * i], n_nodes) || invalid_node(v[3 * i + 1], n_nodes) ||
+                                invalid_node(v[3 * i + 2], n_nodes));
+        inval |= in && !ok;
+        sort3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+        lp[i] = v[3 * i] - lo;
+        lq[i] = v[3 * i + 1] - lo;
+        op[i] = ok && (unsigned long long)lp[i] < (unsigned long long)n_own;
+        oq[i] = ok && v[3 * i + 1] != v[3 * i] && (unsigned long long)lq[i] < (unsigned long long)n_own;
     }
-    if (oq0) kq0 = atomicAdd(cnt + lq0, 1);
-    if (oq1) kq1 = atomicAdd(cnt + lq1, 1);
+    if (inval) atomicOr(&hdr->flags[F_INVALID_NODE], 1);
+    int kp[NT], kq[NT];
+#pragma unroll
+    for (int i = 0; i < NT; i += 2) {
+        kp[i] = kp[i + 1] = 0;
+        if (op[i] && op[i + 1] && lp[i] == lp[i + 1]) {
+            kp[i] = atomicAdd(cnt + lp[i], 2);
+            kp[i + 1] = kp[i] + 1;
+        } else {
+            if (op[i]) kp[i] = atomicAdd(cnt + lp[i], 1);
+            if (op[i + 1]) kp[i + 1] = atomicAdd(cnt + lp[i + 1], 1);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NT; ++i) kq[i] = oq[i] ? atomicAdd(cnt + lq[i], 1) : 0;
     bool over = false;
-    if (op0) fill_put<C>(fan_fix, lp0, kp0, (int)e0, over);
-    if (op1) fill_put<C>(fan_fix, lp1, kp1, (int)e0 + 1, over);
-    if (oq0) fill_put<C>(fan_fix, lq0, kq0, (int)e0, over);
-    if (oq1) fill_put<C>(fan_fix, lq1, kq1, (int)e0 + 1, over);
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+        if (op[i]) fill_put<C>(fan_fix, lp[i], kp[i], (int)e0 + i, over);
+        if (oq[i]) fill_put<C>(fan_fix, lq[i], kq[i], (int)e0 + i, over);
+    }
     if (over) atomicOr(&hdr->flags[F_FAN_OVER], 1);
 }
 
@@ -645,10 +672,10 @@ efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset) {
         EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (size_t)N * 4, s));
         if (T > 0) {
             if (fix_c == 4)
-                k_fan_fill_fixed<4><<<grid_for((T + 1) / 2, 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
+                k_fan_fill_fixed<4><<<grid_for((T + 2 * FILL_NP - 1) / (2 * FILL_NP), 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
                                                                                 p.hdr);
             else
-                k_fan_fill_fixed<FAN_FIXC><<<grid_for((T + 1) / 2, 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
+                k_fan_fill_fixed<FAN_FIXC><<<grid_for((T + 2 * FILL_NP - 1) / (2 * FILL_NP), 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
                                                                               p.hdr);
             EFEM_LAUNCH_CHECK();
         }
