@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(256) k_fan_fill_cond(const int32_t* __restrict
         fan_bucket_one<true>(elems, e, n_nodes, lo, n_own, cnt, fan_ptr, fan, hdr);
 }
 
-// the fallback's exclusive scan cnt[0, n) -> ptr[0, n] (three kernels over
+// the fallback's exclusive scan cnt[0, n) -> ptr[0, n] (two kernels over
 // 2048-count tiles; each exits at once when F_FAN_OVER is clear)
 constexpr int CS_TPB = 256, CS_ITEMS = 8, CS_TILE = CS_TPB * CS_ITEMS;
 
@@ -228,30 +228,15 @@ __global__ void __launch_bounds__(CS_TPB) k_cscan_sum(const int32_t* __restrict_
     }
 }
 
-__global__ void __launch_bounds__(1024) k_cscan_top(int32_t* __restrict__ tsum, int64_t n, const WsHeader* hdr) {
-    if (!__ldg(&hdr->flags[F_FAN_OVER])) return;
-    using BS = cub::BlockScan<int, 1024>;
-    __shared__ typename BS::TempStorage tmp;
-    const int nt = (int)((n + CS_TILE - 1) / CS_TILE);
-    int carry = 0;
-    for (int c0 = 0; c0 < nt; c0 += 1024) {
-        const int i = c0 + threadIdx.x;
-        const int v = i < nt ? tsum[i] : 0;
-        int ex, agg;
-        BS(tmp).ExclusiveSum(v, ex, agg);
-        if (i < nt) tsum[i] = carry + ex;
-        carry += agg;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) tsum[nt] = carry;
-}
-
 __global__ void __launch_bounds__(CS_TPB) k_cscan_down(const int32_t* __restrict__ cnt, int64_t n,
                                                        const int32_t* __restrict__ tsum, int32_t* __restrict__ ptr,
                                                        const WsHeader* hdr) {
     if (!__ldg(&hdr->flags[F_FAN_OVER])) return;
     using BS = cub::BlockScan<int, CS_TPB>;
     __shared__ typename BS::TempStorage tmp;
+    using BR = cub::BlockReduce<int, CS_TPB>;
+    __shared__ typename BR::TempStorage rtmp;
+    __shared__ int s_base;
     const int64_t nt = (n + CS_TILE - 1) / CS_TILE;
     for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
         int v[CS_ITEMS], x[CS_ITEMS];
@@ -259,13 +244,26 @@ __global__ void __launch_bounds__(CS_TPB) k_cscan_down(const int32_t* __restrict
 #pragma unroll
         for (int k = 0; k < CS_ITEMS; ++k) v[k] = b + k < n ? cnt[b + k] : 0;
         BS(tmp).ExclusiveSum(v, x);
-        const int base = tsum[t];
+        // the tile's base: the sum of the tile totals before it (no
+        // single-CTA scan of the totals between the two passes; this path
+        // runs only after a fan overflow)
+        int pre = 0;
+        for (int64_t q = threadIdx.x; q < t; q += CS_TPB) pre += tsum[q];
+        const int bsum = BR(rtmp).Sum(pre);
+        if (threadIdx.x == 0) s_base = bsum;
+        __syncthreads();
+        const int base = s_base;
 #pragma unroll
         for (int k = 0; k < CS_ITEMS; ++k)
             if (b + k < n) ptr[b + k] = base + x[k];
         __syncthreads();
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) ptr[n] = tsum[nt];
+    if (blockIdx.x == 0) {  // ptr[n]: the sum of all tile totals
+        int pre = 0;
+        for (int64_t q = threadIdx.x; q < nt; q += CS_TPB) pre += tsum[q];
+        const int tot = BR(rtmp).Sum(pre);
+        if (threadIdx.x == 0) ptr[n] = tot;
+    }
 }
 
 // ---------------------------------------------------------------------------------
@@ -643,6 +641,28 @@ __global__ void k_fan_init(WsHeader* hdr) {
     }
 }
 
+// one launch before the fill: header reset (reset != 0), the fan counts and
+// the look-back tile states zeroed (in place of two memsets)
+__global__ void __launch_bounds__(256) k_fan_prep(WsHeader* hdr, int reset, int32_t* __restrict__ cnt, int64_t n,
+                                                  unsigned long long* __restrict__ tiles, int64_t ntiles) {
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+    if (reset && blockIdx.x == 0) {
+        const int i = threadIdx.x;
+        if (i < F_NFLAGS) hdr->flags[i] = 0;
+        if (i == 0) {
+            hdr->bad_element = ~0ull;
+            hdr->totals[0] = 0;
+            hdr->totals[1] = 0;
+            hdr->fan_big = 0;
+        }
+    }
+    const int64_t n4 = n >> 2;  // (cnt is 256-byte aligned: int4 stores)
+    int4* c4 = reinterpret_cast<int4*>(cnt);
+    for (int64_t i = i0; i < n4; i += st) c4[i] = make_int4(0, 0, 0, 0);
+    for (int64_t i = 4 * n4 + i0; i < n; i += st) cnt[i] = 0;
+    for (int64_t i = i0; i < ntiles; i += st) tiles[i] = 0ull;
+}
+
 }  // namespace
 
 // The symbolic half (K1-K3): sizes in the header totals, offsets and
@@ -656,20 +676,29 @@ efem_status launch_hdr_reset(Plan& p, cudaStream_t s) {
 efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset) {
     const int64_t Ng = p.n_nodes, T = p.n_elems;
     const int64_t lo = p.own_lo, N = p.own_n < 0 ? Ng : p.own_n;  // owned nodes [lo, lo + N)
-    if (reset) {
-        k_fan_init<<<1, 32, 0, s>>>(p.hdr);
-        EFEM_LAUNCH_CHECK();
-    }  // (else the caller reset the header)
-    const int ntiles = (int)grid_for(N, FAN_TILE);
-    if (ntiles > 0) EFEM_CUDA_TRY(cudaMemsetAsync(p.fan_tiles, 0, (size_t)ntiles * 8, s));
 #ifndef EFEM_FAN_FIXED
 #define EFEM_FAN_FIXED 1
 #endif
     // fixed-capacity fill (4 slots when the plan's last fan pass saw no fan
     // above 4, else 8) with the counting sort as the on-device fallback
     const int fix_c = EFEM_FAN_FIXED ? (p.fan_small ? 4 : FAN_FIXC) : 0;
+    const int ntiles = (int)grid_for(N, FAN_TILE);
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (fix_c) {
-        EFEM_CUDA_TRY(cudaMemsetAsync(p.cnt, 0, (size_t)N * 4, s));
+        const int64_t work = std::max<int64_t>(N / 4, ntiles);
+        const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(work, 256), 8 * sms));
+        k_fan_prep<<<g, 256, 0, s>>>(p.hdr, reset ? 1 : 0, p.cnt, N, p.fan_tiles, ntiles);
+        EFEM_LAUNCH_CHECK();
+    } else {
+        if (reset) {
+            k_fan_init<<<1, 32, 0, s>>>(p.hdr);
+            EFEM_LAUNCH_CHECK();
+        }
+        if (ntiles > 0) EFEM_CUDA_TRY(cudaMemsetAsync(p.fan_tiles, 0, (size_t)ntiles * 8, s));
+    }
+    if (fix_c) {
         if (T > 0) {
             if (fix_c == 4)
                 k_fan_fill_fixed<4><<<grid_for((T + 2 * FILL_NP - 1) / (2 * FILL_NP), 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
@@ -679,12 +708,7 @@ efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset) {
                                                                               p.hdr);
             EFEM_LAUNCH_CHECK();
         }
-        int sms = 148;
-        int dev = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         k_cscan_sum<<<2 * sms, CS_TPB, 0, s>>>(p.cnt, N, p.fan_csum, p.hdr);
-        EFEM_LAUNCH_CHECK();
-        k_cscan_top<<<1, 1024, 0, s>>>(p.fan_csum, N, p.hdr);
         EFEM_LAUNCH_CHECK();
         k_cscan_down<<<2 * sms, CS_TPB, 0, s>>>(p.cnt, N, p.fan_csum, p.fan_ptr, p.hdr);
         EFEM_LAUNCH_CHECK();
