@@ -450,3 +450,29 @@ def test_assemble_async_capacity_flagged(api):
         asm.check()
     assert ei.value.status == -8  # EFEM_ECAPACITY
     assert int(small.col_idx.abs().sum()) == 0  # nothing written
+
+
+@pytest.mark.parametrize("element", [RT0, NED0], ids=["rt0_2d", "ne0_2d"])
+def test_fan_fill_odd_count_and_unaligned_elems(api, element):
+    """The fan fill takes two triangles per thread with 8-byte loads: an odd
+    triangle count (the last thread's single triangle) and an element array
+    only 4-byte aligned (the scalar-load path) give the oracle's CSR too;
+    the triangles of each cell share their smallest vertex (one atomic per
+    pair) in the generator's order, and not after a shuffle."""
+    rc, re = ora.build_mesh(2, 13, 0.2, 31)
+    re = np.ascontiguousarray(re[:-1])  # a boundary triangle removed: T odd
+    assert re.shape[0] % 2 == 1
+    rng = np.random.default_rng(5)
+    for order in (np.arange(re.shape[0]), rng.permutation(re.shape[0])):
+        ee = np.ascontiguousarray(re[order])
+        ref = ora.assemble(2, element, rc, ee)
+        c = torch.from_numpy(rc).cuda()
+        for offset in (0, 1):  # int32 elements before the array: 0 or 4 bytes
+            buf = torch.zeros(ee.size + 4, dtype=torch.int32, device="cuda")
+            e = buf[offset:offset + ee.size].view(ee.shape[0], 3)
+            e.copy_(torch.from_numpy(ee))
+            assert (e.data_ptr() % 8 == 0) == (offset == 0)
+            asm = api.Assembler(c, e, element)
+            _, e2d, _ = asm.enumerate_dofs()
+            assert np.array_equal(e2d.cpu().numpy(), ref.elems2dofs)
+            assert_csr_parity(asm.assemble(), ref, what=f"offset={offset}")
