@@ -40,7 +40,10 @@
 namespace efem {
 namespace {
 
-constexpr int FAN_TPB = 128;
+#ifndef EFEM_FAN_TPB
+#define EFEM_FAN_TPB 128
+#endif
+constexpr int FAN_TPB = EFEM_FAN_TPB;
 // Register fast path: fans of <= FR triangles, 2 FR key registers.  FR = 8
 // covers every node of the meshes in the tests but one in a thousand; FR = 4
 // (all 2D triangulations average 4) leaves registers for 12 CTAs / SM and is
