@@ -117,14 +117,11 @@ __global__ void __launch_bounds__(256) k_fan_bucket(const int32_t* __restrict__ 
 // in the fan pass made its loads wait on the stores, 0.67 -> 1.55 ms; the
 // fallback's fill counts them down to zero).
 // ---------------------------------------------------------------------------------
-// 2 NP consecutive triangles per thread (NP pairs; 24 NP contiguous bytes
-// as 8- or 16-byte loads when the element array is aligned), all atomics
-// issued before the slot stores; the two triangles of a pair sharing their
-// smallest vertex (a structured cell) take both slots with one atomic
-#ifndef EFEM_FILL_NP
-#define EFEM_FILL_NP 1
-#endif
-constexpr int FILL_NP = EFEM_FILL_NP;
+// Two consecutive triangles per thread (24 contiguous bytes: three 8-byte
+// loads when the element array is 8-byte aligned), all atomics issued
+// before the slot stores.  The two triangles of a pair sharing their
+// smallest vertex (a structured cell) take both slots with one atomic.
+// Slot order inside a fan is immaterial (k_fan_nodes sorts).
 template <int C>
 __device__ __forceinline__ void fill_put(int32_t* __restrict__ fan_fix, int64_t l, int k, int e, bool& over) {
     if (k < C) fan_fix[l * C + k] = e;
@@ -135,35 +132,27 @@ __global__ void __launch_bounds__(256) k_fan_fill_fixed(const int32_t* __restric
                                                          int64_t n_nodes, int64_t lo, int64_t n_own,
                                                          int32_t* __restrict__ cnt, int32_t* __restrict__ fan_fix,
                                                          WsHeader* hdr) {
-    constexpr int NP = FILL_NP, NT = 2 * NP;
-    const int64_t e0 = NT * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    const int64_t e0 = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
     if (e0 >= n_elems) return;
-    int v[3 * NT];
-    const bool full = e0 + NT <= n_elems;
-    const uintptr_t al = reinterpret_cast<uintptr_t>(elems);
-    if (full && NT % 4 == 0 && !(al & 15)) {
-        const int4* p4 = reinterpret_cast<const int4*>(elems + 3 * e0);
-#pragma unroll
-        for (int q = 0; q < 3 * NT / 4; ++q) {
-            const int4 x = __ldg(p4 + q);
-            v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
-        }
-    } else if (full && !(al & 7)) {
+    int v[6];
+    const bool full = e0 + 2 <= n_elems;
+    if (full && !(reinterpret_cast<uintptr_t>(elems) & 7)) {
         const int2* p2 = reinterpret_cast<const int2*>(elems + 3 * e0);
 #pragma unroll
-        for (int q = 0; q < 3 * NT / 2; ++q) {
+        for (int q = 0; q < 3; ++q) {
             const int2 x = __ldg(p2 + q);
-            v[2 * q] = x.x; v[2 * q + 1] = x.y;
+            v[2 * q] = x.x;
+            v[2 * q + 1] = x.y;
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < 3 * NT; ++j) v[j] = e0 + j / 3 < n_elems ? __ldg(elems + 3 * e0 + j) : 0;
+        for (int j = 0; j < 6; ++j) v[j] = e0 + j / 3 < n_elems ? __ldg(elems + 3 * e0 + j) : 0;
     }
     bool inval = false;
-    bool op[NT], oq[NT];
-    int64_t lp[NT], lq[NT];
+    bool op[2], oq[2];
+    int64_t lp[2], lq[2];
 #pragma unroll
-    for (int i = 0; i < NT; ++i) {
+    for (int i = 0; i < 2; ++i) {
         const bool in = e0 + i < n_elems;
         const bool ok = in && !(invalid_node(v[3 * i], n_nodes) || invalid_node(v[3 * i + 1], n_nodes) ||
                                 invalid_node(v[3 * i + 2], n_nodes));
@@ -175,26 +164,23 @@ __global__ void __launch_bounds__(256) k_fan_fill_fixed(const int32_t* __restric
         oq[i] = ok && v[3 * i + 1] != v[3 * i] && (unsigned long long)lq[i] < (unsigned long long)n_own;
     }
     if (inval) atomicOr(&hdr->flags[F_INVALID_NODE], 1);
-    int kp[NT], kq[NT];
-#pragma unroll
-    for (int i = 0; i < NT; i += 2) {
-        kp[i] = kp[i + 1] = 0;
-        if (op[i] && op[i + 1] && lp[i] == lp[i + 1]) {
-            kp[i] = atomicAdd(cnt + lp[i], 2);
-            kp[i + 1] = kp[i] + 1;
-        } else {
-            if (op[i]) kp[i] = atomicAdd(cnt + lp[i], 1);
-            if (op[i + 1]) kp[i + 1] = atomicAdd(cnt + lp[i + 1], 1);
-        }
+    const bool pair = op[0] && op[1] && lp[0] == lp[1];
+    int kp0 = 0, kp1 = 0, kq0 = 0, kq1 = 0, base = 0;
+    if (pair) {
+        base = atomicAdd(cnt + lp[0], 2);
+        kp0 = base;
+        kp1 = base + 1;
+    } else {
+        if (op[0]) kp0 = atomicAdd(cnt + lp[0], 1);
+        if (op[1]) kp1 = atomicAdd(cnt + lp[1], 1);
     }
-#pragma unroll
-    for (int i = 0; i < NT; ++i) kq[i] = oq[i] ? atomicAdd(cnt + lq[i], 1) : 0;
+    if (oq[0]) kq0 = atomicAdd(cnt + lq[0], 1);
+    if (oq[1]) kq1 = atomicAdd(cnt + lq[1], 1);
     bool over = false;
-#pragma unroll
-    for (int i = 0; i < NT; ++i) {
-        if (op[i]) fill_put<C>(fan_fix, lp[i], kp[i], (int)e0 + i, over);
-        if (oq[i]) fill_put<C>(fan_fix, lq[i], kq[i], (int)e0 + i, over);
-    }
+    if (op[0]) fill_put<C>(fan_fix, lp[0], kp0, (int)e0, over);
+    if (op[1]) fill_put<C>(fan_fix, lp[1], kp1, (int)e0 + 1, over);
+    if (oq[0]) fill_put<C>(fan_fix, lq[0], kq0, (int)e0, over);
+    if (oq[1]) fill_put<C>(fan_fix, lq[1], kq1, (int)e0 + 1, over);
     if (over) atomicOr(&hdr->flags[F_FAN_OVER], 1);
 }
 
@@ -704,10 +690,10 @@ efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset) {
     if (fix_c) {
         if (T > 0) {
             if (fix_c == 4)
-                k_fan_fill_fixed<4><<<grid_for((T + 2 * FILL_NP - 1) / (2 * FILL_NP), 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
+                k_fan_fill_fixed<4><<<grid_for((T + 1) / 2, 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
                                                                                 p.hdr);
             else
-                k_fan_fill_fixed<FAN_FIXC><<<grid_for((T + 2 * FILL_NP - 1) / (2 * FILL_NP), 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
+                k_fan_fill_fixed<FAN_FIXC><<<grid_for((T + 1) / 2, 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_fix,
                                                                               p.hdr);
             EFEM_LAUNCH_CHECK();
         }
