@@ -14,9 +14,9 @@
 //                        whose return value is the slot of the triangle id
 //                        in the node's C fixed fan slots (C = 4 or 8); two
 //                        triangles per thread, one atomic for a shared p
-//   (fallback)           only when a fan overflows C (F_FAN_OVER): a scan
+//   k_fan_fallback       only when a fan overflows C (F_FAN_OVER): a scan
 //                        of the counts -> fan_ptr and the counting-sort
-//                        fill (k_cscan_*, k_fan_fill_cond: they exit at
+//                        fill, one launch with grid barriers (it exits at
 //                        once otherwise; the plain count / scan / fill
 //                        sequence with EFEM_FAN_FIXED=0)
 //   k_fan_nodes<FR>      per node: the owned edges as sorted (b, element,
@@ -74,7 +74,7 @@ __device__ __forceinline__ void sort3(int& p, int& q, int& r) {
 // ---------------------------------------------------------------------------------
 // (distributed assembly: only the fans of the owned nodes [lo, lo + n_own),
 // indexed from lo; single GPU: lo = 0, n_own = n_nodes)
-template <bool FILL>
+template <bool FILL, bool COH = false>
 __device__ __forceinline__ void fan_bucket_one(const int32_t* __restrict__ elems, int64_t e, int64_t n_nodes,
                                                int64_t lo, int64_t n_own, int32_t* __restrict__ cnt,
                                                const int32_t* __restrict__ fan_ptr, int32_t* __restrict__ fan,
@@ -92,8 +92,9 @@ __device__ __forceinline__ void fan_bucket_one(const int32_t* __restrict__ elems
         if (op) atomicAdd(cnt + lp, 1);
         if (oq) atomicAdd(cnt + lq, 1);
     } else {
-        if (op) fan[__ldg(fan_ptr + lp) + atomicSub(cnt + lp, 1) - 1] = (int)e;
-        if (oq) fan[__ldg(fan_ptr + lq) + atomicSub(cnt + lq, 1) - 1] = (int)e;
+        // (COH: fan_ptr was written by this kernel's other CTAs: no read-only path)
+        if (op) fan[(COH ? __ldcg(fan_ptr + lp) : __ldg(fan_ptr + lp)) + atomicSub(cnt + lp, 1) - 1] = (int)e;
+        if (oq) fan[(COH ? __ldcg(fan_ptr + lq) : __ldg(fan_ptr + lq)) + atomicSub(cnt + lq, 1) - 1] = (int)e;
     }
 }
 
@@ -184,26 +185,40 @@ __global__ void __launch_bounds__(256) k_fan_fill_fixed(const int32_t* __restric
     if (over) atomicOr(&hdr->flags[F_FAN_OVER], 1);
 }
 
-// the fallback (F_FAN_OVER set): the counting-sort fill over a fixed grid
-__global__ void __launch_bounds__(256) k_fan_fill_cond(const int32_t* __restrict__ elems, int64_t n_elems,
-                                                       int64_t n_nodes, int64_t lo, int64_t n_own,
-                                                       int32_t* __restrict__ cnt, const int32_t* __restrict__ fan_ptr,
-                                                       int32_t* __restrict__ fan, WsHeader* hdr) {
-    if (!__ldg(&hdr->flags[F_FAN_OVER])) return;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_elems; e += (int64_t)gridDim.x * blockDim.x)
-        fan_bucket_one<true>(elems, e, n_nodes, lo, n_own, cnt, fan_ptr, fan, hdr);
-}
-
-// the fallback's exclusive scan cnt[0, n) -> ptr[0, n] (two kernels over
-// 2048-count tiles; each exits at once when F_FAN_OVER is clear)
+// the fallback's scan tiles: 2048 counts
 constexpr int CS_TPB = 256, CS_ITEMS = 8, CS_TILE = CS_TPB * CS_ITEMS;
 
-__global__ void __launch_bounds__(CS_TPB) k_cscan_sum(const int32_t* __restrict__ cnt, int64_t n,
-                                                      int32_t* __restrict__ tsum, const WsHeader* hdr) {
-    if (!__ldg(&hdr->flags[F_FAN_OVER])) return;
+// The whole fallback as ONE launch (a step without an overflow pays one
+// launch that exits at once instead of three): the scan's two phases and
+// the counting-sort fill separated by software grid barriers.  The grid is
+// one CTA per SM, so every CTA is resident (the previous kernel on the
+// stream has drained); the barrier counter is the word after the look-back
+// tile states, zeroed by k_fan_prep.
+__device__ __forceinline__ void fb_grid_sync(unsigned* bar, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (*(volatile unsigned*)bar < target) __nanosleep(100);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(CS_TPB) k_fan_fallback(const int32_t* __restrict__ elems, int64_t n_elems,
+                                                         int64_t n_nodes, int64_t lo, int64_t n_own,
+                                                         int32_t* __restrict__ cnt, int32_t* __restrict__ tsum,
+                                                         int32_t* __restrict__ fan_ptr, int32_t* __restrict__ fan,
+                                                         unsigned* bar, WsHeader* hdr) {
+    if (!*(volatile const int*)&hdr->flags[F_FAN_OVER]) return;
+    using BS = cub::BlockScan<int, CS_TPB>;
     using BR = cub::BlockReduce<int, CS_TPB>;
-    __shared__ typename BR::TempStorage tmp;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ typename BR::TempStorage rtmp;
+    __shared__ int s_base;
+    const int64_t n = n_own;
     const int64_t nt = (n + CS_TILE - 1) / CS_TILE;
+    // (1) tile sums of the counts
     for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
         int v = 0;
 #pragma unroll
@@ -211,48 +226,39 @@ __global__ void __launch_bounds__(CS_TPB) k_cscan_sum(const int32_t* __restrict_
             const int64_t i = t * CS_TILE + k * CS_TPB + threadIdx.x;
             if (i < n) v += cnt[i];
         }
-        const int sum = BR(tmp).Sum(v);
+        const int sum = BR(rtmp).Sum(v);
         if (threadIdx.x == 0) tsum[t] = sum;
         __syncthreads();
     }
-}
-
-__global__ void __launch_bounds__(CS_TPB) k_cscan_down(const int32_t* __restrict__ cnt, int64_t n,
-                                                       const int32_t* __restrict__ tsum, int32_t* __restrict__ ptr,
-                                                       const WsHeader* hdr) {
-    if (!__ldg(&hdr->flags[F_FAN_OVER])) return;
-    using BS = cub::BlockScan<int, CS_TPB>;
-    __shared__ typename BS::TempStorage tmp;
-    using BR = cub::BlockReduce<int, CS_TPB>;
-    __shared__ typename BR::TempStorage rtmp;
-    __shared__ int s_base;
-    const int64_t nt = (n + CS_TILE - 1) / CS_TILE;
+    fb_grid_sync(bar, gridDim.x);
+    // (2) exclusive scan of each tile plus the sum of the tile totals before it
     for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
         int v[CS_ITEMS], x[CS_ITEMS];
         const int64_t b = t * CS_TILE + (int64_t)threadIdx.x * CS_ITEMS;  // blocked arrangement
 #pragma unroll
         for (int k = 0; k < CS_ITEMS; ++k) v[k] = b + k < n ? cnt[b + k] : 0;
         BS(tmp).ExclusiveSum(v, x);
-        // the tile's base: the sum of the tile totals before it (no
-        // single-CTA scan of the totals between the two passes; this path
-        // runs only after a fan overflow)
         int pre = 0;
-        for (int64_t q = threadIdx.x; q < t; q += CS_TPB) pre += tsum[q];
+        for (int64_t q = threadIdx.x; q < t; q += CS_TPB) pre += __ldcg(tsum + q);
         const int bsum = BR(rtmp).Sum(pre);
         if (threadIdx.x == 0) s_base = bsum;
         __syncthreads();
         const int base = s_base;
 #pragma unroll
         for (int k = 0; k < CS_ITEMS; ++k)
-            if (b + k < n) ptr[b + k] = base + x[k];
+            if (b + k < n) fan_ptr[b + k] = base + x[k];
         __syncthreads();
     }
-    if (blockIdx.x == 0) {  // ptr[n]: the sum of all tile totals
+    if (blockIdx.x == 0) {  // fan_ptr[n]: the sum of all tile totals
         int pre = 0;
-        for (int64_t q = threadIdx.x; q < nt; q += CS_TPB) pre += tsum[q];
+        for (int64_t q = threadIdx.x; q < nt; q += CS_TPB) pre += __ldcg(tsum + q);
         const int tot = BR(rtmp).Sum(pre);
-        if (threadIdx.x == 0) ptr[n] = tot;
+        if (threadIdx.x == 0) fan_ptr[n] = tot;
     }
+    fb_grid_sync(bar, 2 * gridDim.x);
+    // (3) the counting-sort fill (slots from the top of each count)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_elems; e += (int64_t)gridDim.x * blockDim.x)
+        fan_bucket_one<true, true>(elems, e, n_nodes, lo, n_own, cnt, fan_ptr, fan, hdr);
 }
 
 // ---------------------------------------------------------------------------------
@@ -678,7 +684,7 @@ efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset) {
     if (fix_c) {
         const int64_t work = std::max<int64_t>(N / 4, ntiles);
         const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(work, 256), 8 * sms));
-        k_fan_prep<<<g, 256, 0, s>>>(p.hdr, reset ? 1 : 0, p.cnt, N, p.fan_tiles, ntiles);
+        k_fan_prep<<<g, 256, 0, s>>>(p.hdr, reset ? 1 : 0, p.cnt, N, p.fan_tiles, ntiles + 1);  // (+ the fallback's barrier word)
         EFEM_LAUNCH_CHECK();
     } else {
         if (reset) {
@@ -697,14 +703,9 @@ efem_status launch_fan_symbolic(Plan& p, cudaStream_t s, bool reset) {
                                                                               p.hdr);
             EFEM_LAUNCH_CHECK();
         }
-        k_cscan_sum<<<2 * sms, CS_TPB, 0, s>>>(p.cnt, N, p.fan_csum, p.hdr);
+        k_fan_fallback<<<sms, CS_TPB, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_csum, p.fan_ptr, p.fan,
+                                              reinterpret_cast<unsigned*>(p.fan_tiles + ntiles), p.hdr);
         EFEM_LAUNCH_CHECK();
-        k_cscan_down<<<2 * sms, CS_TPB, 0, s>>>(p.cnt, N, p.fan_csum, p.fan_ptr, p.hdr);
-        EFEM_LAUNCH_CHECK();
-        if (T > 0) {
-            k_fan_fill_cond<<<8 * sms, 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, p.fan_ptr, p.fan, p.hdr);
-            EFEM_LAUNCH_CHECK();
-        }
     } else {
         if (T > 0) {
             k_fan_bucket<false><<<grid_for(T, 256), 256, 0, s>>>(p.elems, T, Ng, lo, N, p.cnt, nullptr, nullptr,
