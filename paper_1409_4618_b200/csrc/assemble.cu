@@ -16,7 +16,13 @@
 
 namespace efem {
 
-constexpr int NUM_TPB = 128;
+#ifndef EFEM_NE3_WARPFLUSH
+#define EFEM_NE3_WARPFLUSH 1
+#endif
+#ifndef EFEM_NE3_TPB
+#define EFEM_NE3_TPB 128
+#endif
+constexpr int NUM_TPB = EFEM_NE3_TPB;
 constexpr int kMaxDevices = 64;
 
 // ---------------------------------------------------------------------------------
@@ -799,7 +805,7 @@ __device__ __forceinline__ void ne3_fast_row(const double* __restrict__ coords, 
 }
 
 template <class KT>
-__global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__ coords,
+__global__ void __launch_bounds__(NUM_TPB, 512 / NUM_TPB) k_rows_ne3(const double* __restrict__ coords,
                                                       const int32_t* __restrict__ elems,
                                                       const int32_t* __restrict__ inc_ptr,
                                                       const int32_t* __restrict__ inc,
@@ -838,11 +844,26 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
     unsigned short* s_map = reinterpret_cast<unsigned short*>(s_off + NUM_TPB + 1);  // CSR position -> slot
     unsigned char* s_pos = reinterpret_cast<unsigned char*>(s_map + NE3_SLOTS * NUM_TPB);  // 16 per thread
 
+#if EFEM_NE3_WARPFLUSH
+    // every warp stages and flushes its own 32 rows (their CSR segment is
+    // contiguous): no CTA barrier between warps of unequal work
+    const int wq = (int)(threadIdx.x >> 5);
+    const int r0 = blockIdx.x * NUM_TPB + 32 * wq;
+    if (r0 >= n_rows) return;
+    const int nr = min(32, n_rows - r0);
+    unsigned short* const wmap = s_map + wq * (NE3_SLOTS * 32);
+    constexpr int FL_N = 32;
+    const int fl_i = (int)(threadIdx.x & 31);
+#else
     const int r0 = blockIdx.x * NUM_TPB;
     const int nr = min(NUM_TPB, n_rows - r0);
+    unsigned short* const wmap = s_map;
+    constexpr int FL_N = NUM_TPB;
+    const int fl_i = (int)threadIdx.x;
+#endif
     const int seg0 = __ldg(row_ptr + r0);
     const int segn = __ldg(row_ptr + r0 + nr) - seg0;
-    const int i = r0 + (int)threadIdx.x;
+    const int i = r0 + fl_i;
     int rlen = 0, ib = 0, t = 0;
     if (i < n_rows) {
         const int rb = __ldg(row_ptr + i);
@@ -855,7 +876,11 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
         ib = __ldg(inc_ptr + i);
         t = __ldg(inc_ptr + i + 1) - ib;
     }
+#if EFEM_NE3_WARPFLUSH
+    const bool staged = __all_sync(0xffffffffu, rlen <= NE3_SLOTS);
+#else
     const bool staged = __syncthreads_and(rlen <= NE3_SLOTS);
+#endif
 
     if (i < n_rows) {
         int* ccol;
@@ -895,14 +920,18 @@ __global__ void __launch_bounds__(NUM_TPB) k_rows_ne3(const double* __restrict__
             const int off = s_off[threadIdx.x];
 #pragma unroll
             for (int q = 0; q < NE3_SLOTS; ++q)
-                if (q < rlen) s_map[off + q] = (unsigned short)(q * NE3_LD + threadIdx.x);
+                if (q < rlen) wmap[off + q] = (unsigned short)(q * NE3_LD + threadIdx.x);
         }
     }
     if (!staged) return;
+#if EFEM_NE3_WARPFLUSH
+    __syncwarp();
+#else
     __syncthreads();
+#endif
     // coalesced flush in CSR order through the position -> slot map
-    for (int x = threadIdx.x; x < segn; x += NUM_TPB) {
-        const int src = s_map[x];
+    for (int x = fl_i; x < segn; x += FL_N) {
+        const int src = wmap[x];
         const int gx = seg0 - out_base + x;
         if (forms & EFEM_PATTERN) col_idx[gx] = s_col[src];
         if (forms & EFEM_MASS) vals_m[gx] = s_vm[src];
