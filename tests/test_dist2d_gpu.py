@@ -128,3 +128,36 @@ def test_group_degenerate_in_other_slab_reported():
     with pytest.raises(api._lib.EfemError) as ei:
         g.assemble()
     assert ei.value.status == -2
+
+
+@pytest.mark.parametrize("element", [RT0, NED0], ids=["rt0", "ne0"])
+def test_group_fan_overflow_off_rank0(element):
+    """A 200-triangle disc whose centre has a middle node id: its fan overflows
+    the fixed fan slots on a rank whose owned node range starts above 0, so
+    the one-launch fallback (k_fan_fallback: scan, grid barriers, counting
+    fill) runs with a node offset.  Slices concatenated = the 1-GPU CSR,
+    bitwise, on the first and a replayed step."""
+    from paper_1409_4618_b200 import api, dist
+    from test_unstructured_gpu import fan_mesh
+
+    pts, el = fan_mesh(200, 3)
+    n = pts.shape[0]
+    rng = np.random.default_rng(4)
+    perm = rng.permutation(n)  # new id of node i
+    perm[[0, int(np.where(perm == n // 2)[0][0])]] = perm[[int(np.where(perm == n // 2)[0][0]), 0]]
+    assert perm[0] == n // 2
+    c2 = np.empty_like(pts)
+    c2[perm] = pts
+    e2 = perm[el].astype(np.int32)
+    coords, elems = torch.from_numpy(c2).cuda(), torch.from_numpy(e2).cuda()
+    want = _single(api, coords, elems, element)
+    offset_seen = False
+    for P in (2, 3, 4):
+        g = dist.DistGroup(coords, elems, element, dist.slab_bounds(elems.shape[0], P))
+        infos = [g.info(r) for r in range(P)]
+        owner = [r for r in range(P) if infos[r][0] <= n // 2 < infos[r][1]][0]
+        offset_seen |= infos[owner][0] > 0  # the overflowing fan above the rank's first node
+        for _ in range(2):
+            g.assemble()
+            _compare(g.concat(), want)
+    assert offset_seen
